@@ -1,0 +1,116 @@
+"""ctypes binding of include/gaplra_cuda.h (libgaplra_cuda.so, built in-tree).
+
+The product path has no CPU fallback: if the shared library is missing or no
+CUDA device is present, loading / context creation raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import re
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+ROOT = PKG.parent
+LIB_PATH = PKG / "libgaplra_cuda.so"
+HEADER = ROOT / "include" / "gaplra_cuda.h"
+
+_dp = C.POINTER(C.c_double)
+_i32p = C.POINTER(C.c_int32)
+_i64p = C.POINTER(C.c_int64)
+_ip = C.POINTER(C.c_int)
+
+
+class SvrgParams(C.Structure):
+    _fields_ = [("eta", C.c_double), ("m", C.c_int64), ("tol", C.c_double), ("epoch_cap", C.c_int),
+                ("monotone_slack", C.c_double), ("root_seed", C.c_uint64)]
+
+
+class Ledger(C.Structure):
+    _fields_ = [(n, C.c_uint64) for n in (
+        "gram_applies", "operator_applies", "qr_factorizations", "linear_solves",
+        "solver_column_samples", "epochs", "outer_iterations")]
+
+    def as_dict(self):
+        return {k: int(getattr(self, k)) for k, _ in self._fields_}
+
+
+class SiConfig(C.Structure):
+    _fields_ = [("k", C.c_int), ("p", C.c_int), ("eps", C.c_double), ("mu", C.c_double),
+                ("delta", C.c_double), ("lambda_", C.c_double), ("seed", C.c_uint64),
+                ("tol_solve", C.c_double), ("tol_tune", C.c_double), ("conv_tol", C.c_double),
+                ("rq_tol", C.c_double), ("max_outer", C.c_int), ("force", C.c_int),
+                ("epoch_cap", C.c_int), ("monotone_slack", C.c_double)]
+
+
+class SiReport(C.Structure):
+    _fields_ = [("lambda_", C.c_double), ("lambda1_hat", C.c_double), ("tune_steps", C.c_int),
+                ("tune_lambda", C.c_double * 64), ("tune_inv", C.c_double * 64),
+                ("outer_iterations", C.c_int), ("outer_cap", C.c_int), ("ledger", Ledger),
+                ("ms_tune", C.c_double), ("ms_subspace", C.c_double),
+                ("ms_rayleigh_ritz", C.c_double), ("ms_total", C.c_double)]
+
+
+_SIGS = {
+    "gaplra_version": (C.c_int, []),
+    "gaplra_ctx_create": (C.c_int, [C.c_int, C.POINTER(C.c_void_p)]),
+    "gaplra_ctx_destroy": (C.c_int, [C.c_void_p]),
+    "gaplra_last_error": (C.c_char_p, [C.c_void_p]),
+    "gaplra_ctx_set_stream": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "gaplra_ctx_synchronize": (C.c_int, [C.c_void_p]),
+    "gaplra_ledger_get": (C.c_int, [C.c_void_p, C.POINTER(Ledger)]),
+    "gaplra_ledger_reset": (C.c_int, [C.c_void_p]),
+    "gaplra_matrix_dense": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int64, C.c_int,
+                                      C.POINTER(C.c_void_p)]),
+    "gaplra_matrix_csc": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
+                                    C.c_int, C.POINTER(C.c_void_p)]),
+    "gaplra_matrix_destroy": (C.c_int, [C.c_void_p]),
+    "gaplra_matrix_info": (C.c_int, [C.c_void_p, _ip, _ip, _i64p, _i64p]),
+    "gaplra_gram_apply": (C.c_int, [C.c_void_p, C.c_void_p, _dp, _dp]),
+    "gaplra_gram_block": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, _dp, _dp, _dp]),
+    "gaplra_gram_block_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_int64,
+                                           C.c_void_p, C.c_int64, C.c_void_p, C.c_int64]),
+    "gaplra_index_stream": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_int64, _i32p]),
+    "gaplra_gaussian_init": (C.c_int, [C.c_int, C.c_int, C.c_uint64, _dp]),
+    "gaplra_qr_orthonormalize": (C.c_int, [C.c_void_p, C.c_int, C.c_int, _dp, _dp, _ip]),
+    "gaplra_orthonormality_defect": (C.c_int, [C.c_void_p, C.c_int, C.c_int, _dp, _dp]),
+    "gaplra_jacobi_eigh": (C.c_int, [C.c_void_p, C.c_int, _dp, _dp, _dp]),
+    "gaplra_svrg_epoch": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, _dp, _dp, _dp, C.c_double,
+                                    C.c_double, C.c_uint64, C.c_int64]),
+    "gaplra_svrg_solve": (C.c_int, [C.c_void_p, C.c_void_p, C.c_double, C.c_int, _dp, _dp,
+                                    C.POINTER(SvrgParams), C.c_int64, _ip, _dp, C.c_int, _ip]),
+    "gaplra_estimate_top": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_double, C.c_double,
+                                      C.c_uint64, C.c_double, C.POINTER(SvrgParams), _i64p, _dp, _ip]),
+    "gaplra_tune_shift": (C.c_int, [C.c_void_p, C.c_void_p, C.c_double, C.POINTER(SiConfig), _i64p,
+                                    C.POINTER(SiReport)]),
+    "gaplra_restricted_projection": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, _dp, C.c_int, _dp, _dp]),
+    "gaplra_shift_invert": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(SiConfig), _dp, _dp, _dp,
+                                      C.POINTER(SiReport)]),
+}
+
+
+def header_symbols() -> list[str]:
+    """Every entry point include/gaplra_cuda.h declares."""
+    return re.findall(r"GAPLRA_API\s+(?:int|const char\*)\s+(gaplra_\w+)\(", HEADER.read_text())
+
+
+_LIB = None
+
+
+def load(path: Path | None = None) -> C.CDLL:
+    """Load libgaplra_cuda.so; raises (no CPU fallback) if it is not built."""
+    global _LIB
+    if _LIB is not None and path is None:
+        return _LIB
+    p = Path(path or os.environ.get("GAPLRA_CUDA_LIB", LIB_PATH))
+    if not p.exists():
+        raise ImportError(f"{p} is not built: run `python -c 'import __graft_entry__ as g; g.build()'` "
+                          "(the product path has no CPU fallback)")
+    lib = C.CDLL(str(p))
+    for name, (res, args) in _SIGS.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    if path is None:
+        _LIB = lib
+    return lib

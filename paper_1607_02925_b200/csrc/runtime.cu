@@ -1,0 +1,1048 @@
+// Native runtime of the B200 shift-and-invert path: context / resident X /
+// workspaces, and the drivers that sequence the device kernels — block SVRG
+// solve, Alg. 3 estimate,
+// tune_shift, subspace_iterate,
+// restricted_projection and the ShiftedInverse pipeline —
+// behind the C ABI of include/gaplra_cuda.h.  Every pinned choice (seeds,
+// stopping rules, W0 = 0, last iterate) matches oracle/oracle.cpp; see
+// DESIGN.md §2.  There is no CPU compute path: every numeric step is a kernel.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "../../include/gaplra_cuda.h"
+#include "common.cuh"
+#include "gram.cuh"
+#include "linalg.cuh"
+#include "rng.cuh"
+#include "svrg.cuh"
+
+namespace gaplra_cuda {
+
+template <class T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  ~DBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  T* ensure(size_t k) {
+    if (k <= n && p) return p;
+    release();
+    GAPLRA_CUDA_CHECK(cudaMalloc(&p, std::max<size_t>(k, 1) * sizeof(T)));
+    GAPLRA_CUDA_CHECK(cudaMemset(p, 0, std::max<size_t>(k, 1) * sizeof(T)));
+    n = k;
+    return p;
+  }
+};
+
+inline int64_t ldp_of(int p) { return p == 1 ? 1 : (p + 1) / 2 * 2; }
+inline int64_t round4(int64_t d) { return (d + 3) / 4 * 4; }
+
+// ---------------------------------------------------------------------------
+// Host Rng (bit-exact with rng.cpp) for gaussian_init: S0 is generated on the
+// host because device libm (log/sin/cos) differs in the last ulp.
+// ---------------------------------------------------------------------------
+struct HostRng {
+  uint64_t s[4];
+  double spare = 0.0;
+  bool has = false;
+  static uint64_t sm(uint64_t& x) {
+    x += 0x9E3779B97F4A7C15ull;
+    uint64_t z = x;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+  }
+  static uint64_t rl(uint64_t x, int k) { return (x << k) | (x >> (64 - k)); }
+  explicit HostRng(uint64_t seed) {
+    uint64_t t = seed;
+    for (auto& w : s) w = sm(t);
+  }
+  uint64_t next() {
+    const uint64_t out = rl(s[0] + s[3], 23) + s[0];
+    const uint64_t t = s[1] << 17;
+    s[2] ^= s[0];
+    s[3] ^= s[1];
+    s[1] ^= s[2];
+    s[0] ^= s[3];
+    s[2] ^= t;
+    s[3] = rl(s[3], 45);
+    return out;
+  }
+  double u01() { return static_cast<double>(next() >> 11) * 0x1.0p-53; }
+  double normal() {
+    if (has) {
+      has = false;
+      return spare;
+    }
+    double u1;
+    do {
+      u1 = u01();
+    } while (u1 <= 0.0);
+    const double u2 = u01();
+    const double radius = std::sqrt(-2.0 * std::log(u1));
+    const double angle = 2.0 * M_PI * u2;
+    spare = radius * std::sin(angle);
+    has = true;
+    return radius * std::cos(angle);
+  }
+};
+
+void gaussian_init_host(int d, int p, uint64_t seed, double* out_rowmajor, int64_t ld) {
+  if (p < 1 || p > d) throw Error(kContractViolation, "gaussian_init: requires 1 <= p <= d");
+  HostRng r(derive_seed(seed, kTagGauss));
+  for (int i = 0; i < d; ++i)
+    for (int c = 0; c < p; ++c) out_rowmajor[static_cast<int64_t>(i) * ld + c] = r.normal();
+}
+
+// ---------------------------------------------------------------------------
+struct Matrix {
+  int kind = 0;  // 0 dense, 1 csc
+  int d = 0, n = 0;
+  int64_t ld = 0, nnz = 0;
+  DBuf<double> xbuf;
+  const double* x = nullptr;
+  DBuf<int64_t> colptr, rowptr;
+  DBuf<int32_t> rowidx, colidx;
+  DBuf<double> val, rval;
+  double maxn2 = -1.0;
+  int device = 0;
+  DenseX dense() const {
+    DenseX X;
+    X.x = x;
+    X.ld = ld;
+    X.d = d;
+    X.n = n;
+    return X;
+  }
+  SparseX sparse() const {
+    SparseX S;
+    S.d = d;
+    S.n = n;
+    S.nnz = nnz;
+    S.colptr = colptr.p;
+    S.rowidx = rowidx.p;
+    S.val = val.p;
+    S.rowptr = rowptr.p;
+    S.colidx = colidx.p;
+    S.rval = rval.p;
+    return S;
+  }
+  int64_t d_pad() const { return kind == 0 ? ld : round4(d); }
+};
+
+struct Ledger {
+  gaplra_ledger v{};
+};
+
+struct Context {
+  int device = 0;
+  cudaStream_t own = nullptr, st = nullptr;
+  std::string err;
+  gaplra_ledger led{};
+  // workspaces
+  DBuf<double> gw, ybuf, hbuf, zbuf, cbuf, wbuf, bbuf, sbuf, tbuf, qrs, small, apart, bnorm, scal, tmp;
+  DBuf<int32_t> idx;
+  DBuf<unsigned int> rej;
+  DBuf<int> status;
+  double* pin = nullptr;  // pinned host scalars
+  int* pin_i = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  ~Context() {
+    if (pin) cudaFreeHost(pin);
+    if (pin_i) cudaFreeHost(pin_i);
+    if (ev0) cudaEventDestroy(ev0);
+    if (ev1) cudaEventDestroy(ev1);
+    if (own) cudaStreamDestroy(own);
+  }
+  void sync() { GAPLRA_CUDA_CHECK(cudaStreamSynchronize(st)); }
+  double read_scalar(const double* dptr) {
+    GAPLRA_CUDA_CHECK(cudaMemcpyAsync(pin, dptr, sizeof(double), cudaMemcpyDeviceToHost, st));
+    sync();
+    return pin[0];
+  }
+};
+
+struct Timer {
+  Context& c;
+  double* acc;
+  cudaEvent_t a, b;
+  Timer(Context& cc, double* out) : c(cc), acc(out) {
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a, c.st);
+  }
+  ~Timer() {
+    cudaEventRecord(b, c.st);
+    cudaEventSynchronize(b);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, a, b);
+    if (acc) *acc += ms;
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+  }
+};
+
+// ---------------------------------------------------------------------------
+// Units
+// ---------------------------------------------------------------------------
+double max_col_norm2(Context& c, Matrix& X) {
+  if (X.maxn2 < 0.0) {
+    double* s = c.scal.ensure(8);
+    X.maxn2 = X.kind == 0 ? max_col_norm2_dense(X.dense(), s, c.st) : max_col_norm2_sparse(X.sparse(), s, c.st);
+  }
+  return X.maxn2;
+}
+
+// Z (d_pad x ldz) = X (Xᵀ W); Y (n x ldy) = Xᵀ W.
+void gram_block_dev(Context& c, const Matrix& X, int p, const double* W, int64_t ldw, double* Z, int64_t ldz,
+                    double* Y, int64_t ldy) {
+  if (!Y) {
+    ldy = ldp_of(p);
+    Y = c.ybuf.ensure(static_cast<size_t>(X.n) * ldy);
+  }
+  if (X.kind == 0) {
+    const DenseX D = X.dense();
+    GramWork w;
+    w.part_elems = gram_work_elems(D, p);
+    w.part = w.part_elems ? c.gw.ensure(w.part_elems) : nullptr;
+    launch_xtw(D, W, ldw, p, Y, ldy, w, c.st);
+    launch_xy(D, Y, ldy, p, Z, ldz, w, c.st);
+  } else {
+    const SparseX S = X.sparse();
+    launch_xtw_sparse(S, W, ldw, p, Y, ldy, c.st);
+    launch_xy_sparse(S, Y, ldy, p, Z, ldz, c.st);
+  }
+  c.led.gram_applies += p;
+}
+
+// QR (two-pass MGS) in place on a row-major device block; throws RankDeficient.
+void qr_dev(Context& c, double* Y, int64_t ldy, int d, int p, bool count = true) {
+  if (d < p || p < 1) throw Error(kContractViolation, "qr_orthonormalize: need 1 <= cols <= rows");
+  double* scratch = c.qrs.ensure(static_cast<size_t>(p) * round4(d));
+  int* status = c.status.ensure(2);
+  launch_qr_mgs2(Y, ldy, d, p, scratch, status, c.st);
+  GAPLRA_CUDA_CHECK(cudaMemcpyAsync(c.pin_i, status, 2 * sizeof(int), cudaMemcpyDeviceToHost, c.st));
+  c.sync();
+  if (count) c.led.qr_factorizations++;
+  if (c.pin_i[0] == kRankDeficient)
+    throw Error(kRankDeficient, "qr_orthonormalize: column " + std::to_string(c.pin_i[1]) +
+                                    " is numerically dependent on earlier columns",
+                c.pin_i[1]);
+}
+
+struct SvrgResult {
+  int epochs = 0;
+  std::vector<double> history;
+};
+
+struct SvrgParams {
+  double eta, tol, slack;
+  int64_t m;
+  int cap;
+  uint64_t root;
+};
+
+SvrgParams resolve(Context& c, Matrix& X, double lambda, const gaplra_svrg_params& prm) {
+  if (!(prm.tol > 0.0)) throw Error(kContractViolation, "solve_svrg: tol must be > 0");
+  SvrgParams s;
+  s.eta = prm.eta > 0.0 ? prm.eta : 1.0 / (4.0 * (lambda + static_cast<double>(X.n) * max_col_norm2(c, X)));
+  s.m = prm.m > 0 ? prm.m : 2 * static_cast<int64_t>(X.n);
+  s.cap = prm.epoch_cap > 0 ? prm.epoch_cap : static_cast<int>(std::ceil(200.0 * std::log(1.0 / prm.tol)));
+  s.tol = prm.tol;
+  s.slack = prm.monotone_slack;
+  s.root = prm.root_seed;
+  return s;
+}
+
+// One stochastic epoch on device blocks (ld = ldp(p)): W in/out, C, Y given;
+// H = Xᵀ C computed here (dense only).
+void epoch_dev(Context& c, Matrix& X, int p, double* W, const double* C, const double* Y, double eta,
+               double lambda, uint64_t stream_seed, int64_t m) {
+  const int64_t ld = ldp_of(p);
+  int32_t* idx = c.idx.ensure(static_cast<size_t>(m));
+  launch_index_stream(stream_seed, static_cast<uint64_t>(X.n), m, idx, c.rej.ensure(1), c.st);
+  const double rho = 1.0 - eta * lambda;
+  const double eta_n = eta * static_cast<double>(X.n);
+  if (X.kind == 0) {
+    double* H = c.hbuf.ensure(static_cast<size_t>(X.n) * ld);
+    GramWork w;
+    const DenseX D = X.dense();
+    w.part_elems = gram_work_elems(D, p);
+    w.part = w.part_elems ? c.gw.ensure(w.part_elems) : nullptr;
+    launch_xtw(D, C, ld, p, H, ld, w, c.st);
+    EpochArgs a{};
+    a.X = X.x;
+    a.ldx = X.ld;
+    a.d_pad = static_cast<int>(X.ld);
+    a.n = X.n;
+    a.idx = idx;
+    a.m = m;
+    a.W = W;
+    a.C = C;
+    a.ldw = ld;
+    a.Y = Y;
+    a.H = H;
+    a.ldy = ld;
+    a.p = p;
+    a.rho = rho;
+    a.eta_n = eta_n;
+    launch_svrg_epoch_dense(a, choose_epoch_config(a.d_pad, p), c.st);
+  } else {
+    SparseEpochArgs a{};
+    a.d = X.d;
+    a.n = X.n;
+    a.p = p;
+    a.colptr = X.colptr.p;
+    a.rowidx = X.rowidx.p;
+    a.val = X.val.p;
+    a.idx = idx;
+    a.m = m;
+    a.W = W;
+    a.C = C;
+    a.ldw = ld;
+    a.Y = Y;
+    a.ldy = ld;
+    a.rho = rho;
+    a.eta_n = eta_n;
+    launch_svrg_epoch_sparse(a, c.st);
+  }
+}
+
+// Block solve (λI − XXᵀ)W = B with W0 = 0; B, W device blocks with ld = ldp(p).
+SvrgResult svrg_solve_dev(Context& c, Matrix& X, double lambda, int p, const double* B, double* W,
+                          const gaplra_svrg_params& prm_in, int64_t solve_id, SvrgResult* partial = nullptr) {
+  const SvrgParams prm = resolve(c, X, lambda, prm_in);
+  const int64_t ld = ldp_of(p), dp = X.d_pad();
+  const size_t blk = static_cast<size_t>(dp) * ld;
+  double* Z = c.zbuf.ensure(blk);
+  double* C = c.cbuf.ensure(blk);
+  double* Y = c.ybuf.ensure(static_cast<size_t>(X.n) * ld);
+  double* part = c.apart.ensure(static_cast<size_t>(anchor_parts(static_cast<int>(dp))) * 64);
+  double* bn = c.bnorm.ensure(64);
+  double* res = c.scal.ensure(8) + 1;
+  // |B_c| via the anchor kernel with W = Z = 0, λ = 0  (M = −B).
+  launch_anchor(nullptr, nullptr, B, ld, static_cast<int>(dp), p, 0.0, 0.0, nullptr, part, nullptr, bn, res, c.st);
+  GAPLRA_CUDA_CHECK(cudaMemsetAsync(W, 0, blk * sizeof(double), c.st));
+  SvrgResult local;
+  SvrgResult& out = partial ? *partial : local;
+  out = SvrgResult{};
+  double best = INFINITY;
+  for (int e = 0;; ++e) {
+    if (e > 0) gram_block_dev(c, X, p, W, ld, Z, ld, Y, ld);
+    else GAPLRA_CUDA_CHECK(cudaMemsetAsync(Y, 0, static_cast<size_t>(X.n) * ld * sizeof(double), c.st));
+    launch_anchor(e > 0 ? W : nullptr, e > 0 ? Z : nullptr, B, ld, static_cast<int>(dp), p, lambda, prm.eta, C, part,
+                  bn, nullptr, res, c.st);
+    const double r = c.read_scalar(res);
+    out.history.push_back(r);
+    if (!std::isfinite(r)) throw Error(kSolverStalled, "solve_svrg: non-finite residual (indefinite shift?)");
+    if (r <= prm.tol) break;
+    if (prm.slack > 0.0 && e >= 1 && r > prm.slack * best)
+      throw Error(kSolverStalled, "solve_svrg: residual grew above slack x best (epoch " + std::to_string(e) + ")");
+    best = std::min(best, r);
+    if (e >= prm.cap) throw Error(kSolverStalled, "solve_svrg: epoch cap reached");
+    epoch_dev(c, X, p, W, C, Y, prm.eta, lambda, svrg_stream_seed(prm.root, solve_id, e), prm.m);
+    out.epochs++;
+    c.led.epochs++;
+    c.led.solver_column_samples += static_cast<uint64_t>(prm.m);
+  }
+  c.led.linear_solves++;
+  return out;
+}
+
+// ---------------------------------------------------------------------------
+// Operators and the subspace engine.
+// ---------------------------------------------------------------------------
+struct Op {
+  virtual ~Op() = default;
+  // out = op(in), device blocks with ld = ldp(p)
+  virtual void apply(const double* in, double* out, int p) = 0;
+};
+
+struct GramOp : Op {
+  Context& c;
+  Matrix& X;
+  GramOp(Context& cc, Matrix& xx) : c(cc), X(xx) {}
+  void apply(const double* in, double* out, int p) override {
+    gram_block_dev(c, X, p, in, ldp_of(p), out, ldp_of(p), nullptr, 0);
+    c.led.operator_applies += p;
+  }
+};
+
+struct InverseOp : Op {
+  Context& c;
+  Matrix& X;
+  double lambda;
+  gaplra_svrg_params prm;
+  int64_t* counter;
+  InverseOp(Context& cc, Matrix& xx, double lam, const gaplra_svrg_params& pr, int64_t* sc)
+      : c(cc), X(xx), lambda(lam), prm(pr), counter(sc) {}
+  void apply(const double* in, double* out, int p) override {
+    svrg_solve_dev(c, X, lambda, p, in, out, prm, (*counter)++);
+    c.led.operator_applies += p;
+  }
+};
+
+// S0 = QR(gaussian_init(d, p, seed)), redraw once with seed + 1.
+void orth_init(Context& c, int d, int64_t dp, int p, uint64_t seed, double* S) {
+  const int64_t ld = ldp_of(p);
+  std::vector<double> h(static_cast<size_t>(dp) * ld, 0.0);
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    gaussian_init_host(d, p, seed + attempt, h.data(), ld);
+    GAPLRA_CUDA_CHECK(cudaMemcpyAsync(S, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice, c.st));
+    try {
+      qr_dev(c, S, ld, d, p, /*count=*/false);
+      return;
+    } catch (const Error& e) {
+      if (e.code != kRankDeficient || attempt == 1) throw;
+    }
+  }
+}
+
+// |S Sᵀ − S' S'ᵀ|_F = sqrt(2) |S' − S (Sᵀ S')|_F
+double projector_diff_dev(Context& c, const double* S, const double* S2, int d, int p) {
+  const int64_t ld = ldp_of(p);
+  double* G = c.small.ensure(static_cast<size_t>(64) * 64 + 8);
+  double* part = c.tmp.ensure(static_cast<size_t>(small_gram_parts(d)) * 64 * 64 + 8);
+  launch_small_gram(S, ld, p, S2, ld, p, d, part, G, c.st);
+  double* R = c.tbuf.ensure(static_cast<size_t>(round4(d)) * ld);
+  GAPLRA_CUDA_CHECK(cudaMemcpyAsync(R, S2, static_cast<size_t>(d) * ld * sizeof(double), cudaMemcpyDeviceToDevice, c.st));
+  launch_small_mul(S, ld, p, G, p, p, d, 1.0, -1.0, R, ld, c.st);
+  double* out = c.scal.ensure(8) + 2;
+  launch_frob2(R, ld, d, p, part, out, c.st);
+  return std::sqrt(2.0 * c.read_scalar(out));
+}
+
+// Alg. 1 with projector early stop; returns the final S in `S` (device).
+int subspace_iterate_dev(Context& c, Op& op, int d, int64_t dp, int p, int L, uint64_t seed, double conv_tol,
+                         double* S) {
+  const int64_t ld = ldp_of(p);
+  orth_init(c, d, dp, p, seed, S);
+  double* Yb = c.sbuf.ensure(static_cast<size_t>(dp) * ld);
+  int it = 0;
+  for (int l = 1; l <= L; ++l) {
+    op.apply(S, Yb, p);
+    qr_dev(c, Yb, ld, d, p);
+    it = l;
+    const bool stop = conv_tol > 0.0 && projector_diff_dev(c, S, Yb, d, p) <= conv_tol;
+    GAPLRA_CUDA_CHECK(cudaMemcpyAsync(S, Yb, static_cast<size_t>(dp) * ld * sizeof(double), cudaMemcpyDeviceToDevice, c.st));
+    if (stop) break;
+  }
+  c.led.outer_iterations += it;
+  return it;
+}
+
+// Alg. 3, k = 1 (Rayleigh quotient of the iterate, relative-change early stop).
+double estimate_top_dev(Context& c, Op& op, int d, int64_t dp, double eps_prime, uint64_t seed, double rq_tol,
+                        int* iters) {
+  const int L = static_cast<int>(std::ceil(4.0 / eps_prime * std::log(d / eps_prime)));
+  DBuf<double> s, y;
+  double* S = s.ensure(static_cast<size_t>(dp));
+  double* Yb = y.ensure(static_cast<size_t>(dp));
+  orth_init(c, d, dp, 1, seed, S);
+  double* G = c.small.ensure(static_cast<size_t>(64) * 64 + 8);
+  double* part = c.tmp.ensure(static_cast<size_t>(small_gram_parts(d)) * 64 * 64 + 8);
+  double prev = 0.0, theta = 0.0;
+  int it = 0;
+  for (int l = 1; l <= L + 1; ++l) {
+    op.apply(S, Yb, 1);
+    it = l;
+    launch_small_gram(S, 1, 1, Yb, 1, 1, d, part, G, c.st);
+    theta = c.read_scalar(G);
+    if (l > 1 && std::fabs(theta - prev) <= rq_tol * std::fabs(theta)) break;
+    if (l == L + 1) break;
+    qr_dev(c, Yb, 1, d, 1);
+    std::swap(S, Yb);
+    prev = theta;
+  }
+  if (iters) *iters = it;
+  return theta;
+}
+
+gaplra_svrg_params prm_from(const gaplra_si_config& cfg, double tol) {
+  gaplra_svrg_params p{};
+  p.eta = 0.0;
+  p.m = 0;
+  p.tol = tol;
+  p.epoch_cap = cfg.epoch_cap;
+  p.monotone_slack = cfg.monotone_slack;
+  p.root_seed = cfg.seed;
+  return p;
+}
+
+void tune_shift_dev(Context& c, Matrix& X, double delta, const gaplra_si_config& cfg, int64_t* counter,
+                    gaplra_si_report& rep) {
+  if (!(delta > 0.0)) throw Error(kContractViolation, "tune_shift: delta must be > 0");
+  const int d = X.d;
+  const int64_t dp = X.d_pad();
+  GramOp a(c, X);
+  const double l1 = estimate_top_dev(c, a, d, dp, 0.25, derive_seed(cfg.seed, kTagEstA), cfg.rq_tol, nullptr);
+  rep.lambda1_hat = l1;
+  rep.tune_steps = 0;
+  if (l1 < 3.0 * delta && !cfg.force)
+    throw Error(kNoPreconditioningNeeded, "tune_shift: lambda1_hat < 3 delta (no preconditioning needed)");
+  double lambda = 1.5 * l1;
+  const double ratio = l1 / delta;
+  const int cap = (ratio > 1.0 ? static_cast<int>(std::ceil(4.0 * std::log2(ratio))) : 0) + 5;
+  const gaplra_svrg_params prm = prm_from(cfg, cfg.tol_tune);
+  for (int t = 0; t < cap; ++t) {
+    InverseOp dinv(c, X, lambda, prm, counter);
+    const double est = estimate_top_dev(c, dinv, d, dp, 1.0 / 9.0, derive_seed(cfg.seed, kTagEstD + t), cfg.rq_tol,
+                                        nullptr);
+    const double inv = 1.0 / std::max(est, 1e-300);
+    if (rep.tune_steps < 64) {
+      rep.tune_lambda[rep.tune_steps] = lambda;
+      rep.tune_inv[rep.tune_steps] = inv;
+    }
+    rep.tune_steps++;
+    if (inv >= delta / 27.0 && inv <= delta / 5.0) {
+      rep.lambda = lambda;
+      return;
+    }
+    lambda = lambda - (4.0 / 9.0) * inv;
+  }
+  rep.lambda = lambda;
+  throw Error(kShiftTuningStalled, "tune_shift: no estimate landed in [delta/27, delta/5]");
+}
+
+// W (d_pad x ldp(k)) = S U_k, ritz[k] (host) from H = Sᵀ X Xᵀ S.
+void restricted_projection_dev(Context& c, Matrix& X, const double* S, int p, int k, double* W, double* ritz_host) {
+  const int d = X.d;
+  const int64_t dp = X.d_pad(), ld = ldp_of(p);
+  if (k < 1 || k > p || p > kJacobiMax) throw Error(kContractViolation, "restricted_projection: need 1 <= k <= p <= 64");
+  DBuf<double> z;
+  double* Z = z.ensure(static_cast<size_t>(dp) * ld);
+  gram_block_dev(c, X, p, S, ld, Z, ld, nullptr, 0);
+  double* H = c.small.ensure(static_cast<size_t>(64) * 64 + 8);
+  double* part = c.tmp.ensure(static_cast<size_t>(small_gram_parts(d)) * 64 * 64 + 8);
+  launch_small_gram(S, ld, p, Z, ld, p, d, part, H, c.st);
+  DBuf<double> vv;
+  double* vals = vv.ensure(static_cast<size_t>(p) + static_cast<size_t>(p) * p);
+  double* vecs = vals + p;
+  launch_jacobi(H, p, vals, vecs, c.st);
+  launch_small_mul(S, ld, p, vecs, p, k, d, 0.0, 1.0, W, ldp_of(k), c.st);
+  GAPLRA_CUDA_CHECK(cudaMemcpyAsync(ritz_host, vals, k * sizeof(double), cudaMemcpyDeviceToHost, c.st));
+  c.sync();
+}
+
+int outer_cap(const gaplra_si_config& cfg, int d) {
+  if (cfg.max_outer > 0) return cfg.max_outer;
+  const double eps_int = cfg.eps / (3.0 * std::max(cfg.mu, 1.0) * cfg.k * d);
+  return static_cast<int>(std::ceil(4.0 * cfg.k * std::log(cfg.k * static_cast<double>(d) / eps_int)));
+}
+
+// ---------------------------------------------------------------------------
+// Host <-> device block helpers for the C ABI (host row-major, ld = p).
+// ---------------------------------------------------------------------------
+void upload_block(Context& c, const double* h, int rows, int p, double* dbuf, int64_t ld) {
+  GAPLRA_CUDA_CHECK(cudaMemcpy2DAsync(dbuf, ld * sizeof(double), h, p * sizeof(double), p * sizeof(double), rows,
+                                      cudaMemcpyHostToDevice, c.st));
+}
+void download_block(Context& c, const double* dbuf, int64_t ld, int rows, int p, double* h) {
+  GAPLRA_CUDA_CHECK(cudaMemcpy2DAsync(h, p * sizeof(double), dbuf, ld * sizeof(double), p * sizeof(double), rows,
+                                      cudaMemcpyDeviceToHost, c.st));
+}
+
+bool all_finite(const double* v, size_t n) {
+  for (size_t i = 0; i < n; ++i)
+    if (!std::isfinite(v[i])) return false;
+  return true;
+}
+
+}  // namespace gaplra_cuda
+
+using namespace gaplra_cuda;
+
+struct gaplra_ctx {
+  Context c;
+};
+struct gaplra_matrix {
+  Matrix m;
+  gaplra_ctx* owner;
+};
+
+namespace {
+
+template <class F>
+int guard(gaplra_ctx* ctx, F&& f) {
+  try {
+    if (ctx) GAPLRA_CUDA_CHECK(cudaSetDevice(ctx->c.device));
+    f();
+    if (ctx) ctx->c.err.clear();
+    return GAPLRA_OK;
+  } catch (const Error& e) {
+    if (ctx) ctx->c.err = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    if (ctx) ctx->c.err = e.what();
+    return GAPLRA_DEVICE_ERROR;
+  }
+}
+
+void require(bool ok, const char* what) {
+  if (!ok) throw Error(kContractViolation, what);
+}
+
+}  // namespace
+
+extern "C" {
+
+int gaplra_version(void) { return 1; }
+
+int gaplra_ctx_create(int device, gaplra_ctx** out) {
+  if (!out) return GAPLRA_CONTRACT_VIOLATION;
+  *out = nullptr;
+  gaplra_ctx* ctx = new gaplra_ctx();
+  int rc = guard(nullptr, [&] {
+    int count = 0;
+    GAPLRA_CUDA_CHECK(cudaGetDeviceCount(&count));
+    if (device < 0 || device >= count) throw Error(kDeviceError, "no such CUDA device");
+    ctx->c.device = device;
+    GAPLRA_CUDA_CHECK(cudaSetDevice(device));
+    GAPLRA_CUDA_CHECK(cudaStreamCreateWithFlags(&ctx->c.own, cudaStreamNonBlocking));
+    ctx->c.st = ctx->c.own;
+    GAPLRA_CUDA_CHECK(cudaMallocHost(&ctx->c.pin, 64 * sizeof(double)));
+    GAPLRA_CUDA_CHECK(cudaMallocHost(&ctx->c.pin_i, 64 * sizeof(int)));
+  });
+  if (rc != GAPLRA_OK) {
+    delete ctx;
+    return rc;
+  }
+  *out = ctx;
+  return GAPLRA_OK;
+}
+
+int gaplra_ctx_destroy(gaplra_ctx* ctx) {
+  if (!ctx) return GAPLRA_OK;
+  cudaSetDevice(ctx->c.device);
+  cudaStreamSynchronize(ctx->c.st);
+  delete ctx;
+  return GAPLRA_OK;
+}
+
+const char* gaplra_last_error(const gaplra_ctx* ctx) { return ctx ? ctx->c.err.c_str() : "null context"; }
+
+int gaplra_ctx_set_stream(gaplra_ctx* ctx, void* s) {
+  if (!ctx) return GAPLRA_CONTRACT_VIOLATION;
+  ctx->c.st = s ? static_cast<cudaStream_t>(s) : ctx->c.own;
+  return GAPLRA_OK;
+}
+
+int gaplra_ctx_synchronize(gaplra_ctx* ctx) {
+  if (!ctx) return GAPLRA_CONTRACT_VIOLATION;
+  return guard(ctx, [&] { ctx->c.sync(); });
+}
+
+int gaplra_ledger_get(const gaplra_ctx* ctx, gaplra_ledger* out) {
+  if (!ctx || !out) return GAPLRA_CONTRACT_VIOLATION;
+  *out = ctx->c.led;
+  return GAPLRA_OK;
+}
+
+int gaplra_ledger_reset(gaplra_ctx* ctx) {
+  if (!ctx) return GAPLRA_CONTRACT_VIOLATION;
+  ctx->c.led = gaplra_ledger{};
+  return GAPLRA_OK;
+}
+
+int gaplra_matrix_dense(gaplra_ctx* ctx, int d, int n, const double* x, int64_t ldx, int on_device,
+                        gaplra_matrix** out) {
+  if (!ctx || !out) return GAPLRA_CONTRACT_VIOLATION;
+  *out = nullptr;
+  gaplra_matrix* M = new gaplra_matrix();
+  M->owner = ctx;
+  int rc = guard(ctx, [&] {
+    require(d > 0 && n > 0 && x && ldx >= d, "matrix_dense: bad dimensions");
+    Matrix& m = M->m;
+    m.kind = 0;
+    m.d = d;
+    m.n = n;
+    m.nnz = static_cast<int64_t>(d) * n;
+    m.device = ctx->c.device;
+    if (on_device) {
+      require(ldx % 4 == 0, "matrix_dense: borrowed device X needs ldx % 4 == 0 (zero pad rows)");
+      m.ld = ldx;
+      m.x = x;
+    } else {
+      m.ld = round4(d);
+      double* buf = m.xbuf.ensure(static_cast<size_t>(m.ld) * n);
+      GAPLRA_CUDA_CHECK(cudaMemcpy2DAsync(buf, m.ld * sizeof(double), x, ldx * sizeof(double), d * sizeof(double), n,
+                                          cudaMemcpyHostToDevice, ctx->c.st));
+      m.x = buf;
+      ctx->c.sync();
+    }
+  });
+  if (rc != GAPLRA_OK) {
+    delete M;
+    return rc;
+  }
+  *out = M;
+  return GAPLRA_OK;
+}
+
+int gaplra_matrix_csc(gaplra_ctx* ctx, int d, int n, const int64_t* colptr, const int32_t* rowidx, const double* val,
+                      int on_device, gaplra_matrix** out) {
+  if (!ctx || !out) return GAPLRA_CONTRACT_VIOLATION;
+  *out = nullptr;
+  gaplra_matrix* M = new gaplra_matrix();
+  M->owner = ctx;
+  int rc = guard(ctx, [&] {
+    require(d > 0 && n > 0 && colptr, "matrix_csc: bad dimensions");
+    Matrix& m = M->m;
+    m.kind = 1;
+    m.d = d;
+    m.n = n;
+    m.device = ctx->c.device;
+    std::vector<int64_t> cp(static_cast<size_t>(n) + 1);
+    if (on_device)
+      GAPLRA_CUDA_CHECK(cudaMemcpy(cp.data(), colptr, cp.size() * sizeof(int64_t), cudaMemcpyDeviceToHost));
+    else
+      std::memcpy(cp.data(), colptr, cp.size() * sizeof(int64_t));
+    const int64_t nnz = cp[n];
+    require(cp[0] == 0 && nnz >= 0, "matrix_csc: colptr must start at 0");
+    std::vector<int32_t> ri(static_cast<size_t>(nnz));
+    std::vector<double> v(static_cast<size_t>(nnz));
+    if (on_device) {
+      GAPLRA_CUDA_CHECK(cudaMemcpy(ri.data(), rowidx, nnz * sizeof(int32_t), cudaMemcpyDeviceToHost));
+      GAPLRA_CUDA_CHECK(cudaMemcpy(v.data(), val, nnz * sizeof(double), cudaMemcpyDeviceToHost));
+    } else {
+      std::memcpy(ri.data(), rowidx, nnz * sizeof(int32_t));
+      std::memcpy(v.data(), val, nnz * sizeof(double));
+    }
+    // Validation as SparseColumnsMatrix's ctor (sparse_matrix.cpp:10-37).
+    for (int j = 0; j < n; ++j) {
+      require(cp[j + 1] >= cp[j], "matrix_csc: colptr not monotone");
+      int prev = -1;
+      for (int64_t e = cp[j]; e < cp[j + 1]; ++e) {
+        require(ri[e] >= 0 && ri[e] < d, "matrix_csc: row index out of range");
+        require(ri[e] > prev, "matrix_csc: indices not strictly increasing");
+        require(std::isfinite(v[e]), "matrix_csc: non-finite value");
+        prev = ri[e];
+      }
+    }
+    // CSR copy (row access) for the gather form of Z = X Y.
+    std::vector<int64_t> rp(static_cast<size_t>(d) + 1, 0);
+    for (int64_t e = 0; e < nnz; ++e) rp[ri[e] + 1]++;
+    for (int r = 0; r < d; ++r) rp[r + 1] += rp[r];
+    std::vector<int32_t> ci(static_cast<size_t>(nnz));
+    std::vector<double> rv(static_cast<size_t>(nnz));
+    std::vector<int64_t> fill(rp.begin(), rp.end() - 1);
+    for (int j = 0; j < n; ++j)
+      for (int64_t e = cp[j]; e < cp[j + 1]; ++e) {
+        const int64_t o = fill[ri[e]]++;
+        ci[o] = j;
+        rv[o] = v[e];
+      }
+    m.nnz = nnz;
+    m.ld = round4(d);
+    auto up = [&](auto& buf, const auto& hv) {
+      buf.ensure(hv.size());
+      GAPLRA_CUDA_CHECK(cudaMemcpy(buf.p, hv.data(), hv.size() * sizeof(hv[0]), cudaMemcpyHostToDevice));
+    };
+    up(m.colptr, cp);
+    up(m.rowidx, ri);
+    up(m.val, v);
+    up(m.rowptr, rp);
+    up(m.colidx, ci);
+    up(m.rval, rv);
+  });
+  if (rc != GAPLRA_OK) {
+    delete M;
+    return rc;
+  }
+  *out = M;
+  return GAPLRA_OK;
+}
+
+int gaplra_matrix_destroy(gaplra_matrix* x) {
+  if (!x) return GAPLRA_OK;
+  cudaSetDevice(x->m.device);
+  delete x;
+  return GAPLRA_OK;
+}
+
+int gaplra_matrix_info(const gaplra_matrix* x, int* d, int* n, int64_t* nnz, int64_t* ld) {
+  if (!x) return GAPLRA_CONTRACT_VIOLATION;
+  if (d) *d = x->m.d;
+  if (n) *n = x->m.n;
+  if (nnz) *nnz = x->m.nnz;
+  if (ld) *ld = x->m.ld;
+  return GAPLRA_OK;
+}
+
+int gaplra_gram_block(gaplra_ctx* ctx, const gaplra_matrix* x, int p, const double* w, double* z, double* y) {
+  if (!ctx || !x) return GAPLRA_CONTRACT_VIOLATION;
+  return guard(ctx, [&] {
+    Context& c = ctx->c;
+    const Matrix& X = const_cast<gaplra_matrix*>(x)->m;
+    require(p >= 1 && w && z, "gram_block: bad arguments");
+    require(all_finite(w, static_cast<size_t>(X.d) * p), "gram_apply: non-finite input");
+    const int64_t ld = ldp_of(p), dp = X.d_pad();
+    DBuf<double> wd, zd, yd;
+    wd.ensure(static_cast<size_t>(dp) * ld);
+    zd.ensure(static_cast<size_t>(dp) * ld);
+    yd.ensure(static_cast<size_t>(X.n) * ld);
+    upload_block(c, w, X.d, p, wd.p, ld);
+    gram_block_dev(c, X, p, wd.p, ld, zd.p, ld, yd.p, ld);
+    download_block(c, zd.p, ld, X.d, p, z);
+    if (y) download_block(c, yd.p, ld, X.n, p, y);
+    c.sync();
+  });
+}
+
+int gaplra_gram_apply(gaplra_ctx* ctx, const gaplra_matrix* x, const double* v, double* out) {
+  const int rc = gaplra_gram_block(ctx, x, 1, v, out, nullptr);
+  if (rc == GAPLRA_OK && ctx) ctx->c.led.operator_applies++;
+  return rc;
+}
+
+int gaplra_gram_block_device(gaplra_ctx* ctx, const gaplra_matrix* x, int p, const double* w, int64_t ldw, double* z,
+                             int64_t ldz, double* y, int64_t ldy) {
+  if (!ctx || !x) return GAPLRA_CONTRACT_VIOLATION;
+  return guard(ctx, [&] {
+    require(p >= 1 && w && z, "gram_block_device: bad arguments");
+    require(p == 1 || (ldw % 2 == 0 && ldz % 2 == 0 && (!y || ldy % 2 == 0)), "gram_block_device: ld must be even");
+    gram_block_dev(ctx->c, x->m, p, w, ldw, z, ldz, y, ldy);
+  });
+}
+
+int gaplra_index_stream(gaplra_ctx* ctx, uint64_t seed, uint64_t n, int64_t m, int32_t* out) {
+  if (!ctx) return GAPLRA_CONTRACT_VIOLATION;
+  return guard(ctx, [&] {
+    require(n >= 1 && n < (1ull << 31) && m >= 0 && (m == 0 || out), "index_stream: bad arguments");
+    Context& c = ctx->c;
+    int32_t* d = c.idx.ensure(static_cast<size_t>(std::max<int64_t>(m, 1)));
+    launch_index_stream(seed, n, m, d, c.rej.ensure(1), c.st);
+    if (m) GAPLRA_CUDA_CHECK(cudaMemcpyAsync(out, d, m * sizeof(int32_t), cudaMemcpyDeviceToHost, c.st));
+    c.sync();
+  });
+}
+
+int gaplra_gaussian_init(int d, int p, uint64_t seed, double* out) {
+  if (!out) return GAPLRA_CONTRACT_VIOLATION;
+  return guard(nullptr, [&] { gaussian_init_host(d, p, seed, out, p); });
+}
+
+int gaplra_qr_orthonormalize(gaplra_ctx* ctx, int d, int p, const double* y, double* q, int* bad_col) {
+  if (!ctx) return GAPLRA_CONTRACT_VIOLATION;
+  if (bad_col) *bad_col = -1;
+  return guard(ctx, [&] {
+    require(y && q && p >= 1 && d >= p, "qr_orthonormalize: need 1 <= cols <= rows");
+    require(all_finite(y, static_cast<size_t>(d) * p), "qr_orthonormalize: non-finite entry");
+    Context& c = ctx->c;
+    const int64_t ld = ldp_of(p);
+    DBuf<double> b;
+    b.ensure(static_cast<size_t>(round4(d)) * ld);
+    upload_block(c, y, d, p, b.p, ld);
+    try {
+      qr_dev(c, b.p, ld, d, p, /*count=*/false);
+    } catch (const Error& e) {
+      if (e.code == kRankDeficient && bad_col) *bad_col = e.payload;
+      throw;
+    }
+    download_block(c, b.p, ld, d, p, q);
+    c.sync();
+  });
+}
+
+int gaplra_orthonormality_defect(gaplra_ctx* ctx, int d, int p, const double* q, double* defect) {
+  if (!ctx || !q || !defect) return GAPLRA_CONTRACT_VIOLATION;
+  return guard(ctx, [&] {
+    require(p >= 1 && p <= 64, "orthonormality_defect: 1 <= p <= 64");
+    Context& c = ctx->c;
+    const int64_t ld = ldp_of(p);
+    DBuf<double> b;
+    b.ensure(static_cast<size_t>(round4(d)) * ld);
+    upload_block(c, q, d, p, b.p, ld);
+    double* G = c.small.ensure(64 * 64 + 8);
+    double* part = c.tmp.ensure(static_cast<size_t>(small_gram_parts(d)) * 64 * 64 + 8);
+    launch_small_gram(b.p, ld, p, b.p, ld, p, d, part, G, c.st);
+    std::vector<double> h(static_cast<size_t>(p) * p);
+    GAPLRA_CUDA_CHECK(cudaMemcpyAsync(h.data(), G, h.size() * sizeof(double), cudaMemcpyDeviceToHost, c.st));
+    c.sync();
+    double worst = 0.0;
+    for (int i = 0; i < p; ++i)
+      for (int j = 0; j < p; ++j) worst = std::max(worst, std::fabs(h[i * p + j] - (i == j ? 1.0 : 0.0)));
+    *defect = worst;
+  });
+}
+
+int gaplra_jacobi_eigh(gaplra_ctx* ctx, int n, const double* h, double* vals, double* vecs) {
+  if (!ctx) return GAPLRA_CONTRACT_VIOLATION;
+  return guard(ctx, [&] {
+    require(h && vals && vecs && n >= 1 && n <= kJacobiMax, "jacobi_eigh: need a square matrix with n <= 64");
+    Context& c = ctx->c;
+    DBuf<double> b;
+    b.ensure(static_cast<size_t>(n) * n * 2 + n);
+    GAPLRA_CUDA_CHECK(cudaMemcpyAsync(b.p, h, static_cast<size_t>(n) * n * sizeof(double), cudaMemcpyHostToDevice, c.st));
+    double* dv = b.p + n * n;
+    double* dvec = dv + n;
+    launch_jacobi(b.p, n, dv, dvec, c.st);
+    GAPLRA_CUDA_CHECK(cudaMemcpyAsync(vals, dv, n * sizeof(double), cudaMemcpyDeviceToHost, c.st));
+    GAPLRA_CUDA_CHECK(cudaMemcpyAsync(vecs, dvec, static_cast<size_t>(n) * n * sizeof(double), cudaMemcpyDeviceToHost, c.st));
+    c.sync();
+  });
+}
+
+int gaplra_svrg_epoch(gaplra_ctx* ctx, const gaplra_matrix* x, int p, double* w, const double* y, const double* cc,
+                      double eta, double lambda, uint64_t stream_seed, int64_t m) {
+  if (!ctx || !x) return GAPLRA_CONTRACT_VIOLATION;
+  return guard(ctx, [&] {
+    require(p >= 1 && w && y && cc && m >= 0, "svrg_epoch: bad arguments");
+    Context& c = ctx->c;
+    Matrix& X = const_cast<gaplra_matrix*>(x)->m;
+    const int64_t ld = ldp_of(p), dp = X.d_pad();
+    DBuf<double> wd, cd, yd;
+    wd.ensure(static_cast<size_t>(dp) * ld);
+    cd.ensure(static_cast<size_t>(dp) * ld);
+    yd.ensure(static_cast<size_t>(X.n) * ld);
+    upload_block(c, w, X.d, p, wd.p, ld);
+    upload_block(c, cc, X.d, p, cd.p, ld);
+    upload_block(c, y, X.n, p, yd.p, ld);
+    epoch_dev(c, X, p, wd.p, cd.p, yd.p, eta, lambda, stream_seed, m);
+    download_block(c, wd.p, ld, X.d, p, w);
+    c.sync();
+  });
+}
+
+int gaplra_svrg_solve(gaplra_ctx* ctx, const gaplra_matrix* x, double lambda, int p, const double* b, double* w,
+                      const gaplra_svrg_params* prm, int64_t solve_id, int* epochs, double* history, int hist_cap,
+                      int* hist_len) {
+  if (!ctx || !x || !prm) return GAPLRA_CONTRACT_VIOLATION;
+  return guard(ctx, [&] {
+    require(p >= 1 && p <= 64 && b && w, "solve_svrg: bad arguments");
+    require(all_finite(b, static_cast<size_t>(x->m.d) * p), "solve_svrg: non-finite right-hand side");
+    Context& c = ctx->c;
+    Matrix& X = const_cast<gaplra_matrix*>(x)->m;
+    const int64_t ld = ldp_of(p), dp = X.d_pad();
+    DBuf<double> bd, wd;
+    bd.ensure(static_cast<size_t>(dp) * ld);
+    wd.ensure(static_cast<size_t>(dp) * ld);
+    upload_block(c, b, X.d, p, bd.p, ld);
+    SvrgResult r;
+    auto report = [&] {
+      if (epochs) *epochs = r.epochs;
+      if (hist_len) *hist_len = static_cast<int>(r.history.size());
+      if (history)
+        for (int i = 0; i < std::min<int>(hist_cap, static_cast<int>(r.history.size())); ++i) history[i] = r.history[i];
+    };
+    try {
+      r = svrg_solve_dev(c, X, lambda, p, bd.p, wd.p, *prm, solve_id, &r);
+    } catch (...) {
+      report();
+      throw;
+    }
+    download_block(c, wd.p, ld, X.d, p, w);
+    c.sync();
+    report();
+  });
+}
+
+int gaplra_estimate_top(gaplra_ctx* ctx, const gaplra_matrix* x, int inverse, double lambda, double eps_prime,
+                        uint64_t seed, double rq_tol, const gaplra_svrg_params* prm, int64_t* solve_counter,
+                        double* value, int* iterations) {
+  if (!ctx || !x || !value) return GAPLRA_CONTRACT_VIOLATION;
+  return guard(ctx, [&] {
+    require(eps_prime > 0.0 && eps_prime < 1.0, "estimate_eigenvalues: eps' in (0, 1)");
+    Context& c = ctx->c;
+    Matrix& X = const_cast<gaplra_matrix*>(x)->m;
+    int64_t local = 0;
+    if (inverse) {
+      require(prm != nullptr, "estimate_top: inverse needs svrg params");
+      InverseOp op(c, X, lambda, *prm, solve_counter ? solve_counter : &local);
+      *value = estimate_top_dev(c, op, X.d, X.d_pad(), eps_prime, seed, rq_tol, iterations);
+    } else {
+      GramOp op(c, X);
+      *value = estimate_top_dev(c, op, X.d, X.d_pad(), eps_prime, seed, rq_tol, iterations);
+    }
+  });
+}
+
+int gaplra_tune_shift(gaplra_ctx* ctx, const gaplra_matrix* x, double delta, const gaplra_si_config* cfg,
+                      int64_t* solve_counter, gaplra_si_report* rep) {
+  if (!ctx || !x || !cfg || !rep) return GAPLRA_CONTRACT_VIOLATION;
+  std::memset(rep, 0, sizeof(*rep));
+  return guard(ctx, [&] {
+    int64_t local = 0;
+    Timer t(ctx->c, &rep->ms_tune);
+    tune_shift_dev(ctx->c, const_cast<gaplra_matrix*>(x)->m, delta, *cfg, solve_counter ? solve_counter : &local, *rep);
+  });
+}
+
+int gaplra_restricted_projection(gaplra_ctx* ctx, const gaplra_matrix* x, int p, const double* s, int k, double* w,
+                                 double* ritz) {
+  if (!ctx || !x) return GAPLRA_CONTRACT_VIOLATION;
+  return guard(ctx, [&] {
+    require(s && w && ritz && k >= 1 && k <= p && p <= 64, "restricted_projection: bad arguments");
+    Context& c = ctx->c;
+    Matrix& X = const_cast<gaplra_matrix*>(x)->m;
+    const int64_t ld = ldp_of(p), dp = X.d_pad();
+    DBuf<double> sd, wd;
+    sd.ensure(static_cast<size_t>(dp) * ld);
+    wd.ensure(static_cast<size_t>(dp) * ldp_of(k));
+    upload_block(c, s, X.d, p, sd.p, ld);
+    restricted_projection_dev(c, X, sd.p, p, k, wd.p, ritz);
+    download_block(c, wd.p, ldp_of(k), X.d, k, w);
+    c.sync();
+  });
+}
+
+int gaplra_shift_invert(gaplra_ctx* ctx, const gaplra_matrix* x, const gaplra_si_config* cfg, double* w, double* ritz,
+                        double* s, gaplra_si_report* rep) {
+  if (!ctx || !x || !cfg || !rep) return GAPLRA_CONTRACT_VIOLATION;
+  std::memset(rep, 0, sizeof(*rep));
+  return guard(ctx, [&] {
+    Context& c = ctx->c;
+    Matrix& X = const_cast<gaplra_matrix*>(x)->m;
+    require(cfg->k >= 1 && cfg->p > cfg->k && cfg->p < X.d && cfg->p <= 64, "shift_invert: need 1 <= k < p < d, p <= 64");
+    require(w && ritz, "shift_invert: null output");
+    const gaplra_ledger before = c.led;
+    Timer total(c, &rep->ms_total);
+    int64_t solves = 0;
+    if (cfg->lambda > 0.0) {
+      rep->lambda = cfg->lambda;
+    } else {
+      Timer t(c, &rep->ms_tune);
+      tune_shift_dev(c, X, cfg->delta, *cfg, &solves, *rep);
+    }
+    const int p = cfg->p, k = cfg->k;
+    const int64_t ld = ldp_of(p), dp = X.d_pad();
+    DBuf<double> sb, wb;
+    double* S = sb.ensure(static_cast<size_t>(dp) * ld);
+    {
+      Timer t(c, &rep->ms_subspace);
+      InverseOp dinv(c, X, rep->lambda, prm_from(*cfg, cfg->tol_solve), &solves);
+      rep->outer_cap = outer_cap(*cfg, X.d);
+      rep->outer_iterations = subspace_iterate_dev(c, dinv, X.d, dp, p, rep->outer_cap,
+                                                   derive_seed(cfg->seed, kTagSubspace), cfg->conv_tol, S);
+    }
+    double* W = wb.ensure(static_cast<size_t>(dp) * ldp_of(k));
+    {
+      Timer t(c, &rep->ms_rayleigh_ritz);
+      restricted_projection_dev(c, X, S, p, k, W, ritz);
+    }
+    download_block(c, W, ldp_of(k), X.d, k, w);
+    if (s) download_block(c, S, ld, X.d, p, s);
+    c.sync();
+    gaplra_ledger& L = rep->ledger;
+    L.gram_applies = c.led.gram_applies - before.gram_applies;
+    L.operator_applies = c.led.operator_applies - before.operator_applies;
+    L.qr_factorizations = c.led.qr_factorizations - before.qr_factorizations;
+    L.linear_solves = c.led.linear_solves - before.linear_solves;
+    L.solver_column_samples = c.led.solver_column_samples - before.solver_column_samples;
+    L.epochs = c.led.epochs - before.epochs;
+    L.outer_iterations = c.led.outer_iterations - before.outer_iterations;
+  });
+}
+
+}  // extern "C"

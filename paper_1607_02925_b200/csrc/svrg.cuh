@@ -1,0 +1,57 @@
+// SVRG epoch + anchor kernels (see svrg.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace gaplra_cuda {
+
+struct EpochArgs {
+  const double* X;  // dense column-major
+  int64_t ldx;
+  int d_pad, n;
+  const int32_t* idx;  // m sampled columns
+  int64_t m;
+  double* W;  // row-major d_pad x ldw (in: anchor W̃, out: W after m steps)
+  const double* C;
+  int64_t ldw;
+  const double* Y;  // n x ldy: Y_i = x_iᵀ W̃
+  const double* H;  // n x ldy: H_i = x_iᵀ C
+  int64_t ldy;
+  int p;
+  double rho, eta_n;
+  int rows_per_cta;
+};
+
+struct SparseEpochArgs {
+  int d, n, p;
+  const int64_t* colptr;
+  const int32_t* rowidx;
+  const double* val;
+  const int32_t* idx;
+  int64_t m;
+  double* W;
+  const double* C;
+  int64_t ldw;
+  const double* Y;
+  int64_t ldy;
+  double rho, eta_n;
+};
+
+struct EpochConfig {
+  int cluster, pc, b, rows_per_cta, groups;
+  size_t smem;
+};
+
+EpochConfig choose_epoch_config(int d_pad, int p);
+void launch_svrg_epoch_dense(const EpochArgs& a, const EpochConfig& cfg, cudaStream_t st);
+void launch_svrg_epoch_sparse(const SparseEpochArgs& a, cudaStream_t st);
+
+// C = η(Z + B), per-column |λW − Z − B|; out_max = max_c |M_c| / bnorm_c
+// (NaN if any is non-finite).  part needs anchor_parts(d) * 64 doubles.
+int anchor_parts(int d);
+void launch_anchor(const double* W, const double* Z, const double* Bm, int64_t ld, int d, int p, double lambda,
+                   double eta, double* C, double* part, const double* bnorm, double* colnorm, double* out_max,
+                   cudaStream_t st);
+
+}  // namespace gaplra_cuda

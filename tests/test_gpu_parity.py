@@ -1,0 +1,221 @@
+"""Device (C-ABI) vs CPU oracle parity on seeded inputs — the parity gate.
+
+Bars: bit-exact for the integer index stream, gaussian_init and Jacobi (the
+device Jacobi uses explicitly rounded intrinsics); floating point within the
+tolerance written in each test (the device sums in a different order and with
+FMA)."""
+import numpy as np
+import pytest
+
+from problems import csc_to_dense, planted_dense, random_csc
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    return np.abs(a - b).max() / max(np.abs(b).max(), 1e-300)
+
+
+@pytest.mark.parametrize("seed,n,m", [(0, 5000, 5), (12345, 1, 7), (7, 2_000_000, 100_003), (2**63 + 5, 100_000, 1024),
+                                      (99, 3, 513), (5, 1_000_000, 0)])
+def test_index_stream_bit_exact(g, oracle, seed, n, m):
+    dev = g.index_stream(seed, n, m)
+    ref = oracle.uniform_index(seed, n, m).astype(np.int64)
+    assert np.array_equal(dev.astype(np.int64), ref)
+
+
+def test_index_stream_golden(g):
+    # Rng(0).uniform_index(5000) x 5 = 1503 1255 4180 330 4874
+    assert g.index_stream(0, 5000, 5).tolist() == [1503, 1255, 4180, 330, 4874]
+
+
+def test_gaussian_init_bit_exact(g, oracle):
+    for d, p, seed in [(4, 2, 0), (257, 7, 3), (1000, 10, 2**40)]:
+        assert np.array_equal(g.gaussian_init(d, p, seed), oracle.gaussian_init(d, p, seed)[1])
+
+
+@pytest.mark.parametrize("p", [1, 2, 3, 5, 8, 10, 16, 20, 31, 32, 33, 64])
+def test_gram_block_dense(g, oracle, p):
+    rng = np.random.default_rng(p)
+    d, n = 300, 1100
+    X = rng.standard_normal((d, n))
+    W = rng.standard_normal((d, p))
+    x = g.DeviceMatrix.dense(X)
+    z, y = g.gram_block(x, W, want_y=True)
+    rc, zo, yo = oracle.gram_block(oracle.dense(X), W, want_y=True)
+    assert rc == 0
+    # |dZ| <= 1e-13 |X|^2 |W|
+    scale = np.linalg.norm(X, 2) ** 2 * np.abs(W).max()
+    assert np.abs(z - zo).max() <= 1e-13 * scale
+    assert np.abs(y - yo).max() <= 1e-13 * np.linalg.norm(X, 2) * np.abs(W).max() * np.sqrt(d)
+
+
+def test_gram_block_deterministic(g):
+    rng = np.random.default_rng(1)
+    X = rng.standard_normal((512, 4096))
+    W = rng.standard_normal((512, 20))
+    x = g.DeviceMatrix.dense(X)
+    a = g.gram_block(x, W)
+    b = g.gram_block(x, W)
+    assert np.array_equal(a, b)
+
+
+def test_gram_apply_kats(g):
+    # I3 (1,2,3) -> (1,2,3); diag(2,3) (1,1) -> (4,9)
+    assert np.allclose(g.gram_apply(g.DeviceMatrix.dense(np.eye(3)), np.array([1.0, 2, 3])), [1, 2, 3], atol=0)
+    assert np.allclose(g.gram_apply(g.DeviceMatrix.dense(np.diag([2.0, 3.0])), np.array([1.0, 1.0])), [4, 9], atol=0)
+
+
+@pytest.mark.parametrize("p", [1, 4, 16])
+def test_gram_block_sparse(g, oracle, p):
+    d, n = 400, 3000
+    cp, ri, v = random_csc(d, n, 20, seed=p)
+    x = g.DeviceMatrix.csc(d, n, cp, ri, v)
+    W = np.random.default_rng(0).standard_normal((d, p))
+    z = g.gram_block(x, W)
+    rc, zo, _ = oracle.gram_block(oracle.csc(d, n, cp, ri, v), W)
+    assert rc == 0
+    assert rel(z, zo) <= 1e-13
+
+
+def test_qr_matches_oracle(g, oracle):
+    rng = np.random.default_rng(3)
+    for d, p in [(10, 4), (1000, 10), (4096, 20), (5000, 16), (9000, 12)]:
+        y = rng.standard_normal((d, p))
+        q = g.qr_orthonormalize(y)
+        rc, qo, _ = oracle.qr(y)
+        assert rc == 0
+        assert rel(q, qo) <= 1e-12
+        assert g.orthonormality_defect(q) <= 1e-12
+
+
+def test_qr_rank_deficient(g):
+    y = np.random.default_rng(0).standard_normal((50, 4))
+    y[:, 2] = y[:, 0] + 2 * y[:, 1]
+    with pytest.raises(g.RankDeficient) as e:
+        g.qr_orthonormalize(y)
+    assert e.value.column == 2
+    with pytest.raises(g.RankDeficient) as e:
+        g.qr_orthonormalize(np.zeros((5, 2)))
+    assert e.value.column == 0
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 10, 33, 64])
+def test_jacobi_bit_exact(g, oracle, n):
+    rng = np.random.default_rng(n)
+    h = rng.standard_normal((n, n))
+    h = h + h.T
+    e = g.jacobi_eigh(h)
+    rc, vals, vecs = oracle.jacobi(h)
+    assert np.array_equal(e.values, vals)
+    assert np.array_equal(e.vectors, vecs)
+
+
+def test_jacobi_golden(g):
+    e = g.jacobi_eigh(np.array([[4.0, 1, 0], [1, 3, 0], [0, 0, 1]]))
+    assert e.values.tolist() == [4.6180339887498931, 2.3819660112501047, 1.0]
+
+
+@pytest.mark.parametrize("p", [1, 3, 8, 20])
+def test_svrg_epoch_lockstep(g, oracle, p):
+    X, _, _ = planted_dense(64, 400, seed=p)
+    rng = np.random.default_rng(p)
+    lam = 1.05
+    m = oracle.dense(X)
+    w0 = rng.standard_normal((64, p))
+    _, z, y = oracle.gram_block(m, w0, want_y=True)
+    b = rng.standard_normal((64, p))
+    eta = 1.0 / (4.0 * (lam + 400 * oracle.max_col_norm2(m)))
+    cblk = eta * (z + b)
+    rc, wo, idx = oracle.svrg_epoch(m, w0, y, cblk, eta, lam, 77, 800)
+    wd = g.svrg_epoch(g.DeviceMatrix.dense(X), w0, y, cblk, eta, lam, 77, 800)
+    assert rel(wd, wo) <= 1e-10
+
+
+def test_svrg_epoch_sparse_lockstep(g, oracle):
+    d, n, p = 120, 500, 4
+    cp, ri, v = random_csc(d, n, 8, seed=2)
+    m = oracle.csc(d, n, cp, ri, v)
+    rng = np.random.default_rng(5)
+    w0 = rng.standard_normal((d, p))
+    _, z, y = oracle.gram_block(m, w0, want_y=True)
+    lam = 2.0
+    eta = 1.0 / (4.0 * (lam + n * oracle.max_col_norm2(m)))
+    cblk = eta * (z + rng.standard_normal((d, p)))
+    rc, wo, _ = oracle.svrg_epoch(m, w0, y, cblk, eta, lam, 9, 1000)
+    wd = g.svrg_epoch(g.DeviceMatrix.csc(d, n, cp, ri, v), w0, y, cblk, eta, lam, 9, 1000)
+    assert rel(wd, wo) <= 1e-10
+
+
+def test_svrg_solve_matches_oracle_and_direct(g, oracle):
+    X, _, sig = planted_dense(60, 300, seed=0)
+    lam = 1.05
+    b = np.random.default_rng(0).standard_normal((60, 3))
+    r = g.solve_svrg(g.DeviceMatrix.dense(X), lam, b, 1e-10, seed=7)
+    rc, wo, ep, hist = oracle.svrg_solve(oracle.dense(X), lam, b, 1e-10, seed=7)
+    assert rc == 0
+    assert abs(r.epochs - ep) <= 1
+    assert rel(r.solution, wo) <= 1e-8
+    wd = np.linalg.solve(lam * np.eye(60) - X @ X.T, b)
+    assert rel(r.solution, wd) <= 1e-8
+
+
+def test_svrg_solve_zero_matrix(g):
+    # X = 0, lambda = 1 -> x = b exactly after epoch 1
+    b = np.arange(1.0, 9.0).reshape(8, 1)
+    r = g.solve_svrg(g.DeviceMatrix.dense(np.zeros((8, 5))), 1.0, b, 1e-12)
+    assert np.allclose(r.solution, b, rtol=1e-12)
+
+
+def test_solver_stalls_on_indefinite_shift(g):
+    X, _, _ = planted_dense(40, 200, seed=1)
+    with pytest.raises(g.SolverStalled) as e:
+        g.solve_svrg(g.DeviceMatrix.dense(X), 0.5, np.ones((40, 1)), 1e-10)
+    assert len(e.value.residual_history) >= 1
+
+
+def test_restricted_projection(g, oracle):
+    X, U, sig = planted_dense(80, 200, seed=4)
+    s = g.qr_orthonormalize(np.random.default_rng(1).standard_normal((80, 8)) + 3 * U[:, :8])
+    w, ritz = g.restricted_projection(g.DeviceMatrix.dense(X), s, 4)
+    rc, wo, ro = oracle.restricted_projection(oracle.dense(X), s, 4)
+    assert rc == 0
+    assert np.allclose(ritz, ro, rtol=1e-12)
+    assert oracle.sin_theta(wo, w) <= 1e-10
+
+
+def test_shift_invert_matches_oracle(g, oracle):
+    from oracle_lib import default_si_config
+
+    X, U, sig = planted_dense(60, 300, k=4, p=8, seed=0)
+    lamv = sig ** 2
+    delta = 2 / 3 * (lamv[3] - lamv[8])
+    cfg = g.SIConfig(k=4, p=8, delta=delta, seed=5)
+    res = g.shift_invert(g.DeviceMatrix.dense(X), cfg)
+    rc, wo, ro, so, rep = oracle.shift_invert(oracle.dense(X), default_si_config(4, 8, delta=delta, seed=5))
+    assert rc == 0
+    assert res.lam == pytest.approx(rep.lambda_, rel=1e-10)
+    assert res.tune_history and len(res.tune_history) == rep.tune_steps
+    assert oracle.sin_theta(wo, res.W) <= 1e-8          # north star: sin theta <= 1e-8 (fp64)
+    assert np.allclose(res.ritz, ro, rtol=1e-10)
+    assert oracle.sin_theta(U[:, :4], res.W) <= 1e-8    # and against the planted truth
+    assert abs(res.outer_iterations - rep.outer_iterations) <= 1
+
+
+def test_shift_invert_sparse(g, oracle):
+    from oracle_lib import default_si_config
+
+    d, n = 100, 400
+    cp, ri, v = random_csc(d, n, 8, seed=8, rank=3)
+    Xd = csc_to_dense(d, n, cp, ri, v)
+    ev = np.sort(np.linalg.eigvalsh(Xd @ Xd.T))[::-1]
+    k, p = 2, 4
+    lam = ev[0] + (ev[k - 1] - ev[p]) / 2
+    cfg = g.SIConfig(k=k, p=p, lam=lam, seed=1, max_outer=40, conv_tol=1e-7)
+    res = g.shift_invert(g.DeviceMatrix.csc(d, n, cp, ri, v), cfg)
+    rc, wo, ro, so, rep = oracle.shift_invert(oracle.csc(d, n, cp, ri, v),
+                                              default_si_config(k, p, lam=lam, seed=1, max_outer=40, conv_tol=1e-7))
+    assert rc == 0
+    assert oracle.sin_theta(wo, res.W) <= 1e-8
+    assert np.allclose(res.ritz, ro, rtol=1e-10)
+    assert np.allclose(res.ritz, ev[:k], rtol=1e-9)
