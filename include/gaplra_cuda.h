@@ -67,6 +67,8 @@ typedef struct {
   int epoch_cap;         /* <= 0: ceil(200 ln(1/tol)) */
   double monotone_slack; /* > 0: stall if residual > slack * best so far */
   uint64_t root_seed;    /* stream = derive_seed(root, 0x73767267 ^ (solve_id << 20) ^ epoch) */
+  double lambda1_hint;   /* > 0: upper estimate of lambda_1 for step sizing:
+                            eta = min(eta, (lambda - hint) / (|X|_F^2 hint)) */
 } gaplra_svrg_params;
 
 /* CostLedger (linear_operator.hpp:16-30) plus epoch/outer counters. */
@@ -91,11 +93,13 @@ typedef struct {
   int force;
   int epoch_cap;
   double monotone_slack;
+  double lambda1_hint; /* with an explicit lambda: upper estimate of lambda_1 (0: none) */
 } gaplra_si_config;
 
 typedef struct {
   double lambda;
   double lambda1_hat;
+  double lambda1_hint;
   int tune_steps;
   double tune_lambda[64];
   double tune_inv[64];
@@ -106,6 +110,18 @@ typedef struct {
   double ms_tune, ms_subspace, ms_rayleigh_ritz, ms_total;
 } gaplra_si_report;
 
+/* Live per-kernel-class device time (CUDA events on the context stream) and
+ * the algorithmic bytes / flops of those launches.
+ * Classes: 0 gram pass X(XᵀW), 1 SVRG epoch steps, 2 H = XᵀC pass,
+ * 3 index stream, 4 QR (MGS2), 5 anchor epilogue, 6 per-block Gram/T precompute. */
+#define GAPLRA_PROF_CLASSES 8
+typedef struct {
+  double ms[GAPLRA_PROF_CLASSES];
+  uint64_t count[GAPLRA_PROF_CLASSES];
+  double bytes[GAPLRA_PROF_CLASSES];
+  double flops[GAPLRA_PROF_CLASSES];
+} gaplra_profile;
+
 /* ---- context ---- */
 GAPLRA_API int gaplra_ctx_create(int device, gaplra_ctx** out);
 GAPLRA_API int gaplra_ctx_destroy(gaplra_ctx* ctx);
@@ -115,6 +131,9 @@ GAPLRA_API int gaplra_ctx_synchronize(gaplra_ctx* ctx);
 GAPLRA_API int gaplra_ledger_get(const gaplra_ctx* ctx, gaplra_ledger* out);
 GAPLRA_API int gaplra_ledger_reset(gaplra_ctx* ctx);
 GAPLRA_API int gaplra_version(void);
+GAPLRA_API int gaplra_profile_enable(gaplra_ctx* ctx, int on);
+GAPLRA_API int gaplra_profile_get(gaplra_ctx* ctx, gaplra_profile* out);
+GAPLRA_API int gaplra_profile_reset(gaplra_ctx* ctx);
 
 /* ---- X (resident in HBM) ----
  * dense: column-major, ldx >= d.  on_device = 0: host pointer, copied in.

@@ -344,8 +344,22 @@ SvrgSetup svrg_setup(const Mat& x, double lambda, const orc_svrg_params* prm) {
   if (prm->eta > 0.0) {
     s.eta = prm->eta;
   } else {
-    for (int j = 0; j < x.n(); ++j) maxn2 = std::max(maxn2, x.column_norm_squared(j));
-    s.eta = 1.0 / (4.0 * (lambda + static_cast<double>(x.n()) * maxn2));
+    double fro2 = 0.0;  // frobenius_norm_squared (sparse_matrix.cpp:117-121)
+    for (int j = 0; j < x.n(); ++j) {
+      const double c = x.column_norm_squared(j);
+      maxn2 = std::max(maxn2, c);
+      fro2 += c;
+    }
+    const double L = static_cast<double>(x.n()) * maxn2;
+    s.eta = 1.0 / (4.0 * (lambda + L));
+    // Stability cap: within an epoch the error's second moment
+    // contracts only if eta < 2 (lambda - lambda_1) / (|X|_F^2 lambda_1); use
+    // half of it with the caller's lambda_1 upper estimate (the
+    // ShiftedSystem hint "used for step sizing").
+    if (prm->lambda1_hint > 0.0) {
+      if (!(lambda > prm->lambda1_hint)) throw Status(ORC_INDEFINITE_SHIFT);
+      if (fro2 > 0.0) s.eta = std::min(s.eta, (lambda - prm->lambda1_hint) / (fro2 * prm->lambda1_hint));
+    }
   }
   s.rho = 1.0 - s.eta * lambda;
   s.eta_n = s.eta * static_cast<double>(x.n());
@@ -601,6 +615,7 @@ orc_svrg_params make_prm(const orc_si_config* cfg, double tol) {
   prm.epoch_cap = cfg->epoch_cap;
   prm.monotone_slack = cfg->monotone_slack;
   prm.root_seed = cfg->seed;
+  prm.lambda1_hint = 0.0;
   return prm;
 }
 
@@ -618,8 +633,14 @@ void tune_shift(const Mat& x, double delta, const orc_si_config* cfg, int64_t* s
   double lambda = 1.5 * l1;
   const double ratio = l1 / delta;
   const int cap = (ratio > 1.0 ? static_cast<int>(std::ceil(4.0 * std::log2(ratio))) : 0) + 5;
-  const orc_svrg_params prm = make_prm(cfg, cfg->tol_tune);
+  orc_svrg_params prm = make_prm(cfg, cfg->tol_tune);
+  // lambda_1 upper estimates: Alg. 3 at eps' = 1/4 gives lambda1_hat >= (3/4) lambda_1;
+  // after an update lambda_t = lambda_{t-1} - (4/9) inv_{t-1} with inv <= (9/8)(lambda_{t-1} -
+  // lambda_1), lambda_1 <= 2 lambda_t - lambda_{t-1}.
+  double hint = l1 / 0.75, prev_lambda = lambda;
   for (int t = 0; t < cap; ++t) {
+    if (t > 0) hint = 2.0 * lambda - prev_lambda;
+    prm.lambda1_hint = hint;
     InverseOp dinv(x, lambda, prm, solve_counter, &rep->ledger, nthreads);
     const double est = estimate_top(dinv, d, 1.0 / 9.0, derive_seed(cfg->seed, kTagEstD + t),
                                     cfg->rq_tol, nullptr, &rep->ledger);
@@ -631,8 +652,10 @@ void tune_shift(const Mat& x, double delta, const orc_si_config* cfg, int64_t* s
     rep->tune_steps++;
     if (inv >= delta / 27.0 && inv <= delta / 5.0) {
       rep->lambda = lambda;
+      rep->lambda1_hint = lambda - (8.0 / 9.0) * inv;
       return;
     }
+    prev_lambda = lambda;
     lambda = lambda - (4.0 / 9.0) * inv;
   }
   rep->lambda = lambda;
@@ -849,10 +872,12 @@ int orc_shift_invert(const orc_mat* x, const orc_si_config* cfg, double* w, doub
     int64_t solves = 0;
     if (cfg->lambda > 0.0) {
       rep->lambda = cfg->lambda;
+      rep->lambda1_hint = cfg->lambda1_hint;
     } else {
       tune_shift(m, cfg->delta, cfg, &solves, rep, nthreads);
     }
-    const orc_svrg_params prm = make_prm(cfg, cfg->tol_solve);
+    orc_svrg_params prm = make_prm(cfg, cfg->tol_solve);
+    prm.lambda1_hint = rep->lambda1_hint;
     InverseOp dinv(m, rep->lambda, prm, &solves, &rep->ledger, nthreads);
     rep->outer_cap = outer_cap(cfg, x->d);
     Block s = subspace_iterate(dinv, x->d, cfg->p, rep->outer_cap, derive_seed(cfg->seed, kTagSubspace),

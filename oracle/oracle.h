@@ -57,6 +57,8 @@ typedef struct {
   int epoch_cap;         /* <= 0: ceil(200 ln(1/tol)) */
   double monotone_slack; /* > 0: stall if res_e > slack * min_{e'<e} res */
   uint64_t root_seed;    /* stream seed = derive_seed(root, TAG_SVRG ^ (solve_id<<20) ^ epoch) */
+  double lambda1_hint;   /* > 0: upper estimate of lambda_1 used for step sizing:
+                            eta = min(eta_spec, (lambda - hint) / (|X|_F^2 hint)) */
 } orc_svrg_params;
 
 typedef struct {
@@ -83,11 +85,13 @@ typedef struct {
   int force;          /* ignore NoPreconditioningNeeded                    */
   int epoch_cap;      /* 0: spec cap                                       */
   double monotone_slack;
+  double lambda1_hint; /* with an explicit lambda: upper estimate of lambda_1 (0: none) */
 } orc_si_config;
 
 typedef struct {
   double lambda;
   double lambda1_hat;
+  double lambda1_hint; /* lambda_1 upper estimate handed to the main solves */
   int tune_steps;
   double tune_lambda[64];
   double tune_inv[64];

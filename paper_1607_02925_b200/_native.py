@@ -23,7 +23,7 @@ _ip = C.POINTER(C.c_int)
 
 class SvrgParams(C.Structure):
     _fields_ = [("eta", C.c_double), ("m", C.c_int64), ("tol", C.c_double), ("epoch_cap", C.c_int),
-                ("monotone_slack", C.c_double), ("root_seed", C.c_uint64)]
+                ("monotone_slack", C.c_double), ("root_seed", C.c_uint64), ("lambda1_hint", C.c_double)]
 
 
 class Ledger(C.Structure):
@@ -40,18 +40,34 @@ class SiConfig(C.Structure):
                 ("delta", C.c_double), ("lambda_", C.c_double), ("seed", C.c_uint64),
                 ("tol_solve", C.c_double), ("tol_tune", C.c_double), ("conv_tol", C.c_double),
                 ("rq_tol", C.c_double), ("max_outer", C.c_int), ("force", C.c_int),
-                ("epoch_cap", C.c_int), ("monotone_slack", C.c_double)]
+                ("epoch_cap", C.c_int), ("monotone_slack", C.c_double), ("lambda1_hint", C.c_double)]
 
 
 class SiReport(C.Structure):
-    _fields_ = [("lambda_", C.c_double), ("lambda1_hat", C.c_double), ("tune_steps", C.c_int),
+    _fields_ = [("lambda_", C.c_double), ("lambda1_hat", C.c_double), ("lambda1_hint", C.c_double),
+                ("tune_steps", C.c_int),
                 ("tune_lambda", C.c_double * 64), ("tune_inv", C.c_double * 64),
                 ("outer_iterations", C.c_int), ("outer_cap", C.c_int), ("ledger", Ledger),
                 ("ms_tune", C.c_double), ("ms_subspace", C.c_double),
                 ("ms_rayleigh_ritz", C.c_double), ("ms_total", C.c_double)]
 
 
+PROF_CLASSES = ["gram", "epoch", "h_pass", "index", "qr", "anchor", "block_gram", "r7"]
+
+
+class Profile(C.Structure):
+    _fields_ = [("ms", C.c_double * 8), ("count", C.c_uint64 * 8), ("bytes", C.c_double * 8),
+                ("flops", C.c_double * 8)]
+
+    def as_dict(self):
+        return {name: {"ms": self.ms[i], "count": int(self.count[i]), "bytes": self.bytes[i],
+                       "flops": self.flops[i]} for i, name in enumerate(PROF_CLASSES[:7])}
+
+
 _SIGS = {
+    "gaplra_profile_enable": (C.c_int, [C.c_void_p, C.c_int]),
+    "gaplra_profile_get": (C.c_int, [C.c_void_p, C.POINTER(Profile)]),
+    "gaplra_profile_reset": (C.c_int, [C.c_void_p]),
     "gaplra_version": (C.c_int, []),
     "gaplra_ctx_create": (C.c_int, [C.c_int, C.POINTER(C.c_void_p)]),
     "gaplra_ctx_destroy": (C.c_int, [C.c_void_p]),

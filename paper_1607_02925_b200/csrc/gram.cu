@@ -362,8 +362,7 @@ struct XySparseRun {
   }
 };
 
-__global__ void k_colnorm2_dense(const double* __restrict__ X, int64_t ldx, int d, int n,
-                                 unsigned long long* __restrict__ best) {
+__global__ void k_colnorm2_dense(const double* __restrict__ X, int64_t ldx, int d, int n, double* __restrict__ out) {
   const int lane = threadIdx.x & 31;
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -372,17 +371,33 @@ __global__ void k_colnorm2_dense(const double* __restrict__ X, int64_t ldx, int 
     double s = 0.0;
     for (int i = lane; i < d; i += 32) s = fma(col[i], col[i], s);
     s = warp_sum(s);
-    if (lane == 0) atomicMax(best, __double_as_longlong(s));
+    if (lane == 0) out[j] = s;
   }
 }
 
 __global__ void k_colnorm2_sparse(int n, const int64_t* __restrict__ colptr, const double* __restrict__ val,
-                                  unsigned long long* __restrict__ best) {
+                                  double* __restrict__ out) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= n) return;
   double s = 0.0;
   for (int64_t e = colptr[j]; e < colptr[j + 1]; ++e) s = fma(val[e], val[e], s);
-  atomicMax(best, __double_as_longlong(s));
+  out[j] = s;
+}
+
+// out[0] = sum, out[1] = max of v[0..n) — one CTA, fixed order (deterministic)
+__global__ void k_sum_max(const double* __restrict__ v, int n, double* __restrict__ out) {
+  __shared__ double red[32];
+  double s = 0.0, m = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    s += v[i];
+    m = fmax(m, v[i]);
+  }
+  s = block_sum(s, red);
+  m = block_max(m, red);
+  if (threadIdx.x == 0) {
+    out[0] = s;
+    out[1] = m;
+  }
 }
 
 }  // namespace
@@ -431,26 +446,19 @@ void launch_xy_sparse(const SparseX& X, const double* Y, int64_t ldy, int p, dou
   }
 }
 
-double max_col_norm2_dense(const DenseX& X, double* scratch, cudaStream_t st) {
-  GAPLRA_CUDA_CHECK(cudaMemsetAsync(scratch, 0, sizeof(double), st));
-  k_colnorm2_dense<<<sm_count() * 8, 256, 0, st>>>(X.x, X.ld, X.d, X.n,
-                                                   reinterpret_cast<unsigned long long*>(scratch));
+void col_norm2_dense(const DenseX& X, double* out, cudaStream_t st) {
+  k_colnorm2_dense<<<sm_count() * 8, 256, 0, st>>>(X.x, X.ld, X.d, X.n, out);
   GAPLRA_LAUNCH_CHECK();
-  double h = 0.0;
-  GAPLRA_CUDA_CHECK(cudaMemcpyAsync(&h, scratch, sizeof(double), cudaMemcpyDeviceToHost, st));
-  GAPLRA_CUDA_CHECK(cudaStreamSynchronize(st));
-  return h;
 }
 
-double max_col_norm2_sparse(const SparseX& X, double* scratch, cudaStream_t st) {
-  GAPLRA_CUDA_CHECK(cudaMemsetAsync(scratch, 0, sizeof(double), st));
-  k_colnorm2_sparse<<<ceil_div(X.n, 256), 256, 0, st>>>(X.n, X.colptr, X.val,
-                                                         reinterpret_cast<unsigned long long*>(scratch));
+void col_norm2_sparse(const SparseX& X, double* out, cudaStream_t st) {
+  k_colnorm2_sparse<<<ceil_div(X.n, 256), 256, 0, st>>>(X.n, X.colptr, X.val, out);
   GAPLRA_LAUNCH_CHECK();
-  double h = 0.0;
-  GAPLRA_CUDA_CHECK(cudaMemcpyAsync(&h, scratch, sizeof(double), cudaMemcpyDeviceToHost, st));
-  GAPLRA_CUDA_CHECK(cudaStreamSynchronize(st));
-  return h;
+}
+
+void reduce_sum_max(const double* v, int n, double* out2, cudaStream_t st) {
+  k_sum_max<<<1, 1024, 0, st>>>(v, n, out2);
+  GAPLRA_LAUNCH_CHECK();
 }
 
 }  // namespace gaplra_cuda

@@ -54,8 +54,9 @@ void launch_xtw_sparse(const SparseX& X, const double* W, int64_t ldw, int p, do
 void launch_xy_sparse(const SparseX& X, const double* Y, int64_t ldy, int p, double* Z,
                       int64_t ldz, cudaStream_t st);
 
-// Per-column max |x_j|^2 (for the SVRG step size).
-double max_col_norm2_dense(const DenseX& X, double* scratch, cudaStream_t st);
-double max_col_norm2_sparse(const SparseX& X, double* scratch, cudaStream_t st);
+// Per-column |x_j|^2 into out[n]; reduce_sum_max: out2 = {sum, max} (SVRG step size).
+void col_norm2_dense(const DenseX& X, double* out, cudaStream_t st);
+void col_norm2_sparse(const SparseX& X, double* out, cudaStream_t st);
+void reduce_sum_max(const double* v, int n, double* out2, cudaStream_t st);
 
 }  // namespace gaplra_cuda

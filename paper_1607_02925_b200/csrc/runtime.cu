@@ -7,6 +7,7 @@
 // stopping rules, W0 = 0, last iterate) matches oracle/oracle.cpp; see
 // DESIGN.md §2.  There is no CPU compute path: every numeric step is a kernel.
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -39,7 +40,10 @@ struct DBuf {
     if (k <= n && p) return p;
     release();
     GAPLRA_CUDA_CHECK(cudaMalloc(&p, std::max<size_t>(k, 1) * sizeof(T)));
+    // cudaMemset runs on the legacy stream, which does not order against the
+    // context's non-blocking stream: complete it before the buffer is used.
     GAPLRA_CUDA_CHECK(cudaMemset(p, 0, std::max<size_t>(k, 1) * sizeof(T)));
+    GAPLRA_CUDA_CHECK(cudaDeviceSynchronize());
     n = k;
     return p;
   }
@@ -115,7 +119,7 @@ struct Matrix {
   DBuf<int64_t> colptr, rowptr;
   DBuf<int32_t> rowidx, colidx;
   DBuf<double> val, rval;
-  double maxn2 = -1.0;
+  double maxn2 = -1.0, fro2 = -1.0;
   int device = 0;
   DenseX dense() const {
     DenseX X;
@@ -141,8 +145,14 @@ struct Matrix {
   int64_t d_pad() const { return kind == 0 ? ld : round4(d); }
 };
 
-struct Ledger {
-  gaplra_ledger v{};
+// Live per-kernel-class timing (CUDA events on the launching stream), with the
+// algorithmic bytes / flops of each launch for the roofline report.
+enum ProfClass { kProfGram = 0, kProfEpoch, kProfHPass, kProfIndex, kProfQr, kProfAnchor, kProfBlockGram, kProfClasses };
+constexpr int kEpochBlock = 16;  // s-step block (svrg.cu kBlock)
+
+struct ProfPending {
+  int cls;
+  cudaEvent_t a, b;
 };
 
 struct Context {
@@ -151,25 +161,76 @@ struct Context {
   std::string err;
   gaplra_ledger led{};
   // workspaces
-  DBuf<double> gw, ybuf, hbuf, zbuf, cbuf, wbuf, bbuf, sbuf, tbuf, qrs, small, apart, bnorm, scal, tmp;
+  DBuf<double> gw, ybuf, hbuf, zbuf, cbuf, wbuf, bbuf, sbuf, tbuf, qrs, small, apart, bnorm, scal, tmp, tmat, zcol;
   DBuf<int32_t> idx;
   DBuf<unsigned int> rej;
   DBuf<int> status;
   double* pin = nullptr;  // pinned host scalars
   int* pin_i = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  bool profiling = false;
+  gaplra_profile prof{};
+  std::vector<ProfPending> pending;
+  std::vector<cudaEvent_t> spare;
+  cudaEvent_t new_event() {
+    if (!spare.empty()) {
+      cudaEvent_t e = spare.back();
+      spare.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    GAPLRA_CUDA_CHECK(cudaEventCreate(&e));
+    return e;
+  }
+  void resolve() {
+    for (auto& p : pending) {
+      float ms = 0.f;
+      if (cudaEventSynchronize(p.b) == cudaSuccess && cudaEventElapsedTime(&ms, p.a, p.b) == cudaSuccess)
+        prof.ms[p.cls] += ms;
+      spare.push_back(p.a);
+      spare.push_back(p.b);
+    }
+    pending.clear();
+  }
   ~Context() {
+    resolve();
+    for (auto e : spare) cudaEventDestroy(e);
     if (pin) cudaFreeHost(pin);
     if (pin_i) cudaFreeHost(pin_i);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
     if (own) cudaStreamDestroy(own);
   }
-  void sync() { GAPLRA_CUDA_CHECK(cudaStreamSynchronize(st)); }
+  void sync() {
+    GAPLRA_CUDA_CHECK(cudaStreamSynchronize(st));
+    if (!pending.empty()) resolve();
+  }
   double read_scalar(const double* dptr) {
     GAPLRA_CUDA_CHECK(cudaMemcpyAsync(pin, dptr, sizeof(double), cudaMemcpyDeviceToHost, st));
     sync();
     return pin[0];
+  }
+};
+
+// RAII: time one launch (or launch group) of class `cls` when profiling.
+struct Prof {
+  Context& c;
+  int cls;
+  cudaEvent_t a = nullptr;
+  double bytes, flops;
+  Prof(Context& cc, int k, double by, double fl) : c(cc), cls(k), bytes(by), flops(fl) {
+    if (!c.profiling) return;
+    a = c.new_event();
+    cudaEventRecord(a, c.st);
+  }
+  ~Prof() {
+    if (!c.profiling) return;
+    cudaEvent_t b = c.new_event();
+    cudaEventRecord(b, c.st);
+    c.pending.push_back({cls, a, b});
+    c.prof.count[cls] += 1;
+    c.prof.bytes[cls] += bytes;
+    c.prof.flops[cls] += flops;
   }
 };
 
@@ -196,12 +257,21 @@ struct Timer {
 // ---------------------------------------------------------------------------
 // Units
 // ---------------------------------------------------------------------------
-double max_col_norm2(Context& c, Matrix& X) {
-  if (X.maxn2 < 0.0) {
-    double* s = c.scal.ensure(8);
-    X.maxn2 = X.kind == 0 ? max_col_norm2_dense(X.dense(), s, c.st) : max_col_norm2_sparse(X.sparse(), s, c.st);
-  }
-  return X.maxn2;
+// max_j |x_j|^2 and |X|_F^2 (deterministic, cached on the matrix)
+void col_norms(Context& c, Matrix& X) {
+  if (X.maxn2 >= 0.0) return;
+  DBuf<double> nb;
+  double* norms = nb.ensure(static_cast<size_t>(X.n));
+  double* s = c.scal.ensure(8) + 4;
+  if (X.kind == 0)
+    col_norm2_dense(X.dense(), norms, c.st);
+  else
+    col_norm2_sparse(X.sparse(), norms, c.st);
+  reduce_sum_max(norms, X.n, s, c.st);
+  GAPLRA_CUDA_CHECK(cudaMemcpyAsync(c.pin, s, 2 * sizeof(double), cudaMemcpyDeviceToHost, c.st));
+  c.sync();
+  X.fro2 = c.pin[0];
+  X.maxn2 = c.pin[1];
 }
 
 // Z (d_pad x ldz) = X (Xᵀ W); Y (n x ldy) = Xᵀ W.
@@ -211,6 +281,8 @@ void gram_block_dev(Context& c, const Matrix& X, int p, const double* W, int64_t
     ldy = ldp_of(p);
     Y = c.ybuf.ensure(static_cast<size_t>(X.n) * ldy);
   }
+  const double xbytes = X.kind == 0 ? 8.0 * X.d * X.n : 12.0 * X.nnz + 8.0 * (X.n + 1);
+  Prof prof(c, kProfGram, xbytes, 4.0 * X.nnz * p);
   if (X.kind == 0) {
     const DenseX D = X.dense();
     GramWork w;
@@ -231,7 +303,10 @@ void qr_dev(Context& c, double* Y, int64_t ldy, int d, int p, bool count = true)
   if (d < p || p < 1) throw Error(kContractViolation, "qr_orthonormalize: need 1 <= cols <= rows");
   double* scratch = c.qrs.ensure(static_cast<size_t>(p) * round4(d));
   int* status = c.status.ensure(2);
-  launch_qr_mgs2(Y, ldy, d, p, scratch, status, c.st);
+  {
+    Prof prof(c, kProfQr, 8.0 * d * p * 2, 4.0 * d * p * p);
+    launch_qr_mgs2(Y, ldy, d, p, scratch, status, c.st);
+  }
   GAPLRA_CUDA_CHECK(cudaMemcpyAsync(c.pin_i, status, 2 * sizeof(int), cudaMemcpyDeviceToHost, c.st));
   c.sync();
   if (count) c.led.qr_factorizations++;
@@ -247,7 +322,7 @@ struct SvrgResult {
 };
 
 struct SvrgParams {
-  double eta, tol, slack;
+  double eta, tol, slack, hint;
   int64_t m;
   int cap;
   uint64_t root;
@@ -256,7 +331,19 @@ struct SvrgParams {
 SvrgParams resolve(Context& c, Matrix& X, double lambda, const gaplra_svrg_params& prm) {
   if (!(prm.tol > 0.0)) throw Error(kContractViolation, "solve_svrg: tol must be > 0");
   SvrgParams s;
-  s.eta = prm.eta > 0.0 ? prm.eta : 1.0 / (4.0 * (lambda + static_cast<double>(X.n) * max_col_norm2(c, X)));
+  col_norms(c, X);
+  s.hint = prm.lambda1_hint;
+  if (prm.eta > 0.0) {
+    s.eta = prm.eta;
+  } else {
+    s.eta = 1.0 / (4.0 * (lambda + static_cast<double>(X.n) * X.maxn2));
+    // stability cap (oracle.cpp svrg_setup): eta <= (lambda - hint) / (|X|_F^2 hint)
+    if (prm.lambda1_hint > 0.0) {
+      if (!(lambda > prm.lambda1_hint))
+        throw Error(kIndefiniteShift, "solve_svrg: lambda must exceed the lambda_1 hint");
+      if (X.fro2 > 0.0) s.eta = std::min(s.eta, (lambda - prm.lambda1_hint) / (X.fro2 * prm.lambda1_hint));
+    }
+  }
   s.m = prm.m > 0 ? prm.m : 2 * static_cast<int64_t>(X.n);
   s.cap = prm.epoch_cap > 0 ? prm.epoch_cap : static_cast<int>(std::ceil(200.0 * std::log(1.0 / prm.tol)));
   s.tol = prm.tol;
@@ -271,7 +358,12 @@ void epoch_dev(Context& c, Matrix& X, int p, double* W, const double* C, const d
                double lambda, uint64_t stream_seed, int64_t m) {
   const int64_t ld = ldp_of(p);
   int32_t* idx = c.idx.ensure(static_cast<size_t>(m));
-  launch_index_stream(stream_seed, static_cast<uint64_t>(X.n), m, idx, c.rej.ensure(1), c.st);
+  {
+    Prof prof(c, kProfIndex, 4.0 * m, 0.0);
+    launch_index_stream(stream_seed, static_cast<uint64_t>(X.n), m, idx, c.rej.ensure(1), c.st);
+  }
+  const double col_nnz = static_cast<double>(X.nnz) / X.n;
+  const double col_bytes = X.kind == 0 ? 8.0 * X.d : 12.0 * col_nnz;
   const double rho = 1.0 - eta * lambda;
   const double eta_n = eta * static_cast<double>(X.n);
   if (X.kind == 0) {
@@ -280,7 +372,10 @@ void epoch_dev(Context& c, Matrix& X, int p, double* W, const double* C, const d
     const DenseX D = X.dense();
     w.part_elems = gram_work_elems(D, p);
     w.part = w.part_elems ? c.gw.ensure(w.part_elems) : nullptr;
-    launch_xtw(D, C, ld, p, H, ld, w, c.st);
+    {
+      Prof prof(c, kProfHPass, 8.0 * X.d * X.n, 2.0 * X.nnz * p);
+      launch_xtw(D, C, ld, p, H, ld, w, c.st);
+    }
     EpochArgs a{};
     a.X = X.x;
     a.ldx = X.ld;
@@ -297,7 +392,30 @@ void epoch_dev(Context& c, Matrix& X, int p, double* W, const double* C, const d
     a.p = p;
     a.rho = rho;
     a.eta_n = eta_n;
-    launch_svrg_epoch_dense(a, choose_epoch_config(a.d_pad, p), c.st);
+    const EpochConfig cfg = choose_epoch_config(a.d_pad, p);
+    a.slab = c.tmat.ensure(epoch_slab_elems(m, cfg));
+    a.zcol = c.zcol.ensure(static_cast<size_t>(X.ld));
+    {
+      Prof prof(c, kProfBlockGram, col_bytes * m, 3.0 * kEpochBlock * col_nnz * m);
+      launch_block_prep(a, cfg, c.st);
+    }
+    static const bool timing = getenv("GAPLRA_EPOCH_TIMING") != nullptr;
+    DBuf<long long> dbg;
+    if (timing) a.dbg = dbg.ensure(static_cast<size_t>(cfg.cluster) * cfg.groups * 8);
+    {
+      Prof prof(c, kProfEpoch, col_bytes * m, 4.0 * col_nnz * p * m);
+      launch_svrg_epoch_dense(a, cfg, c.st);
+    }
+    if (timing) {
+      std::vector<long long> h(static_cast<size_t>(cfg.cluster) * cfg.groups * 8);
+      GAPLRA_CUDA_CHECK(cudaMemcpyAsync(h.data(), dbg.p, h.size() * sizeof(long long), cudaMemcpyDeviceToHost, c.st));
+      c.sync();
+      const double nbk = static_cast<double>(ceil_div(m, cfg.b));
+      fprintf(stderr, "{\"epoch_phase_cycles_per_block\": [");
+      for (int k = 0; k < 8; ++k) fprintf(stderr, "%s%.0f", k ? ", " : "", h[k] / nbk);
+      fprintf(stderr, "], \"cluster\": %d, \"pc\": %d, \"groups\": %d, \"stages\": %d}\n", cfg.cluster, cfg.pc,
+              cfg.groups, cfg.stages);
+    }
   } else {
     SparseEpochArgs a{};
     a.d = X.d;
@@ -315,6 +433,7 @@ void epoch_dev(Context& c, Matrix& X, int p, double* W, const double* C, const d
     a.ldy = ld;
     a.rho = rho;
     a.eta_n = eta_n;
+    Prof prof(c, kProfEpoch, col_bytes * m, 4.0 * col_nnz * p * m);
     launch_svrg_epoch_sparse(a, c.st);
   }
 }
@@ -477,6 +596,7 @@ gaplra_svrg_params prm_from(const gaplra_si_config& cfg, double tol) {
   p.epoch_cap = cfg.epoch_cap;
   p.monotone_slack = cfg.monotone_slack;
   p.root_seed = cfg.seed;
+  p.lambda1_hint = 0.0;
   return p;
 }
 
@@ -494,8 +614,13 @@ void tune_shift_dev(Context& c, Matrix& X, double delta, const gaplra_si_config&
   double lambda = 1.5 * l1;
   const double ratio = l1 / delta;
   const int cap = (ratio > 1.0 ? static_cast<int>(std::ceil(4.0 * std::log2(ratio))) : 0) + 5;
-  const gaplra_svrg_params prm = prm_from(cfg, cfg.tol_tune);
+  gaplra_svrg_params prm = prm_from(cfg, cfg.tol_tune);
+  // lambda_1 upper estimates (oracle.cpp tune_shift): l1_hat >= (3/4) lambda_1, then
+  // lambda_1 <= 2 lambda_t - lambda_{t-1}
+  double hint = l1 / 0.75, prev_lambda = lambda;
   for (int t = 0; t < cap; ++t) {
+    if (t > 0) hint = 2.0 * lambda - prev_lambda;
+    prm.lambda1_hint = hint;
     InverseOp dinv(c, X, lambda, prm, counter);
     const double est = estimate_top_dev(c, dinv, d, dp, 1.0 / 9.0, derive_seed(cfg.seed, kTagEstD + t), cfg.rq_tol,
                                         nullptr);
@@ -507,8 +632,10 @@ void tune_shift_dev(Context& c, Matrix& X, double delta, const gaplra_si_config&
     rep.tune_steps++;
     if (inv >= delta / 27.0 && inv <= delta / 5.0) {
       rep.lambda = lambda;
+      rep.lambda1_hint = lambda - (8.0 / 9.0) * inv;
       return;
     }
+    prev_lambda = lambda;
     lambda = lambda - (4.0 / 9.0) * inv;
   }
   rep.lambda = lambda;
@@ -653,6 +780,30 @@ int gaplra_ledger_reset(gaplra_ctx* ctx) {
   if (!ctx) return GAPLRA_CONTRACT_VIOLATION;
   ctx->c.led = gaplra_ledger{};
   return GAPLRA_OK;
+}
+
+int gaplra_profile_enable(gaplra_ctx* ctx, int on) {
+  if (!ctx) return GAPLRA_CONTRACT_VIOLATION;
+  return guard(ctx, [&] {
+    ctx->c.sync();
+    ctx->c.profiling = on != 0;
+  });
+}
+
+int gaplra_profile_get(gaplra_ctx* ctx, gaplra_profile* out) {
+  if (!ctx || !out) return GAPLRA_CONTRACT_VIOLATION;
+  return guard(ctx, [&] {
+    ctx->c.sync();
+    *out = ctx->c.prof;
+  });
+}
+
+int gaplra_profile_reset(gaplra_ctx* ctx) {
+  if (!ctx) return GAPLRA_CONTRACT_VIOLATION;
+  return guard(ctx, [&] {
+    ctx->c.sync();
+    ctx->c.prof = gaplra_profile{};
+  });
 }
 
 int gaplra_matrix_dense(gaplra_ctx* ctx, int d, int n, const double* x, int64_t ldx, int on_device,
@@ -1011,6 +1162,7 @@ int gaplra_shift_invert(gaplra_ctx* ctx, const gaplra_matrix* x, const gaplra_si
     int64_t solves = 0;
     if (cfg->lambda > 0.0) {
       rep->lambda = cfg->lambda;
+      rep->lambda1_hint = cfg->lambda1_hint;
     } else {
       Timer t(c, &rep->ms_tune);
       tune_shift_dev(c, X, cfg->delta, *cfg, &solves, *rep);
@@ -1021,7 +1173,9 @@ int gaplra_shift_invert(gaplra_ctx* ctx, const gaplra_matrix* x, const gaplra_si
     double* S = sb.ensure(static_cast<size_t>(dp) * ld);
     {
       Timer t(c, &rep->ms_subspace);
-      InverseOp dinv(c, X, rep->lambda, prm_from(*cfg, cfg->tol_solve), &solves);
+      gaplra_svrg_params prm = prm_from(*cfg, cfg->tol_solve);
+      prm.lambda1_hint = rep->lambda1_hint;
+      InverseOp dinv(c, X, rep->lambda, prm, &solves);
       rep->outer_cap = outer_cap(*cfg, X.d);
       rep->outer_iterations = subspace_iterate_dev(c, dinv, X.d, dp, p, rep->outer_cap,
                                                    derive_seed(cfg->seed, kTagSubspace), cfg->conv_tol, S);

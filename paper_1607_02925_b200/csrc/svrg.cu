@@ -5,14 +5,19 @@
 //     r = ηn (x_iᵀ W − Y_i),   W ← ρ W + C + x_i rᵀ,   ρ = 1 − ηλ,  C = η(X Xᵀ W̃ + B)
 // with Y = Xᵀ W̃ from the anchor.  The device evaluates it in exact-arithmetic-
 // equivalent s-step blocks of b steps:
-//     P_j = x_{i_j}ᵀ W_0,  K_jl = x_{i_j}ᵀ x_{i_l},  H_i = x_iᵀ C (precomputed pass)
-//     r_j = ηn (ρ^j P_j + γ_j H_{i_j} + Σ_{l<j} ρ^{j−1−l} K_jl r_l − Y_{i_j})
-//     W_b = ρ^b W_0 + γ_b C + Σ_l ρ^{b−1−l} x_{i_l} r_lᵀ,      γ_j = Σ_{t<j} ρ^t
-// Dense kernel: one thread-block cluster per group of ≤ PC columns; the G CTAs
-// of a cluster split the d rows, keep their W and C row slices resident in
-// shared memory for the whole epoch, stage the b sampled column slices, and
-// all-reduce the b·PC + b(b−1)/2 partial dots through distributed shared
-// memory (fixed rank order ⇒ deterministic, identical in every CTA).
+//     P_j = x_{i_j}ᵀ W_0,   H_i = x_iᵀ C (one precomputed pass per epoch)
+//     v_j = ηn (ρ^j P_j + γ_j H_{i_j} − Y_{i_j}),   γ_j = Σ_{t<j} ρ^t
+//     (I − L) r = v,   L_jl = ηn ρ^{j−1−l} x_{i_j}ᵀ x_{i_l}  (l < j)
+//     W_b = ρ^b W_0 + γ_b C + Σ_l ρ^{b−1−l} x_{i_l} r_lᵀ
+// L depends only on the index stream and X, so T = (I − L)⁻¹ is computed for
+// every block of the epoch up front by k_block_gram_t (fully parallel, DMMA
+// fp64 Gram of the b sampled columns).  The sequential part, k_svrg_chain,
+// then needs per block only: the partial dots P over the CTA's rows, ONE
+// cluster all-reduce through distributed shared memory, r = T v, and the W
+// update on its rows.  One thread-block cluster (G CTAs splitting d rows,
+// W/C row slices resident in shared memory for the whole epoch) per group of
+// PC right-hand-side columns; sampled column slices and T are streamed one
+// block ahead by TMA bulk copies (cp.async.bulk + mbarrier).
 #include <cooperative_groups.h>
 
 #include <algorithm>
@@ -26,154 +31,540 @@ namespace gaplra_cuda {
 
 namespace {
 
-constexpr int kEpochThreads = 256;
+// ---------------------------------------------------------------------------
+// PTX helpers: mbarrier + TMA 1D bulk copies + cp.async (LDGSTS) + DMMA.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
-struct Smem {
-  int rows, rows_pad, pc_pad, entries;
-  size_t off_x, off_w, off_c, off_part, off_full, off_coef, off_pow, off_gam, off_idx, total;
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+// ---------------------------------------------------------------------------
+// k_block_prep: everything of s-step block t that does not depend on W.
+//   K_t   = X_{B_t}ᵀ X_{B_t}   (strict lower part), Kx_t = X_{B_t}ᵀ X_{B_{t−1}}
+//   T_t   = (I − L_t)⁻¹,  L_jl = ηn ρ^{j−1−l} K_jl
+//   TT_t  = diag(ρ^{b−1−j}) T_t diag(ηn ρ^l)          (coef = TT P̂ + U)
+//   M_t   = TT_t Kx_t                                  (lookahead correction)
+//   U_t   = diag(ρ^{b−1−j}) T_t q,  q_l = ηn((ρ^l β_t + γ_l) H_{i_l} − Y_{i_l})
+// with W = Ŵ + β C tracked lazily (β_t = γ_{tB} = Σ_{k<tB} ρ^k), so C never has
+// to be resident.  Gram by DMMA m8n8k4 fp64, warps split the d rows, fixed
+// order reductions.  Slab per block: [TT | M | U(group 0) | U(group 1) | ...].
+// ---------------------------------------------------------------------------
+constexpr int kPrepThreads = 256;
+constexpr int kMaxP = 64;
+
+template <int B>
+__global__ void __launch_bounds__(kPrepThreads) k_block_prep(EpochArgs a) {
+  constexpr int G8 = B / 8;
+  constexpr int NW = G8 * (G8 + 1) / 2;  // within-block lower tiles
+  constexpr int NX = G8 * G8;            // cross tiles
+  constexpr int NT = NW + NX;
+  constexpr int NWARP = kPrepThreads / 32;
+  __shared__ double red[NWARP][NT][64];
+  __shared__ double K[B][B + 1];
+  __shared__ double Kx[B][B + 1];
+  __shared__ double T[B][B + 1];
+  __shared__ double TT[B][B + 1];
+  __shared__ double q[B][kMaxP];
+  __shared__ double rp[B + 1], gm[B + 1];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t nblocks = (a.m + B - 1) / B;
+  const double one_minus_rho = 1.0 - a.rho;  // exact (Sterbenz) for rho in [0.5, 1]
+  const double lr = log1p(a.rho - 1.0);
+  for (int64_t t = blockIdx.x; t < nblocks; t += gridDim.x) {
+    const int64_t s0 = t * B;
+    const int bt = static_cast<int>(a.m - s0 < B ? a.m - s0 : B);
+    const bool has_prev = t > 0;
+    const double* base[G8];
+    const double* pbase[G8];
+#pragma unroll
+    for (int g = 0; g < G8; ++g) {
+      const int jj = g * 8 + (lane >> 2);
+      base[g] = (jj < bt ? a.X + static_cast<int64_t>(a.idx[s0 + jj]) * a.ldx : a.zcol) + (lane & 3);
+      pbase[g] = (has_prev ? a.X + static_cast<int64_t>(a.idx[s0 - B + jj]) * a.ldx : a.zcol) + (lane & 3);
+    }
+    double acc[NT][2];
+#pragma unroll
+    for (int qq = 0; qq < NT; ++qq) acc[qq][0] = acc[qq][1] = 0.0;
+    const int ksteps = a.d_pad / 4;
+    auto step = [&](const double (&f)[G8], const double (&fp)[G8]) {
+      int qq = 0;
+#pragma unroll
+      for (int gj = 0; gj < G8; ++gj)
+#pragma unroll
+        for (int gl = 0; gl <= gj; ++gl, ++qq) dmma(acc[qq][0], acc[qq][1], f[gj], f[gl]);
+#pragma unroll
+      for (int gj = 0; gj < G8; ++gj)
+#pragma unroll
+        for (int gl = 0; gl < G8; ++gl, ++qq) dmma(acc[qq][0], acc[qq][1], f[gj], fp[gl]);
+    };
+    // register double-buffered batches of U k-steps: the next batch's loads
+    // are in flight while the current batch's DMMAs run (MLP for HBM latency)
+    constexpr int U = 8;
+    double fa[U][G8], fpa[U][G8], fb[U][G8], fpb[U][G8];
+    auto load = [&](int ks0, double (&f)[U][G8], double (&fp)[U][G8]) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int ks = ks0 + u * NWARP;
+        const int o = 4 * (ks < ksteps ? ks : 0);
+#pragma unroll
+        for (int g = 0; g < G8; ++g) {
+          f[u][g] = ks < ksteps ? __ldg(base[g] + o) : 0.0;
+          fp[u][g] = ks < ksteps ? __ldg(pbase[g] + o) : 0.0;
+        }
+      }
+    };
+    auto run = [&](double (&f)[U][G8], double (&fp)[U][G8]) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) step(f[u], fp[u]);
+    };
+    int ks = warp;
+    if (ks < ksteps) load(ks, fa, fpa);
+    while (ks < ksteps) {
+      const int nx = ks + U * NWARP;
+      if (nx < ksteps) load(nx, fb, fpb);
+      run(fa, fpa);
+      ks = nx;
+      if (ks >= ksteps) break;
+      const int nx2 = ks + U * NWARP;
+      if (nx2 < ksteps) load(nx2, fa, fpa);
+      run(fb, fpb);
+      ks = nx2;
+    }
+#pragma unroll
+    for (int qq = 0; qq < NT; ++qq) {
+      red[warp][qq][2 * lane] = acc[qq][0];
+      red[warp][qq][2 * lane + 1] = acc[qq][1];
+    }
+    // q_l[c] = ηn((ρ^l β_t + γ_l) H[i_l][c] − Y[i_l][c]),  β_t = γ_{tB}
+    if (threadIdx.x == 0) {
+      rp[0] = 1.0;
+      gm[0] = 0.0;
+      for (int j = 1; j <= B; ++j) {
+        rp[j] = rp[j - 1] * a.rho;
+        gm[j] = gm[j - 1] + rp[j - 1];
+      }
+    }
+    __syncthreads();
+    const double beta = -expm1(static_cast<double>(s0) * lr) / one_minus_rho;
+    for (int e = threadIdx.x; e < B * a.p; e += kPrepThreads) {
+      const int l = e / a.p, c = e - (e / a.p) * a.p;
+      double v = 0.0;
+      if (l < bt) {
+        const int64_t i = a.idx[s0 + l];
+        v = a.eta_n * (fma(rp[l], beta, gm[l]) * a.H[i * a.ldy + c] - a.Y[i * a.ldy + c]);
+      }
+      q[l][c] = v;
+    }
+    for (int e = threadIdx.x; e < NT * 64; e += kPrepThreads) {
+      const int qq = e / 64, o = e % 64;
+      double s = 0.0;
+#pragma unroll
+      for (int w = 0; w < NWARP; ++w) s += red[w][qq][o];
+      const int ln = o >> 1;
+      const int mi = ln >> 2, ni = 2 * (ln & 3) + (o & 1);
+      if (qq < NW) {
+        int gj = 0, rem = qq;
+        while (rem > gj) {
+          rem -= gj + 1;
+          ++gj;
+        }
+        K[gj * 8 + mi][rem * 8 + ni] = s;
+      } else {
+        const int x = qq - NW;
+        Kx[(x / G8) * 8 + mi][(x % G8) * 8 + ni] = s;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x < B) {  // column l of T = (I − L)⁻¹ (forward substitution)
+      const int l = threadIdx.x;
+      for (int j = 0; j < B; ++j) T[j][l] = 0.0;
+      if (l < bt) {
+        T[l][l] = 1.0;
+        for (int j = l + 1; j < bt; ++j) {
+          double s = 0.0;
+          for (int k = l; k < j; ++k) s = fma(a.eta_n * rp[j - 1 - k] * K[j][k], T[k][l], s);
+          T[j][l] = s;
+        }
+      }
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < B * B; e += kPrepThreads) {
+      const int j = e / B, l = e % B;
+      TT[j][l] = (j < bt && l <= j) ? rp[bt - 1 - j] * T[j][l] * (a.eta_n * rp[l]) : 0.0;
+    }
+    __syncthreads();
+    double* slab = a.slab + t * a.slab_len;
+    for (int e = threadIdx.x; e < B * B; e += kPrepThreads) {
+      const int j = e / B, l = e % B;
+      slab[e] = TT[j][l];
+      double s = 0.0;
+      if (has_prev)
+        for (int k = 0; k <= j; ++k) s = fma(TT[j][k], Kx[k][l], s);
+      slab[B * B + e] = s;
+    }
+    for (int e = threadIdx.x; e < B * a.groups * a.pc; e += kPrepThreads) {
+      const int grp = e / (B * a.pc), rem = e - grp * (B * a.pc);
+      const int j = rem / a.pc, cc = rem - (rem / a.pc) * a.pc;
+      const int c = grp * a.pc + cc;
+      double s = 0.0;
+      if (j < bt && c < a.p) {
+        for (int l = 0; l <= j; ++l) s = fma(T[j][l], q[l][c], s);
+        s *= rp[bt - 1 - j];
+      }
+      slab[2 * B * B + e] = s;
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// k_svrg_chain: the sequential recurrence with one-block lookahead.
+// State per CTA: V = ρ^{b_t} Ŵ_t on its rows (W = Ŵ + βC, β folded into U).
+// Iteration t (all quantities for the cluster's PC columns):
+//   (a) coef_t = TT_t Â_t + M_t coef_{t−1} + U_t            (local, redundant)
+//   (b) Â_{t+1} partial = X_{B_{t+1}}ᵀ V_t on own rows; pushed into every
+//       peer's receive slot (DSMEM stores); cluster arrive.release
+//   (c) Ŵ_{t+1} = V_t + X_{B_t} coef_t;  V_{t+1} = ρ^{b_{t+1}} Ŵ_{t+1}
+//   (d) cluster wait.acquire; Â_{t+1} = Σ_q slot_q (fixed order)
+// so the cluster all-reduce latency overlaps the W update.  X slices and the
+// block slab stream through an S-stage TMA ring (cp.async.bulk + mbarrier).
+// ---------------------------------------------------------------------------
+constexpr int kChainThreads = 256;
+constexpr int kMaxCluster = 16;
+
+struct ChainSmem {
+  int rows_pad, stages;
+  size_t stage_len, off_stage, off_v, off_recv, off_a, off_coef, off_rprev, off_idx, off_red, off_bar, total;
 };
 
 template <int PC, int B>
-__host__ __device__ inline Smem smem_layout(int rows) {
-  Smem s;
-  s.rows = rows;
-  s.rows_pad = rows + 4;  // odd-ish pitch keeps column slices on distinct banks
-  s.pc_pad = PC;
-  s.entries = B * PC + B * (B - 1) / 2;
+__host__ __device__ inline ChainSmem chain_smem(int rows, int stages) {
+  ChainSmem s;
+  s.rows_pad = (rows + 1) / 2 * 2 + 2;
+  s.stages = stages;
+  s.stage_len = static_cast<size_t>(B) * s.rows_pad + 2 * B * B + B * PC;  // X slices | TT | M | U
   size_t o = 0;
-  s.off_x = o;
-  o += static_cast<size_t>(B) * s.rows_pad;
-  s.off_w = o;
+  s.off_stage = o;
+  o += s.stage_len * stages;
+  s.off_v = o;
   o += static_cast<size_t>(rows) * PC;
-  s.off_c = o;
-  o += static_cast<size_t>(rows) * PC;
-  s.off_part = o;
-  o += 2 * static_cast<size_t>(s.entries);
-  s.off_full = o;
-  o += s.entries;
+  s.off_recv = o;
+  o += 2 * kMaxCluster * B * PC;
+  s.off_a = o;
+  o += B * PC;
   s.off_coef = o;
-  o += static_cast<size_t>(B) * PC;
-  s.off_pow = o;
-  o += B + 1;
-  s.off_gam = o;
-  o += B + 1;
+  o += B * PC;
+  s.off_rprev = o;
+  o += B * PC;
   s.off_idx = o;
-  o += B;  // ints stored in double slots
+  o += 0;
+  s.off_red = o;
+  o += (kChainThreads / 32) * (B / 8) * 64;
+  s.off_bar = o;
+  o += 12;
   s.total = o * sizeof(double);
   return s;
 }
 
+__device__ __forceinline__ uint32_t mapa(uint32_t local_smem_addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local_smem_addr), "r"(rank));
+  return r;
+}
+// Remote (DSMEM) 8-byte store that completes 8 transaction bytes on the
+// receiver's mbarrier: no fence / cluster barrier on the critical path.
+__device__ __forceinline__ void st_async_f64(uint32_t remote_addr, double v, uint32_t remote_bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(remote_addr),
+               "l"(__double_as_longlong(v)), "r"(remote_bar)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void consumers_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kChainThreads) : "memory"); }
+
 template <int PC, int B>
-__global__ void __launch_bounds__(kEpochThreads, 1) k_svrg_epoch_dense(EpochArgs a) {
-  extern __shared__ __align__(16) double sm[];
+__global__ void __launch_bounds__(kChainThreads + 32, 1) k_svrg_chain(EpochArgs a) {
+  extern __shared__ __align__(128) double sm[];
   cg::cluster_group cluster = cg::this_cluster();
   const int G = static_cast<int>(cluster.num_blocks());
   const int g = static_cast<int>(cluster.block_rank());
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int c0 = blockIdx.y * PC;
+  const int grp = blockIdx.y;
+  const int c0 = grp * PC;
   const int pc = min(PC, a.p - c0);
-  const Smem L = smem_layout<PC, B>(a.rows_per_cta);
+  const ChainSmem L = chain_smem<PC, B>(a.rows_per_cta, a.stages);
+  const int S = L.stages;
   const int r0 = g * a.rows_per_cta;
   const int rc = max(0, min(a.rows_per_cta, a.d_pad - r0));
-
-  double* Xs = sm + L.off_x;
-  double* Ws = sm + L.off_w;
-  double* Cs = sm + L.off_c;
-  double* part = sm + L.off_part;
-  double* full = sm + L.off_full;
+  const int RP = L.rows_pad;
+  double* V = sm + L.off_v;
+  double* recv = sm + L.off_recv;  // [2][kMaxCluster][B*PC]
+  double* Ahat = sm + L.off_a;
   double* coef = sm + L.off_coef;
-  double* rpow = sm + L.off_pow;
-  double* gam = sm + L.off_gam;
-  int* idxs = reinterpret_cast<int*>(sm + L.off_idx);
+  double* rprev = sm + L.off_rprev;
+  double* red = sm + L.off_red;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + L.off_bar);  // [S] TMA landed
+  uint64_t* empty = full + 4;                                     // [S] consumers done
+  uint64_t* rbar = full + 8;                                      // [2] all-reduce slots
+  auto stage = [&](int64_t t) { return sm + L.off_stage + static_cast<size_t>(t % S) * L.stage_len; };
 
-  // Resident W / C row slices (row-major r x PC, zero beyond pc).
-  for (int e = tid; e < rc * PC; e += kEpochThreads) {
+  const int64_t nb = (a.m + B - 1) / B;
+  auto bt_of = [&](int64_t t) { return static_cast<int>(a.m - t * B < B ? a.m - t * B : B); };
+  for (int e = tid; e < rc * PC; e += blockDim.x) {
     const int r = e / PC, c = e - (e / PC) * PC;
-    const int64_t gr = static_cast<int64_t>(r0 + r) * a.ldw + c0 + c;
-    Ws[e] = c < pc ? a.W[gr] : 0.0;
-    Cs[e] = c < pc ? a.C[gr] : 0.0;
+    V[e] = c < pc ? a.W[static_cast<int64_t>(r0 + r) * a.ldw + c0 + c] : 0.0;
   }
+  for (int e = tid; e < B * PC; e += blockDim.x) rprev[e] = 0.0;
   if (tid == 0) {
-    rpow[0] = 1.0;
-    gam[0] = 0.0;
-    for (int j = 1; j <= B; ++j) {
-      rpow[j] = rpow[j - 1] * a.rho;
-      gam[j] = gam[j - 1] + rpow[j - 1];
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kChainThreads);
     }
+    mbar_init(&rbar[0], 1);
+    mbar_init(&rbar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  __syncthreads();
+  cluster.sync();  // barriers initialised cluster-wide before any push / TMA
 
-  int par = 0;
-  for (int64_t s0 = 0; s0 < a.m; s0 += B, par ^= 1) {
-    const int bt = a.m - s0 < B ? static_cast<int>(a.m - s0) : B;
-    if (tid < bt) idxs[tid] = a.idx[s0 + tid];
-    __syncthreads();
-    // Stage the sampled column slices x_{i_j}[r0 : r0 + rc).
-    for (int e = tid; e < bt * rc; e += kEpochThreads) {
-      const int j = e / rc, r = e - (e / rc) * rc;
-      Xs[j * L.rows_pad + r] = __ldg(a.X + static_cast<int64_t>(idxs[j]) * a.ldx + r0 + r);
+  if (warp == kChainThreads / 32) {
+    // ===== producer warp: stream X slices + the block slab through the ring
+    for (int64_t t = 0; t < nb; ++t) {
+      const int s = static_cast<int>(t % S);
+      if (t >= S) mbar_wait(&empty[s], static_cast<uint32_t>((t / S - 1) & 1));
+      const int bt = bt_of(t);
+      double* st = stage(t);
+      if (lane == 0) {
+        fence_proxy_async();
+        mbar_expect_tx(&full[s], static_cast<uint32_t>((rc > 0 ? bt * rc : 0) + 2 * B * B + B * PC) * 8u);
+      }
+      __syncwarp();
+      if (lane < bt && rc > 0)
+        tma_load_1d(st + lane * RP, a.X + static_cast<int64_t>(__ldg(a.idx + t * B + lane)) * a.ldx + r0, rc * 8u,
+                    &full[s]);
+      if (lane == 31) {
+        const double* slab = a.slab + t * a.slab_len;
+        tma_load_1d(st + B * RP, slab, 2 * B * B * 8u, &full[s]);
+        tma_load_1d(st + B * RP + 2 * B * B, slab + 2 * B * B + static_cast<size_t>(grp) * B * PC, B * PC * 8u,
+                    &full[s]);
+      }
     }
-    __syncthreads();
-    // Local partial dots: P[j][c] (bt*PC entries) then K[j][l], l < j.
-    const int np = bt * PC;
-    const int ne = np + bt * (bt - 1) / 2;
-    double* mypart = part + par * L.entries;
-    for (int ent = warp; ent < ne; ent += kEpochThreads / 32) {
-      double s = 0.0;
-      if (ent < np) {
-        const int j = ent / PC, c = ent - (ent / PC) * PC;
-        const double* xj = Xs + j * L.rows_pad;
-        for (int r = lane; r < rc; r += 32) s = fma(xj[r], Ws[r * PC + c], s);
-      } else {
-        int k = ent - np, j = 1;
-        while (k >= j) {
-          k -= j;
-          ++j;
+  } else {
+    // ===== 8 consumer warps
+    auto wait_block = [&](int64_t t) { mbar_wait(&full[t % S], static_cast<uint32_t>((t / S) & 1)); };
+    // Partial Â = X_Bᵀ V over the owned rows (DMMA: M = j, N = columns, K =
+    // rows split over the 8 warps), fixed-order cross-warp sum, then st.async
+    // of every entry into slot g of every peer (completing on its rbar).
+    auto dots_push = [&](const double* xb, int bt, int64_t u) {
+      const int par = static_cast<int>(u & 1);
+      const int gq = lane >> 2, tq = lane & 3;
+      constexpr int NA = 4;  // independent accumulation chains per tile
+      double acc[NA][B / 8][2];
+#pragma unroll
+      for (int q = 0; q < NA; ++q)
+#pragma unroll
+        for (int mt = 0; mt < B / 8; ++mt) acc[q][mt][0] = acc[q][mt][1] = 0.0;
+      const int nks = rc / 4;
+      constexpr int WS = kChainThreads / 32;
+      int ks = warp;
+      for (; ks + (NA - 1) * WS < nks; ks += NA * WS) {
+#pragma unroll
+        for (int q = 0; q < NA; ++q) {
+          const int r = 4 * (ks + q * WS) + tq;
+          const double bv = gq < PC ? V[r * PC + gq] : 0.0;
+#pragma unroll
+          for (int mt = 0; mt < B / 8; ++mt) dmma(acc[q][mt][0], acc[q][mt][1], xb[(8 * mt + gq) * RP + r], bv);
         }
-        const double* xj = Xs + j * L.rows_pad;
-        const double* xl = Xs + k * L.rows_pad;
-        for (int r = lane; r < rc; r += 32) s = fma(xj[r], xl[r], s);
       }
-      s = warp_sum(s);
-      if (lane == 0) mypart[ent] = s;
-    }
-    cluster.sync();
-    for (int ent = tid; ent < ne; ent += kEpochThreads) {
-      double s = 0.0;
-      for (int q = 0; q < G; ++q) s += cluster.map_shared_rank(mypart, q)[ent];
-      full[ent] = s;
-    }
-    __syncthreads();
-    // Recurrence for the bt coefficients of each column (thread = column).
-    if (tid < pc) {
-      const int c = tid;
-      const double* K = full + np;
-      for (int j = 0; j < bt; ++j) {
-        const int64_t i = idxs[j];
-        double v = fma(rpow[j], full[j * PC + c], gam[j] * a.H[i * a.ldy + c0 + c]) - a.Y[i * a.ldy + c0 + c];
-        const double* Kj = K + j * (j - 1) / 2;
-        for (int l = 0; l < j; ++l) v = fma(rpow[j - 1 - l] * Kj[l], coef[l * PC + c], v);
-        coef[j * PC + c] = a.eta_n * v;
+      for (; ks < nks; ks += WS) {
+        const int r = 4 * ks + tq;
+        const double bv = gq < PC ? V[r * PC + gq] : 0.0;
+#pragma unroll
+        for (int mt = 0; mt < B / 8; ++mt) dmma(acc[0][mt][0], acc[0][mt][1], xb[(8 * mt + gq) * RP + r], bv);
       }
-      for (int l = 0; l < bt; ++l) coef[l * PC + c] *= rpow[bt - 1 - l];
+#pragma unroll
+      for (int mt = 0; mt < B / 8; ++mt) {
+        red[(warp * (B / 8) + mt) * 64 + 2 * lane] = (acc[0][mt][0] + acc[1][mt][0]) + (acc[2][mt][0] + acc[3][mt][0]);
+        red[(warp * (B / 8) + mt) * 64 + 2 * lane + 1] =
+            (acc[0][mt][1] + acc[1][mt][1]) + (acc[2][mt][1] + acc[3][mt][1]);
+      }
+      consumers_sync();
+      const uint32_t slot = smem_u32(recv + (par * kMaxCluster + g) * B * PC);
+      const uint32_t rbl = smem_u32(&rbar[par]);
+      for (int e = tid; e < bt * PC; e += kChainThreads) {
+        const int j = e / PC, c = e - (e / PC) * PC;
+        // C fragment position of (j, c): tile j/8, lane 4*(j%8) + c/2, element c%2
+        const int o = ((j >> 3) * 64) + 2 * (4 * (j & 7) + (c >> 1)) + (c & 1);
+        double s = 0.0;
+#pragma unroll
+        for (int w = 0; w < kChainThreads / 32; ++w) s += red[w * (B / 8) * 64 + o];
+        for (int q = 0; q < G; ++q) st_async_f64(mapa(slot, q) + e * 8u, s, mapa(rbl, q));
+      }
+    };
+    auto arm_recv = [&](int64_t u) {
+      mbar_expect_tx(&rbar[u & 1], static_cast<uint32_t>(G * bt_of(u) * PC * 8));
+    };
+    auto recv_sum = [&](int64_t u) {
+      const int par = static_cast<int>(u & 1);
+      mbar_wait(&rbar[par], static_cast<uint32_t>((u >> 1) & 1));
+      const int n = bt_of(u) * PC;
+      for (int e = tid; e < n; e += kChainThreads) {
+        double s = 0.0;
+        for (int q = 0; q < G; ++q) s += recv[(par * kMaxCluster + q) * B * PC + e];
+        Ahat[e] = s;
+      }
+    };
+    if (nb > 0) {
+      if (tid == 0) arm_recv(0);
+      wait_block(0);
+      dots_push(stage(0), bt_of(0), 0);
+      recv_sum(0);
+      double rb = 1.0;
+      for (int j = 0; j < bt_of(0); ++j) rb *= a.rho;
+      for (int e = tid; e < rc * PC; e += kChainThreads) V[e] *= rb;
     }
-    __syncthreads();
-    // W_b = ρ^b W_0 + γ_b C + Σ_l x_{i_l} coef_l   on the owned rows.
-    const double rb = rpow[bt], gb = gam[bt];
-    for (int e = tid; e < rc * PC; e += kEpochThreads) {
+    long long tacc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    long long tp = clock64();
+    auto tick = [&](int k) {
+      if (a.dbg) {
+        const long long now = clock64();
+        tacc[k] += now - tp;
+        tp = now;
+      }
+    };
+    for (int64_t t = 0; t < nb; ++t) {
+      const int bt = bt_of(t);
+      const bool more = t + 1 < nb;
+      if (tid == 0 && more) arm_recv(t + 1);
+      if (more) wait_block(t + 1);
+      tick(0);
+      consumers_sync();
+      tick(1);
+      const double* xb = stage(t);
+      const double* TT = xb + B * RP;
+      const double* M = TT + B * B;
+      const double* Ub = M + B * B;
+      // (a) coef_t = TT Â + M coef_{t−1} + U  — warps 0/1 own row tiles j in [8w, 8w+8),
+      //     DMMA m8n8k4 (A = TT/M rows, B = Â / coef_{t−1} columns padded to 8)
+      if (warp < B / 8) {
+        const int gq = lane >> 2, tq = lane & 3, j = warp * 8 + gq;
+        double cA[B / 4][2], cR[B / 4][2];  // independent accumulation chains
+#pragma unroll
+        for (int ks = 0; ks < B / 4; ++ks) {
+          const int l = 4 * ks + tq;
+          cA[ks][0] = cA[ks][1] = cR[ks][0] = cR[ks][1] = 0.0;
+          dmma(cA[ks][0], cA[ks][1], TT[j * B + l], gq < PC ? Ahat[l * PC + gq] : 0.0);
+          dmma(cR[ks][0], cR[ks][1], M[j * B + l], gq < PC ? rprev[l * PC + gq] : 0.0);
+        }
+        double c0 = 2 * tq < PC ? Ub[j * PC + 2 * tq] : 0.0;
+        double c1 = 2 * tq + 1 < PC ? Ub[j * PC + 2 * tq + 1] : 0.0;
+#pragma unroll
+        for (int ks = 0; ks < B / 4; ++ks) {
+          c0 += cA[ks][0] + cR[ks][0];
+          c1 += cA[ks][1] + cR[ks][1];
+        }
+        if (2 * tq < PC) coef[j * PC + 2 * tq] = c0;
+        if (2 * tq + 1 < PC) coef[j * PC + 2 * tq + 1] = c1;
+      }
+      tick(2);
+      consumers_sync();
+      tick(3);
+      // (b) lookahead partials of block t+1 → every peer
+      if (more) dots_push(stage(t + 1), bt_of(t + 1), t + 1);
+      tick(4);
+      consumers_sync();
+      tick(5);
+      // (c) Ŵ_{t+1} = V_t + X_{B_t} coef_t ; V_{t+1} = ρ^{b_{t+1}} Ŵ_{t+1}   (thread = row)
+      double rn = 1.0;
+      if (more)
+        for (int j = 0; j < bt_of(t + 1); ++j) rn *= a.rho;
+      {
+        // DMMA: rows in tiles of 8 (M), columns padded to 8 (N), K = the b steps
+        const int gq = lane >> 2, tq = lane & 3;
+        double bc[B / 4];
+#pragma unroll
+        for (int ks = 0; ks < B / 4; ++ks) bc[ks] = gq < PC ? coef[(4 * ks + tq) * PC + gq] : 0.0;
+        constexpr int WS = kChainThreads / 32, NT = 4;
+        const int ntiles = (rc + 7) / 8;
+        for (int rt0 = warp; rt0 < ntiles; rt0 += NT * WS) {
+          double c[NT][2][2];  // [tile][chain][elem]: two K chains per tile, tiles interleaved
+#pragma unroll
+          for (int u = 0; u < NT; ++u) {
+            const int r = 8 * (rt0 + u * WS) + gq;
+            const bool live = rt0 + u * WS < ntiles && r < rc;
+            c[u][0][0] = live && 2 * tq < PC ? V[r * PC + 2 * tq] : 0.0;
+            c[u][0][1] = live && 2 * tq + 1 < PC ? V[r * PC + 2 * tq + 1] : 0.0;
+            c[u][1][0] = c[u][1][1] = 0.0;
+          }
+#pragma unroll
+          for (int ks = 0; ks < B / 4; ++ks)
+#pragma unroll
+            for (int u = 0; u < NT; ++u) {
+              const int r = 8 * (rt0 + u * WS) + gq;
+              const double av = (rt0 + u * WS < ntiles && r < rc) ? xb[(4 * ks + tq) * RP + r] : 0.0;
+              dmma(c[u][ks & 1][0], c[u][ks & 1][1], av, bc[ks]);
+            }
+#pragma unroll
+          for (int u = 0; u < NT; ++u) {
+            const int r = 8 * (rt0 + u * WS) + gq;
+            if (rt0 + u * WS < ntiles && r < rc) {
+              if (2 * tq < PC) V[r * PC + 2 * tq] = (c[u][0][0] + c[u][1][0]) * rn;
+              if (2 * tq + 1 < PC) V[r * PC + 2 * tq + 1] = (c[u][0][1] + c[u][1][1]) * rn;
+            }
+          }
+        }
+      }
+      mbar_arrive(&empty[t % S]);  // stage t fully consumed (its lookahead use was at t−1)
+      tick(6);
+      // (d) gather Â_{t+1}
+      for (int e = tid; e < B * PC; e += kChainThreads) rprev[e] = coef[e];
+      if (more) recv_sum(t + 1);
+      tick(7);
+    }
+    if (a.dbg && tid == 0) {
+      const int cta = blockIdx.y * gridDim.x + blockIdx.x;
+      for (int k = 0; k < 8; ++k) a.dbg[cta * 8 + k] = tacc[k];
+    }
+    consumers_sync();
+    const double beta = -expm1(static_cast<double>(a.m) * log1p(a.rho - 1.0)) / (1.0 - a.rho);
+    for (int e = tid; e < rc * PC; e += kChainThreads) {
       const int r = e / PC, c = e - (e / PC) * PC;
-      if (c >= pc) continue;
-      double w = fma(rb, Ws[e], gb * Cs[e]);
-      for (int l = 0; l < bt; ++l) w = fma(Xs[l * L.rows_pad + r], coef[l * PC + c], w);
-      Ws[e] = w;
+      if (c < pc) {
+        const int64_t o = static_cast<int64_t>(r0 + r) * a.ldw + c0 + c;
+        a.W[o] = fma(beta, a.C[o], V[e]);
+      }
     }
-    __syncthreads();
   }
-  for (int e = tid; e < rc * PC; e += kEpochThreads) {
-    const int r = e / PC, c = e - (e / PC) * PC;
-    if (c < pc) a.W[static_cast<int64_t>(r0 + r) * a.ldw + c0 + c] = Ws[e];
-  }
-  cluster.sync();  // keep shared memory alive until every peer finished its DSMEM reads
+  cluster.sync();
 }
 
 // Sparse (CSC) epoch, lazy form W = α Ŵ + β C (O(nnz(x_i)) per step).  One
@@ -266,29 +657,91 @@ __global__ void k_anchor_final(const double* __restrict__ part, int nparts, int 
   }
 }
 
+
+int sm_count_dev() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return sms;
+}
+
+constexpr int kBlock = 16;
+
+template <int PC>
+size_t chain_smem_bytes(int rows, int stages) {
+  return chain_smem<PC, kBlock>(rows, stages).total;
+}
+
+size_t smem_for(int pc, int rows, int stages) {
+  switch (pc) {
+    case 1: return chain_smem_bytes<1>(rows, stages);
+    case 2: return chain_smem_bytes<2>(rows, stages);
+    case 3: return chain_smem_bytes<3>(rows, stages);
+    case 4: return chain_smem_bytes<4>(rows, stages);
+    case 6: return chain_smem_bytes<6>(rows, stages);
+    default: return chain_smem_bytes<8>(rows, stages);
+  }
+}
+
+int round_pc(int pc) {
+  if (pc <= 4) return pc;
+  if (pc <= 6) return 6;
+  return 8;
+}
+
 }  // namespace
 
 EpochConfig choose_epoch_config(int d_pad, int p) {
   EpochConfig cfg;
-  cfg.cluster = d_pad <= 4096 ? 8 : 16;
-  cfg.pc = 8;
-  cfg.b = 16;
+  cfg.b = kBlock;
+  cfg.cluster = d_pad >= 1024 ? 16 : 8;
+  const int max_clusters = std::max(1, sm_count_dev() / cfg.cluster);
+  cfg.pc = round_pc(static_cast<int>(ceil_div(p, max_clusters)));
   cfg.rows_per_cta = static_cast<int>(ceil_div(ceil_div(d_pad, cfg.cluster), 4) * 4);
+  const size_t cap = 227 * 1024;
+  for (;;) {
+    cfg.stages = 4;
+    while (cfg.stages > 2 && smem_for(cfg.pc, cfg.rows_per_cta, cfg.stages) > cap) --cfg.stages;
+    if (smem_for(cfg.pc, cfg.rows_per_cta, cfg.stages) <= cap || cfg.pc == 1) break;
+    cfg.pc = round_pc(cfg.pc - 1);
+  }
   cfg.groups = static_cast<int>(ceil_div(p, cfg.pc));
-  cfg.smem = smem_layout<8, 16>(cfg.rows_per_cta).total;
+  cfg.smem = smem_for(cfg.pc, cfg.rows_per_cta, cfg.stages);
   return cfg;
 }
 
-void launch_svrg_epoch_dense(const EpochArgs& a, const EpochConfig& cfg, cudaStream_t st) {
-  auto kern = k_svrg_epoch_dense<8, 16>;
-  if (cfg.pc != 8 || cfg.b != 16) throw Error(kContractViolation, "epoch: unsupported config");
-  if (cfg.smem > 227 * 1024) throw Error(kContractViolation, "epoch: d too large for the cluster row split");
+int64_t epoch_slab_len(const EpochConfig& cfg) {
+  return 2 * kBlock * kBlock + static_cast<int64_t>(kBlock) * cfg.pc * cfg.groups;
+}
+
+size_t epoch_slab_elems(int64_t m, const EpochConfig& cfg) {
+  return static_cast<size_t>(ceil_div(m, kBlock)) * epoch_slab_len(cfg);
+}
+
+void launch_block_prep(const EpochArgs& a, const EpochConfig& cfg, cudaStream_t st) {
+  if (a.p > kMaxP) throw Error(kContractViolation, "epoch: p > 64");
+  EpochArgs args = a;
+  args.pc = cfg.pc;
+  args.groups = cfg.groups;
+  args.slab_len = epoch_slab_len(cfg);
+  const int64_t nblocks = ceil_div(a.m, kBlock);
+  const int grid = static_cast<int>(std::min<int64_t>(nblocks, sm_count_dev() * 8));
+  k_block_prep<kBlock><<<grid, kPrepThreads, 0, st>>>(args);
+  GAPLRA_LAUNCH_CHECK();
+}
+
+template <int PC>
+void launch_chain_pc(const EpochArgs& a, const EpochConfig& cfg, cudaStream_t st) {
+  auto kern = k_svrg_chain<PC, kBlock>;
   GAPLRA_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(cfg.smem)));
-  if (cfg.cluster > 8)
-    GAPLRA_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  if (cfg.cluster > 8) GAPLRA_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   cudaLaunchConfig_t lc = {};
   lc.gridDim = dim3(cfg.cluster, cfg.groups, 1);
-  lc.blockDim = dim3(kEpochThreads, 1, 1);
+  lc.blockDim = dim3(kChainThreads + 32, 1, 1);
   lc.dynamicSmemBytes = cfg.smem;
   lc.stream = st;
   cudaLaunchAttribute attr[1];
@@ -300,7 +753,23 @@ void launch_svrg_epoch_dense(const EpochArgs& a, const EpochConfig& cfg, cudaStr
   lc.numAttrs = 1;
   EpochArgs args = a;
   args.rows_per_cta = cfg.rows_per_cta;
+  args.stages = cfg.stages;
+  args.pc = cfg.pc;
+  args.groups = cfg.groups;
+  args.slab_len = epoch_slab_len(cfg);
   GAPLRA_CUDA_CHECK(cudaLaunchKernelEx(&lc, kern, args));
+}
+
+void launch_svrg_epoch_dense(const EpochArgs& a, const EpochConfig& cfg, cudaStream_t st) {
+  if (cfg.smem > 227 * 1024) throw Error(kContractViolation, "epoch: d too large for the cluster row split");
+  switch (cfg.pc) {
+    case 1: launch_chain_pc<1>(a, cfg, st); break;
+    case 2: launch_chain_pc<2>(a, cfg, st); break;
+    case 3: launch_chain_pc<3>(a, cfg, st); break;
+    case 4: launch_chain_pc<4>(a, cfg, st); break;
+    case 6: launch_chain_pc<6>(a, cfg, st); break;
+    default: launch_chain_pc<8>(a, cfg, st); break;
+  }
 }
 
 void launch_svrg_epoch_sparse(const SparseEpochArgs& a, cudaStream_t st) {

@@ -18,9 +18,13 @@ struct EpochArgs {
   const double* Y;  // n x ldy: Y_i = x_iᵀ W̃
   const double* H;  // n x ldy: H_i = x_iᵀ C
   int64_t ldy;
+  const double* zcol;  // d_pad zeros (masked Gram columns)
+  double* slab;     // per s-step block: [TT | M | U(groups)] (launch_block_prep)
+  int64_t slab_len;
   int p;
   double rho, eta_n;
-  int rows_per_cta;
+  int rows_per_cta, stages, pc, groups;
+  long long* dbg;  // optional per-CTA phase cycle counters (8 per CTA)
 };
 
 struct SparseEpochArgs {
@@ -39,11 +43,15 @@ struct SparseEpochArgs {
 };
 
 struct EpochConfig {
-  int cluster, pc, b, rows_per_cta, groups;
+  int cluster, pc, b, rows_per_cta, groups, stages;
   size_t smem;
 };
 
 EpochConfig choose_epoch_config(int d_pad, int p);
+// doubles of the per-block slabs of an m-step epoch
+size_t epoch_slab_elems(int64_t m, const EpochConfig& cfg);
+// W-independent per-block coefficients (needs X, idx, m, rho, eta_n, d_pad, Y, H, slab)
+void launch_block_prep(const EpochArgs& a, const EpochConfig& cfg, cudaStream_t st);
 void launch_svrg_epoch_dense(const EpochArgs& a, const EpochConfig& cfg, cudaStream_t st);
 void launch_svrg_epoch_sparse(const SparseEpochArgs& a, cudaStream_t st);
 

@@ -136,6 +136,17 @@ class Context:
     def reset_ledger(self):
         self.check(self.lib.gaplra_ledger_reset(self.h))
 
+    def enable_profiling(self, on: bool = True):
+        self.check(self.lib.gaplra_profile_enable(self.h, int(on)))
+
+    def profile(self) -> dict:
+        P = N.Profile()
+        self.check(self.lib.gaplra_profile_get(self.h, C.byref(P)))
+        return P.as_dict()
+
+    def reset_profile(self):
+        self.check(self.lib.gaplra_profile_reset(self.h))
+
 
 _DEFAULT: dict[int, Context] = {}
 
@@ -311,14 +322,15 @@ class SolverReport:
 
 
 def solve_svrg(x: DeviceMatrix, lam: float, b: np.ndarray, tol: float, seed: int = 0, solve_id: int = 0,
-               eta: float = 0.0, steps: int = 0, epoch_cap: int = 0, slack: float = 10.0) -> SolverReport:
+               eta: float = 0.0, steps: int = 0, epoch_cap: int = 0, slack: float = 10.0,
+               lambda1_hint: float = 0.0) -> SolverReport:
     """Block SVRG solve of (λI − XXᵀ)W = B."""
     b = _f64(b)
     if b.ndim == 1:
         b = b[:, None]
     p = b.shape[1]
     w = np.zeros_like(b)
-    prm = N.SvrgParams(eta, steps, tol, epoch_cap, slack, seed)
+    prm = N.SvrgParams(eta, steps, tol, epoch_cap, slack, seed, lambda1_hint)
     ep, hl = C.c_int(0), C.c_int(0)
     hist = np.zeros(8192)
     rc = x.ctx.lib.gaplra_svrg_solve(x.ctx.h, x.h, lam, p, _p(b), _p(w), C.byref(prm), solve_id, C.byref(ep),
@@ -330,9 +342,10 @@ def solve_svrg(x: DeviceMatrix, lam: float, b: np.ndarray, tol: float, seed: int
 
 
 def estimate_top(x: DeviceMatrix, eps_prime: float, seed: int, *, inverse: bool = False, lam: float = 0.0,
-                 rq_tol: float = 1e-4, tol: float = 1e-7, svrg_seed: int = 0, solve_counter: int = 0):
+                 rq_tol: float = 1e-3, tol: float = 1e-6, svrg_seed: int = 0, solve_counter: int = 0,
+                 lambda1_hint: float = 0.0):
     """Alg. 3 (estimate_eigenvalues) for k = 1, on A = XXᵀ or D⁻¹."""
-    prm = N.SvrgParams(0.0, 0, tol, 0, 10.0, svrg_seed)
+    prm = N.SvrgParams(0.0, 0, tol, 0, 10.0, svrg_seed, lambda1_hint)
     sc = C.c_int64(solve_counter)
     val, it = C.c_double(), C.c_int()
     x.ctx.check(x.ctx.lib.gaplra_estimate_top(x.ctx.h, x.h, int(inverse), lam, eps_prime, seed, rq_tol,
@@ -351,18 +364,19 @@ class SIConfig:
     lam: float = 0.0
     seed: int = 0
     tol_solve: float = 1e-10
-    tol_tune: float = 1e-7
+    tol_tune: float = 1e-6
     conv_tol: float = 1e-9
-    rq_tol: float = 1e-4
+    rq_tol: float = 1e-3
     max_outer: int = 0
     force: bool = False
     epoch_cap: int = 0
     monotone_slack: float = 10.0
+    lambda1_hint: float = 0.0
 
     def native(self) -> N.SiConfig:
         return N.SiConfig(self.k, self.p, self.eps, self.mu, self.delta, self.lam, self.seed, self.tol_solve,
                           self.tol_tune, self.conv_tol, self.rq_tol, self.max_outer, int(self.force),
-                          self.epoch_cap, self.monotone_slack)
+                          self.epoch_cap, self.monotone_slack, self.lambda1_hint)
 
 
 @dataclass

@@ -32,7 +32,7 @@ class OrcMat(C.Structure):
 class OrcSvrgParams(C.Structure):
     _fields_ = [("eta", C.c_double), ("m", C.c_int64), ("tol", C.c_double),
                 ("epoch_cap", C.c_int), ("monotone_slack", C.c_double),
-                ("root_seed", C.c_uint64)]
+                ("root_seed", C.c_uint64), ("lambda1_hint", C.c_double)]
 
 
 class OrcLedger(C.Structure):
@@ -46,11 +46,12 @@ class OrcSiConfig(C.Structure):
                 ("delta", C.c_double), ("lambda_", C.c_double), ("seed", C.c_uint64),
                 ("tol_solve", C.c_double), ("tol_tune", C.c_double), ("conv_tol", C.c_double),
                 ("rq_tol", C.c_double), ("max_outer", C.c_int), ("force", C.c_int),
-                ("epoch_cap", C.c_int), ("monotone_slack", C.c_double)]
+                ("epoch_cap", C.c_int), ("monotone_slack", C.c_double), ("lambda1_hint", C.c_double)]
 
 
 class OrcSiReport(C.Structure):
-    _fields_ = [("lambda_", C.c_double), ("lambda1_hat", C.c_double), ("tune_steps", C.c_int),
+    _fields_ = [("lambda_", C.c_double), ("lambda1_hat", C.c_double), ("lambda1_hint", C.c_double),
+                ("tune_steps", C.c_int),
                 ("tune_lambda", C.c_double * 64), ("tune_inv", C.c_double * 64),
                 ("outer_iterations", C.c_int), ("outer_cap", C.c_int), ("ledger", OrcLedger)]
 
@@ -164,10 +165,10 @@ class Oracle:
         return rc, w, idx
 
     def svrg_solve(self, m, lam, b, tol, seed=0, solve_id=0, eta=0.0, steps=0, epoch_cap=0,
-                   slack=10.0):
+                   slack=10.0, hint=0.0):
         b = c64(b)
         w = np.zeros_like(b)
-        prm = OrcSvrgParams(eta, steps, tol, epoch_cap, slack, seed)
+        prm = OrcSvrgParams(eta, steps, tol, epoch_cap, slack, seed, hint)
         ep, hl = C.c_int(0), C.c_int(0)
         hist = np.zeros(4096)
         rc = self.lib.orc_svrg_solve(C.byref(m), C.c_double(lam), b.shape[1], _ptr(b), _ptr(w),
@@ -277,7 +278,7 @@ class Reference:
 
 
 def default_si_config(k, p, *, eps=1e-8, mu=1.0, delta=0.0, lam=0.0, seed=0, tol_solve=1e-10,
-                      tol_tune=1e-7, conv_tol=1e-9, rq_tol=1e-4, max_outer=0, force=0,
-                      epoch_cap=0, slack=10.0):
+                      tol_tune=1e-6, conv_tol=1e-9, rq_tol=1e-3, max_outer=0, force=0,
+                      epoch_cap=0, slack=10.0, hint=0.0):
     return OrcSiConfig(k, p, eps, mu, delta, lam, seed, tol_solve, tol_tune, conv_tol, rq_tol,
-                       max_outer, force, epoch_cap, slack)
+                       max_outer, force, epoch_cap, slack, hint)
