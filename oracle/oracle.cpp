@@ -431,10 +431,11 @@ struct SolveResult {
 //   steps on the stream derive_seed(root, TAG_SVRG ^ (solve_id << 20) ^ e).
 SolveResult svrg_solve(const Mat& x, double lambda, const Block& b, Block& w,
                        const orc_svrg_params* prm, int64_t solve_id, orc_ledger* led,
-                       int nthreads) {
+                       int nthreads, const Block* guess = nullptr) {
   const int d = x.d(), n = x.n(), p = b.p;
   const SvrgSetup st = svrg_setup(x, lambda, prm);
-  w = Block(d, p);
+  const bool warm = guess != nullptr;
+  w = warm ? *guess : Block(d, p);
   std::vector<double> bnorm(p);
   for (int c = 0; c < p; ++c) {
     double acc = 0.0;
@@ -447,7 +448,7 @@ SolveResult svrg_solve(const Mat& x, double lambda, const Block& b, Block& w,
   std::vector<int32_t> idx;
   double best = INFINITY;
   for (int e = 0;; ++e) {
-    if (e > 0) {
+    if (e > 0 || warm) {
       gram_block(x, w, z, &y, nthreads);
       if (led) led->gram_applies += p;
     }
@@ -492,7 +493,8 @@ SolveResult svrg_solve(const Mat& x, double lambda, const Block& b, Block& w,
 // ---------------------------------------------------------------------------
 struct BlockOp {
   virtual ~BlockOp() = default;
-  virtual void apply(const Block& in, Block& out) = 0;
+  // `guess` (optional): warm start for operators that iterate
+  virtual void apply(const Block& in, Block& out, const Block* guess = nullptr) = 0;
 };
 
 struct GramOp : BlockOp {
@@ -500,7 +502,7 @@ struct GramOp : BlockOp {
   orc_ledger* led;
   int nthreads;
   GramOp(const Mat& xx, orc_ledger* l, int nt) : x(xx), led(l), nthreads(nt) {}
-  void apply(const Block& in, Block& out) override {
+  void apply(const Block& in, Block& out, const Block* = nullptr) override {
     gram_block(x, in, out, nullptr, nthreads);
     if (led) {
       led->gram_applies += in.p;
@@ -519,22 +521,51 @@ struct InverseOp : BlockOp {
   int nthreads;
   InverseOp(const Mat& xx, double lam, const orc_svrg_params& pr, int64_t* sc, orc_ledger* l, int nt)
       : x(xx), lambda(lam), prm(pr), solve_counter(sc), led(l), nthreads(nt) {}
-  void apply(const Block& in, Block& out) override {
-    svrg_solve(x, lambda, in, out, &prm, (*solve_counter)++, led, nthreads);
+  void apply(const Block& in, Block& out, const Block* guess = nullptr) override {
+    svrg_solve(x, lambda, in, out, &prm, (*solve_counter)++, led, nthreads, guess);
     if (led) led->operator_applies += in.p;
   }
 };
 
-// ||S S^T - S' S'^T||_F = sqrt(2) |S' - S (S^T S')|_F (stable form).
-double projector_diff(const Block& s, const Block& s2) {
-  const int d = s.d, p = s.p;
-  std::vector<double> g(static_cast<size_t>(p) * p, 0.0);
-  for (int a = 0; a < p; ++a)
-    for (int b = 0; b < p; ++b) {
+// G = Aᵀ B (p x q, row-major), sequential row sums
+std::vector<double> gram_ab(const Block& a, const Block& b) {
+  std::vector<double> g(static_cast<size_t>(a.p) * b.p, 0.0);
+  for (int i = 0; i < a.p; ++i)
+    for (int j = 0; j < b.p; ++j) {
       double acc = 0.0;
-      for (int i = 0; i < d; ++i) acc += s.at(i, a) * s2.at(i, b);
-      g[static_cast<size_t>(a) * p + b] = acc;
+      for (int r = 0; r < a.d; ++r) acc += a.at(r, i) * b.at(r, j);
+      g[static_cast<size_t>(i) * b.p + j] = acc;
     }
+  return g;
+}
+
+// Warm start for the next solve D⁻¹ S_new: in the converged
+// limit D⁻¹ S_new = S_new (S_newᵀ Y)(S_oldᵀ S_new), with Y = D⁻¹ S_old.
+Block warm_guess(const Block& s_new, const Block& y, const std::vector<double>& g_old_new) {
+  const int p = s_new.p;
+  const std::vector<double> r = gram_ab(s_new, y);
+  std::vector<double> rg(static_cast<size_t>(p) * p, 0.0);
+  for (int i = 0; i < p; ++i)
+    for (int j = 0; j < p; ++j) {
+      double acc = 0.0;
+      for (int k = 0; k < p; ++k) acc += r[static_cast<size_t>(i) * p + k] * g_old_new[static_cast<size_t>(k) * p + j];
+      rg[static_cast<size_t>(i) * p + j] = acc;
+    }
+  Block w(s_new.d, p);
+  for (int r0 = 0; r0 < s_new.d; ++r0)
+    for (int j = 0; j < p; ++j) {
+      double acc = 0.0;
+      for (int k = 0; k < p; ++k) acc += s_new.at(r0, k) * rg[static_cast<size_t>(k) * p + j];
+      w.at(r0, j) = acc;
+    }
+  return w;
+}
+
+// ||S S^T - S' S'^T||_F = sqrt(2) |S' - S (S^T S')|_F (stable form).
+double projector_diff(const Block& s, const Block& s2, std::vector<double>* g_out = nullptr) {
+  const int d = s.d, p = s.p;
+  std::vector<double> g = gram_ab(s, s2);
+  if (g_out) *g_out = g;
   double tot = 0.0;
   for (int b = 0; b < p; ++b)
     for (int i = 0; i < d; ++i) {
@@ -564,15 +595,21 @@ Block orth_init(int d, int p, uint64_t seed) {
 Block subspace_iterate(BlockOp& op, int d, int p, int L, uint64_t seed, double conv_tol,
                        int* iters, orc_ledger* led) {
   Block s = orth_init(d, p, seed);
-  Block y;
+  Block y, guess;
+  bool have_guess = false;
   int it = 0;
+  std::vector<double> g;
   for (int l = 1; l <= L; ++l) {
-    op.apply(s, y);
-    qr_inplace(y);
+    op.apply(s, y, have_guess ? &guess : nullptr);
+    Block q = y;
+    qr_inplace(q);
     if (led) led->qr_factorizations++;
     it = l;
-    const bool stop = conv_tol > 0.0 && projector_diff(s, y) <= conv_tol;
-    s = y;
+    const double diff = projector_diff(s, q, &g);
+    const bool stop = conv_tol > 0.0 && diff <= conv_tol;
+    guess = warm_guess(q, y, g);
+    have_guess = true;
+    s = q;
     if (stop) break;
   }
   if (iters) *iters = it;
@@ -587,20 +624,24 @@ double estimate_top(BlockOp& op, int d, double eps_prime, uint64_t seed, double 
                     orc_ledger* led) {
   const int L = static_cast<int>(std::ceil(4.0 / eps_prime * std::log(d / eps_prime)));
   Block s = orth_init(d, 1, seed);
-  Block y;
+  Block y, guess;
+  bool have_guess = false;
   double prev = 0.0, theta = 0.0;
   int it = 0;
   for (int l = 1; l <= L + 1; ++l) {
-    op.apply(s, y);
+    op.apply(s, y, have_guess ? &guess : nullptr);
     it = l;
     double acc = 0.0;
     for (int i = 0; i < d; ++i) acc += s.at(i, 0) * y.at(i, 0);
     theta = acc;
     if (l > 1 && std::fabs(theta - prev) <= rq_tol * std::fabs(theta)) break;
     if (l == L + 1) break;
-    qr_inplace(y);
+    Block q = y;
+    qr_inplace(q);
     if (led) led->qr_factorizations++;
-    s = y;
+    guess = warm_guess(q, y, gram_ab(s, q));
+    have_guess = true;
+    s = q;
     prev = theta;
   }
   if (iters) *iters = it;

@@ -439,8 +439,10 @@ void epoch_dev(Context& c, Matrix& X, int p, double* W, const double* C, const d
 }
 
 // Block solve (λI − XXᵀ)W = B with W0 = 0; B, W device blocks with ld = ldp(p).
+// warm = true: W holds the initial guess on entry, else W0 = 0.
 SvrgResult svrg_solve_dev(Context& c, Matrix& X, double lambda, int p, const double* B, double* W,
-                          const gaplra_svrg_params& prm_in, int64_t solve_id, SvrgResult* partial = nullptr) {
+                          const gaplra_svrg_params& prm_in, int64_t solve_id, SvrgResult* partial = nullptr,
+                          bool warm = false) {
   const SvrgParams prm = resolve(c, X, lambda, prm_in);
   const int64_t ld = ldp_of(p), dp = X.d_pad();
   const size_t blk = static_cast<size_t>(dp) * ld;
@@ -452,15 +454,16 @@ SvrgResult svrg_solve_dev(Context& c, Matrix& X, double lambda, int p, const dou
   double* res = c.scal.ensure(8) + 1;
   // |B_c| via the anchor kernel with W = Z = 0, λ = 0  (M = −B).
   launch_anchor(nullptr, nullptr, B, ld, static_cast<int>(dp), p, 0.0, 0.0, nullptr, part, nullptr, bn, res, c.st);
-  GAPLRA_CUDA_CHECK(cudaMemsetAsync(W, 0, blk * sizeof(double), c.st));
+  if (!warm) GAPLRA_CUDA_CHECK(cudaMemsetAsync(W, 0, blk * sizeof(double), c.st));
   SvrgResult local;
   SvrgResult& out = partial ? *partial : local;
   out = SvrgResult{};
   double best = INFINITY;
   for (int e = 0;; ++e) {
-    if (e > 0) gram_block_dev(c, X, p, W, ld, Z, ld, Y, ld);
+    const bool zero = e == 0 && !warm;
+    if (!zero) gram_block_dev(c, X, p, W, ld, Z, ld, Y, ld);
     else GAPLRA_CUDA_CHECK(cudaMemsetAsync(Y, 0, static_cast<size_t>(X.n) * ld * sizeof(double), c.st));
-    launch_anchor(e > 0 ? W : nullptr, e > 0 ? Z : nullptr, B, ld, static_cast<int>(dp), p, lambda, prm.eta, C, part,
+    launch_anchor(zero ? nullptr : W, zero ? nullptr : Z, B, ld, static_cast<int>(dp), p, lambda, prm.eta, C, part,
                   bn, nullptr, res, c.st);
     const double r = c.read_scalar(res);
     out.history.push_back(r);
@@ -484,15 +487,16 @@ SvrgResult svrg_solve_dev(Context& c, Matrix& X, double lambda, int p, const dou
 // ---------------------------------------------------------------------------
 struct Op {
   virtual ~Op() = default;
-  // out = op(in), device blocks with ld = ldp(p)
-  virtual void apply(const double* in, double* out, int p) = 0;
+  // out = op(in), device blocks with ld = ldp(p); `guess` (optional, may be
+  // consumed) warm-starts iterative operators
+  virtual void apply(const double* in, double* out, int p, const double* guess = nullptr) = 0;
 };
 
 struct GramOp : Op {
   Context& c;
   Matrix& X;
   GramOp(Context& cc, Matrix& xx) : c(cc), X(xx) {}
-  void apply(const double* in, double* out, int p) override {
+  void apply(const double* in, double* out, int p, const double* = nullptr) override {
     gram_block_dev(c, X, p, in, ldp_of(p), out, ldp_of(p), nullptr, 0);
     c.led.operator_applies += p;
   }
@@ -506,8 +510,11 @@ struct InverseOp : Op {
   int64_t* counter;
   InverseOp(Context& cc, Matrix& xx, double lam, const gaplra_svrg_params& pr, int64_t* sc)
       : c(cc), X(xx), lambda(lam), prm(pr), counter(sc) {}
-  void apply(const double* in, double* out, int p) override {
-    svrg_solve_dev(c, X, lambda, p, in, out, prm, (*counter)++);
+  void apply(const double* in, double* out, int p, const double* guess = nullptr) override {
+    if (guess)
+      GAPLRA_CUDA_CHECK(cudaMemcpyAsync(out, guess, static_cast<size_t>(X.d_pad()) * ldp_of(p) * sizeof(double),
+                                        cudaMemcpyDeviceToDevice, c.st));
+    svrg_solve_dev(c, X, lambda, p, in, out, prm, (*counter)++, nullptr, guess != nullptr);
     c.led.operator_applies += p;
   }
 };
@@ -528,10 +535,10 @@ void orth_init(Context& c, int d, int64_t dp, int p, uint64_t seed, double* S) {
   }
 }
 
-// |S Sᵀ − S' S'ᵀ|_F = sqrt(2) |S' − S (Sᵀ S')|_F
+// |S Sᵀ − S' S'ᵀ|_F = sqrt(2) |S' − S (Sᵀ S')|_F ; G = Sᵀ S' is left in c.small
 double projector_diff_dev(Context& c, const double* S, const double* S2, int d, int p) {
   const int64_t ld = ldp_of(p);
-  double* G = c.small.ensure(static_cast<size_t>(64) * 64 + 8);
+  double* G = c.small.ensure(static_cast<size_t>(64) * 64 * 4 + 8);
   double* part = c.tmp.ensure(static_cast<size_t>(small_gram_parts(d)) * 64 * 64 + 8);
   launch_small_gram(S, ld, p, S2, ld, p, d, part, G, c.st);
   double* R = c.tbuf.ensure(static_cast<size_t>(round4(d)) * ld);
@@ -542,19 +549,40 @@ double projector_diff_dev(Context& c, const double* S, const double* S2, int d, 
   return std::sqrt(2.0 * c.read_scalar(out));
 }
 
-// Alg. 1 with projector early stop; returns the final S in `S` (device).
+// guess = Q (Qᵀ Y) G  with G = S_oldᵀ Q already in c.small (oracle.cpp warm_guess)
+void warm_guess_dev(Context& c, const double* Q, const double* Y, int d, int p, double* guess) {
+  const int64_t ld = ldp_of(p);
+  double* G = c.small.p;
+  double* R = G + 64 * 64;
+  double* RG = R + 64 * 64;
+  double* part = c.tmp.ensure(static_cast<size_t>(small_gram_parts(d)) * 64 * 64 + 8);
+  launch_small_gram(Q, ld, p, Y, ld, p, d, part, R, c.st);
+  launch_small_mul(R, p, p, G, p, p, p, 0.0, 1.0, RG, p, c.st);
+  launch_small_mul(Q, ld, p, RG, p, p, d, 0.0, 1.0, guess, ld, c.st);
+}
+
+// Alg. 1 with projector early stop and warm-started solves; final S in `S`.
 int subspace_iterate_dev(Context& c, Op& op, int d, int64_t dp, int p, int L, uint64_t seed, double conv_tol,
                          double* S) {
   const int64_t ld = ldp_of(p);
+  const size_t blk = static_cast<size_t>(dp) * ld;
   orth_init(c, d, dp, p, seed, S);
-  double* Yb = c.sbuf.ensure(static_cast<size_t>(dp) * ld);
+  DBuf<double> qb, gb;
+  double* Yb = c.sbuf.ensure(blk);
+  double* Q = qb.ensure(blk);
+  double* guess = gb.ensure(blk);
+  bool have_guess = false;
   int it = 0;
   for (int l = 1; l <= L; ++l) {
-    op.apply(S, Yb, p);
-    qr_dev(c, Yb, ld, d, p);
+    op.apply(S, Yb, p, have_guess ? guess : nullptr);
+    GAPLRA_CUDA_CHECK(cudaMemcpyAsync(Q, Yb, blk * sizeof(double), cudaMemcpyDeviceToDevice, c.st));
+    qr_dev(c, Q, ld, d, p);
     it = l;
-    const bool stop = conv_tol > 0.0 && projector_diff_dev(c, S, Yb, d, p) <= conv_tol;
-    GAPLRA_CUDA_CHECK(cudaMemcpyAsync(S, Yb, static_cast<size_t>(dp) * ld * sizeof(double), cudaMemcpyDeviceToDevice, c.st));
+    const double diff = projector_diff_dev(c, S, Q, d, p);
+    const bool stop = conv_tol > 0.0 && diff <= conv_tol;
+    warm_guess_dev(c, Q, Yb, d, p, guess);
+    have_guess = true;
+    GAPLRA_CUDA_CHECK(cudaMemcpyAsync(S, Q, blk * sizeof(double), cudaMemcpyDeviceToDevice, c.st));
     if (stop) break;
   }
   c.led.outer_iterations += it;
@@ -565,23 +593,31 @@ int subspace_iterate_dev(Context& c, Op& op, int d, int64_t dp, int p, int L, ui
 double estimate_top_dev(Context& c, Op& op, int d, int64_t dp, double eps_prime, uint64_t seed, double rq_tol,
                         int* iters) {
   const int L = static_cast<int>(std::ceil(4.0 / eps_prime * std::log(d / eps_prime)));
-  DBuf<double> s, y;
+  DBuf<double> s, y, q, gs;
   double* S = s.ensure(static_cast<size_t>(dp));
   double* Yb = y.ensure(static_cast<size_t>(dp));
+  double* Q = q.ensure(static_cast<size_t>(dp));
+  double* guess = gs.ensure(static_cast<size_t>(dp));
   orth_init(c, d, dp, 1, seed, S);
-  double* G = c.small.ensure(static_cast<size_t>(64) * 64 + 8);
+  double* G = c.small.ensure(static_cast<size_t>(64) * 64 * 4 + 8);
   double* part = c.tmp.ensure(static_cast<size_t>(small_gram_parts(d)) * 64 * 64 + 8);
+  double* th = G + 3 * 64 * 64;
   double prev = 0.0, theta = 0.0;
+  bool have_guess = false;
   int it = 0;
   for (int l = 1; l <= L + 1; ++l) {
-    op.apply(S, Yb, 1);
+    op.apply(S, Yb, 1, have_guess ? guess : nullptr);
     it = l;
-    launch_small_gram(S, 1, 1, Yb, 1, 1, d, part, G, c.st);
-    theta = c.read_scalar(G);
+    launch_small_gram(S, 1, 1, Yb, 1, 1, d, part, th, c.st);
+    theta = c.read_scalar(th);
     if (l > 1 && std::fabs(theta - prev) <= rq_tol * std::fabs(theta)) break;
     if (l == L + 1) break;
-    qr_dev(c, Yb, 1, d, 1);
-    std::swap(S, Yb);
+    GAPLRA_CUDA_CHECK(cudaMemcpyAsync(Q, Yb, static_cast<size_t>(dp) * sizeof(double), cudaMemcpyDeviceToDevice, c.st));
+    qr_dev(c, Q, 1, d, 1);
+    launch_small_gram(S, 1, 1, Q, 1, 1, d, part, G, c.st);  // G = s_oldᵀ q
+    warm_guess_dev(c, Q, Yb, d, 1, guess);
+    have_guess = true;
+    std::swap(S, Q);
     prev = theta;
   }
   if (iters) *iters = it;
@@ -650,10 +686,10 @@ void restricted_projection_dev(Context& c, Matrix& X, const double* S, int p, in
   DBuf<double> z;
   double* Z = z.ensure(static_cast<size_t>(dp) * ld);
   gram_block_dev(c, X, p, S, ld, Z, ld, nullptr, 0);
-  double* H = c.small.ensure(static_cast<size_t>(64) * 64 + 8);
+  double* H = c.small.ensure(static_cast<size_t>(64) * 64 * 4 + 8);
   double* part = c.tmp.ensure(static_cast<size_t>(small_gram_parts(d)) * 64 * 64 + 8);
   launch_small_gram(S, ld, p, Z, ld, p, d, part, H, c.st);
-  DBuf<double> vv;
+  DBuf<double> vv;  // (H lives in c.small)
   double* vals = vv.ensure(static_cast<size_t>(p) + static_cast<size_t>(p) * p);
   double* vecs = vals + p;
   launch_jacobi(H, p, vals, vecs, c.st);
@@ -1015,7 +1051,7 @@ int gaplra_orthonormality_defect(gaplra_ctx* ctx, int d, int p, const double* q,
     DBuf<double> b;
     b.ensure(static_cast<size_t>(round4(d)) * ld);
     upload_block(c, q, d, p, b.p, ld);
-    double* G = c.small.ensure(64 * 64 + 8);
+    double* G = c.small.ensure(static_cast<size_t>(64) * 64 * 4 + 8);
     double* part = c.tmp.ensure(static_cast<size_t>(small_gram_parts(d)) * 64 * 64 + 8);
     launch_small_gram(b.p, ld, p, b.p, ld, p, d, part, G, c.st);
     std::vector<double> h(static_cast<size_t>(p) * p);
