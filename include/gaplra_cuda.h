@@ -112,9 +112,10 @@ typedef struct {
 
 /* Live per-kernel-class device time (CUDA events on the context stream) and
  * the algorithmic bytes / flops of those launches.
- * Classes: 0 gram pass X(XᵀW), 1 SVRG epoch steps, 2 H = XᵀC pass,
- * 3 index stream, 4 QR (MGS2), 5 anchor epilogue, 6 per-block Gram/T precompute. */
-#define GAPLRA_PROF_CLASSES 8
+ * Classes: 0 gram pass X(XᵀW) (p > 1), 1 SVRG epoch chain (p > 1), 2 H = XᵀC
+ * pass, 3 index stream, 4 QR (MGS2), 5 anchor epilogue, 6 per-block Gram/T
+ * precompute, 7 gram pass (p = 1), 8 SVRG epoch chain (p = 1). */
+#define GAPLRA_PROF_CLASSES 12
 typedef struct {
   double ms[GAPLRA_PROF_CLASSES];
   uint64_t count[GAPLRA_PROF_CLASSES];
@@ -131,6 +132,8 @@ GAPLRA_API int gaplra_ctx_synchronize(gaplra_ctx* ctx);
 GAPLRA_API int gaplra_ledger_get(const gaplra_ctx* ctx, gaplra_ledger* out);
 GAPLRA_API int gaplra_ledger_reset(gaplra_ctx* ctx);
 GAPLRA_API int gaplra_version(void);
+/* number of kernels this library has launched (process-wide) */
+GAPLRA_API unsigned long long gaplra_launch_count(void);
 GAPLRA_API int gaplra_profile_enable(gaplra_ctx* ctx, int on);
 GAPLRA_API int gaplra_profile_get(gaplra_ctx* ctx, gaplra_profile* out);
 GAPLRA_API int gaplra_profile_reset(gaplra_ctx* ctx);

@@ -52,19 +52,21 @@ class SiReport(C.Structure):
                 ("ms_rayleigh_ritz", C.c_double), ("ms_total", C.c_double)]
 
 
-PROF_CLASSES = ["gram", "epoch", "h_pass", "index", "qr", "anchor", "block_gram", "r7"]
+PROF_CLASSES = ["gram", "epoch", "h_pass", "index", "qr", "anchor", "block_gram", "gram_p1", "epoch_p1",
+                "r9", "r10", "r11"]
 
 
 class Profile(C.Structure):
-    _fields_ = [("ms", C.c_double * 8), ("count", C.c_uint64 * 8), ("bytes", C.c_double * 8),
-                ("flops", C.c_double * 8)]
+    _fields_ = [("ms", C.c_double * 12), ("count", C.c_uint64 * 12), ("bytes", C.c_double * 12),
+                ("flops", C.c_double * 12)]
 
     def as_dict(self):
         return {name: {"ms": self.ms[i], "count": int(self.count[i]), "bytes": self.bytes[i],
-                       "flops": self.flops[i]} for i, name in enumerate(PROF_CLASSES[:7])}
+                       "flops": self.flops[i]} for i, name in enumerate(PROF_CLASSES[:9])}
 
 
 _SIGS = {
+    "gaplra_launch_count": (C.c_ulonglong, []),
     "gaplra_profile_enable": (C.c_int, [C.c_void_p, C.c_int]),
     "gaplra_profile_get": (C.c_int, [C.c_void_p, C.POINTER(Profile)]),
     "gaplra_profile_reset": (C.c_int, [C.c_void_p]),
@@ -107,7 +109,7 @@ _SIGS = {
 
 def header_symbols() -> list[str]:
     """Every entry point include/gaplra_cuda.h declares."""
-    return re.findall(r"GAPLRA_API\s+(?:int|const char\*)\s+(gaplra_\w+)\(", HEADER.read_text())
+    return re.findall(r"GAPLRA_API\s+(?:int|const char\*|unsigned long long)\s+(gaplra_\w+)\(", HEADER.read_text())
 
 
 _LIB = None

@@ -39,7 +39,14 @@ struct Error : std::runtime_error {
     }                                                                                        \
   } while (0)
 
-#define GAPLRA_LAUNCH_CHECK() GAPLRA_CUDA_CHECK(cudaGetLastError())
+// Every kernel launch of the library goes through this check, which also
+// counts it (gaplra_launch_count in the C ABI).
+unsigned long long& launch_counter();
+#define GAPLRA_LAUNCH_CHECK()                          \
+  do {                                                 \
+    ++::gaplra_cuda::launch_counter();                 \
+    GAPLRA_CUDA_CHECK(cudaGetLastError());             \
+  } while (0)
 
 constexpr int kWarp = 32;
 

@@ -23,6 +23,11 @@
 
 namespace gaplra_cuda {
 
+unsigned long long& launch_counter() {
+  static unsigned long long n = 0;
+  return n;
+}
+
 template <class T>
 struct DBuf {
   T* p = nullptr;
@@ -147,7 +152,18 @@ struct Matrix {
 
 // Live per-kernel-class timing (CUDA events on the launching stream), with the
 // algorithmic bytes / flops of each launch for the roofline report.
-enum ProfClass { kProfGram = 0, kProfEpoch, kProfHPass, kProfIndex, kProfQr, kProfAnchor, kProfBlockGram, kProfClasses };
+enum ProfClass {
+  kProfGram = 0,  // X(XᵀW) pass, p > 1
+  kProfEpoch,     // SVRG epoch chain, p > 1
+  kProfHPass,
+  kProfIndex,
+  kProfQr,
+  kProfAnchor,
+  kProfBlockGram,
+  kProfGramP1,   // X(Xᵀv) pass, p = 1 (Alg. 3 / tuning)
+  kProfEpochP1,  // SVRG epoch chain, p = 1
+  kProfClasses
+};
 constexpr int kEpochBlock = 16;  // s-step block (svrg.cu kBlock)
 
 struct ProfPending {
@@ -282,7 +298,7 @@ void gram_block_dev(Context& c, const Matrix& X, int p, const double* W, int64_t
     Y = c.ybuf.ensure(static_cast<size_t>(X.n) * ldy);
   }
   const double xbytes = X.kind == 0 ? 8.0 * X.d * X.n : 12.0 * X.nnz + 8.0 * (X.n + 1);
-  Prof prof(c, kProfGram, xbytes, 4.0 * X.nnz * p);
+  Prof prof(c, p > 1 ? kProfGram : kProfGramP1, xbytes, 4.0 * X.nnz * p);
   if (X.kind == 0) {
     const DenseX D = X.dense();
     GramWork w;
@@ -403,7 +419,7 @@ void epoch_dev(Context& c, Matrix& X, int p, double* W, const double* C, const d
     DBuf<long long> dbg;
     if (timing) a.dbg = dbg.ensure(static_cast<size_t>(cfg.cluster) * cfg.groups * 8);
     {
-      Prof prof(c, kProfEpoch, col_bytes * m, 4.0 * col_nnz * p * m);
+      Prof prof(c, p > 1 ? kProfEpoch : kProfEpochP1, col_bytes * m, 4.0 * col_nnz * p * m);
       launch_svrg_epoch_dense(a, cfg, c.st);
     }
     if (timing) {
@@ -433,7 +449,7 @@ void epoch_dev(Context& c, Matrix& X, int p, double* W, const double* C, const d
     a.ldy = ld;
     a.rho = rho;
     a.eta_n = eta_n;
-    Prof prof(c, kProfEpoch, col_bytes * m, 4.0 * col_nnz * p * m);
+    Prof prof(c, p > 1 ? kProfEpoch : kProfEpochP1, col_bytes * m, 4.0 * col_nnz * p * m);
     launch_svrg_epoch_sparse(a, c.st);
   }
 }
@@ -817,6 +833,8 @@ int gaplra_ledger_reset(gaplra_ctx* ctx) {
   ctx->c.led = gaplra_ledger{};
   return GAPLRA_OK;
 }
+
+unsigned long long gaplra_launch_count(void) { return launch_counter(); }
 
 int gaplra_profile_enable(gaplra_ctx* ctx, int on) {
   if (!ctx) return GAPLRA_CONTRACT_VIOLATION;

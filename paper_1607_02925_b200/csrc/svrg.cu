@@ -758,6 +758,7 @@ void launch_chain_pc(const EpochArgs& a, const EpochConfig& cfg, cudaStream_t st
   args.groups = cfg.groups;
   args.slab_len = epoch_slab_len(cfg);
   GAPLRA_CUDA_CHECK(cudaLaunchKernelEx(&lc, kern, args));
+  GAPLRA_LAUNCH_CHECK();
 }
 
 void launch_svrg_epoch_dense(const EpochArgs& a, const EpochConfig& cfg, cudaStream_t st) {

@@ -177,6 +177,14 @@ class DeviceMatrix:
         return cls(ctx, h)
 
     @classmethod
+    def from_host_pointer(cls, ptr: int, d: int, n: int, ldx: int, ctx: Context | None = None):
+        """Copy a host column-major X (e.g. pinned memory) into HBM."""
+        ctx = ctx or default_context()
+        h = C.c_void_p()
+        ctx.check(ctx.lib.gaplra_matrix_dense(ctx.h, d, n, C.c_void_p(ptr), ldx, 0, C.byref(h)))
+        return cls(ctx, h)
+
+    @classmethod
     def from_device(cls, ptr: int, d: int, n: int, ldx: int, ctx: Context | None = None, keep=None):
         """Borrow a device column-major X (ldx % 4 == 0); `keep` holds its owner."""
         ctx = ctx or default_context()
