@@ -7,6 +7,7 @@
 #include "gram.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 
 namespace gaplra_cuda {
 
@@ -176,6 +177,211 @@ __global__ void __launch_bounds__(kXyThreads) k_xy(const double* __restrict__ X,
     }
 }
 
+__device__ __forceinline__ void mma884(double& c0, double& c1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+      : "+d"(c0), "+d"(c1)
+      : "d"(a), "d"(b));
+}
+
+// smem pitch (doubles) for a KC x (8*NT) B-operand tile: ≡ 8 (mod 16) keeps the
+// 4 rows x 8 columns of an m8n8k4 B fragment on distinct bank pairs.
+template <int NT>
+__host__ __device__ constexpr int b_pitch() {
+  return (8 * NT) % 16 == 8 ? 8 * NT : 8 * NT + 8;
+}
+
+// ---------------------------------------------------------------------------
+// Y = Xᵀ W on the FP64 tensor path (DMMA m8n8k4).  M = columns of X (a warp owns
+// MW m-tiles of 8 columns), N = right-hand sides (NT n-tiles of 8, zero padded),
+// K = rows of X.  The CTA stages each KC-row chunk of W in shared memory (double
+// buffered, shared by its 8 warps).  A fragments come straight from X with one
+// 256-bit load per lane per 4 k-steps: lane (g, q) loads rows 16kb+4q..+3 of its
+// column, so k-step (kb, u) contracts rows {16kb + 4q' + u}; the B fragment uses
+// the same permutation.
+// ---------------------------------------------------------------------------
+constexpr int kMmaThreads = 256;
+constexpr int kKC = 64;  // rows of W per smem chunk (4 groups of 16)
+
+template <int NT, int MW>
+__global__ void __launch_bounds__(kMmaThreads) k_xtw_mma(const double* __restrict__ X, int64_t ldx, int n,
+                                                         int rows_per_split, int rows_total,
+                                                         const double* __restrict__ W, int64_t ldw, int pc,
+                                                         double* __restrict__ out, int64_t ldo,
+                                                         size_t split_stride) {
+  constexpr int BP = b_pitch<NT>();
+  __shared__ __align__(16) double Ws[2][kKC * BP];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int gq = lane >> 2, tq = lane & 3;
+  const int col0 = (blockIdx.x * (kMmaThreads / 32) + warp) * (8 * MW);
+  const int r0 = blockIdx.y * rows_per_split;
+  const int r1 = min(r0 + rows_per_split, rows_total);
+  double acc[MW][NT][2];
+#pragma unroll
+  for (int mt = 0; mt < MW; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+  const double* xc[MW];
+  bool live[MW];
+#pragma unroll
+  for (int mt = 0; mt < MW; ++mt) {
+    const int col = col0 + mt * 8 + gq;
+    live[mt] = col < n;
+    xc[mt] = X + static_cast<int64_t>(live[mt] ? col : 0) * ldx + 4 * tq;
+  }
+  auto stage_w = [&](int buf, int rbase) {
+    for (int e = threadIdx.x; e < kKC * 8 * NT; e += kMmaThreads) {
+      const int rr = e / (8 * NT), c = e - rr * (8 * NT);
+      const int r = rbase + rr;
+      Ws[buf][rr * BP + c] = (c < pc && r < r1) ? __ldg(W + static_cast<int64_t>(r) * ldw + c) : 0.0;
+    }
+  };
+  int buf = 0;
+  if (r0 < r1) stage_w(0, r0);
+  __syncthreads();
+  for (int rb = r0; rb < r1; rb += kKC) {
+    if (rb + kKC < r1) stage_w(buf ^ 1, rb + kKC);
+    const double* ws = Ws[buf];
+    const int nkb = (min(kKC, r1 - rb) + 15) / 16;
+    double av[4][MW][4];
+#pragma unroll
+    for (int kb = 0; kb < 4; ++kb)
+#pragma unroll
+      for (int mt = 0; mt < MW; ++mt) {
+        if (kb < nkb && rb + 16 * kb + 4 * tq < r1) {  // 4-row groups never straddle r1 (multiples of 4)
+          asm("ld.global.nc.L1::no_allocate.v4.f64 {%0,%1,%2,%3}, [%4];"
+              : "=d"(av[kb][mt][0]), "=d"(av[kb][mt][1]), "=d"(av[kb][mt][2]), "=d"(av[kb][mt][3])
+              : "l"(xc[mt] + rb + 16 * kb));
+        } else {
+          av[kb][mt][0] = av[kb][mt][1] = av[kb][mt][2] = av[kb][mt][3] = 0.0;
+        }
+      }
+#pragma unroll
+    for (int kb = 0; kb < 4; ++kb) {
+      if (kb >= nkb) break;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const double* wr = ws + (16 * kb + 4 * tq + u) * BP + gq;
+        double bfr[NT];
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) bfr[nt] = wr[nt * 8];
+#pragma unroll
+        for (int mt = 0; mt < MW; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) mma884(acc[mt][nt][0], acc[mt][nt][1], av[kb][mt][u], bfr[nt]);
+      }
+    }
+    __syncthreads();
+    buf ^= 1;
+  }
+  double* o = out + blockIdx.y * split_stride;
+#pragma unroll
+  for (int mt = 0; mt < MW; ++mt) {
+    const int col = col0 + mt * 8 + gq;
+    if (col >= n) continue;
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      const int c = nt * 8 + 2 * tq;
+      double* dst = o + static_cast<int64_t>(col) * ldo + c;
+      if (c + 1 < pc) {
+        dst[0] = acc[mt][nt][0];
+        dst[1] = acc[mt][nt][1];
+      } else if (c < pc) {
+        dst[0] = acc[mt][nt][0];
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Z = X Y on the FP64 tensor path.  M = rows of X (a warp owns MW = 4 m-tiles:
+// 32 rows, loaded 2 consecutive rows per lane with a 128-bit load, so tile
+// pairs hold the even / odd rows of 16), N = NT n-tiles, K = columns of X in
+// KC-column chunks whose Y rows are staged in shared memory.  Column splits
+// write partials (fixed-order sum afterwards).
+// ---------------------------------------------------------------------------
+template <int NT>
+__global__ void __launch_bounds__(kMmaThreads) k_xy_mma(const double* __restrict__ X, int64_t ldx, int rows_total,
+                                                        int cols_per_split, int n, const double* __restrict__ Y,
+                                                        int64_t ldy, int pc, double* __restrict__ out, int64_t ldo,
+                                                        size_t split_stride) {
+  constexpr int BP = b_pitch<NT>();
+  constexpr int MW = 4;
+  __shared__ __align__(16) double Ys[2][kKC * BP];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int gq = lane >> 2, tq = lane & 3;
+  const int rbase = blockIdx.x * (kMmaThreads / 32) * 32 + warp * 32;  // 32 rows per warp
+  const int j0 = blockIdx.y * cols_per_split;
+  const int j1 = min(j0 + cols_per_split, n);
+  double acc[MW][NT][2];
+#pragma unroll
+  for (int mt = 0; mt < MW; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+  // lane's two row pairs: rows rbase + 16h + 2g + {0, 1}, h = 0, 1
+  const bool live0 = rbase + 2 * gq + 1 < rows_total, live1 = rbase + 16 + 2 * gq + 1 < rows_total;
+  const double* xr0 = X + (live0 ? rbase + 2 * gq : 0);
+  const double* xr1 = X + (live1 ? rbase + 16 + 2 * gq : 0);
+  auto stage_y = [&](int buf, int jb) {
+    for (int e = threadIdx.x; e < kKC * 8 * NT; e += kMmaThreads) {
+      const int jj = e / (8 * NT), c = e - jj * (8 * NT);
+      const int j = jb + jj;
+      Ys[buf][jj * BP + c] = (c < pc && j < j1) ? __ldg(Y + static_cast<int64_t>(j) * ldy + c) : 0.0;
+    }
+  };
+  int buf = 0;
+  if (j0 < j1) stage_y(0, j0);
+  __syncthreads();
+  for (int jb = j0; jb < j1; jb += kKC) {
+    if (jb + kKC < j1) stage_y(buf ^ 1, jb + kKC);
+    const double* ys = Ys[buf];
+    const int nk = min(kKC, j1 - jb);
+    for (int k0 = 0; k0 < nk; k0 += 16) {
+      double2 a0[4], a1[4];
+#pragma unroll
+      for (int s4 = 0; s4 < 4; ++s4) {
+        const int j = jb + k0 + 4 * s4 + tq;
+        const bool ok = k0 + 4 * s4 + tq < nk;
+        a0[s4] = ok ? ldg2(xr0 + static_cast<int64_t>(j) * ldx) : make_double2(0.0, 0.0);
+        a1[s4] = ok ? ldg2(xr1 + static_cast<int64_t>(j) * ldx) : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int s4 = 0; s4 < 4; ++s4) {
+        const double* yr = ys + (k0 + 4 * s4 + tq) * BP + gq;
+        double bfr[NT];
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) bfr[nt] = yr[nt * 8];
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          mma884(acc[0][nt][0], acc[0][nt][1], a0[s4].x, bfr[nt]);  // even rows of 0..15
+          mma884(acc[1][nt][0], acc[1][nt][1], a0[s4].y, bfr[nt]);  // odd rows of 0..15
+          mma884(acc[2][nt][0], acc[2][nt][1], a1[s4].x, bfr[nt]);  // even rows of 16..31
+          mma884(acc[3][nt][0], acc[3][nt][1], a1[s4].y, bfr[nt]);  // odd rows of 16..31
+        }
+      }
+    }
+    __syncthreads();
+    buf ^= 1;
+  }
+  double* o = out + blockIdx.y * split_stride;
+#pragma unroll
+  for (int mt = 0; mt < MW; ++mt) {
+    // C fragment row index gq of tile mt -> physical row
+    const int row = rbase + 16 * (mt >> 1) + 2 * gq + (mt & 1);
+    if (row >= rows_total) continue;
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      const int c = nt * 8 + 2 * tq;
+      double* dst = o + static_cast<int64_t>(row) * ldo + c;
+      if (c + 1 < pc) {
+        dst[0] = acc[mt][nt][0];
+        dst[1] = acc[mt][nt][1];
+      } else if (c < pc) {
+        dst[0] = acc[mt][nt][0];
+      }
+    }
+  }
+}
+
 int sm_count() {
   static int sms = 0;
   if (!sms) {
@@ -268,6 +474,72 @@ void xy_chunk(const DenseX& X, const double* Y, int64_t ldy, int pc, double* Z, 
   GAPLRA_LAUNCH_CHECK();
   k_sum_splits<<<sm_count() * 4, 256, 0, st>>>(work.part, pl.s, stride, rows_total, pc, pc, Z, ldz);
   GAPLRA_LAUNCH_CHECK();
+}
+
+// ---- tensor-path launchers (pc >= 3) ----------------------------------------
+template <int NT>
+void xtw_mma_chunk(const DenseX& X, const double* W, int64_t ldw, int pc, double* Y, int64_t ldy, GramWork& work,
+                   cudaStream_t st, int rs, int rows_per_split) {
+  constexpr int MW = 2;
+  const int rows_total = static_cast<int>(X.ld);
+  const int col_tiles = static_cast<int>(ceil_div(X.n, (kMmaThreads / 32) * 8 * MW));
+  dim3 grid(col_tiles, rs);
+  if (rs == 1) {
+    k_xtw_mma<NT, MW><<<grid, kMmaThreads, 0, st>>>(X.x, X.ld, X.n, rows_per_split, rows_total, W, ldw, pc, Y, ldy, 0);
+    GAPLRA_LAUNCH_CHECK();
+    return;
+  }
+  const size_t stride = static_cast<size_t>(X.n) * pc;
+  if (work.part_elems < stride * rs) throw Error(kContractViolation, "xtw_mma: workspace too small");
+  k_xtw_mma<NT, MW><<<grid, kMmaThreads, 0, st>>>(X.x, X.ld, X.n, rows_per_split, rows_total, W, ldw, pc, work.part,
+                                                  pc, stride);
+  GAPLRA_LAUNCH_CHECK();
+  k_sum_splits<<<sm_count() * 4, 256, 0, st>>>(work.part, rs, stride, X.n, pc, pc, Y, ldy);
+  GAPLRA_LAUNCH_CHECK();
+}
+
+struct MmaPlan {
+  int rs, rows_per_split;   // xtw
+  int s, cols_per_split;    // xy
+};
+
+MmaPlan mma_plan(const DenseX& X) {
+  MmaPlan pl;
+  const int rows_total = static_cast<int>(X.ld);
+  const int col_tiles = static_cast<int>(ceil_div(X.n, (kMmaThreads / 32) * 16));
+  const int slots = sm_count() * 2;
+  int rs = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(3 * slots, col_tiles), rows_total / 512)));
+  pl.rows_per_split = static_cast<int>(ceil_div(ceil_div(rows_total, rs), kKC) * kKC);
+  pl.rs = static_cast<int>(ceil_div(rows_total, pl.rows_per_split));
+  const int row_blocks = static_cast<int>(ceil_div(rows_total, 256));
+  int s = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(3 * slots, row_blocks), ceil_div(X.n, 256))));
+  pl.cols_per_split = static_cast<int>(ceil_div(ceil_div(X.n, s), kKC) * kKC);
+  pl.s = static_cast<int>(ceil_div(X.n, pl.cols_per_split));
+  return pl;
+}
+
+template <int NT>
+void xy_mma_chunk(const DenseX& X, const double* Y, int64_t ldy, int pc, double* Z, int64_t ldz, GramWork& work,
+                  cudaStream_t st, int s, int cols_per_split) {
+  const int rows_total = static_cast<int>(X.ld);
+  dim3 grid(static_cast<unsigned>(ceil_div(rows_total, 256)), s);
+  const size_t stride = static_cast<size_t>(rows_total) * pc;
+  if (s == 1) {
+    k_xy_mma<NT><<<grid, kMmaThreads, 0, st>>>(X.x, X.ld, rows_total, cols_per_split, X.n, Y, ldy, pc, Z, ldz, 0);
+    GAPLRA_LAUNCH_CHECK();
+    return;
+  }
+  if (work.part_elems < stride * s) throw Error(kContractViolation, "xy_mma: workspace too small");
+  k_xy_mma<NT><<<grid, kMmaThreads, 0, st>>>(X.x, X.ld, rows_total, cols_per_split, X.n, Y, ldy, pc, work.part, pc,
+                                             stride);
+  GAPLRA_LAUNCH_CHECK();
+  k_sum_splits<<<sm_count() * 4, 256, 0, st>>>(work.part, s, stride, rows_total, pc, pc, Z, ldz);
+  GAPLRA_LAUNCH_CHECK();
+}
+
+bool use_mma(int pc) {
+  static const int mode = getenv("GAPLRA_GRAM_MMA") ? atoi(getenv("GAPLRA_GRAM_MMA")) : 1;
+  return mode != 0 && pc >= 3;
 }
 
 template <template <int> class F, class... A>
@@ -406,6 +678,12 @@ size_t gram_work_elems(const DenseX& X, int p) {
   size_t need = 0;
   for (int c0 = 0; c0 < p; c0 += 32) {
     const int pc = std::min(32, p - c0);
+    if (use_mma(pc)) {
+      const MmaPlan m = mma_plan(X);
+      if (m.rs > 1) need = std::max(need, static_cast<size_t>(m.rs) * X.n * pc);
+      if (m.s > 1) need = std::max(need, static_cast<size_t>(m.s) * X.ld * pc);
+      continue;
+    }
     const XtwPlan a = xtw_plan(X, pick_nc(pc));
     if (a.rs > 1) need = std::max(need, static_cast<size_t>(a.rs) * X.n * pc);
     const XyPlan b = xy_plan(X);
@@ -418,6 +696,16 @@ void launch_xtw(const DenseX& X, const double* W, int64_t ldw, int p, double* Y,
                 cudaStream_t st) {
   for (int c0 = 0; c0 < p; c0 += 32) {
     const int pc = std::min(32, p - c0);
+    if (use_mma(pc)) {
+      const MmaPlan m = mma_plan(X);
+      switch ((pc + 7) / 8) {
+        case 1: xtw_mma_chunk<1>(X, W + c0, ldw, pc, Y + c0, ldy, work, st, m.rs, m.rows_per_split); break;
+        case 2: xtw_mma_chunk<2>(X, W + c0, ldw, pc, Y + c0, ldy, work, st, m.rs, m.rows_per_split); break;
+        case 3: xtw_mma_chunk<3>(X, W + c0, ldw, pc, Y + c0, ldy, work, st, m.rs, m.rows_per_split); break;
+        default: xtw_mma_chunk<4>(X, W + c0, ldw, pc, Y + c0, ldy, work, st, m.rs, m.rows_per_split); break;
+      }
+      continue;
+    }
     dispatch_nc<XtwRun>(pick_nc(pc), X, W + c0, ldw, pc, Y + c0, ldy, work, st);
   }
 }
@@ -426,6 +714,16 @@ void launch_xy(const DenseX& X, const double* Y, int64_t ldy, int p, double* Z, 
                cudaStream_t st) {
   for (int c0 = 0; c0 < p; c0 += 32) {
     const int pc = std::min(32, p - c0);
+    if (use_mma(pc)) {
+      const MmaPlan m = mma_plan(X);
+      switch ((pc + 7) / 8) {
+        case 1: xy_mma_chunk<1>(X, Y + c0, ldy, pc, Z + c0, ldz, work, st, m.s, m.cols_per_split); break;
+        case 2: xy_mma_chunk<2>(X, Y + c0, ldy, pc, Z + c0, ldz, work, st, m.s, m.cols_per_split); break;
+        case 3: xy_mma_chunk<3>(X, Y + c0, ldy, pc, Z + c0, ldz, work, st, m.s, m.cols_per_split); break;
+        default: xy_mma_chunk<4>(X, Y + c0, ldy, pc, Z + c0, ldz, work, st, m.s, m.cols_per_split); break;
+      }
+      continue;
+    }
     dispatch_nc<XyRun>(pick_nc(pc), X, Y + c0, ldy, pc, Z + c0, ldz, work, st);
   }
 }

@@ -416,6 +416,8 @@ void epoch_dev(Context& c, Matrix& X, int p, double* W, const double* C, const d
       launch_block_prep(a, cfg, c.st);
     }
     static const bool timing = getenv("GAPLRA_EPOCH_TIMING") != nullptr;
+    static const int skip = getenv("GAPLRA_EPOCH_SKIP") ? atoi(getenv("GAPLRA_EPOCH_SKIP")) : 0;
+    a.skip = skip;
     DBuf<long long> dbg;
     if (timing) a.dbg = dbg.ensure(static_cast<size_t>(cfg.cluster) * cfg.groups * 8);
     {

@@ -21,6 +21,7 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "svrg.cuh"
@@ -275,7 +276,7 @@ __host__ __device__ inline ChainSmem chain_smem(int rows, int stages) {
   s.off_stage = o;
   o += s.stage_len * stages;
   s.off_v = o;
-  o += static_cast<size_t>(rows) * PC;
+  o += static_cast<size_t>(s.rows_pad) * PC;  // row-major [r][PC] or column-major [c][RP]
   s.off_recv = o;
   o += 2 * kMaxCluster * B * PC;
   s.off_a = o;
@@ -312,7 +313,7 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 }
 __device__ __forceinline__ void consumers_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kChainThreads) : "memory"); }
 
-template <int PC, int B>
+template <int PC, int B, bool SCALAR>
 __global__ void __launch_bounds__(kChainThreads + 32, 1) k_svrg_chain(EpochArgs a) {
   extern __shared__ __align__(128) double sm[];
   cg::cluster_group cluster = cg::this_cluster();
@@ -340,9 +341,12 @@ __global__ void __launch_bounds__(kChainThreads + 32, 1) k_svrg_chain(EpochArgs 
 
   const int64_t nb = (a.m + B - 1) / B;
   auto bt_of = [&](int64_t t) { return static_cast<int>(a.m - t * B < B ? a.m - t * B : B); };
+  // V row slice: row-major [r][PC] for the DMMA phases, column-major [c][RP]
+  // (lane-consecutive rows, conflict-free) for the scalar phases.
+  auto vix = [&](int r, int c) { return SCALAR ? c * RP + r : r * PC + c; };
   for (int e = tid; e < rc * PC; e += blockDim.x) {
     const int r = e / PC, c = e - (e / PC) * PC;
-    V[e] = c < pc ? a.W[static_cast<int64_t>(r0 + r) * a.ldw + c0 + c] : 0.0;
+    V[vix(r, c)] = c < pc ? a.W[static_cast<int64_t>(r0 + r) * a.ldw + c0 + c] : 0.0;
   }
   for (int e = tid; e < B * PC; e += blockDim.x) rprev[e] = 0.0;
   if (tid == 0) {
@@ -381,10 +385,56 @@ __global__ void __launch_bounds__(kChainThreads + 32, 1) k_svrg_chain(EpochArgs 
   } else {
     // ===== 8 consumer warps
     auto wait_block = [&](int64_t t) { mbar_wait(&full[t % S], static_cast<uint32_t>((t / S) & 1)); };
+    // Scalar form: warp w owns steps j = w, w + 8 (lanes stride the rows),
+    // xor-shuffle sums leave the totals in every lane, lane q < G st.async's
+    // its copy to rank q.
+    auto dots_push_scalar = [&](const double* xb, int bt, int64_t u) {
+      const int par = static_cast<int>(u & 1);
+      constexpr int NWC = kChainThreads / 32;
+      const uint32_t rb = mapa(smem_u32(&rbar[par]), lane < G ? lane : 0);
+      const uint32_t rslot = mapa(smem_u32(recv + (par * kMaxCluster + g) * B * PC), lane < G ? lane : 0);
+      for (int j0 = warp; j0 < bt; j0 += 2 * NWC) {
+        const int j1 = j0 + NWC;
+        const bool two = j1 < bt;
+        double s0[PC], s1[PC];
+#pragma unroll
+        for (int c = 0; c < PC; ++c) s0[c] = s1[c] = 0.0;
+        const double* x0 = xb + j0 * RP;
+        const double* x1 = xb + (two ? j1 : j0) * RP;
+#pragma unroll 2
+        for (int r = lane; r < rc; r += 32) {
+          const double u0 = x0[r], u1 = x1[r];
+#pragma unroll
+          for (int c = 0; c < PC; ++c) {
+            const double v = V[c * RP + r];
+            s0[c] = fma(u0, v, s0[c]);
+            s1[c] = fma(u1, v, s1[c]);
+          }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+          for (int c = 0; c < PC; ++c) {
+            s0[c] += __shfl_xor_sync(0xffffffffu, s0[c], o);
+            s1[c] += __shfl_xor_sync(0xffffffffu, s1[c], o);
+          }
+        if (lane < G) {
+#pragma unroll
+          for (int c = 0; c < PC; ++c) {
+            st_async_f64(rslot + (j0 * PC + c) * 8u, s0[c], rb);
+            if (two) st_async_f64(rslot + (j1 * PC + c) * 8u, s1[c], rb);
+          }
+        }
+      }
+    };
     // Partial Â = X_Bᵀ V over the owned rows (DMMA: M = j, N = columns, K =
     // rows split over the 8 warps), fixed-order cross-warp sum, then st.async
     // of every entry into slot g of every peer (completing on its rbar).
     auto dots_push = [&](const double* xb, int bt, int64_t u) {
+      if constexpr (SCALAR) {
+        dots_push_scalar(xb, bt, u);
+        return;
+      }
       const int par = static_cast<int>(u & 1);
       const int gq = lane >> 2, tq = lane & 3;
       constexpr int NA = 4;  // independent accumulation chains per tile
@@ -450,7 +500,10 @@ __global__ void __launch_bounds__(kChainThreads + 32, 1) k_svrg_chain(EpochArgs 
       recv_sum(0);
       double rb = 1.0;
       for (int j = 0; j < bt_of(0); ++j) rb *= a.rho;
-      for (int e = tid; e < rc * PC; e += kChainThreads) V[e] *= rb;
+      for (int e = tid; e < rc * PC; e += kChainThreads) {
+        const int r = e / PC, c = e - (e / PC) * PC;
+        V[vix(r, c)] *= rb;
+      }
     }
     long long tacc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     long long tp = clock64();
@@ -475,7 +528,22 @@ __global__ void __launch_bounds__(kChainThreads + 32, 1) k_svrg_chain(EpochArgs 
       const double* Ub = M + B * B;
       // (a) coef_t = TT Â + M coef_{t−1} + U  — warps 0/1 own row tiles j in [8w, 8w+8),
       //     DMMA m8n8k4 (A = TT/M rows, B = Â / coef_{t−1} columns padded to 8)
-      if (warp < B / 8) {
+      if (SCALAR && !(a.skip & 1)) {
+        // thread (j, c): coef = U + Σ_l TT[j][l] Â[l][c] + M[j][l] coef_prev[l][c]
+        for (int e = tid; e < bt * PC; e += kChainThreads) {
+          const int j = e / PC, c = e - (e / PC) * PC;
+          double s0 = Ub[e], s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+          for (int l = 0; l < B; l += 2) {
+            s0 = fma(TT[j * B + l], Ahat[l * PC + c], s0);
+            s1 = fma(TT[j * B + l + 1], Ahat[(l + 1) * PC + c], s1);
+            s2 = fma(M[j * B + l], rprev[l * PC + c], s2);
+            s3 = fma(M[j * B + l + 1], rprev[(l + 1) * PC + c], s3);
+          }
+          coef[e] = (s0 + s1) + (s2 + s3);
+        }
+        for (int e = bt * PC + tid; e < B * PC; e += kChainThreads) coef[e] = 0.0;
+      } else if (!SCALAR && warp < B / 8 && !(a.skip & 1)) {
         const int gq = lane >> 2, tq = lane & 3, j = warp * 8 + gq;
         double cA[B / 4][2], cR[B / 4][2];  // independent accumulation chains
 #pragma unroll
@@ -499,7 +567,16 @@ __global__ void __launch_bounds__(kChainThreads + 32, 1) k_svrg_chain(EpochArgs 
       consumers_sync();
       tick(3);
       // (b) lookahead partials of block t+1 → every peer
-      if (more) dots_push(stage(t + 1), bt_of(t + 1), t + 1);
+      if (more) {
+        if (!(a.skip & 2)) {
+          dots_push(stage(t + 1), bt_of(t + 1), t + 1);
+        } else if (tid < G) {  // ablation: push zeros only
+          const int par = static_cast<int>((t + 1) & 1);
+          const uint32_t slot = mapa(smem_u32(recv + (par * kMaxCluster + g) * B * PC), tid);
+          const uint32_t rb = mapa(smem_u32(&rbar[par]), tid);
+          for (int e = 0; e < bt_of(t + 1) * PC; ++e) st_async_f64(slot + e * 8u, 0.0, rb);
+        }
+      }
       tick(4);
       consumers_sync();
       tick(5);
@@ -507,7 +584,28 @@ __global__ void __launch_bounds__(kChainThreads + 32, 1) k_svrg_chain(EpochArgs 
       double rn = 1.0;
       if (more)
         for (int j = 0; j < bt_of(t + 1); ++j) rn *= a.rho;
-      {
+      if (SCALAR && !(a.skip & 4)) {
+        // thread = row: V[c][r] = rn (V[c][r] + Σ_l X_B[l][r] coef[l][c])
+        for (int r = tid; r < rc; r += kChainThreads) {
+          double w[PC], w2[PC];
+#pragma unroll
+          for (int c = 0; c < PC; ++c) {
+            w[c] = V[c * RP + r];
+            w2[c] = 0.0;
+          }
+#pragma unroll
+          for (int l = 0; l < B; l += 2) {
+            const double x = xb[l * RP + r], x2 = xb[(l + 1) * RP + r];
+#pragma unroll
+            for (int c = 0; c < PC; ++c) {
+              w[c] = fma(x, coef[l * PC + c], w[c]);
+              w2[c] = fma(x2, coef[(l + 1) * PC + c], w2[c]);
+            }
+          }
+#pragma unroll
+          for (int c = 0; c < PC; ++c) V[c * RP + r] = (w[c] + w2[c]) * rn;
+        }
+      } else if (!SCALAR && !(a.skip & 4)) {
         // DMMA: rows in tiles of 8 (M), columns padded to 8 (N), K = the b steps
         const int gq = lane >> 2, tq = lane & 3;
         double bc[B / 4];
@@ -560,7 +658,7 @@ __global__ void __launch_bounds__(kChainThreads + 32, 1) k_svrg_chain(EpochArgs 
       const int r = e / PC, c = e - (e / PC) * PC;
       if (c < pc) {
         const int64_t o = static_cast<int64_t>(r0 + r) * a.ldw + c0 + c;
-        a.W[o] = fma(beta, a.C[o], V[e]);
+        a.W[o] = fma(beta, a.C[o], V[vix(r, c)]);
       }
     }
   }
@@ -736,7 +834,8 @@ void launch_block_prep(const EpochArgs& a, const EpochConfig& cfg, cudaStream_t 
 
 template <int PC>
 void launch_chain_pc(const EpochArgs& a, const EpochConfig& cfg, cudaStream_t st) {
-  auto kern = k_svrg_chain<PC, kBlock>;
+  static const int mode = getenv("GAPLRA_CHAIN_MMA") ? atoi(getenv("GAPLRA_CHAIN_MMA")) : 0;
+  auto kern = mode ? k_svrg_chain<PC, kBlock, false> : k_svrg_chain<PC, kBlock, true>;
   GAPLRA_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(cfg.smem)));
   if (cfg.cluster > 8) GAPLRA_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   cudaLaunchConfig_t lc = {};

@@ -25,6 +25,7 @@ struct EpochArgs {
   double rho, eta_n;
   int rows_per_cta, stages, pc, groups;
   long long* dbg;  // optional per-CTA phase cycle counters (8 per CTA)
+  int skip;        // debug ablation mask: 1 coef, 2 dots, 4 update (results invalid)
 };
 
 struct SparseEpochArgs {
