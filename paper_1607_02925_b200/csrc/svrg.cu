@@ -223,13 +223,15 @@ __global__ void __launch_bounds__(kPrepThreads) k_block_prep(EpochArgs a) {
     }
     __syncthreads();
     double* slab = a.slab + t * a.slab_len;
+    // TT and M are stored transposed ([l][j]): consumers index them with j
+    // varying across lanes (bank-conflict free).
     for (int e = threadIdx.x; e < B * B; e += kPrepThreads) {
       const int j = e / B, l = e % B;
-      slab[e] = TT[j][l];
+      slab[l * B + j] = TT[j][l];
       double s = 0.0;
       if (has_prev)
         for (int k = 0; k <= j; ++k) s = fma(TT[j][k], Kx[k][l], s);
-      slab[B * B + e] = s;
+      slab[B * B + l * B + j] = s;
     }
     for (int e = threadIdx.x; e < B * a.groups * a.pc; e += kPrepThreads) {
       const int grp = e / (B * a.pc), rem = e - grp * (B * a.pc);
@@ -337,10 +339,16 @@ __global__ void __launch_bounds__(kChainThreads + 32, 1) k_svrg_chain(EpochArgs 
   uint64_t* full = reinterpret_cast<uint64_t*>(sm + L.off_bar);  // [S] TMA landed
   uint64_t* empty = full + 4;                                     // [S] consumers done
   uint64_t* rbar = full + 8;                                      // [2] all-reduce slots
-  auto stage = [&](int64_t t) { return sm + L.off_stage + static_cast<size_t>(t % S) * L.stage_len; };
+  // stage of block t is t mod S; callers track it incrementally (no 64-bit
+  // division on the critical path)
+  auto stage_at = [&](int s_idx) { return sm + L.off_stage + static_cast<size_t>(s_idx) * L.stage_len; };
 
-  const int64_t nb = (a.m + B - 1) / B;
-  auto bt_of = [&](int64_t t) { return static_cast<int>(a.m - t * B < B ? a.m - t * B : B); };
+  const int nb = static_cast<int>((a.m + B - 1) / B);
+  const int last_bt = static_cast<int>(a.m - static_cast<int64_t>(nb - 1) * B);
+  auto bt_of = [&](int t) { return t == nb - 1 ? last_bt : B; };
+  double rho_b = 1.0, rho_last = 1.0;  // ρ^B and ρ^{b of the last block}
+  for (int j = 0; j < B; ++j) rho_b *= a.rho;
+  for (int j = 0; j < last_bt; ++j) rho_last *= a.rho;
   // V row slice: row-major [r][PC] for the DMMA phases, column-major [c][RP]
   // (lane-consecutive rows, conflict-free) for the scalar phases.
   auto vix = [&](int r, int c) { return SCALAR ? c * RP + r : r * PC + c; };
@@ -352,7 +360,7 @@ __global__ void __launch_bounds__(kChainThreads + 32, 1) k_svrg_chain(EpochArgs 
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kChainThreads);
+      mbar_init(&empty[s], kChainThreads / 32);  // one arrival per consumer warp
     }
     mbar_init(&rbar[0], 1);
     mbar_init(&rbar[1], 1);
@@ -362,33 +370,47 @@ __global__ void __launch_bounds__(kChainThreads + 32, 1) k_svrg_chain(EpochArgs 
 
   if (warp == kChainThreads / 32) {
     // ===== producer warp: stream X slices + the block slab through the ring
-    for (int64_t t = 0; t < nb; ++t) {
-      const int s = static_cast<int>(t % S);
-      if (t >= S) mbar_wait(&empty[s], static_cast<uint32_t>((t / S - 1) & 1));
+    int s = 0;
+    uint32_t eph = 0;  // parity of the next empty-barrier completion per wrap
+    for (int t = 0; t < nb; ++t) {
+      if (t >= S) mbar_wait(&empty[s], eph);
       const int bt = bt_of(t);
-      double* st = stage(t);
+      double* st = stage_at(s);
       if (lane == 0) {
         fence_proxy_async();
         mbar_expect_tx(&full[s], static_cast<uint32_t>((rc > 0 ? bt * rc : 0) + 2 * B * B + B * PC) * 8u);
       }
       __syncwarp();
       if (lane < bt && rc > 0)
-        tma_load_1d(st + lane * RP, a.X + static_cast<int64_t>(__ldg(a.idx + t * B + lane)) * a.ldx + r0, rc * 8u,
+        tma_load_1d(st + lane * RP, a.X + static_cast<int64_t>(__ldg(a.idx + static_cast<int64_t>(t) * B + lane)) * a.ldx + r0, rc * 8u,
                     &full[s]);
       if (lane == 31) {
-        const double* slab = a.slab + t * a.slab_len;
+        const double* slab = a.slab + static_cast<int64_t>(t) * a.slab_len;
         tma_load_1d(st + B * RP, slab, 2 * B * B * 8u, &full[s]);
         tma_load_1d(st + B * RP + 2 * B * B, slab + 2 * B * B + static_cast<size_t>(grp) * B * PC, B * PC * 8u,
                     &full[s]);
       }
+      if (++s == S) {
+        s = 0;
+        if (t >= S) eph ^= 1u;
+      }
     }
   } else {
     // ===== 8 consumer warps
-    auto wait_block = [&](int64_t t) { mbar_wait(&full[t % S], static_cast<uint32_t>((t / S) & 1)); };
+    // stage index / full-barrier parity of the block being waited for
+    int ws = 0;
+    uint32_t wph = 0;
+    auto wait_next = [&]() {  // blocks are waited for in order 0, 1, 2, ...
+      mbar_wait(&full[ws], wph);
+      if (++ws == S) {
+        ws = 0;
+        wph ^= 1u;
+      }
+    };
     // Scalar form: warp w owns steps j = w, w + 8 (lanes stride the rows),
     // xor-shuffle sums leave the totals in every lane, lane q < G st.async's
     // its copy to rank q.
-    auto dots_push_scalar = [&](const double* xb, int bt, int64_t u) {
+    auto dots_push_scalar = [&](const double* xb, int bt, int u) {
       const int par = static_cast<int>(u & 1);
       constexpr int NWC = kChainThreads / 32;
       const uint32_t rb = mapa(smem_u32(&rbar[par]), lane < G ? lane : 0);
@@ -430,7 +452,7 @@ __global__ void __launch_bounds__(kChainThreads + 32, 1) k_svrg_chain(EpochArgs 
     // Partial Â = X_Bᵀ V over the owned rows (DMMA: M = j, N = columns, K =
     // rows split over the 8 warps), fixed-order cross-warp sum, then st.async
     // of every entry into slot g of every peer (completing on its rbar).
-    auto dots_push = [&](const double* xb, int bt, int64_t u) {
+    auto dots_push = [&](const double* xb, int bt, int u) {
       if constexpr (SCALAR) {
         dots_push_scalar(xb, bt, u);
         return;
@@ -480,10 +502,10 @@ __global__ void __launch_bounds__(kChainThreads + 32, 1) k_svrg_chain(EpochArgs 
         for (int q = 0; q < G; ++q) st_async_f64(mapa(slot, q) + e * 8u, s, mapa(rbl, q));
       }
     };
-    auto arm_recv = [&](int64_t u) {
+    auto arm_recv = [&](int u) {
       mbar_expect_tx(&rbar[u & 1], static_cast<uint32_t>(G * bt_of(u) * PC * 8));
     };
-    auto recv_sum = [&](int64_t u) {
+    auto recv_sum = [&](int u) {
       const int par = static_cast<int>(u & 1);
       mbar_wait(&rbar[par], static_cast<uint32_t>((u >> 1) & 1));
       const int n = bt_of(u) * PC;
@@ -495,8 +517,8 @@ __global__ void __launch_bounds__(kChainThreads + 32, 1) k_svrg_chain(EpochArgs 
     };
     if (nb > 0) {
       if (tid == 0) arm_recv(0);
-      wait_block(0);
-      dots_push(stage(0), bt_of(0), 0);
+      wait_next();
+      dots_push(stage_at(0), bt_of(0), 0);
       recv_sum(0);
       double rb = 1.0;
       for (int j = 0; j < bt_of(0); ++j) rb *= a.rho;
@@ -514,15 +536,17 @@ __global__ void __launch_bounds__(kChainThreads + 32, 1) k_svrg_chain(EpochArgs 
         tp = now;
       }
     };
-    for (int64_t t = 0; t < nb; ++t) {
+    int cs = 0;  // stage of block t
+    for (int t = 0; t < nb; ++t) {
       const int bt = bt_of(t);
       const bool more = t + 1 < nb;
+      const int ns = cs + 1 == S ? 0 : cs + 1;  // stage of block t + 1
       if (tid == 0 && more) arm_recv(t + 1);
-      if (more) wait_block(t + 1);
+      if (more) wait_next();
       tick(0);
       consumers_sync();
       tick(1);
-      const double* xb = stage(t);
+      const double* xb = stage_at(cs);
       const double* TT = xb + B * RP;
       const double* M = TT + B * B;
       const double* Ub = M + B * B;
@@ -535,10 +559,10 @@ __global__ void __launch_bounds__(kChainThreads + 32, 1) k_svrg_chain(EpochArgs 
           double s0 = Ub[e], s1 = 0.0, s2 = 0.0, s3 = 0.0;
 #pragma unroll
           for (int l = 0; l < B; l += 2) {
-            s0 = fma(TT[j * B + l], Ahat[l * PC + c], s0);
-            s1 = fma(TT[j * B + l + 1], Ahat[(l + 1) * PC + c], s1);
-            s2 = fma(M[j * B + l], rprev[l * PC + c], s2);
-            s3 = fma(M[j * B + l + 1], rprev[(l + 1) * PC + c], s3);
+            s0 = fma(TT[l * B + j], Ahat[l * PC + c], s0);
+            s1 = fma(TT[(l + 1) * B + j], Ahat[(l + 1) * PC + c], s1);
+            s2 = fma(M[l * B + j], rprev[l * PC + c], s2);
+            s3 = fma(M[(l + 1) * B + j], rprev[(l + 1) * PC + c], s3);
           }
           coef[e] = (s0 + s1) + (s2 + s3);
         }
@@ -550,8 +574,8 @@ __global__ void __launch_bounds__(kChainThreads + 32, 1) k_svrg_chain(EpochArgs 
         for (int ks = 0; ks < B / 4; ++ks) {
           const int l = 4 * ks + tq;
           cA[ks][0] = cA[ks][1] = cR[ks][0] = cR[ks][1] = 0.0;
-          dmma(cA[ks][0], cA[ks][1], TT[j * B + l], gq < PC ? Ahat[l * PC + gq] : 0.0);
-          dmma(cR[ks][0], cR[ks][1], M[j * B + l], gq < PC ? rprev[l * PC + gq] : 0.0);
+          dmma(cA[ks][0], cA[ks][1], TT[l * B + j], gq < PC ? Ahat[l * PC + gq] : 0.0);
+          dmma(cR[ks][0], cR[ks][1], M[l * B + j], gq < PC ? rprev[l * PC + gq] : 0.0);
         }
         double c0 = 2 * tq < PC ? Ub[j * PC + 2 * tq] : 0.0;
         double c1 = 2 * tq + 1 < PC ? Ub[j * PC + 2 * tq + 1] : 0.0;
@@ -569,7 +593,7 @@ __global__ void __launch_bounds__(kChainThreads + 32, 1) k_svrg_chain(EpochArgs 
       // (b) lookahead partials of block t+1 → every peer
       if (more) {
         if (!(a.skip & 2)) {
-          dots_push(stage(t + 1), bt_of(t + 1), t + 1);
+          dots_push(stage_at(ns), bt_of(t + 1), t + 1);
         } else if (tid < G) {  // ablation: push zeros only
           const int par = static_cast<int>((t + 1) & 1);
           const uint32_t slot = mapa(smem_u32(recv + (par * kMaxCluster + g) * B * PC), tid);
@@ -581,9 +605,7 @@ __global__ void __launch_bounds__(kChainThreads + 32, 1) k_svrg_chain(EpochArgs 
       consumers_sync();
       tick(5);
       // (c) Ŵ_{t+1} = V_t + X_{B_t} coef_t ; V_{t+1} = ρ^{b_{t+1}} Ŵ_{t+1}   (thread = row)
-      double rn = 1.0;
-      if (more)
-        for (int j = 0; j < bt_of(t + 1); ++j) rn *= a.rho;
+      const double rn = !more ? 1.0 : (t + 1 == nb - 1 ? rho_last : rho_b);
       if (SCALAR && !(a.skip & 4)) {
         // thread = row: V[c][r] = rn (V[c][r] + Σ_l X_B[l][r] coef[l][c])
         for (int r = tid; r < rc; r += kChainThreads) {
@@ -641,12 +663,14 @@ __global__ void __launch_bounds__(kChainThreads + 32, 1) k_svrg_chain(EpochArgs 
           }
         }
       }
-      mbar_arrive(&empty[t % S]);  // stage t fully consumed (its lookahead use was at t−1)
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[cs]);  // stage t fully consumed (its lookahead use was at t−1)
       tick(6);
       // (d) gather Â_{t+1}
       for (int e = tid; e < B * PC; e += kChainThreads) rprev[e] = coef[e];
       if (more) recv_sum(t + 1);
       tick(7);
+      cs = ns;
     }
     if (a.dbg && tid == 0) {
       const int cta = blockIdx.y * gridDim.x + blockIdx.x;
@@ -660,6 +684,285 @@ __global__ void __launch_bounds__(kChainThreads + 32, 1) k_svrg_chain(EpochArgs 
         const int64_t o = static_cast<int64_t>(r0 + r) * a.ldw + c0 + c;
         a.W[o] = fma(beta, a.C[o], V[vix(r, c)]);
       }
+    }
+  }
+  cluster.sync();
+}
+
+// ---------------------------------------------------------------------------
+// k_svrg_chain_rr: register-row variant for small PC (<= 4).  Each consumer
+// thread owns R_T rows of the CTA's W slice and keeps them in REGISTERS for
+// the whole epoch.  Per block t:
+//   (b) products X_{B_{t+1}}[j][r] · V[r][c] of the owned rows (independent of
+//       coef_t, so it runs first), a warp reduce-scatter by shuffles, the 8
+//       warp slices summed in fixed order, st.async to every peer;
+//   (a) coef_t = TT Â + M coef_{t−1} + U      (threads (j, c), transposed TT / M)
+//   (c) V ← ρ^{b'} (V + X_{B_t} coef_t) on registers;
+//   (d) wait for the peers' pushes, sum the 16 slots (fixed order).
+// ---------------------------------------------------------------------------
+template <int PC, int B, int RT>
+__global__ void __launch_bounds__(kChainThreads + 32, 1) k_svrg_chain_rr(EpochArgs a) {
+  extern __shared__ __align__(128) double sm[];
+  cg::cluster_group cluster = cg::this_cluster();
+  const int G = static_cast<int>(cluster.num_blocks());
+  const int g = static_cast<int>(cluster.block_rank());
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NW = kChainThreads / 32;
+  constexpr int NV = B * PC;                 // dot entries per block (j-major: e = j*PC + c)
+  constexpr int NVP = (NV + 31) / 32 * 32;   // padded to whole 32-entry chunks
+  const int grp = blockIdx.y;
+  const int c0 = grp * PC;
+  const int pc = min(PC, a.p - c0);
+  const ChainSmem L = chain_smem<PC, B>(a.rows_per_cta, a.stages);
+  const int S = L.stages;
+  const int r0 = g * a.rows_per_cta;
+  const int rc = max(0, min(a.rows_per_cta, a.d_pad - r0));
+  const int RP = L.rows_pad;
+  double* recv = sm + L.off_recv;  // [2][kMaxCluster][NV]
+  double* Ahat = sm + L.off_a;
+  double* coef = sm + L.off_coef;
+  double* rprev = sm + L.off_rprev;
+  double* red = sm + L.off_red;    // [NW][NV]
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + L.off_bar);
+  uint64_t* empty = full + 4;
+  uint64_t* rbar = full + 8;
+  auto stage_at = [&](int s_idx) { return sm + L.off_stage + static_cast<size_t>(s_idx) * L.stage_len; };
+  const int nb = static_cast<int>((a.m + B - 1) / B);
+  const int last_bt = static_cast<int>(a.m - static_cast<int64_t>(nb - 1) * B);
+  auto bt_of = [&](int t) { return t == nb - 1 ? last_bt : B; };
+  double rho_b = 1.0, rho_last = 1.0;  // ρ^B and ρ^{b of the last block}
+  for (int j = 0; j < B; ++j) rho_b *= a.rho;
+  for (int j = 0; j < last_bt; ++j) rho_last *= a.rho;
+
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kChainThreads / 32);  // one arrival per consumer warp
+    }
+    mbar_init(&rbar[0], 1);
+    mbar_init(&rbar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int e = tid; e < NV; e += blockDim.x) rprev[e] = 0.0;
+  cluster.sync();
+
+  if (warp == NW) {
+    // ===== producer warp (identical to k_svrg_chain)
+    int s = 0;
+    uint32_t eph = 0;
+    for (int t = 0; t < nb; ++t) {
+      if (t >= S) mbar_wait(&empty[s], eph);
+      const int bt = bt_of(t);
+      double* st = stage_at(s);
+      if (lane == 0) {
+        fence_proxy_async();
+        mbar_expect_tx(&full[s], static_cast<uint32_t>((rc > 0 ? bt * rc : 0) + 2 * B * B + B * PC) * 8u);
+      }
+      __syncwarp();
+      if (lane < bt && rc > 0)
+        tma_load_1d(st + lane * RP,
+                    a.X + static_cast<int64_t>(__ldg(a.idx + static_cast<int64_t>(t) * B + lane)) * a.ldx + r0,
+                    rc * 8u, &full[s]);
+      if (lane == 31) {
+        const double* slab = a.slab + static_cast<int64_t>(t) * a.slab_len;
+        tma_load_1d(st + B * RP, slab, 2 * B * B * 8u, &full[s]);
+        tma_load_1d(st + B * RP + 2 * B * B, slab + 2 * B * B + static_cast<size_t>(grp) * B * PC, B * PC * 8u,
+                    &full[s]);
+      }
+      if (++s == S) {
+        s = 0;
+        if (t >= S) eph ^= 1u;
+      }
+    }
+  } else {
+    // ===== consumers: rows r = tid + k * 256 (k < RT) in registers
+    double v[RT][PC];
+    bool own[RT];
+#pragma unroll
+    for (int k = 0; k < RT; ++k) {
+      const int r = tid + k * kChainThreads;
+      own[k] = r < rc;
+#pragma unroll
+      for (int c = 0; c < PC; ++c)
+        v[k][c] = own[k] && c < pc ? a.W[static_cast<int64_t>(r0 + r) * a.ldw + c0 + c] : 0.0;
+    }
+    int ws = 0;
+    uint32_t wph = 0;
+    auto wait_next = [&]() {
+      mbar_wait(&full[ws], wph);
+      if (++ws == S) {
+        ws = 0;
+        wph ^= 1u;
+      }
+    };
+    auto arm_recv = [&](int u) { mbar_expect_tx(&rbar[u & 1], static_cast<uint32_t>(G * bt_of(u) * PC * 8)); };
+    // products of the owned rows in chunks of 32 entries (e = j*PC + c), each
+    // chunk reduce-scattered over the 32 lanes by recursive halving (1 value
+    // per lane), the 8 warp slices summed in fixed order, st.async to peers
+    auto dots_push = [&](const double* xb, int bt, int u) {
+      const int par = u & 1;
+#pragma unroll
+      for (int ch = 0; ch < NVP / 32; ++ch) {
+        double val[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) val[i] = 0.0;
+#pragma unroll
+        for (int k = 0; k < RT; ++k) {
+          if (!own[k]) continue;
+          const int r = tid + k * kChainThreads;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const int e = ch * 32 + i;
+            if (e >= NV) break;
+            const int j = e / PC, c = e % PC;
+            if (c == 0 || i == 0) {
+              // one load of x_j[r] per j (the compiler keeps it across c)
+            }
+            val[i] = fma(xb[j * RP + r], v[k][c], val[i]);
+          }
+        }
+        int base = 0;
+#pragma unroll
+        for (int o = 16, n = 32; o >= 1; o >>= 1, n >>= 1) {
+          const bool hi = (lane & o) != 0;
+          const int half = n / 2;
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            if (i >= half) break;
+            const double keep = hi ? val[i + half] : val[i];
+            const double send = hi ? val[i] : val[i + half];
+            val[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+          }
+          if (hi) base += half;
+        }
+        red[warp * NVP + ch * 32 + base] = val[0];
+      }
+      consumers_sync();
+      const uint32_t slot = smem_u32(recv + (par * kMaxCluster + g) * NV);
+      const uint32_t rbl = smem_u32(&rbar[par]);
+      for (int e = tid; e < bt * PC; e += kChainThreads) {
+        double s = 0.0;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) s += red[w * NVP + e];
+        for (int q = 0; q < G; ++q) st_async_f64(mapa(slot, q) + e * 8u, s, mapa(rbl, q));
+      }
+    };
+    auto recv_sum = [&](int u) {
+      const int par = u & 1;
+      mbar_wait(&rbar[par], static_cast<uint32_t>((u >> 1) & 1));
+      for (int e = tid; e < bt_of(u) * PC; e += kChainThreads) {
+        double s = 0.0;
+        for (int q = 0; q < G; ++q) s += recv[(par * kMaxCluster + q) * NV + e];
+        Ahat[e] = s;
+      }
+    };
+    long long tacc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    long long tp = clock64();
+    auto tick = [&](int k) {
+      if (a.dbg) {
+        const long long now = clock64();
+        tacc[k] += now - tp;
+        tp = now;
+      }
+    };
+    if (nb > 0) {
+      if (tid == 0) arm_recv(0);
+      wait_next();
+      dots_push(stage_at(0), bt_of(0), 0);
+      recv_sum(0);
+      double rb = 1.0;
+      for (int j = 0; j < bt_of(0); ++j) rb *= a.rho;
+#pragma unroll
+      for (int k = 0; k < RT; ++k)
+#pragma unroll
+        for (int c = 0; c < PC; ++c) v[k][c] *= rb;
+    }
+    int cs = 0;
+    for (int t = 0; t < nb; ++t) {
+      const int bt = bt_of(t);
+      const bool more = t + 1 < nb;
+      const int ns = cs + 1 == S ? 0 : cs + 1;
+      if (tid == 0 && more) arm_recv(t + 1);
+      if (more) wait_next();
+      tick(0);
+      consumers_sync();  // Â_t, coef_{t−1} (rprev) visible; stage t+1 landed
+      tick(1);
+      // (b) lookahead dots of block t+1 (needs only V_t)
+      if (more) dots_push(stage_at(ns), bt_of(t + 1), t + 1);
+      tick(2);
+      const double* xb = stage_at(cs);
+      const double* TT = xb + B * RP;
+      const double* M = TT + B * B;
+      const double* Ub = M + B * B;
+      // (a) coef_t
+      for (int e = tid; e < NV; e += kChainThreads) {
+        const int j = e / PC, c = e - (e / PC) * PC;
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        if (j < bt) {
+          s0 = Ub[e];
+#pragma unroll
+          for (int l = 0; l < B; l += 2) {
+            s0 = fma(TT[l * B + j], Ahat[l * PC + c], s0);
+            s1 = fma(TT[(l + 1) * B + j], Ahat[(l + 1) * PC + c], s1);
+            s2 = fma(M[l * B + j], rprev[l * PC + c], s2);
+            s3 = fma(M[(l + 1) * B + j], rprev[(l + 1) * PC + c], s3);
+          }
+        }
+        coef[e] = (s0 + s1) + (s2 + s3);
+      }
+      tick(3);
+      consumers_sync();
+      tick(4);
+      // (c) V ← ρ^{b'} (V + X_B coef)
+      const double rn = !more ? 1.0 : (t + 1 == nb - 1 ? rho_last : rho_b);
+      double cf[B][PC];
+#pragma unroll
+      for (int l = 0; l < B; ++l)
+#pragma unroll
+        for (int c = 0; c < PC; ++c) cf[l][c] = coef[l * PC + c];
+#pragma unroll
+      for (int k = 0; k < RT; ++k) {
+        if (!own[k]) continue;
+        const int r = tid + k * kChainThreads;
+        double w2[PC];
+#pragma unroll
+        for (int c = 0; c < PC; ++c) w2[c] = 0.0;
+#pragma unroll
+        for (int l = 0; l < B; l += 2) {
+          const double x = xb[l * RP + r], x2 = xb[(l + 1) * RP + r];
+#pragma unroll
+          for (int c = 0; c < PC; ++c) {
+            v[k][c] = fma(x, cf[l][c], v[k][c]);
+            w2[c] = fma(x2, cf[l + 1][c], w2[c]);
+          }
+        }
+#pragma unroll
+        for (int c = 0; c < PC; ++c) v[k][c] = (v[k][c] + w2[c]) * rn;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[cs]);
+      tick(5);
+      // (d) Â_{t+1}
+      for (int e = tid; e < NV; e += kChainThreads) rprev[e] = coef[e];
+      if (more) recv_sum(t + 1);
+      tick(6);
+      cs = ns;
+    }
+    if (a.dbg && tid == 0) {
+      const int cta = blockIdx.y * gridDim.x + blockIdx.x;
+      for (int k = 0; k < 8; ++k) a.dbg[cta * 8 + k] = tacc[k];
+    }
+    const double beta = -expm1(static_cast<double>(a.m) * log1p(a.rho - 1.0)) / (1.0 - a.rho);
+#pragma unroll
+    for (int k = 0; k < RT; ++k) {
+      if (!own[k]) continue;
+      const int r = tid + k * kChainThreads;
+#pragma unroll
+      for (int c = 0; c < PC; ++c)
+        if (c < pc) {
+          const int64_t o = static_cast<int64_t>(r0 + r) * a.ldw + c0 + c;
+          a.W[o] = fma(beta, a.C[o], v[k][c]);
+        }
     }
   }
   cluster.sync();
@@ -834,8 +1137,16 @@ void launch_block_prep(const EpochArgs& a, const EpochConfig& cfg, cudaStream_t 
 
 template <int PC>
 void launch_chain_pc(const EpochArgs& a, const EpochConfig& cfg, cudaStream_t st) {
-  static const int mode = getenv("GAPLRA_CHAIN_MMA") ? atoi(getenv("GAPLRA_CHAIN_MMA")) : 0;
-  auto kern = mode ? k_svrg_chain<PC, kBlock, false> : k_svrg_chain<PC, kBlock, true>;
+  // 0: auto (scalar smem phases for PC <= 2, DMMA phases above), 1: DMMA,
+  // 2: scalar smem, 3: register-row (PC <= 4).  Measured r01 (cycles per
+  // 16-step block, C2): PC=1 scalar 3030 / DMMA 3976 / reg-row 3738;
+  // PC=3 DMMA 4449 / scalar 5014 / reg-row 5092.
+  static const int env_mode = getenv("GAPLRA_CHAIN_MODE") ? atoi(getenv("GAPLRA_CHAIN_MODE")) : 0;
+  const int mode = env_mode ? env_mode : (PC <= 2 ? 2 : 1);
+  auto kern = mode == 1 ? k_svrg_chain<PC, kBlock, false> : k_svrg_chain<PC, kBlock, true>;
+  if constexpr (PC <= 4) {
+    if (mode == 3) kern = cfg.rows_per_cta <= kChainThreads ? k_svrg_chain_rr<PC, kBlock, 1> : k_svrg_chain_rr<PC, kBlock, 2>;
+  }
   GAPLRA_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(cfg.smem)));
   if (cfg.cluster > 8) GAPLRA_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   cudaLaunchConfig_t lc = {};
