@@ -59,6 +59,9 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
@@ -81,13 +84,49 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
 constexpr int kPrepThreads = 256;
 constexpr int kMaxP = 64;
 
+// 16x16 (B x B) product C = A·Bm by 256 threads (thread = entry), smem operands.
 template <int B>
-__global__ void __launch_bounds__(kPrepThreads) k_block_prep(EpochArgs a) {
+__device__ __forceinline__ void mat_mul_bb(const double (*A)[B + 1], const double (*Bm)[B + 1], double (*Cm)[B + 1],
+                                           int tid) {
+  for (int e = tid; e < B * B; e += kPrepThreads) {
+    const int i = e / B, j = e % B;
+    double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+    for (int k = 0; k < B; k += 2) {
+      s0 = fma(A[i][k], Bm[k][j], s0);
+      s1 = fma(A[i][k + 1], Bm[k + 1][j], s1);
+    }
+    Cm[i][j] = s0 + s1;
+  }
+}
+
+// Column ring of k_block_prep: 32 columns (16 of block t, 16 of block t−1) ×
+// kPrepKC rows per stage, filled by one producer warp with cp.async.bulk.
+// Pitch ≡ 4 (mod 16) doubles: the m8n8k4 fragment LDS (lane → column lane>>2,
+// row lane&3) touches 16 distinct bank pairs per half warp.
+constexpr int kPrepKC = 128;
+constexpr int kPrepPitch = kPrepKC + 4;
+constexpr int kPrepStages = 4;
+constexpr int kPrepCols = 32;
+constexpr size_t kPrepRingBytes = size_t(kPrepStages) * kPrepCols * kPrepPitch * sizeof(double);
+// cp.async.bulk takes warp-uniform operands, so one warp issues its lanes'
+// copies one after another (~50 cycles each): 4 producer warps, one per SM
+// sub-partition, 8 columns each.
+constexpr int kPrepProducers = 4;
+constexpr int kPrepColsPerProducer = kPrepCols / kPrepProducers;
+
+__device__ __forceinline__ void prep_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kPrepThreads) : "memory"); }
+
+template <int B>
+__global__ void __launch_bounds__(kPrepThreads + 32 * kPrepProducers, 1) k_block_prep(EpochArgs a) {
+  static_assert(B == 16, "T = (I+L)(I+L^2)(I+L^4)(I+L^8) and the 32-column ring assume B = 16");
   constexpr int G8 = B / 8;
   constexpr int NW = G8 * (G8 + 1) / 2;  // within-block lower tiles
   constexpr int NX = G8 * G8;            // cross tiles
   constexpr int NT = NW + NX;
   constexpr int NWARP = kPrepThreads / 32;
+  static_assert(NWARP * 16 == kPrepKC, "each consumer warp owns 16 rows of a chunk");
+  extern __shared__ __align__(128) double ring[];
   __shared__ double red[NWARP][NT][64];
   __shared__ double K[B][B + 1];
   __shared__ double Kx[B][B + 1];
@@ -95,87 +134,81 @@ __global__ void __launch_bounds__(kPrepThreads) k_block_prep(EpochArgs a) {
   __shared__ double TT[B][B + 1];
   __shared__ double q[B][kMaxP];
   __shared__ double rp[B + 1], gm[B + 1];
+  __shared__ __align__(8) uint64_t full[kPrepStages], empty[kPrepStages];
+  static_assert(sizeof(red) >= 4 * B * (B + 1) * sizeof(double), "P aliases red");
+  // L, L², L⁴, L⁸ then the running products; red is dead once K/Kx are reduced
+  auto P = reinterpret_cast<double (*)[B][B + 1]>(&red[0][0][0]);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t nblocks = (a.m + B - 1) / B;
+  // Grid-stride blocks: CTA c+1 reads block t+1's "previous" columns while CTA
+  // c reads the same columns as block t's current ones, so one of the two
+  // requests hits L2 (a contiguous range per CTA would re-read them after
+  // ~148 MB of other traffic, i.e. from DRAM).
+  const int64_t t_begin = blockIdx.x, t_step = gridDim.x, t_end = nblocks;
+  const int nkc = (a.d_pad + kPrepKC - 1) / kPrepKC;
+  if (threadIdx.x == 0) {
+    rp[0] = 1.0;
+    gm[0] = 0.0;
+    for (int j = 1; j <= B; ++j) {
+      rp[j] = rp[j - 1] * a.rho;
+      gm[j] = gm[j - 1] + rp[j - 1];
+    }
+    for (int s = 0; s < kPrepStages; ++s) {
+      mbar_init(&full[s], kPrepProducers);
+      mbar_init(&empty[s], NWARP);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp < kPrepProducers) {  // ------------------------------------- producers
+    // producer warp w stages ring columns [8w, 8w+8): 0..15 block t, 16..31 block t−1
+    const int rc = warp * kPrepColsPerProducer + lane;
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int64_t t = t_begin; t < t_end; t += t_step) {
+      const int64_t s0 = t * B;
+      const int bt = static_cast<int>(a.m - s0 < B ? a.m - s0 : B);
+      const double* col = a.zcol;
+      if (lane < kPrepColsPerProducer) {
+        if (rc < B) {
+          if (rc < bt) col = a.X + static_cast<int64_t>(a.idx[s0 + rc]) * a.ldx;
+        } else if (t > 0) {
+          col = a.X + static_cast<int64_t>(a.idx[s0 - B + (rc - B)]) * a.ldx;
+        }
+      }
+      for (int kc = 0; kc < nkc; ++kc) {
+        const int k0 = kc * kPrepKC;
+        const int len = a.d_pad - k0 < kPrepKC ? a.d_pad - k0 : kPrepKC;
+        const uint32_t bytes = static_cast<uint32_t>(len) * sizeof(double);
+        mbar_wait(&empty[stage], phase ^ 1);
+        if (lane == 0) mbar_expect_tx(&full[stage], bytes * kPrepColsPerProducer);
+        __syncwarp();
+        if (lane < kPrepColsPerProducer)
+          tma_load_1d(ring + (static_cast<size_t>(stage) * kPrepCols + rc) * kPrepPitch, col + k0, bytes,
+                      &full[stage]);
+        if (++stage == kPrepStages) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+    return;
+  }
+  // -------------------------------------------------------------- consumers
+  const int ct = threadIdx.x - 32 * kPrepProducers, cw = warp - kPrepProducers;
+  const int fr = lane >> 2, fc = lane & 3;
   const double one_minus_rho = 1.0 - a.rho;  // exact (Sterbenz) for rho in [0.5, 1]
   const double lr = log1p(a.rho - 1.0);
-  for (int64_t t = blockIdx.x; t < nblocks; t += gridDim.x) {
+  int stage = 0;
+  uint32_t phase = 0;
+  for (int64_t t = t_begin; t < t_end; t += t_step) {
     const int64_t s0 = t * B;
     const int bt = static_cast<int>(a.m - s0 < B ? a.m - s0 : B);
     const bool has_prev = t > 0;
-    const double* base[G8];
-    const double* pbase[G8];
-#pragma unroll
-    for (int g = 0; g < G8; ++g) {
-      const int jj = g * 8 + (lane >> 2);
-      base[g] = (jj < bt ? a.X + static_cast<int64_t>(a.idx[s0 + jj]) * a.ldx : a.zcol) + (lane & 3);
-      pbase[g] = (has_prev ? a.X + static_cast<int64_t>(a.idx[s0 - B + jj]) * a.ldx : a.zcol) + (lane & 3);
-    }
-    double acc[NT][2];
-#pragma unroll
-    for (int qq = 0; qq < NT; ++qq) acc[qq][0] = acc[qq][1] = 0.0;
-    const int ksteps = a.d_pad / 4;
-    auto step = [&](const double (&f)[G8], const double (&fp)[G8]) {
-      int qq = 0;
-#pragma unroll
-      for (int gj = 0; gj < G8; ++gj)
-#pragma unroll
-        for (int gl = 0; gl <= gj; ++gl, ++qq) dmma(acc[qq][0], acc[qq][1], f[gj], f[gl]);
-#pragma unroll
-      for (int gj = 0; gj < G8; ++gj)
-#pragma unroll
-        for (int gl = 0; gl < G8; ++gl, ++qq) dmma(acc[qq][0], acc[qq][1], f[gj], fp[gl]);
-    };
-    // register double-buffered batches of U k-steps: the next batch's loads
-    // are in flight while the current batch's DMMAs run (MLP for HBM latency)
-    constexpr int U = 8;
-    double fa[U][G8], fpa[U][G8], fb[U][G8], fpb[U][G8];
-    auto load = [&](int ks0, double (&f)[U][G8], double (&fp)[U][G8]) {
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int ks = ks0 + u * NWARP;
-        const int o = 4 * (ks < ksteps ? ks : 0);
-#pragma unroll
-        for (int g = 0; g < G8; ++g) {
-          f[u][g] = ks < ksteps ? __ldg(base[g] + o) : 0.0;
-          fp[u][g] = ks < ksteps ? __ldg(pbase[g] + o) : 0.0;
-        }
-      }
-    };
-    auto run = [&](double (&f)[U][G8], double (&fp)[U][G8]) {
-#pragma unroll
-      for (int u = 0; u < U; ++u) step(f[u], fp[u]);
-    };
-    int ks = warp;
-    if (ks < ksteps) load(ks, fa, fpa);
-    while (ks < ksteps) {
-      const int nx = ks + U * NWARP;
-      if (nx < ksteps) load(nx, fb, fpb);
-      run(fa, fpa);
-      ks = nx;
-      if (ks >= ksteps) break;
-      const int nx2 = ks + U * NWARP;
-      if (nx2 < ksteps) load(nx2, fa, fpa);
-      run(fb, fpb);
-      ks = nx2;
-    }
-#pragma unroll
-    for (int qq = 0; qq < NT; ++qq) {
-      red[warp][qq][2 * lane] = acc[qq][0];
-      red[warp][qq][2 * lane + 1] = acc[qq][1];
-    }
-    // q_l[c] = ηn((ρ^l β_t + γ_l) H[i_l][c] − Y[i_l][c]),  β_t = γ_{tB}
-    if (threadIdx.x == 0) {
-      rp[0] = 1.0;
-      gm[0] = 0.0;
-      for (int j = 1; j <= B; ++j) {
-        rp[j] = rp[j - 1] * a.rho;
-        gm[j] = gm[j - 1] + rp[j - 1];
-      }
-    }
-    __syncthreads();
+    // q_l[c] = ηn((ρ^l β_t + γ_l) H[i_l][c] − Y[i_l][c]) — issued first so the
+    // gathers overlap the Gram loop
     const double beta = -expm1(static_cast<double>(s0) * lr) / one_minus_rho;
-    for (int e = threadIdx.x; e < B * a.p; e += kPrepThreads) {
+    for (int e = ct; e < B * a.p; e += kPrepThreads) {
       const int l = e / a.p, c = e - (e / a.p) * a.p;
       double v = 0.0;
       if (l < bt) {
@@ -184,7 +217,48 @@ __global__ void __launch_bounds__(kPrepThreads) k_block_prep(EpochArgs a) {
       }
       q[l][c] = v;
     }
-    for (int e = threadIdx.x; e < NT * 64; e += kPrepThreads) {
+    double acc[NT][2];
+#pragma unroll
+    for (int qq = 0; qq < NT; ++qq) acc[qq][0] = acc[qq][1] = 0.0;
+    for (int kc = 0; kc < nkc; ++kc) {
+      const int len = a.d_pad - kc * kPrepKC < kPrepKC ? a.d_pad - kc * kPrepKC : kPrepKC;
+      mbar_wait(&full[stage], phase);
+      const double* sb = ring + static_cast<size_t>(stage) * kPrepCols * kPrepPitch + fr * kPrepPitch + fc;
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks) {
+        const int kk = cw * 16 + ks * 4;
+        if (kk < len) {
+          double f[G8], fp[G8];
+#pragma unroll
+          for (int g = 0; g < G8; ++g) {
+            f[g] = sb[g * 8 * kPrepPitch + kk];
+            fp[g] = sb[(B + g * 8) * kPrepPitch + kk];
+          }
+          int qq = 0;
+#pragma unroll
+          for (int gj = 0; gj < G8; ++gj)
+#pragma unroll
+            for (int gl = 0; gl <= gj; ++gl, ++qq) dmma(acc[qq][0], acc[qq][1], f[gj], f[gl]);
+#pragma unroll
+          for (int gj = 0; gj < G8; ++gj)
+#pragma unroll
+            for (int gl = 0; gl < G8; ++gl, ++qq) dmma(acc[qq][0], acc[qq][1], f[gj], fp[gl]);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[stage]);
+      if (++stage == kPrepStages) {
+        stage = 0;
+        phase ^= 1;
+      }
+    }
+#pragma unroll
+    for (int qq = 0; qq < NT; ++qq) {
+      red[cw][qq][2 * lane] = acc[qq][0];
+      red[cw][qq][2 * lane + 1] = acc[qq][1];
+    }
+    prep_sync();
+    for (int e = ct; e < NT * 64; e += kPrepThreads) {
       const int qq = e / 64, o = e % 64;
       double s = 0.0;
 #pragma unroll
@@ -203,48 +277,64 @@ __global__ void __launch_bounds__(kPrepThreads) k_block_prep(EpochArgs a) {
         Kx[(x / G8) * 8 + mi][(x % G8) * 8 + ni] = s;
       }
     }
-    __syncthreads();
-    if (threadIdx.x < B) {  // column l of T = (I − L)⁻¹ (forward substitution)
-      const int l = threadIdx.x;
-      for (int j = 0; j < B; ++j) T[j][l] = 0.0;
-      if (l < bt) {
-        T[l][l] = 1.0;
-        for (int j = l + 1; j < bt; ++j) {
-          double s = 0.0;
-          for (int k = l; k < j; ++k) s = fma(a.eta_n * rp[j - 1 - k] * K[j][k], T[k][l], s);
-          T[j][l] = s;
-        }
-      }
+    prep_sync();
+    // L_jl = ηn ρ^{j−1−l} K_jl (l < j < bt), nilpotent: T = (I+L)(I+L²)(I+L⁴)(I+L⁸)
+    for (int e = ct; e < B * B; e += kPrepThreads) {
+      const int j = e / B, l = e % B;
+      P[0][j][l] = (l < j && j < bt) ? a.eta_n * rp[j - 1 - l] * K[j][l] : 0.0;
     }
-    __syncthreads();
-    for (int e = threadIdx.x; e < B * B; e += kPrepThreads) {
+    prep_sync();
+    mat_mul_bb<B>(P[0], P[0], P[1], ct);  // L²
+    prep_sync();
+    mat_mul_bb<B>(P[1], P[1], P[2], ct);  // L⁴
+    prep_sync();
+    mat_mul_bb<B>(P[2], P[2], P[3], ct);  // L⁸
+    prep_sync();
+    for (int e = ct; e < B * B; e += kPrepThreads) {  // T = I + L, P[k] += I
+      const int j = e / B, l = e % B;
+      const double id = j == l ? 1.0 : 0.0;
+      T[j][l] = P[0][j][l] + id;
+      P[1][j][l] += id;
+      P[2][j][l] += id;
+      P[3][j][l] += id;
+    }
+    prep_sync();
+    mat_mul_bb<B>(T, P[1], P[0], ct);  // (I+L)(I+L²)
+    prep_sync();
+    mat_mul_bb<B>(P[0], P[2], P[1], ct);  // ·(I+L⁴)
+    prep_sync();
+    mat_mul_bb<B>(P[1], P[3], T, ct);  // ·(I+L⁸)
+    prep_sync();
+    for (int e = ct; e < B * B; e += kPrepThreads) {
       const int j = e / B, l = e % B;
       TT[j][l] = (j < bt && l <= j) ? rp[bt - 1 - j] * T[j][l] * (a.eta_n * rp[l]) : 0.0;
     }
-    __syncthreads();
+    prep_sync();
     double* slab = a.slab + t * a.slab_len;
     // TT and M are stored transposed ([l][j]): consumers index them with j
     // varying across lanes (bank-conflict free).
-    for (int e = threadIdx.x; e < B * B; e += kPrepThreads) {
+    for (int e = ct; e < B * B; e += kPrepThreads) {
       const int j = e / B, l = e % B;
       slab[l * B + j] = TT[j][l];
       double s = 0.0;
       if (has_prev)
-        for (int k = 0; k <= j; ++k) s = fma(TT[j][k], Kx[k][l], s);
+#pragma unroll
+        for (int k = 0; k < B; ++k) s = fma(TT[j][k], Kx[k][l], s);
       slab[B * B + l * B + j] = s;
     }
-    for (int e = threadIdx.x; e < B * a.groups * a.pc; e += kPrepThreads) {
+    for (int e = ct; e < B * a.groups * a.pc; e += kPrepThreads) {
       const int grp = e / (B * a.pc), rem = e - grp * (B * a.pc);
       const int j = rem / a.pc, cc = rem - (rem / a.pc) * a.pc;
       const int c = grp * a.pc + cc;
       double s = 0.0;
       if (j < bt && c < a.p) {
-        for (int l = 0; l <= j; ++l) s = fma(T[j][l], q[l][c], s);
+#pragma unroll
+        for (int l = 0; l < B; ++l) s = fma(T[j][l], q[l][c], s);
         s *= rp[bt - 1 - j];
       }
       slab[2 * B * B + e] = s;
     }
-    __syncthreads();
+    prep_sync();
   }
 }
 
@@ -310,9 +400,6 @@ __device__ __forceinline__ void st_async_f64(uint32_t remote_addr, double v, uin
                : "memory");
 }
 
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
 __device__ __forceinline__ void consumers_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kChainThreads) : "memory"); }
 
 template <int PC, int B, bool SCALAR>
@@ -1130,8 +1217,14 @@ void launch_block_prep(const EpochArgs& a, const EpochConfig& cfg, cudaStream_t 
   args.groups = cfg.groups;
   args.slab_len = epoch_slab_len(cfg);
   const int64_t nblocks = ceil_div(a.m, kBlock);
-  const int grid = static_cast<int>(std::min<int64_t>(nblocks, sm_count_dev() * 8));
-  k_block_prep<kBlock><<<grid, kPrepThreads, 0, st>>>(args);
+  const int grid = static_cast<int>(std::min<int64_t>(nblocks, sm_count_dev()));
+  static const bool attr = [] {
+    GAPLRA_CUDA_CHECK(cudaFuncSetAttribute(k_block_prep<kBlock>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           static_cast<int>(kPrepRingBytes)));
+    return true;
+  }();
+  (void)attr;
+  k_block_prep<kBlock><<<grid, kPrepThreads + 32 * kPrepProducers, kPrepRingBytes, st>>>(args);
   GAPLRA_LAUNCH_CHECK();
 }
 
