@@ -104,7 +104,7 @@ __device__ __forceinline__ void mat_mul_bb(const double (*A)[B + 1], const doubl
 // kPrepKC rows per stage, filled by one producer warp with cp.async.bulk.
 // Pitch ≡ 4 (mod 16) doubles: the m8n8k4 fragment LDS (lane → column lane>>2,
 // row lane&3) touches 16 distinct bank pairs per half warp.
-constexpr int kPrepKC = 128;
+constexpr int kPrepKC = 64;
 constexpr int kPrepPitch = kPrepKC + 4;
 constexpr int kPrepStages = 4;
 constexpr int kPrepCols = 32;
@@ -113,19 +113,21 @@ constexpr size_t kPrepRingBytes = size_t(kPrepStages) * kPrepCols * kPrepPitch *
 // copies one after another (~50 cycles each): 4 producer warps, one per SM
 // sub-partition, 8 columns each.
 constexpr int kPrepProducers = 4;
+constexpr int kPrepCtas = 2;  // CTAs per SM: one's serial tail overlaps the other's Gram loop
 constexpr int kPrepColsPerProducer = kPrepCols / kPrepProducers;
 
 __device__ __forceinline__ void prep_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kPrepThreads) : "memory"); }
 
 template <int B>
-__global__ void __launch_bounds__(kPrepThreads + 32 * kPrepProducers, 1) k_block_prep(EpochArgs a) {
+__global__ void __launch_bounds__(kPrepThreads + 32 * kPrepProducers, kPrepCtas) k_block_prep(EpochArgs a) {
   static_assert(B == 16, "T = (I+L)(I+L^2)(I+L^4)(I+L^8) and the 32-column ring assume B = 16");
   constexpr int G8 = B / 8;
   constexpr int NW = G8 * (G8 + 1) / 2;  // within-block lower tiles
   constexpr int NX = G8 * G8;            // cross tiles
   constexpr int NT = NW + NX;
   constexpr int NWARP = kPrepThreads / 32;
-  static_assert(NWARP * 16 == kPrepKC, "each consumer warp owns 16 rows of a chunk");
+  constexpr int RPW = kPrepKC / NWARP;  // rows of a chunk per consumer warp
+  static_assert(RPW % 4 == 0, "whole m8n8k4 k-steps per warp");
   extern __shared__ __align__(128) double ring[];
   __shared__ double red[NWARP][NT][64];
   __shared__ double K[B][B + 1];
@@ -225,8 +227,8 @@ __global__ void __launch_bounds__(kPrepThreads + 32 * kPrepProducers, 1) k_block
       mbar_wait(&full[stage], phase);
       const double* sb = ring + static_cast<size_t>(stage) * kPrepCols * kPrepPitch + fr * kPrepPitch + fc;
 #pragma unroll
-      for (int ks = 0; ks < 4; ++ks) {
-        const int kk = cw * 16 + ks * 4;
+      for (int ks = 0; ks < RPW / 4; ++ks) {
+        const int kk = cw * RPW + ks * 4;
         if (kk < len) {
           double f[G8], fp[G8];
 #pragma unroll
@@ -1217,7 +1219,7 @@ void launch_block_prep(const EpochArgs& a, const EpochConfig& cfg, cudaStream_t 
   args.groups = cfg.groups;
   args.slab_len = epoch_slab_len(cfg);
   const int64_t nblocks = ceil_div(a.m, kBlock);
-  const int grid = static_cast<int>(std::min<int64_t>(nblocks, sm_count_dev()));
+  const int grid = static_cast<int>(std::min<int64_t>(nblocks, sm_count_dev() * kPrepCtas));
   static const bool attr = [] {
     GAPLRA_CUDA_CHECK(cudaFuncSetAttribute(k_block_prep<kBlock>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            static_cast<int>(kPrepRingBytes)));
