@@ -431,6 +431,13 @@ void epoch_dev(Context& c, Matrix& X, int p, double* W, const double* C, const d
       const double nbk = static_cast<double>(ceil_div(m, cfg.b));
       fprintf(stderr, "{\"epoch_phase_cycles_per_block\": [");
       for (int k = 0; k < 8; ++k) fprintf(stderr, "%s%.0f", k ? ", " : "", h[k] / nbk);
+      fprintf(stderr, "], \"mean_over_ctas\": [");
+      const size_t nct = h.size() / 8;
+      for (int k = 0; k < 8; ++k) {
+        double sum = 0;
+        for (size_t q = 0; q < nct; ++q) sum += static_cast<double>(h[q * 8 + k]);
+        fprintf(stderr, "%s%.0f", k ? ", " : "", sum / nct / nbk);
+      }
       fprintf(stderr, "], \"cluster\": %d, \"pc\": %d, \"groups\": %d, \"stages\": %d}\n", cfg.cluster, cfg.pc,
               cfg.groups, cfg.stages);
     }

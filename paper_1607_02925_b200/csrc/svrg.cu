@@ -53,11 +53,34 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// Producer-side wait: producers run stages ahead, so a failed poll backs off
+// instead of spinning (a spinning warp takes issue slots from the consumers
+// on its SM sub-partition).
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity) {
+  uint32_t done;
+  for (;;) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (done) return;
+    __nanosleep(128);
+  }
+}
 __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
+}
+// 16-byte variant: two entries per remote message
+__device__ __forceinline__ void st_async_f64x2(uint32_t remote_addr, double v0, double v1, uint32_t remote_bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(remote_addr),
+               "d"(v0), "d"(v1), "r"(remote_bar)
+               : "memory");
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
@@ -182,7 +205,7 @@ __global__ void __launch_bounds__(kPrepThreads + 32 * kPrepProducers, kPrepCtas)
         const int k0 = kc * kPrepKC;
         const int len = a.d_pad - k0 < kPrepKC ? a.d_pad - k0 : kPrepKC;
         const uint32_t bytes = static_cast<uint32_t>(len) * sizeof(double);
-        mbar_wait(&empty[stage], phase ^ 1);
+        mbar_wait_backoff(&empty[stage], phase ^ 1);
         if (lane == 0) mbar_expect_tx(&full[stage], bytes * kPrepColsPerProducer);
         __syncwarp();
         if (lane < kPrepColsPerProducer)
@@ -344,26 +367,34 @@ __global__ void __launch_bounds__(kPrepThreads + 32 * kPrepProducers, kPrepCtas)
 // k_svrg_chain: the sequential recurrence with one-block lookahead.
 // State per CTA: V = ρ^{b_t} Ŵ_t on its rows (W = Ŵ + βC, β folded into U).
 // Iteration t (all quantities for the cluster's PC columns):
+//   (b) Â_{t+1} partial = X_{B_{t+1}}ᵀ V_t on own rows (needs only V_t);
+//       st.async into every peer's receive slot
+//   (d) wait for Â_t (pushed one iteration earlier); Â_t = Σ_q slot_q (fixed order)
 //   (a) coef_t = TT_t Â_t + M_t coef_{t−1} + U_t            (local, redundant)
-//   (b) Â_{t+1} partial = X_{B_{t+1}}ᵀ V_t on own rows; pushed into every
-//       peer's receive slot (DSMEM stores); cluster arrive.release
 //   (c) Ŵ_{t+1} = V_t + X_{B_t} coef_t;  V_{t+1} = ρ^{b_{t+1}} Ŵ_{t+1}
-//   (d) cluster wait.acquire; Â_{t+1} = Σ_q slot_q (fixed order)
-// so the cluster all-reduce latency overlaps the W update.  X slices and the
+// so the cluster all-reduce of Â_{t+1} overlaps (d), (a), (c) of block t and
+// (b) of block t+1.  X slices and the
 // block slab stream through an S-stage TMA ring (cp.async.bulk + mbarrier).
 // ---------------------------------------------------------------------------
 constexpr int kChainThreads = 256;
 constexpr int kMaxCluster = 16;
+// Â_u lives in receive slot u mod 4.  A CTA pushes Â_{t+1} at the start of
+// its iteration t, after it received Â_{t−1} from every peer, i.e. after every
+// peer started iteration t−2 and so finished reading Â_{t−3} (same slot).
+constexpr int kRecvSlots = 4;
 
 struct ChainSmem {
   int rows_pad, stages;
   size_t stage_len, off_stage, off_v, off_recv, off_a, off_coef, off_rprev, off_idx, off_red, off_bar, total;
 };
 
-template <int PC, int B>
+// rows_pad ≡ 2 (mod 16) doubles by default (DMMA / scalar phases: fragment
+// loads across 8 slices are conflict-free); PAD16 gives rows_pad ≡ 0 (mod 16)
+// for k_svrg_chain_v2, whose lane-permuted slice loads are then conflict-free.
+template <int PC, int B, bool PAD16 = false>
 __host__ __device__ inline ChainSmem chain_smem(int rows, int stages) {
   ChainSmem s;
-  s.rows_pad = (rows + 1) / 2 * 2 + 2;
+  s.rows_pad = PAD16 ? (rows + 15) / 16 * 16 : (rows + 1) / 2 * 2 + 2;
   s.stages = stages;
   s.stage_len = static_cast<size_t>(B) * s.rows_pad + 2 * B * B + B * PC;  // X slices | TT | M | U
   size_t o = 0;
@@ -372,7 +403,7 @@ __host__ __device__ inline ChainSmem chain_smem(int rows, int stages) {
   s.off_v = o;
   o += static_cast<size_t>(s.rows_pad) * PC;  // row-major [r][PC] or column-major [c][RP]
   s.off_recv = o;
-  o += 2 * kMaxCluster * B * PC;
+  o += kRecvSlots * kMaxCluster * B * PC;
   s.off_a = o;
   o += B * PC;
   s.off_coef = o;
@@ -404,8 +435,51 @@ __device__ __forceinline__ void st_async_f64(uint32_t remote_addr, double v, uin
 
 __device__ __forceinline__ void consumers_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kChainThreads) : "memory"); }
 
+// Producer side of the chain kernels: block t's X slices (rows [r0, r0+rc) of
+// the bt sampled columns) and its slab part stream into stage t mod S.  The
+// bulk copies take warp-uniform operands (one warp issues its lanes' copies in
+// turn), so kChainProducers warps share the columns.
+constexpr int kChainProducers = 4;
+
+template <int PC, int B, int NP = kChainProducers>
+__device__ __forceinline__ void chain_produce(const EpochArgs& a, int pw, int lane, int nb, int last_bt, int S, int rc,
+                                              int r0, int RP, int grp, double* stages, size_t stage_len,
+                                              uint64_t* full, uint64_t* empty) {
+  constexpr int CPP = B / NP;  // columns per producer warp
+  static_assert(B % NP == 0 && CPP <= 31, "producers cover the B columns; lane 31 issues the slab");
+  int s = 0;
+  uint32_t eph = 0;  // parity of the next empty-barrier completion per wrap
+  for (int t = 0; t < nb; ++t) {
+    if (t >= S) mbar_wait_backoff(&empty[s], eph);
+    const int bt = t == nb - 1 ? last_bt : B;
+    double* st = stages + static_cast<size_t>(s) * stage_len;
+    const int j0 = pw * CPP;
+    const int mine = rc > 0 ? max(0, min(CPP, bt - j0)) : 0;
+    if (lane == 0) {
+      fence_proxy_async();
+      mbar_expect_tx(&full[s], static_cast<uint32_t>(mine * rc + (pw == 0 ? 2 * B * B + B * PC : 0)) * 8u);
+    }
+    __syncwarp();
+    if (lane < mine) {
+      const int j = j0 + lane;
+      tma_load_1d(st + j * RP, a.X + static_cast<int64_t>(__ldg(a.idx + static_cast<int64_t>(t) * B + j)) * a.ldx + r0,
+                  rc * 8u, &full[s]);
+    }
+    if (pw == 0 && lane == 31) {
+      const double* slab = a.slab + static_cast<int64_t>(t) * a.slab_len;
+      tma_load_1d(st + B * RP, slab, 2 * B * B * 8u, &full[s]);
+      tma_load_1d(st + B * RP + 2 * B * B, slab + 2 * B * B + static_cast<size_t>(grp) * B * PC, B * PC * 8u,
+                  &full[s]);
+    }
+    if (++s == S) {
+      s = 0;
+      if (t >= S) eph ^= 1u;
+    }
+  }
+}
+
 template <int PC, int B, bool SCALAR>
-__global__ void __launch_bounds__(kChainThreads + 32, 1) k_svrg_chain(EpochArgs a) {
+__global__ void __launch_bounds__(kChainThreads + 32 * kChainProducers, 1) k_svrg_chain(EpochArgs a) {
   extern __shared__ __align__(128) double sm[];
   cg::cluster_group cluster = cg::this_cluster();
   const int G = static_cast<int>(cluster.num_blocks());
@@ -420,14 +494,14 @@ __global__ void __launch_bounds__(kChainThreads + 32, 1) k_svrg_chain(EpochArgs 
   const int rc = max(0, min(a.rows_per_cta, a.d_pad - r0));
   const int RP = L.rows_pad;
   double* V = sm + L.off_v;
-  double* recv = sm + L.off_recv;  // [2][kMaxCluster][B*PC]
+  double* recv = sm + L.off_recv;  // [kRecvSlots][kMaxCluster][B*PC]
   double* Ahat = sm + L.off_a;
   double* coef = sm + L.off_coef;
   double* rprev = sm + L.off_rprev;
   double* red = sm + L.off_red;
   uint64_t* full = reinterpret_cast<uint64_t*>(sm + L.off_bar);  // [S] TMA landed
   uint64_t* empty = full + 4;                                     // [S] consumers done
-  uint64_t* rbar = full + 8;                                      // [2] all-reduce slots
+  uint64_t* rbar = full + 8;                                      // [4] all-reduce slots
   // stage of block t is t mod S; callers track it incrementally (no 64-bit
   // division on the critical path)
   auto stage_at = [&](int s_idx) { return sm + L.off_stage + static_cast<size_t>(s_idx) * L.stage_len; };
@@ -448,42 +522,17 @@ __global__ void __launch_bounds__(kChainThreads + 32, 1) k_svrg_chain(EpochArgs 
   for (int e = tid; e < B * PC; e += blockDim.x) rprev[e] = 0.0;
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
-      mbar_init(&full[s], 1);
+      mbar_init(&full[s], kChainProducers);
       mbar_init(&empty[s], kChainThreads / 32);  // one arrival per consumer warp
     }
-    mbar_init(&rbar[0], 1);
-    mbar_init(&rbar[1], 1);
+    for (int q = 0; q < kRecvSlots; ++q) mbar_init(&rbar[q], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   cluster.sync();  // barriers initialised cluster-wide before any push / TMA
 
-  if (warp == kChainThreads / 32) {
-    // ===== producer warp: stream X slices + the block slab through the ring
-    int s = 0;
-    uint32_t eph = 0;  // parity of the next empty-barrier completion per wrap
-    for (int t = 0; t < nb; ++t) {
-      if (t >= S) mbar_wait(&empty[s], eph);
-      const int bt = bt_of(t);
-      double* st = stage_at(s);
-      if (lane == 0) {
-        fence_proxy_async();
-        mbar_expect_tx(&full[s], static_cast<uint32_t>((rc > 0 ? bt * rc : 0) + 2 * B * B + B * PC) * 8u);
-      }
-      __syncwarp();
-      if (lane < bt && rc > 0)
-        tma_load_1d(st + lane * RP, a.X + static_cast<int64_t>(__ldg(a.idx + static_cast<int64_t>(t) * B + lane)) * a.ldx + r0, rc * 8u,
-                    &full[s]);
-      if (lane == 31) {
-        const double* slab = a.slab + static_cast<int64_t>(t) * a.slab_len;
-        tma_load_1d(st + B * RP, slab, 2 * B * B * 8u, &full[s]);
-        tma_load_1d(st + B * RP + 2 * B * B, slab + 2 * B * B + static_cast<size_t>(grp) * B * PC, B * PC * 8u,
-                    &full[s]);
-      }
-      if (++s == S) {
-        s = 0;
-        if (t >= S) eph ^= 1u;
-      }
-    }
+  if (warp >= kChainThreads / 32) {
+    chain_produce<PC, B>(a, warp - kChainThreads / 32, lane, nb, last_bt, S, rc, r0, RP, grp, sm + L.off_stage,
+                         L.stage_len, full, empty);
   } else {
     // ===== 8 consumer warps
     // stage index / full-barrier parity of the block being waited for
@@ -500,7 +549,7 @@ __global__ void __launch_bounds__(kChainThreads + 32, 1) k_svrg_chain(EpochArgs 
     // xor-shuffle sums leave the totals in every lane, lane q < G st.async's
     // its copy to rank q.
     auto dots_push_scalar = [&](const double* xb, int bt, int u) {
-      const int par = static_cast<int>(u & 1);
+      const int par = u & (kRecvSlots - 1);
       constexpr int NWC = kChainThreads / 32;
       const uint32_t rb = mapa(smem_u32(&rbar[par]), lane < G ? lane : 0);
       const uint32_t rslot = mapa(smem_u32(recv + (par * kMaxCluster + g) * B * PC), lane < G ? lane : 0);
@@ -546,7 +595,7 @@ __global__ void __launch_bounds__(kChainThreads + 32, 1) k_svrg_chain(EpochArgs 
         dots_push_scalar(xb, bt, u);
         return;
       }
-      const int par = static_cast<int>(u & 1);
+      const int par = u & (kRecvSlots - 1);
       const int gq = lane >> 2, tq = lane & 3;
       constexpr int NA = 4;  // independent accumulation chains per tile
       double acc[NA][B / 8][2];
@@ -592,11 +641,11 @@ __global__ void __launch_bounds__(kChainThreads + 32, 1) k_svrg_chain(EpochArgs 
       }
     };
     auto arm_recv = [&](int u) {
-      mbar_expect_tx(&rbar[u & 1], static_cast<uint32_t>(G * bt_of(u) * PC * 8));
+      mbar_expect_tx(&rbar[u & (kRecvSlots - 1)], static_cast<uint32_t>(G * bt_of(u) * PC * 8));
     };
     auto recv_sum = [&](int u) {
-      const int par = static_cast<int>(u & 1);
-      mbar_wait(&rbar[par], static_cast<uint32_t>((u >> 1) & 1));
+      const int par = u & (kRecvSlots - 1);
+      mbar_wait(&rbar[par], static_cast<uint32_t>((u >> 2) & 1));
       const int n = bt_of(u) * PC;
       for (int e = tid; e < n; e += kChainThreads) {
         double s = 0.0;
@@ -604,11 +653,11 @@ __global__ void __launch_bounds__(kChainThreads + 32, 1) k_svrg_chain(EpochArgs 
         Ahat[e] = s;
       }
     };
-    if (nb > 0) {
+    if (nb > 0) {  // push Â_0 = X_{B_0}ᵀ Ŵ_0, then V_0 = ρ^{b_0} Ŵ_0
       if (tid == 0) arm_recv(0);
       wait_next();
       dots_push(stage_at(0), bt_of(0), 0);
-      recv_sum(0);
+      consumers_sync();
       double rb = 1.0;
       for (int j = 0; j < bt_of(0); ++j) rb *= a.rho;
       for (int e = tid; e < rc * PC; e += kChainThreads) {
@@ -620,7 +669,8 @@ __global__ void __launch_bounds__(kChainThreads + 32, 1) k_svrg_chain(EpochArgs 
     long long tp = clock64();
     auto tick = [&](int k) {
       if (a.dbg) {
-        const long long now = clock64();
+        long long now;
+        asm volatile("mov.u64 %0, %%clock64;" : "=l"(now)::"memory");
         tacc[k] += now - tp;
         tp = now;
       }
@@ -633,8 +683,25 @@ __global__ void __launch_bounds__(kChainThreads + 32, 1) k_svrg_chain(EpochArgs 
       if (tid == 0 && more) arm_recv(t + 1);
       if (more) wait_next();
       tick(0);
-      consumers_sync();
+      consumers_sync();  // V_t complete
       tick(1);
+      // (b) lookahead partials of block t+1 → every peer
+      if (more) {
+        if (!(a.skip & 2)) {
+          dots_push(stage_at(ns), bt_of(t + 1), t + 1);
+        } else if (tid < G) {  // ablation: push zeros only
+          const int par = (t + 1) & (kRecvSlots - 1);
+          const uint32_t slot = mapa(smem_u32(recv + (par * kMaxCluster + g) * B * PC), tid);
+          const uint32_t rb = mapa(smem_u32(&rbar[par]), tid);
+          for (int e = 0; e < bt_of(t + 1) * PC; ++e) st_async_f64(slot + e * 8u, 0.0, rb);
+        }
+      }
+      tick(2);
+      // (d) Â_t
+      recv_sum(t);
+      tick(3);
+      consumers_sync();  // Â_t, coef_{t−1} visible; V reads of (b) done
+      tick(4);
       const double* xb = stage_at(cs);
       const double* TT = xb + B * RP;
       const double* M = TT + B * B;
@@ -676,23 +743,9 @@ __global__ void __launch_bounds__(kChainThreads + 32, 1) k_svrg_chain(EpochArgs 
         if (2 * tq < PC) coef[j * PC + 2 * tq] = c0;
         if (2 * tq + 1 < PC) coef[j * PC + 2 * tq + 1] = c1;
       }
-      tick(2);
-      consumers_sync();
-      tick(3);
-      // (b) lookahead partials of block t+1 → every peer
-      if (more) {
-        if (!(a.skip & 2)) {
-          dots_push(stage_at(ns), bt_of(t + 1), t + 1);
-        } else if (tid < G) {  // ablation: push zeros only
-          const int par = static_cast<int>((t + 1) & 1);
-          const uint32_t slot = mapa(smem_u32(recv + (par * kMaxCluster + g) * B * PC), tid);
-          const uint32_t rb = mapa(smem_u32(&rbar[par]), tid);
-          for (int e = 0; e < bt_of(t + 1) * PC; ++e) st_async_f64(slot + e * 8u, 0.0, rb);
-        }
-      }
-      tick(4);
-      consumers_sync();
       tick(5);
+      consumers_sync();  // coef_t visible
+      tick(6);
       // (c) Ŵ_{t+1} = V_t + X_{B_t} coef_t ; V_{t+1} = ρ^{b_{t+1}} Ŵ_{t+1}   (thread = row)
       const double rn = !more ? 1.0 : (t + 1 == nb - 1 ? rho_last : rho_b);
       if (SCALAR && !(a.skip & 4)) {
@@ -754,10 +807,7 @@ __global__ void __launch_bounds__(kChainThreads + 32, 1) k_svrg_chain(EpochArgs 
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[cs]);  // stage t fully consumed (its lookahead use was at t−1)
-      tick(6);
-      // (d) gather Â_{t+1}
       for (int e = tid; e < B * PC; e += kChainThreads) rprev[e] = coef[e];
-      if (more) recv_sum(t + 1);
       tick(7);
       cs = ns;
     }
@@ -790,7 +840,7 @@ __global__ void __launch_bounds__(kChainThreads + 32, 1) k_svrg_chain(EpochArgs 
 //   (d) wait for the peers' pushes, sum the 16 slots (fixed order).
 // ---------------------------------------------------------------------------
 template <int PC, int B, int RT>
-__global__ void __launch_bounds__(kChainThreads + 32, 1) k_svrg_chain_rr(EpochArgs a) {
+__global__ void __launch_bounds__(kChainThreads + 32 * kChainProducers, 1) k_svrg_chain_rr(EpochArgs a) {
   extern __shared__ __align__(128) double sm[];
   cg::cluster_group cluster = cg::this_cluster();
   const int G = static_cast<int>(cluster.num_blocks());
@@ -807,7 +857,7 @@ __global__ void __launch_bounds__(kChainThreads + 32, 1) k_svrg_chain_rr(EpochAr
   const int r0 = g * a.rows_per_cta;
   const int rc = max(0, min(a.rows_per_cta, a.d_pad - r0));
   const int RP = L.rows_pad;
-  double* recv = sm + L.off_recv;  // [2][kMaxCluster][NV]
+  double* recv = sm + L.off_recv;  // [kRecvSlots][kMaxCluster][NV]
   double* Ahat = sm + L.off_a;
   double* coef = sm + L.off_coef;
   double* rprev = sm + L.off_rprev;
@@ -825,44 +875,18 @@ __global__ void __launch_bounds__(kChainThreads + 32, 1) k_svrg_chain_rr(EpochAr
 
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
-      mbar_init(&full[s], 1);
+      mbar_init(&full[s], kChainProducers);
       mbar_init(&empty[s], kChainThreads / 32);  // one arrival per consumer warp
     }
-    mbar_init(&rbar[0], 1);
-    mbar_init(&rbar[1], 1);
+    for (int q = 0; q < kRecvSlots; ++q) mbar_init(&rbar[q], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   for (int e = tid; e < NV; e += blockDim.x) rprev[e] = 0.0;
   cluster.sync();
 
-  if (warp == NW) {
-    // ===== producer warp (identical to k_svrg_chain)
-    int s = 0;
-    uint32_t eph = 0;
-    for (int t = 0; t < nb; ++t) {
-      if (t >= S) mbar_wait(&empty[s], eph);
-      const int bt = bt_of(t);
-      double* st = stage_at(s);
-      if (lane == 0) {
-        fence_proxy_async();
-        mbar_expect_tx(&full[s], static_cast<uint32_t>((rc > 0 ? bt * rc : 0) + 2 * B * B + B * PC) * 8u);
-      }
-      __syncwarp();
-      if (lane < bt && rc > 0)
-        tma_load_1d(st + lane * RP,
-                    a.X + static_cast<int64_t>(__ldg(a.idx + static_cast<int64_t>(t) * B + lane)) * a.ldx + r0,
-                    rc * 8u, &full[s]);
-      if (lane == 31) {
-        const double* slab = a.slab + static_cast<int64_t>(t) * a.slab_len;
-        tma_load_1d(st + B * RP, slab, 2 * B * B * 8u, &full[s]);
-        tma_load_1d(st + B * RP + 2 * B * B, slab + 2 * B * B + static_cast<size_t>(grp) * B * PC, B * PC * 8u,
-                    &full[s]);
-      }
-      if (++s == S) {
-        s = 0;
-        if (t >= S) eph ^= 1u;
-      }
-    }
+  if (warp >= NW) {
+    chain_produce<PC, B>(a, warp - NW, lane, nb, last_bt, S, rc, r0, RP, grp, sm + L.off_stage, L.stage_len, full,
+                         empty);
   } else {
     // ===== consumers: rows r = tid + k * 256 (k < RT) in registers
     double v[RT][PC];
@@ -884,12 +908,14 @@ __global__ void __launch_bounds__(kChainThreads + 32, 1) k_svrg_chain_rr(EpochAr
         wph ^= 1u;
       }
     };
-    auto arm_recv = [&](int u) { mbar_expect_tx(&rbar[u & 1], static_cast<uint32_t>(G * bt_of(u) * PC * 8)); };
+    auto arm_recv = [&](int u) {
+      mbar_expect_tx(&rbar[u & (kRecvSlots - 1)], static_cast<uint32_t>(G * bt_of(u) * PC * 8));
+    };
     // products of the owned rows in chunks of 32 entries (e = j*PC + c), each
     // chunk reduce-scattered over the 32 lanes by recursive halving (1 value
     // per lane), the 8 warp slices summed in fixed order, st.async to peers
     auto dots_push = [&](const double* xb, int bt, int u) {
-      const int par = u & 1;
+      const int par = u & (kRecvSlots - 1);
 #pragma unroll
       for (int ch = 0; ch < NVP / 32; ++ch) {
         double val[32];
@@ -937,8 +963,8 @@ __global__ void __launch_bounds__(kChainThreads + 32, 1) k_svrg_chain_rr(EpochAr
       }
     };
     auto recv_sum = [&](int u) {
-      const int par = u & 1;
-      mbar_wait(&rbar[par], static_cast<uint32_t>((u >> 1) & 1));
+      const int par = u & (kRecvSlots - 1);
+      mbar_wait(&rbar[par], static_cast<uint32_t>((u >> 2) & 1));
       for (int e = tid; e < bt_of(u) * PC; e += kChainThreads) {
         double s = 0.0;
         for (int q = 0; q < G; ++q) s += recv[(par * kMaxCluster + q) * NV + e];
@@ -949,7 +975,8 @@ __global__ void __launch_bounds__(kChainThreads + 32, 1) k_svrg_chain_rr(EpochAr
     long long tp = clock64();
     auto tick = [&](int k) {
       if (a.dbg) {
-        const long long now = clock64();
+        long long now;
+        asm volatile("mov.u64 %0, %%clock64;" : "=l"(now)::"memory");
         tacc[k] += now - tp;
         tp = now;
       }
@@ -958,7 +985,6 @@ __global__ void __launch_bounds__(kChainThreads + 32, 1) k_svrg_chain_rr(EpochAr
       if (tid == 0) arm_recv(0);
       wait_next();
       dots_push(stage_at(0), bt_of(0), 0);
-      recv_sum(0);
       double rb = 1.0;
       for (int j = 0; j < bt_of(0); ++j) rb *= a.rho;
 #pragma unroll
@@ -974,11 +1000,13 @@ __global__ void __launch_bounds__(kChainThreads + 32, 1) k_svrg_chain_rr(EpochAr
       if (tid == 0 && more) arm_recv(t + 1);
       if (more) wait_next();
       tick(0);
-      consumers_sync();  // Â_t, coef_{t−1} (rprev) visible; stage t+1 landed
-      tick(1);
-      // (b) lookahead dots of block t+1 (needs only V_t)
+      // (b) lookahead dots of block t+1 (needs only V_t, in registers)
       if (more) dots_push(stage_at(ns), bt_of(t + 1), t + 1);
+      tick(1);
+      // (d) Â_t
+      recv_sum(t);
       tick(2);
+      consumers_sync();  // Â_t, coef_{t−1} (rprev) visible
       const double* xb = stage_at(cs);
       const double* TT = xb + B * RP;
       const double* M = TT + B * B;
@@ -1031,9 +1059,7 @@ __global__ void __launch_bounds__(kChainThreads + 32, 1) k_svrg_chain_rr(EpochAr
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[cs]);
       tick(5);
-      // (d) Â_{t+1}
       for (int e = tid; e < NV; e += kChainThreads) rprev[e] = coef[e];
-      if (more) recv_sum(t + 1);
       tick(6);
       cs = ns;
     }
@@ -1163,7 +1189,7 @@ constexpr int kBlock = 16;
 
 template <int PC>
 size_t chain_smem_bytes(int rows, int stages) {
-  return chain_smem<PC, kBlock>(rows, stages).total;
+  return std::max(chain_smem<PC, kBlock>(rows, stages).total, chain_smem<PC, kBlock, true>(rows, stages).total);
 }
 
 size_t smem_for(int pc, int rows, int stages) {
@@ -1230,6 +1256,359 @@ void launch_block_prep(const EpochArgs& a, const EpochConfig& cfg, cudaStream_t 
   GAPLRA_LAUNCH_CHECK();
 }
 
+// ---------------------------------------------------------------------------
+// k_svrg_chain_v2: the chain laid out for the SM's 128 B/clk shared-memory
+// datapath and the block's dependency chain.  Thread = row (RT rows per
+// thread): V and the block's X slice rows live in registers, so every slice
+// element crosses the shared-memory port once (TMA write + one LDS).
+// Per block t, two CTA barriers:
+//   (b) load X_{B_{t+1}} rows into registers (kept for (c) of block t+1);
+//       products X_{B_{t+1}}[j][r] V[r][c] summed over the warp by a
+//       select-free recursive halving (lane L orders its products as
+//       j = i XOR (L>>1), so every level keeps the low half and sends the
+//       high half); red[warp][e];  barrier;  every thread sums one
+//       (entry, peer) pair over the 8 warps (fixed tree) and st.async's it
+//   (d) warp 0: wait for Â_t (pushed one block earlier), fixed-order slot sum
+//   (a) warp 0: coef_t = TT_t Â_t + pre_t  (pre_t = M_t coef_{t−1} + U_t was
+//       formed during block t−1);  barrier
+//   (c) V ← ρ^{b'} (V + X_{B_t} coef_t) from the registers of (b);
+//       warp 7 forms pre_{t+1}
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double sum8_tree(const double* p, int stride) {
+  return ((p[0] + p[stride]) + (p[2 * stride] + p[3 * stride])) +
+         ((p[4 * stride] + p[5 * stride]) + (p[6 * stride] + p[7 * stride]));
+}
+
+// No producer warp: 8 warps (2 per SM sub-partition) leave 255 registers per
+// thread.  Block u's stage is refilled at the start of block u+1 (its last
+// shared-memory reader, warp 0's coef, finished before block u's second
+// barrier) by lanes of warps 4..7, 4 slices each, warp 4 adding the slab part.
+constexpr int kChainV2MaxStages = 6;
+
+// Column index of slice (4 iw + lane) of block u (loaded one block ahead of its
+// use so the copy issue never waits on global memory).
+__device__ __forceinline__ int v2_col(const EpochArgs& a, int u, int nb, int iw, int lane) {
+  const int64_t s = static_cast<int64_t>(u) * 16 + iw * 4 + lane;
+  return (u < nb && lane < 4 && s < a.m) ? __ldg(a.idx + s) : 0;
+}
+
+template <int PC, int B>
+__device__ __forceinline__ void v2_issue(const EpochArgs& a, int u, int nb, int last_bt, int rc, int r0, int RP,
+                                         int grp, double* st, uint64_t* fb, int iw, int lane, int col) {
+  const int bt = u == nb - 1 ? last_bt : B;
+  const int j0 = iw * 4;
+  const int mine = rc > 0 && !(a.skip & 8) ? max(0, min(4, bt - j0)) : 0;  // skip & 8: timing ablation
+  fence_proxy_async();  // generic-proxy reads of the stage (ordered by the CTA barrier) before the async writes
+  if (lane == 0) mbar_expect_tx(fb, static_cast<uint32_t>(mine * rc + (iw == 0 ? 2 * B * B + B * PC : 0)) * 8u);
+  __syncwarp();
+  if (lane < mine) {
+    const int j = j0 + lane;
+    tma_load_1d(st + j * RP, a.X + static_cast<int64_t>(col) * a.ldx + r0, rc * 8u, fb);
+  }
+  if (iw == 0 && lane == 31) {
+    const double* slab = a.slab + static_cast<int64_t>(u) * a.slab_len;
+    tma_load_1d(st + B * RP, slab, 2 * B * B * 8u, fb);
+    tma_load_1d(st + B * RP + 2 * B * B, slab + 2 * B * B + static_cast<size_t>(grp) * B * PC, B * PC * 8u, fb);
+  }
+}
+
+template <int PC, int B, int RT>
+__global__ void __launch_bounds__(kChainThreads, 1) k_svrg_chain_v2(EpochArgs a) {
+  static_assert(B == 16, "lane permutation j = i ^ (lane >> 1) covers 16 slices");
+  extern __shared__ __align__(128) double sm[];
+  cg::cluster_group cluster = cg::this_cluster();
+  const int G = static_cast<int>(cluster.num_blocks());
+  const int lgG = G == 16 ? 4 : (G == 8 ? 3 : (G == 4 ? 2 : (G == 2 ? 1 : 0)));
+  const int g = static_cast<int>(cluster.block_rank());
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NW = kChainThreads / 32;
+  static_assert(NW == 8, "sum8_tree");
+  constexpr int NV = B * PC;  // entries per block (j-major: e = j*PC + c)
+  const int grp = blockIdx.y;
+  const int c0 = grp * PC;
+  const int pc = min(PC, a.p - c0);
+  const ChainSmem L = chain_smem<PC, B, true>(a.rows_per_cta, a.stages);
+  static_assert(NW * NV <= kChainThreads / 32 * (B / 8) * 64, "red fits");
+  const int S = L.stages;
+  const int r0 = g * a.rows_per_cta;
+  const int rc = max(0, min(a.rows_per_cta, a.d_pad - r0));
+  const int RP = L.rows_pad;
+  double* recv = sm + L.off_recv;  // [kRecvSlots][kMaxCluster][NV]
+  double* Ahat = sm + L.off_a;
+  double* coef = sm + L.off_coef;
+  double* pre = sm + L.off_rprev;
+  double* red = sm + L.off_red;  // [NW][NV]
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + L.off_bar);  // [S <= 8]
+  uint64_t* rbar = full + 8;
+  auto stage_at = [&](int s_idx) { return sm + L.off_stage + static_cast<size_t>(s_idx) * L.stage_len; };
+  const int nb = static_cast<int>((a.m + B - 1) / B);
+  const int last_bt = static_cast<int>(a.m - static_cast<int64_t>(nb - 1) * B);
+  auto bt_of = [&](int t) { return t == nb - 1 ? last_bt : B; };
+  double rho_b = 1.0, rho_last = 1.0;
+  for (int j = 0; j < B; ++j) rho_b *= a.rho;
+  for (int j = 0; j < last_bt; ++j) rho_last *= a.rho;
+  // slices j >= bt of a ragged last block are never written: zero the stage
+  // ring once so that those rows read as 0
+#pragma unroll 1
+  for (size_t e = tid; e < L.off_v; e += blockDim.x) sm[e] = 0.0;
+
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) mbar_init(&full[s], 4);
+    for (int q = 0; q < kRecvSlots; ++q) mbar_init(&rbar[q], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  int ncol = 0;  // column index for the next refill (block S, then S+1, ...)
+  if (warp >= 4) {  // first S blocks
+    fence_proxy_async();
+    for (int u = 0; u < S && u < nb; ++u)
+      v2_issue<PC, B>(a, u, nb, last_bt, rc, r0, RP, grp, stage_at(u), &full[u], warp - 4, lane,
+                      v2_col(a, u, nb, warp - 4, lane));
+    ncol = v2_col(a, S, nb, warp - 4, lane);
+  }
+  cluster.sync();
+
+  {
+    const int pm = lane >> 1;  // product order j = i ^ pm
+    double v[RT][PC];
+    bool own[RT];
+#pragma unroll
+    for (int k = 0; k < RT; ++k) {
+      const int r = tid + k * kChainThreads;
+      own[k] = r < rc;
+#pragma unroll
+      for (int c = 0; c < PC; ++c)
+        v[k][c] = own[k] && c < pc ? a.W[static_cast<int64_t>(r0 + r) * a.ldw + c0 + c] : 0.0;
+    }
+    int ws = 0;
+    uint32_t wph = 0;
+    auto wait_next = [&]() {
+      mbar_wait(&full[ws], wph);
+      if (++ws == S) {
+        ws = 0;
+        wph ^= 1u;
+      }
+    };
+    // entries travel in pairs (16-byte st.async): a peer sends ceil(nv/2) pairs
+    auto arm_recv = [&](int u) {
+      mbar_expect_tx(&rbar[u & (kRecvSlots - 1)], static_cast<uint32_t>(G * ((bt_of(u) * PC + 1) & ~1) * 8));
+    };
+    // X slice rows of one block, lane-permuted: xr[k][i] = X_B[i ^ pm][row k]
+    double xa[RT][B], xn[RT][B];
+    auto load_rows = [&](const double* xb, double (&xr)[RT][B]) {
+#pragma unroll
+      for (int k = 0; k < RT; ++k) {
+        const double* col = xb + tid + k * kChainThreads;
+#pragma unroll
+        for (int i = 0; i < B; ++i) xr[k][i] = own[k] ? col[(i ^ pm) * RP] : 0.0;
+      }
+    };
+    // (b) products of the loaded rows with V, select-free warp halving, red
+    auto products = [&](const double (&xr)[RT][B]) {
+      double val[B][PC];
+#pragma unroll
+      for (int i = 0; i < B; ++i)
+#pragma unroll
+        for (int c = 0; c < PC; ++c) {
+          double s = 0.0;
+#pragma unroll
+          for (int k = 0; k < RT; ++k) s = fma(xr[k][i], v[k][c], s);
+          val[i][c] = s;
+        }
+#pragma unroll
+      for (int o = 16, n = B / 2; o >= 2; o >>= 1, n >>= 1)
+#pragma unroll
+        for (int i = 0; i < n; ++i)
+#pragma unroll
+          for (int c = 0; c < PC; ++c) val[i][c] += __shfl_xor_sync(0xffffffffu, val[i + n][c], o);
+#pragma unroll
+      for (int c = 0; c < PC; ++c) val[0][c] += __shfl_xor_sync(0xffffffffu, val[0][c], 1);
+      // lane L now holds the warp total of j = L >> 1
+      if (!(lane & 1))
+#pragma unroll
+        for (int c = 0; c < PC; ++c) red[warp * NV + pm * PC + c] = val[0][c];
+    };
+    // every thread: (entry, peer) pairs, the 8 warp partials summed in a fixed tree
+    auto push = [&](int u) {
+      const int par = u & (kRecvSlots - 1);
+      const int nv = bt_of(u) * PC;
+      const uint32_t slot = smem_u32(recv + (par * kMaxCluster + g) * NV);
+      const uint32_t rbl = smem_u32(&rbar[par]);
+      const int np = (nv + 1) >> 1;
+#pragma unroll 1
+      for (int i = tid; i < (np << lgG); i += kChainThreads) {
+        const int e = (i >> lgG) * 2, q = i & (G - 1);
+        st_async_f64x2(mapa(slot, q) + e * 8u, sum8_tree(red + e, NV), sum8_tree(red + e + 1, NV), mapa(rbl, q));
+      }
+    };
+    long long tacc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    long long tp;
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(tp)::"memory");
+    auto tick = [&](int k) {
+      if (a.dbg) {
+        long long now;
+        asm volatile("mov.u64 %0, %%clock64;" : "=l"(now)::"memory");
+        tacc[k] += now - tp;
+        tp = now;
+      }
+    };
+    // (c) V ← ρ^{b'} (V + X_B coef) with the lane-permuted rows: coef read at j = i ^ pm
+    auto update = [&](const double (&xr)[RT][B], int bt, double rn) {
+      double cf[B][PC];
+#pragma unroll
+      for (int i = 0; i < B; ++i)
+#pragma unroll
+        for (int c = 0; c < PC; ++c) cf[i][c] = coef[(i ^ pm) * PC + c];
+      (void)bt;  // coef rows j >= bt are 0 and so are the slice rows
+#pragma unroll
+      for (int k = 0; k < RT; ++k) {
+        double w2[PC];
+#pragma unroll
+        for (int c = 0; c < PC; ++c) w2[c] = 0.0;
+#pragma unroll
+        for (int i = 0; i < B; i += 2)
+#pragma unroll
+          for (int c = 0; c < PC; ++c) {
+            v[k][c] = fma(xr[k][i], cf[i][c], v[k][c]);
+            w2[c] = fma(xr[k][i + 1], cf[i + 1][c], w2[c]);
+          }
+#pragma unroll
+        for (int c = 0; c < PC; ++c) v[k][c] = own[k] ? (v[k][c] + w2[c]) * rn : 0.0;
+      }
+    };
+    auto step = [&](int t, int& cs, double (&xcur)[RT][B], double (&xnext)[RT][B]) {
+      const int bt = bt_of(t);
+      const bool more = t + 1 < nb;
+      const int ns = cs + 1 == S ? 0 : cs + 1;
+      if (tid == 0 && more) arm_recv(t + 1);
+      // refill block t−1's stage with block t−1+S
+      if (warp >= 4 && t >= 1 && t - 1 + S < nb) {
+        const int ps = cs == 0 ? S - 1 : cs - 1;
+        v2_issue<PC, B>(a, t - 1 + S, nb, last_bt, rc, r0, RP, grp, stage_at(ps), &full[ps], warp - 4, lane, ncol);
+        ncol = v2_col(a, t + S, nb, warp - 4, lane);
+      }
+      tick(0);
+      if (more) wait_next();
+      tick(7);
+      if (more) {
+        load_rows(stage_at(ns), xnext);
+        products(xnext);
+      }
+      tick(1);
+      consumers_sync();  // red complete; pre_t visible; coef reads of block t−1 done
+      tick(2);
+      if (more) push(t + 1);
+      tick(3);
+      const double* xb = stage_at(cs);
+      if (warp == 0) {
+        // (d) Â_t
+        const int par = t & (kRecvSlots - 1);
+        mbar_wait(&rbar[par], static_cast<uint32_t>((t >> 2) & 1));
+        const int nv = bt * PC;
+        for (int e = lane; e < NV; e += 32) {
+          double s = 0.0;
+          if (e < nv) {
+            const double* sl = recv + par * kMaxCluster * NV + e;
+            double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll 1
+            for (int q = 0; q < G; q += 4) {
+              s0 += sl[q * NV];
+              s1 += sl[(q + 1) * NV];
+              s2 += sl[(q + 2) * NV];
+              s3 += sl[(q + 3) * NV];
+            }
+            s = (s0 + s1) + (s2 + s3);
+          }
+          Ahat[e] = s;
+        }
+        __syncwarp();
+        // (a) coef_t = TT_t Â_t + pre_t   (TT stored transposed: TT[l*B + j])
+        const double* TT = xb + B * RP;
+        for (int e = lane; e < NV; e += 32) {
+          const int j = e / PC, c = e - (e / PC) * PC;
+          double s0 = pre[e], s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+          for (int l = 0; l < B; l += 4) {
+            s0 = fma(TT[l * B + j], Ahat[l * PC + c], s0);
+            s1 = fma(TT[(l + 1) * B + j], Ahat[(l + 1) * PC + c], s1);
+            s2 = fma(TT[(l + 2) * B + j], Ahat[(l + 2) * PC + c], s2);
+            s3 = fma(TT[(l + 3) * B + j], Ahat[(l + 3) * PC + c], s3);
+          }
+          coef[e] = (s0 + s1) + (s2 + s3);
+        }
+      }
+      tick(4);
+      consumers_sync();  // coef_t visible
+      tick(5);
+      const double rn = !more ? 1.0 : (t + 1 == nb - 1 ? rho_last : rho_b);
+      update(xcur, bt, rn);
+      // pre_{t+1} = M_{t+1} coef_t + U_{t+1}   (M stored transposed: M[l*B + j])
+      if (warp == NW - 1 && more) {
+        const double* M = stage_at(ns) + B * RP + B * B;
+        const double* Ub = M + B * B;
+        for (int e = lane; e < NV; e += 32) {
+          const int j = e / PC, c = e - (e / PC) * PC;
+          double s0 = Ub[e], s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+          for (int l = 0; l < B; l += 4) {
+            s0 = fma(M[l * B + j], coef[l * PC + c], s0);
+            s1 = fma(M[(l + 1) * B + j], coef[(l + 1) * PC + c], s1);
+            s2 = fma(M[(l + 2) * B + j], coef[(l + 2) * PC + c], s2);
+            s3 = fma(M[(l + 3) * B + j], coef[(l + 3) * PC + c], s3);
+          }
+          pre[e] = (s0 + s1) + (s2 + s3);
+        }
+      }
+      tick(6);
+      cs = ns;
+    };
+    int cs = 0;
+    if (nb > 0) {  // Â_0 = X_{B_0}ᵀ Ŵ_0, then V_0 = ρ^{b_0} Ŵ_0, pre_0 = U_0
+      if (tid == 0) arm_recv(0);
+      wait_next();
+      load_rows(stage_at(0), xa);
+      products(xa);
+      consumers_sync();
+      push(0);
+      double rb = 1.0;
+      for (int j = 0; j < bt_of(0); ++j) rb *= a.rho;
+#pragma unroll
+      for (int k = 0; k < RT; ++k)
+#pragma unroll
+        for (int c = 0; c < PC; ++c) v[k][c] *= rb;
+      if (warp == NW - 1) {
+        const double* Ub = stage_at(0) + B * RP + 2 * B * B;
+        for (int e = lane; e < NV; e += 32) pre[e] = Ub[e];
+      }
+    }
+#pragma unroll 1
+    for (int t = 0; t < nb; ++t) {
+      step(t, cs, xa, xn);
+#pragma unroll
+      for (int k = 0; k < RT; ++k)
+#pragma unroll
+        for (int i = 0; i < B; ++i) xa[k][i] = xn[k][i];
+    }
+    if (a.dbg && tid == 0) {
+      const int cta = blockIdx.y * gridDim.x + blockIdx.x;
+      for (int k = 0; k < 8; ++k) a.dbg[cta * 8 + k] = tacc[k];
+    }
+    const double beta = -expm1(static_cast<double>(a.m) * log1p(a.rho - 1.0)) / (1.0 - a.rho);
+#pragma unroll
+    for (int k = 0; k < RT; ++k) {
+      if (!own[k]) continue;
+      const int r = tid + k * kChainThreads;
+#pragma unroll
+      for (int c = 0; c < PC; ++c)
+        if (c < pc) {
+          const int64_t o = static_cast<int64_t>(r0 + r) * a.ldw + c0 + c;
+          a.W[o] = fma(beta, a.C[o], v[k][c]);
+        }
+    }
+  }
+  cluster.sync();
+}
+
 template <int PC>
 void launch_chain_pc(const EpochArgs& a, const EpochConfig& cfg, cudaStream_t st) {
   // 0: auto (scalar smem phases for PC <= 2, DMMA phases above), 1: DMMA,
@@ -1242,12 +1621,27 @@ void launch_chain_pc(const EpochArgs& a, const EpochConfig& cfg, cudaStream_t st
   if constexpr (PC <= 4) {
     if (mode == 3) kern = cfg.rows_per_cta <= kChainThreads ? k_svrg_chain_rr<PC, kBlock, 1> : k_svrg_chain_rr<PC, kBlock, 2>;
   }
-  GAPLRA_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(cfg.smem)));
+  if constexpr (PC <= 3) {
+    if (mode == 4)
+      kern = cfg.rows_per_cta <= kChainThreads ? k_svrg_chain_v2<PC, kBlock, 1> : k_svrg_chain_v2<PC, kBlock, 2>;
+  }
+  int stages = cfg.stages;
+  size_t smem = cfg.smem;
+  if (mode == 4) {  // v2: no empty barriers, deeper ring where shared memory allows
+    stages = 2;
+    for (int sN = kChainV2MaxStages; sN > 2; --sN)
+      if (chain_smem<PC, kBlock, true>(cfg.rows_per_cta, sN).total <= 227 * 1024) {
+        stages = sN;
+        break;
+      }
+    smem = chain_smem<PC, kBlock, true>(cfg.rows_per_cta, stages).total;
+  }
+  GAPLRA_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   if (cfg.cluster > 8) GAPLRA_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   cudaLaunchConfig_t lc = {};
   lc.gridDim = dim3(cfg.cluster, cfg.groups, 1);
-  lc.blockDim = dim3(kChainThreads + 32, 1, 1);
-  lc.dynamicSmemBytes = cfg.smem;
+  lc.blockDim = dim3(kChainThreads + (mode == 4 ? 0 : 32 * kChainProducers), 1, 1);
+  lc.dynamicSmemBytes = smem;
   lc.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -1258,7 +1652,7 @@ void launch_chain_pc(const EpochArgs& a, const EpochConfig& cfg, cudaStream_t st
   lc.numAttrs = 1;
   EpochArgs args = a;
   args.rows_per_cta = cfg.rows_per_cta;
-  args.stages = cfg.stages;
+  args.stages = stages;
   args.pc = cfg.pc;
   args.groups = cfg.groups;
   args.slab_len = epoch_slab_len(cfg);
