@@ -1609,14 +1609,326 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_svrg_chain_v2(EpochArgs a)
   cluster.sync();
 }
 
+// ---------------------------------------------------------------------------
+// k_svrg_chain_v3: warp-specialised chain, the form measured fastest with
+// tools/chain_skeleton.cu (p = 1: 1408 vs 1903 cycles per block for the
+// 8-consumer form).  7 warps:
+//   warps 0..3  rows: thread = rows 2·tid, 2·tid+1 (LDS.128 per slice),
+//               V in registers; per block t: load block t+1's slice rows,
+//               products with V_t, select-free warp halving, red; barrier
+//               (rows); push Â_{t+1} (16-byte st.async); wait coef_t; update
+//   warp 4      reducer: wait Â_t, fixed-order slot sum, coef_t = TT_t Â_t +
+//               pre_t, signal the rows, then pre_{t+1} = M_{t+1} coef_t + U_{t+1}
+//               — concurrently with the rows' products of block t+1
+//   warps 5, 6  producers (8 slices each; warp 5 also the slab part)
+// The coef hand-off alternates two named barriers (even / odd blocks), so the
+// reducer can never arrive twice on one barrier phase.
+// ---------------------------------------------------------------------------
+constexpr int kV3Rows = 4;       // row warps
+constexpr int kV3Producers = 2;  // producer warps
+constexpr int kV3Threads = 32 * (kV3Rows + 1 + kV3Producers);
+
+template <int PC, int B>
+__global__ void __launch_bounds__(kV3Threads, 1) k_svrg_chain_v3(EpochArgs a) {
+  static_assert(B == 16, "lane permutation j = i ^ (lane >> 1) covers 16 slices");
+  constexpr bool XREG = PC == 1;  // update from the products' registers (else re-read the stage)
+  extern __shared__ __align__(128) double sm[];
+  cg::cluster_group cluster = cg::this_cluster();
+  const int G = static_cast<int>(cluster.num_blocks());
+  const int lgG = G == 16 ? 4 : (G == 8 ? 3 : (G == 4 ? 2 : (G == 2 ? 1 : 0)));
+  const int g = static_cast<int>(cluster.block_rank());
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NV = B * PC;
+  const int grp = blockIdx.y;
+  const int c0 = grp * PC;
+  const int pc = min(PC, a.p - c0);
+  const ChainSmem L = chain_smem<PC, B, true>(a.rows_per_cta, a.stages);
+  static_assert(kV3Rows * NV + 4 * NV <= kChainThreads / 32 * (B / 8) * 64, "red + coef + ahat + pre fit in red");
+  const int S = L.stages;
+  const int r0 = g * a.rows_per_cta;
+  const int rc = max(0, min(a.rows_per_cta, a.d_pad - r0));
+  const int RP = L.rows_pad;
+  double* recv = sm + L.off_recv;  // [kRecvSlots][kMaxCluster][NV]
+  double* red = sm + L.off_red;    // [kV3Rows][NV]
+  double* coef = red + kV3Rows * NV;  // [2][NV]
+  double* Ahat = coef + 2 * NV;       // [NV]
+  double* pre = Ahat + NV;            // [NV]
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + L.off_bar);  // [S <= 4]
+  uint64_t* empty = full + 4;                                     // [S]
+  uint64_t* rbar = full + 8;                                      // [kRecvSlots]
+  auto stage_at = [&](int s_idx) { return sm + L.off_stage + static_cast<size_t>(s_idx) * L.stage_len; };
+  const int nb = static_cast<int>((a.m + B - 1) / B);
+  const int last_bt = static_cast<int>(a.m - static_cast<int64_t>(nb - 1) * B);
+  auto bt_of = [&](int t) { return t == nb - 1 ? last_bt : B; };
+  double rho_b = 1.0, rho_last = 1.0;
+  for (int j = 0; j < B; ++j) rho_b *= a.rho;
+  for (int j = 0; j < last_bt; ++j) rho_last *= a.rho;
+#pragma unroll 1
+  for (size_t e = tid; e < L.off_v; e += blockDim.x) sm[e] = 0.0;  // pad rows / unwritten slices read as 0
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], kV3Producers);
+      mbar_init(&empty[s], kV3Rows + 1);
+    }
+    for (int q = 0; q < kRecvSlots; ++q) mbar_init(&rbar[q], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  cluster.sync();
+
+  if (warp > kV3Rows) {  // ------------------------------------------------ producers
+    chain_produce<PC, B, kV3Producers>(a, warp - kV3Rows - 1, lane, nb, last_bt, S, rc, r0, RP, grp,
+                                       sm + L.off_stage, L.stage_len, full, empty);
+  } else if (warp == kV3Rows) {  // ------------------------------------------ reducer
+    auto arm = [&](int u) {
+      if (lane == 0)
+        mbar_expect_tx(&rbar[u & (kRecvSlots - 1)], static_cast<uint32_t>(G * ((bt_of(u) * PC + 1) & ~1) * 8));
+    };
+    if (nb > 0) {
+      arm(0);
+      mbar_wait(&full[0], 0);
+      const double* Ub = stage_at(0) + B * RP + 2 * B * B;
+      for (int e = lane; e < NV; e += 32) pre[e] = Ub[e];
+    }
+    int cs = 0;
+    uint32_t cph = 0;  // full-barrier parity of stage cs
+#pragma unroll 1
+    for (int t = 0; t < nb; ++t) {
+      const bool more = t + 1 < nb;
+      const int ns = cs + 1 == S ? 0 : cs + 1;
+      const uint32_t nph = ns == 0 ? cph ^ 1u : cph;
+      if (more) arm(t + 1);
+      const int par = t & (kRecvSlots - 1);
+      mbar_wait(&rbar[par], static_cast<uint32_t>((t >> 2) & 1));
+      const int nv = bt_of(t) * PC;
+      for (int e = lane; e < NV; e += 32) {
+        double s = 0.0;
+        if (e < nv) {
+          const double* sl = recv + par * kMaxCluster * NV + e;
+          double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll 1
+          for (int q = 0; q < G; q += 4) {
+            s0 += sl[q * NV];
+            s1 += sl[(q + 1) * NV];
+            s2 += sl[(q + 2) * NV];
+            s3 += sl[(q + 3) * NV];
+          }
+          s = (s0 + s1) + (s2 + s3);
+        }
+        Ahat[e] = s;
+      }
+      __syncwarp();
+      const double* TT = stage_at(cs) + B * RP;
+      double* cf = coef + (t & 1) * NV;
+      for (int e = lane; e < NV; e += 32) {
+        const int j = e / PC, c = e - (e / PC) * PC;
+        double s0 = pre[e], s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+        for (int l = 0; l < B; l += 4) {
+          s0 = fma(TT[l * B + j], Ahat[l * PC + c], s0);
+          s1 = fma(TT[(l + 1) * B + j], Ahat[(l + 1) * PC + c], s1);
+          s2 = fma(TT[(l + 2) * B + j], Ahat[(l + 2) * PC + c], s2);
+          s3 = fma(TT[(l + 3) * B + j], Ahat[(l + 3) * PC + c], s3);
+        }
+        cf[e] = (s0 + s1) + (s2 + s3);
+      }
+      // coef_t ready for the rows (even / odd barrier)
+      if (t & 1)
+        asm volatile("bar.arrive 3, %0;" ::"n"(32 * (kV3Rows + 1)) : "memory");
+      else
+        asm volatile("bar.arrive 2, %0;" ::"n"(32 * (kV3Rows + 1)) : "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[cs]);  // TT_t was the reducer's last use of stage t
+      if (more) {  // pre_{t+1} = M_{t+1} coef_t + U_{t+1}
+        mbar_wait(&full[ns], nph);
+        const double* M = stage_at(ns) + B * RP + B * B;
+        const double* Ub = M + B * B;
+        for (int e = lane; e < NV; e += 32) {
+          const int j = e / PC, c = e - (e / PC) * PC;
+          double s0 = Ub[e], s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+          for (int l = 0; l < B; l += 4) {
+            s0 = fma(M[l * B + j], cf[l * PC + c], s0);
+            s1 = fma(M[(l + 1) * B + j], cf[(l + 1) * PC + c], s1);
+            s2 = fma(M[(l + 2) * B + j], cf[(l + 2) * PC + c], s2);
+            s3 = fma(M[(l + 3) * B + j], cf[(l + 3) * PC + c], s3);
+          }
+          pre[e] = (s0 + s1) + (s2 + s3);
+        }
+        __syncwarp();
+      }
+      cs = ns;
+      cph = nph;
+    }
+  } else {  // --------------------------------------------------------------- rows
+    const int pm = lane >> 1;  // product order j = i ^ pm
+    const int ra = 2 * tid;    // rows ra, ra + 1
+    const bool own0 = ra < rc, own1 = ra + 1 < rc;
+    double v0[PC], v1[PC];
+#pragma unroll
+    for (int c = 0; c < PC; ++c) {
+      v0[c] = own0 && c < pc ? a.W[static_cast<int64_t>(r0 + ra) * a.ldw + c0 + c] : 0.0;
+      v1[c] = own1 && c < pc ? a.W[static_cast<int64_t>(r0 + ra + 1) * a.ldw + c0 + c] : 0.0;
+    }
+    int ws = 0;
+    uint32_t wph = 0;
+    auto wait_stage = [&]() {  // blocks are waited for in order 0, 1, 2, ...
+      mbar_wait(&full[ws], wph);
+      const int s = ws;
+      if (++ws == S) {
+        ws = 0;
+        wph ^= 1u;
+      }
+      return s;
+    };
+    auto load_rows = [&](const double* xb, double2 (&xr)[B]) {
+#pragma unroll
+      for (int i = 0; i < B; ++i) xr[i] = *reinterpret_cast<const double2*>(xb + (i ^ pm) * RP + ra);
+    };
+    auto products = [&](const double2 (&xr)[B]) {
+      double val[B][PC];
+#pragma unroll
+      for (int i = 0; i < B; ++i)
+#pragma unroll
+        for (int c = 0; c < PC; ++c) val[i][c] = fma(xr[i].x, v0[c], xr[i].y * v1[c]);
+#pragma unroll
+      for (int o = 16, n = B / 2; o >= 2; o >>= 1, n >>= 1)
+#pragma unroll
+        for (int i = 0; i < n; ++i)
+#pragma unroll
+          for (int c = 0; c < PC; ++c) val[i][c] += __shfl_xor_sync(0xffffffffu, val[i + n][c], o);
+#pragma unroll
+      for (int c = 0; c < PC; ++c) val[0][c] += __shfl_xor_sync(0xffffffffu, val[0][c], 1);
+      if (!(lane & 1))
+#pragma unroll
+        for (int c = 0; c < PC; ++c) red[warp * NV + pm * PC + c] = val[0][c];
+    };
+    auto push = [&](int u) {  // entry pairs (16-byte st.async), the 4 warp partials summed in fixed order
+      const int par = u & (kRecvSlots - 1);
+      const int np = (bt_of(u) * PC + 1) >> 1;
+      const uint32_t slot = smem_u32(recv + (par * kMaxCluster + g) * NV);
+      const uint32_t rbl = smem_u32(&rbar[par]);
+#pragma unroll 1
+      for (int i = tid; i < (np << lgG); i += 32 * kV3Rows) {
+        const int e = (i >> lgG) * 2, q = i & (G - 1);
+        const double s0 = (red[e] + red[NV + e]) + (red[2 * NV + e] + red[3 * NV + e]);
+        const double s1 = (red[e + 1] + red[NV + e + 1]) + (red[2 * NV + e + 1] + red[3 * NV + e + 1]);
+        st_async_f64x2(mapa(slot, q) + e * 8u, s0, s1, mapa(rbl, q));
+      }
+    };
+    auto rows_sync = []() { asm volatile("bar.sync 1, %0;" ::"n"(32 * kV3Rows) : "memory"); };
+    auto update = [&](const double2 (&xr)[B], int t, double rn) {
+      if (t & 1)
+        asm volatile("bar.sync 3, %0;" ::"n"(32 * (kV3Rows + 1)) : "memory");
+      else
+        asm volatile("bar.sync 2, %0;" ::"n"(32 * (kV3Rows + 1)) : "memory");
+      const double* cf = coef + (t & 1) * NV;
+      double a0[PC], a1[PC];
+#pragma unroll
+      for (int c = 0; c < PC; ++c) a0[c] = a1[c] = 0.0;
+#pragma unroll
+      for (int i = 0; i < B; i += 2)
+#pragma unroll
+        for (int c = 0; c < PC; ++c) {
+          const double k0 = cf[(i ^ pm) * PC + c], k1 = cf[((i + 1) ^ pm) * PC + c];
+          v0[c] = fma(xr[i].x, k0, v0[c]);
+          v1[c] = fma(xr[i].y, k0, v1[c]);
+          a0[c] = fma(xr[i + 1].x, k1, a0[c]);
+          a1[c] = fma(xr[i + 1].y, k1, a1[c]);
+        }
+#pragma unroll
+      for (int c = 0; c < PC; ++c) {
+        v0[c] = own0 ? (v0[c] + a0[c]) * rn : 0.0;
+        v1[c] = own1 ? (v1[c] + a1[c]) * rn : 0.0;
+      }
+    };
+    double2 xa[B], xn[B];
+    if (nb > 0) {  // Â_0 = X_{B_0}ᵀ Ŵ_0, then V_0 = ρ^{b_0} Ŵ_0
+      const int s = wait_stage();
+      load_rows(stage_at(s), xa);
+      if (!XREG) {
+        // stage 0 stays until its update; released below
+      } else {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+      }
+      products(xa);
+      rows_sync();
+      push(0);
+      double rb = 1.0;
+      for (int j = 0; j < bt_of(0); ++j) rb *= a.rho;
+#pragma unroll
+      for (int c = 0; c < PC; ++c) {
+        v0[c] *= rb;
+        v1[c] *= rb;
+      }
+    }
+    // block t: products of t+1 (stage ns) then the update of t
+    auto step = [&](int t, double2 (&xr)[B], double2 (&xq)[B]) {
+      const bool more = t + 1 < nb;
+      if (more) {
+        const int s = wait_stage();
+        load_rows(stage_at(s), xq);
+        if (XREG) {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty[s]);
+        }
+        products(xq);
+        rows_sync();  // red complete (and the previous push's red reads done: they preceded the coef barrier)
+        push(t + 1);
+      }
+      const double rn = !more ? 1.0 : (t + 1 == nb - 1 ? rho_last : rho_b);
+      if (XREG) {
+        update(xr, t, rn);
+      } else {
+        const int cs = t % S;
+        double2 xt[B];
+        load_rows(stage_at(cs), xt);
+        update(xt, t, rn);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[cs]);
+      }
+      // the next products' red writes follow the coef barrier, which every row
+      // thread passes after its push reads
+    };
+    if (XREG) {
+      int t = 0;
+#pragma unroll 1
+      for (; t + 1 < nb; t += 2) {
+        step(t, xa, xn);
+        step(t + 1, xn, xa);
+      }
+      if (t < nb) step(t, xa, xn);
+    } else {
+#pragma unroll 1
+      for (int t = 0; t < nb; ++t) step(t, xa, xn);
+    }
+    const double beta = -expm1(static_cast<double>(a.m) * log1p(a.rho - 1.0)) / (1.0 - a.rho);
+#pragma unroll
+    for (int c = 0; c < PC; ++c)
+      if (c < pc) {
+        if (own0) {
+          const int64_t o = static_cast<int64_t>(r0 + ra) * a.ldw + c0 + c;
+          a.W[o] = fma(beta, a.C[o], v0[c]);
+        }
+        if (own1) {
+          const int64_t o = static_cast<int64_t>(r0 + ra + 1) * a.ldw + c0 + c;
+          a.W[o] = fma(beta, a.C[o], v1[c]);
+        }
+      }
+  }
+  cluster.sync();
+}
+
 template <int PC>
 void launch_chain_pc(const EpochArgs& a, const EpochConfig& cfg, cudaStream_t st) {
-  // 0: auto (scalar smem phases for PC <= 2, DMMA phases above), 1: DMMA,
-  // 2: scalar smem, 3: register-row (PC <= 4).  Measured r01 (cycles per
-  // 16-step block, C2): PC=1 scalar 3030 / DMMA 3976 / reg-row 3738;
-  // PC=3 DMMA 4449 / scalar 5014 / reg-row 5092.
+  // 0: auto (warp-specialised v3 where it fits: PC <= 3 and <= 256 rows per
+  // CTA; else scalar smem phases for PC <= 2, DMMA phases above), 1: DMMA,
+  // 2: scalar smem, 3: register-row, 4: register-row v2, 5: v3.
+  // Measured r01 on C2 (ms per epoch, p = 1 / p = 20 at PC = 3):
+  // v3 9.97 / 18.95; scalar 19.1 / 29.4; DMMA 25.1 / 28.0.
   static const int env_mode = getenv("GAPLRA_CHAIN_MODE") ? atoi(getenv("GAPLRA_CHAIN_MODE")) : 0;
-  const int mode = env_mode ? env_mode : (PC <= 2 ? 2 : 1);
+  const bool v3_fits = PC <= 3 && cfg.rows_per_cta <= 2 * 32 * kV3Rows;
+  const int mode = env_mode ? env_mode : (v3_fits ? 5 : (PC <= 2 ? 2 : 1));
   auto kern = mode == 1 ? k_svrg_chain<PC, kBlock, false> : k_svrg_chain<PC, kBlock, true>;
   if constexpr (PC <= 4) {
     if (mode == 3) kern = cfg.rows_per_cta <= kChainThreads ? k_svrg_chain_rr<PC, kBlock, 1> : k_svrg_chain_rr<PC, kBlock, 2>;
@@ -1625,8 +1937,21 @@ void launch_chain_pc(const EpochArgs& a, const EpochConfig& cfg, cudaStream_t st
     if (mode == 4)
       kern = cfg.rows_per_cta <= kChainThreads ? k_svrg_chain_v2<PC, kBlock, 1> : k_svrg_chain_v2<PC, kBlock, 2>;
   }
+  if constexpr (PC <= 3) {
+    if (mode == 5 && cfg.rows_per_cta <= 2 * 32 * kV3Rows) kern = k_svrg_chain_v3<PC, kBlock>;
+  }
+  const bool v3 = mode == 5 && PC <= 3 && cfg.rows_per_cta <= 2 * 32 * kV3Rows;
   int stages = cfg.stages;
   size_t smem = cfg.smem;
+  if (v3) {  // pitch ≡ 0 (mod 16) layout, at most 4 stages (barrier slots)
+    stages = 2;
+    for (int sN = 4; sN > 2; --sN)
+      if (chain_smem<PC, kBlock, true>(cfg.rows_per_cta, sN).total <= 227 * 1024) {
+        stages = sN;
+        break;
+      }
+    smem = chain_smem<PC, kBlock, true>(cfg.rows_per_cta, stages).total;
+  }
   if (mode == 4) {  // v2: no empty barriers, deeper ring where shared memory allows
     stages = 2;
     for (int sN = kChainV2MaxStages; sN > 2; --sN)
@@ -1640,7 +1965,7 @@ void launch_chain_pc(const EpochArgs& a, const EpochConfig& cfg, cudaStream_t st
   if (cfg.cluster > 8) GAPLRA_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   cudaLaunchConfig_t lc = {};
   lc.gridDim = dim3(cfg.cluster, cfg.groups, 1);
-  lc.blockDim = dim3(kChainThreads + (mode == 4 ? 0 : 32 * kChainProducers), 1, 1);
+  lc.blockDim = dim3(v3 ? kV3Threads : kChainThreads + (mode == 4 ? 0 : 32 * kChainProducers), 1, 1);
   lc.dynamicSmemBytes = smem;
   lc.stream = st;
   cudaLaunchAttribute attr[1];

@@ -394,10 +394,191 @@ void run3(const double* X, const int* idx, int nb, long long* d) {
   fflush(stdout);
 }
 
+// ---- k4: 4 row warps x 2 rows/thread (LDS.128), warp 4 reducer, warp 5 producer
+template <int S, int NP = 1>
+__global__ void __cluster_dims__(16, 1, 1) __launch_bounds__(256, 1) k4(const double* X, const int* idx, int nb, long long* out) {
+  extern __shared__ __align__(128) double sm[];
+  const size_t SL = B * RP + 512;
+  double* stage = sm;
+  double* recv = sm + S * SL;          // [4][16][16]
+  double* red = recv + 4 * 256;        // [4][16]
+  double* coef = red + 64;             // [2][16]
+  double* ahat = coef + 32;            // [16]
+  uint64_t* full = reinterpret_cast<uint64_t*>(ahat + 16);
+  uint64_t* empty = full + S;
+  uint64_t* rbar = empty + S;
+  cg::cluster_group cl = cg::this_cluster();
+  const int g = cl.block_rank(), tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, pm = lane >> 1;
+  if (tid == 0) {
+    for (int i = 0; i < S; ++i) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(&full[i])), "r"(NP));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 5;" ::"r"(su32(&empty[i])));
+    }
+    for (int i = 0; i < 4; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&rbar[i])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int e = tid; e < S * SL; e += blockDim.x) stage[e] = 0.001 * (e & 7);
+  for (int e = tid; e < 32; e += blockDim.x) coef[e] = 0.0;
+  __syncthreads();
+  cl.sync();
+  long long t0 = clock64();
+  long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0}, tp = clock64();
+  auto tk = [&](int k) {
+    long long now;
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(now)::"memory");
+    ph[k] += now - tp;
+    tp = now;
+  };
+  if (warp >= 5) {
+    const int pw = warp - 5, per = 16 / NP;
+    for (int u = 0; u < nb; ++u) {
+      const int s = u % S;
+      if (u >= S) mwait(&empty[s], ((u / S) - 1) & 1);
+      if (lane == 0) expect(&full[s], (per * RC + (pw == 0 ? 512 : 0)) * 8);
+      __syncwarp();
+      if (lane < per) {
+        const int jj = pw * per + lane;
+        const double* src = X + static_cast<int64_t>(idx[u * B + jj]) * 4096 + g * RC;
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(su32(stage + s * SL + jj * RP)),
+                     "l"(src), "r"(RC * 8), "r"(su32(&full[s])) : "memory");
+      }
+      if (lane == 31 && pw == 0)
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(su32(stage + s * SL + B * RP)),
+                     "l"(X), "r"(512 * 8), "r"(su32(&full[s])) : "memory");
+    }
+  } else if (warp == 4) {
+    if (lane == 0) expect(&rbar[0], 16 * 16 * 8);
+    for (int t = 0; t < nb; ++t) {
+      if (lane == 0 && t + 1 < nb) expect(&rbar[(t + 1) & 3], 16 * 16 * 8);
+      tk(0);
+      mwait(&full[t % S], (t / S) & 1);
+      tk(1);
+      mwait(&rbar[t & 3], (t >> 2) & 1);
+      tk(2);
+      double a = 0;
+      if (lane < 16) {
+        double s0 = 0, s1 = 0, s2 = 0, s3 = 0;
+        const double* sl = recv + (t & 3) * 256 + lane;
+        for (int q = 0; q < 16; q += 4) {
+          s0 += sl[q * 16];
+          s1 += sl[(q + 1) * 16];
+          s2 += sl[(q + 2) * 16];
+          s3 += sl[(q + 3) * 16];
+        }
+        a = (s0 + s1) + (s2 + s3);
+      }
+      tk(3);
+      {  // coef via shuffles of Â (no smem round trip)
+        double s0 = 0, s1 = 0, s2 = 0, s3 = 0;
+        const double* TT = stage + (t % S) * SL + B * RP;
+        const int j = lane & 15;
+        for (int l = 0; l < 16; l += 4) {
+          s0 = fma(TT[l * 16 + j], __shfl_sync(0xffffffffu, a, l), s0);
+          s1 = fma(TT[(l + 1) * 16 + j], __shfl_sync(0xffffffffu, a, l + 1), s1);
+          s2 = fma(TT[(l + 2) * 16 + j], __shfl_sync(0xffffffffu, a, l + 2), s2);
+          s3 = fma(TT[(l + 3) * 16 + j], __shfl_sync(0xffffffffu, a, l + 3), s3);
+        }
+        if (lane < 16) coef[(t & 1) * 16 + lane] = ((s0 + s1) + (s2 + s3)) * 1e-3;
+      }
+      tk(4);
+      asm volatile("bar.arrive 2, 160;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&empty[t % S])) : "memory");
+      tk(5);
+    }
+  } else {  // 4 row warps, rows 2 tid, 2 tid + 1
+    double v0 = 1.0 + tid * 1e-6, v1 = 1.0 - tid * 1e-6;
+    double2 xa[B], xb2[B];
+    mwait(&full[0], 0);
+    for (int i = 0; i < B; ++i) xa[i] = *reinterpret_cast<const double2*>(stage + (i ^ pm) * RP + 2 * tid);
+    __syncwarp();
+    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&empty[0])) : "memory");
+    for (int rep = tid; rep < 256; rep += 128) {
+      const int e = rep >> 4, q = rep & 15;
+      asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(mapa(su32(recv + g * 16), q) + e * 8),
+                   "l"(__double_as_longlong(v0)), "r"(mapa(su32(&rbar[0]), q)) : "memory");
+    }
+    auto step = [&](int t, double2 (&xr)[B], double2 (&xn)[B]) {
+      const bool more = t + 1 < nb;
+      tk(0);
+      if (more) {
+        mwait(&full[(t + 1) % S], ((t + 1) / S) & 1);
+        tk(1);
+        const double* xb = stage + ((t + 1) % S) * SL;
+        double val[B];
+        for (int i = 0; i < B; ++i) xn[i] = *reinterpret_cast<const double2*>(xb + (i ^ pm) * RP + 2 * tid);
+        __syncwarp();
+        if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&empty[(t + 1) % S])) : "memory");
+        for (int i = 0; i < B; ++i) val[i] = fma(xn[i].x, v0, xn[i].y * v1);
+        for (int o = 16, n = B / 2; o >= 2; o >>= 1, n >>= 1)
+          for (int i = 0; i < n; ++i) val[i] += __shfl_xor_sync(0xffffffffu, val[i + n], o);
+        val[0] += __shfl_xor_sync(0xffffffffu, val[0], 1);
+        if (!(lane & 1)) red[warp * 16 + pm] = val[0];
+        tk(2);
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        tk(3);
+        const int par = (t + 1) & 3;
+        for (int rep = tid; rep < 256; rep += 128) {
+          const int e = rep >> 4, q = rep & 15;
+          const double s = (red[e] + red[16 + e]) + (red[32 + e] + red[48 + e]);
+          asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(mapa(su32(recv + (par * 16 + g) * 16), q) + e * 8),
+                       "l"(__double_as_longlong(s)), "r"(mapa(su32(&rbar[par]), q)) : "memory");
+        }
+      }
+      tk(4);
+      asm volatile("bar.sync 2, 160;" ::: "memory");
+      tk(5);
+      const double* cf = coef + (t & 1) * 16;
+      double a0 = 0, a1 = 0;
+      for (int i = 0; i < B; ++i) {
+        const double c = cf[i ^ pm];
+        v0 = fma(xr[i].x, c, v0);
+        v1 = fma(xr[i].y, c, v1);
+      }
+      v0 = (v0 + a0) * 0.999;
+      v1 = (v1 + a1) * 0.999;
+      tk(6);
+    };
+    int t = 0;
+    for (; t + 1 < nb; t += 2) {
+      step(t, xa, xb2);
+      step(t + 1, xb2, xa);
+    }
+    if (t < nb) step(t, xa, xb2);
+    if (v0 + v1 == 12345.0) out[1] = 1;
+  }
+  long long t1 = clock64();
+  if (tid == 0 && g == 0) out[0] = (t1 - t0) / nb;
+  if ((tid == 0 || tid == 128) && g == 0)
+    for (int k = 0; k < 8; ++k) out[2 + (tid == 128 ? 8 : 0) + k] = ph[k] / nb;
+  cl.sync();
+}
+template <int S, int NP = 1>
+void run4(const double* X, const int* idx, int nb, long long* d) {
+  const size_t smem = (S * (B * RP + 512) + 4 * 256 + 64 + 64) * 8 + 256;
+  cudaFuncSetAttribute(k4<S, NP>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaFuncSetAttribute(k4<S, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  k4<S, NP><<<16, 160 + 32 * NP, smem>>>(X, idx, nb, d);
+  long long h = -1;
+  cudaError_t e = cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
+  printf("k4 S=%d NP=%d cycles_per_block %lld err %s\n", S, NP, h, cudaGetErrorString(e));
+  long long hp[16];
+  cudaMemcpy(hp, d + 2, 16 * 8, cudaMemcpyDeviceToHost);
+  printf("  row warp0 [top, wait_full, load+products, bar1, push, bar2(coef), update]:");
+  for (int k = 0; k < 7; ++k) printf(" %lld", hp[k]);
+  printf("\n  reducer [top, wait_full, wait_rbar, sum, coef, arrive]:");
+  for (int k = 0; k < 6; ++k) printf(" %lld", hp[8 + k]);
+  printf("\n");
+  fflush(stdout);
+}
+
 int main() {
   double* X; int* idx; long long* d;
   main_old(&X, &idx, &d);
   run3<4>(X, idx, 12500, d);
-  run3<4, true>(X, idx, 12500, d);
+  run4<4, 1>(X, idx, 12500, d);
+  run4<4, 2>(X, idx, 12500, d);
+  run4<4, 4>(X, idx, 12500, d);
+  run4<5, 2>(X, idx, 12500, d);
   return 0;
 }
