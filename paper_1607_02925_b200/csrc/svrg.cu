@@ -82,6 +82,14 @@ __device__ __forceinline__ void st_async_f64x2(uint32_t remote_addr, double v0, 
                "d"(v0), "d"(v1), "r"(remote_bar)
                : "memory");
 }
+// Bulk shared::cta -> shared::cluster copy completing on the receiver's mbarrier.
+__device__ __forceinline__ void dsmem_bulk_copy(uint32_t remote_dst, uint32_t local_src, uint32_t bytes,
+                                                uint32_t remote_bar) {
+  asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   remote_dst),
+               "r"(local_src), "r"(bytes), "r"(remote_bar)
+               : "memory");
+}
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
@@ -1626,24 +1634,30 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_svrg_chain_v2(EpochArgs a)
 // ---------------------------------------------------------------------------
 constexpr int kV3Rows = 4;       // row warps
 constexpr int kV3Producers = 2;  // producer warps
-constexpr int kV3Threads = 32 * (kV3Rows + 1 + kV3Producers);
+// reducer warps: 2 once the block has more than 32 entries per column group
+// (they split the entries; measured p = 20 / PC = 3: one reducer warp was busy
+// 2818 of 2900 cycles per block)
+__host__ __device__ constexpr int v3_reducers(int pc) { return pc >= 2 ? 2 : 1; }
+__host__ __device__ constexpr int v3_threads(int pc) { return 32 * (kV3Rows + v3_reducers(pc) + kV3Producers); }
 
 template <int PC, int B>
-__global__ void __launch_bounds__(kV3Threads, 1) k_svrg_chain_v3(EpochArgs a) {
+__global__ void __launch_bounds__(v3_threads(PC), 1) k_svrg_chain_v3(EpochArgs a) {
   static_assert(B == 16, "lane permutation j = i ^ (lane >> 1) covers 16 slices");
   constexpr bool XREG = PC == 1;  // update from the products' registers (else re-read the stage)
   extern __shared__ __align__(128) double sm[];
   cg::cluster_group cluster = cg::this_cluster();
   const int G = static_cast<int>(cluster.num_blocks());
-  const int lgG = G == 16 ? 4 : (G == 8 ? 3 : (G == 4 ? 2 : (G == 2 ? 1 : 0)));
   const int g = static_cast<int>(cluster.block_rank());
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int NV = B * PC;
+  constexpr int NRD = v3_reducers(PC);
+  constexpr int EPW = (NV + NRD - 1) / NRD;  // entries per reducer warp
+  static_assert(EPW <= 32, "one entry per reducer lane");
   const int grp = blockIdx.y;
   const int c0 = grp * PC;
   const int pc = min(PC, a.p - c0);
   const ChainSmem L = chain_smem<PC, B, true>(a.rows_per_cta, a.stages);
-  static_assert(kV3Rows * NV + 4 * NV <= kChainThreads / 32 * (B / 8) * 64, "red + coef + ahat + pre fit in red");
+  static_assert(kV3Rows * NV + 6 * NV <= kChainThreads / 32 * (B / 8) * 64, "red + coef + ahat + pre + outv fit");
   const int S = L.stages;
   const int r0 = g * a.rows_per_cta;
   const int rc = max(0, min(a.rows_per_cta, a.d_pad - r0));
@@ -1653,6 +1667,7 @@ __global__ void __launch_bounds__(kV3Threads, 1) k_svrg_chain_v3(EpochArgs a) {
   double* coef = red + kV3Rows * NV;  // [2][NV]
   double* Ahat = coef + 2 * NV;       // [NV]
   double* pre = Ahat + NV;            // [NV]
+  double* outv = pre + NV;            // [2][NV] this CTA's summed partials, bulk-copied to every peer
   uint64_t* full = reinterpret_cast<uint64_t*>(sm + L.off_bar);  // [S <= 4]
   uint64_t* empty = full + 4;                                     // [S]
   uint64_t* rbar = full + 8;                                      // [kRecvSlots]
@@ -1668,26 +1683,47 @@ __global__ void __launch_bounds__(kV3Threads, 1) k_svrg_chain_v3(EpochArgs a) {
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], kV3Producers);
-      mbar_init(&empty[s], kV3Rows + 1);
+      mbar_init(&empty[s], kV3Rows + NRD);
     }
     for (int q = 0; q < kRecvSlots; ++q) mbar_init(&rbar[q], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   cluster.sync();
+  // GAPLRA_EPOCH_TIMING: cycles per block; rows (tid 0) in slots 0..5, reducer (lane 0) in 6..7
+  long long tacc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long tp;
+  asm volatile("mov.u64 %0, %%clock64;" : "=l"(tp)::"memory");
+  auto tick = [&](int kk) {
+    if (a.dbg) {
+      long long now;
+      asm volatile("mov.u64 %0, %%clock64;" : "=l"(now)::"memory");
+      tacc[kk] += now - tp;
+      tp = now;
+    }
+  };
 
-  if (warp > kV3Rows) {  // ------------------------------------------------ producers
-    chain_produce<PC, B, kV3Producers>(a, warp - kV3Rows - 1, lane, nb, last_bt, S, rc, r0, RP, grp,
+  if (warp >= kV3Rows + NRD) {  // ----------------------------------------- producers
+    chain_produce<PC, B, kV3Producers>(a, warp - kV3Rows - NRD, lane, nb, last_bt, S, rc, r0, RP, grp,
                                        sm + L.off_stage, L.stage_len, full, empty);
-  } else if (warp == kV3Rows) {  // ------------------------------------------ reducer
+  } else if (warp >= kV3Rows) {  // ------------------------------------------ reducers
+    const int rw = warp - kV3Rows;
+    const int me = rw * EPW + lane;  // this lane's entry
+    const bool mine = lane < EPW && me < NV;
+    auto red_sync = [&]() {
+      if constexpr (NRD > 1)
+        asm volatile("bar.sync 4, %0;" ::"n"(32 * NRD) : "memory");
+      else
+        __syncwarp();
+    };
     auto arm = [&](int u) {
-      if (lane == 0)
-        mbar_expect_tx(&rbar[u & (kRecvSlots - 1)], static_cast<uint32_t>(G * ((bt_of(u) * PC + 1) & ~1) * 8));
+      if (rw == 0 && lane == 0)
+        mbar_expect_tx(&rbar[u & (kRecvSlots - 1)], static_cast<uint32_t>(G * NV * 8));  // full vectors
     };
     if (nb > 0) {
       arm(0);
       mbar_wait(&full[0], 0);
       const double* Ub = stage_at(0) + B * RP + 2 * B * B;
-      for (int e = lane; e < NV; e += 32) pre[e] = Ub[e];
+      if (mine) pre[me] = Ub[me];
     }
     int cs = 0;
     uint32_t cph = 0;  // full-barrier parity of stage cs
@@ -1698,9 +1734,12 @@ __global__ void __launch_bounds__(kV3Threads, 1) k_svrg_chain_v3(EpochArgs a) {
       const uint32_t nph = ns == 0 ? cph ^ 1u : cph;
       if (more) arm(t + 1);
       const int par = t & (kRecvSlots - 1);
+      tick(7);
       mbar_wait(&rbar[par], static_cast<uint32_t>((t >> 2) & 1));
+      tick(6);
       const int nv = bt_of(t) * PC;
-      for (int e = lane; e < NV; e += 32) {
+      if (mine) {
+        const int e = me;
         double s = 0.0;
         if (e < nv) {
           const double* sl = recv + par * kMaxCluster * NV + e;
@@ -1716,10 +1755,11 @@ __global__ void __launch_bounds__(kV3Threads, 1) k_svrg_chain_v3(EpochArgs a) {
         }
         Ahat[e] = s;
       }
-      __syncwarp();
+      red_sync();  // Â_t complete
       const double* TT = stage_at(cs) + B * RP;
       double* cf = coef + (t & 1) * NV;
-      for (int e = lane; e < NV; e += 32) {
+      if (mine) {
+        const int e = me;
         const int j = e / PC, c = e - (e / PC) * PC;
         double s0 = pre[e], s1 = 0.0, s2 = 0.0, s3 = 0.0;
 #pragma unroll
@@ -1733,16 +1773,18 @@ __global__ void __launch_bounds__(kV3Threads, 1) k_svrg_chain_v3(EpochArgs a) {
       }
       // coef_t ready for the rows (even / odd barrier)
       if (t & 1)
-        asm volatile("bar.arrive 3, %0;" ::"n"(32 * (kV3Rows + 1)) : "memory");
+        asm volatile("bar.arrive 3, %0;" ::"n"(32 * (kV3Rows + NRD)) : "memory");
       else
-        asm volatile("bar.arrive 2, %0;" ::"n"(32 * (kV3Rows + 1)) : "memory");
+        asm volatile("bar.arrive 2, %0;" ::"n"(32 * (kV3Rows + NRD)) : "memory");
       __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[cs]);  // TT_t was the reducer's last use of stage t
+      if (lane == 0) mbar_arrive(&empty[cs]);  // TT_t was the reducers' last use of stage t
       if (more) {  // pre_{t+1} = M_{t+1} coef_t + U_{t+1}
+        red_sync();  // coef_t complete (the other reducer's half); its Â reads done
         mbar_wait(&full[ns], nph);
         const double* M = stage_at(ns) + B * RP + B * B;
         const double* Ub = M + B * B;
-        for (int e = lane; e < NV; e += 32) {
+        if (mine) {
+          const int e = me;
           const int j = e / PC, c = e - (e / PC) * PC;
           double s0 = Ub[e], s1 = 0.0, s2 = 0.0, s3 = 0.0;
 #pragma unroll
@@ -1758,6 +1800,10 @@ __global__ void __launch_bounds__(kV3Threads, 1) k_svrg_chain_v3(EpochArgs a) {
       }
       cs = ns;
       cph = nph;
+    }
+    if (a.dbg && lane == 0 && rw == 0) {
+      const int cta = blockIdx.y * gridDim.x + blockIdx.x;
+      for (int kk = 6; kk < 8; ++kk) a.dbg[cta * 8 + kk] = tacc[kk];
     }
   } else {  // --------------------------------------------------------------- rows
     const int pm = lane >> 1;  // product order j = i ^ pm
@@ -1784,7 +1830,13 @@ __global__ void __launch_bounds__(kV3Threads, 1) k_svrg_chain_v3(EpochArgs a) {
 #pragma unroll
       for (int i = 0; i < B; ++i) xr[i] = *reinterpret_cast<const double2*>(xb + (i ^ pm) * RP + ra);
     };
+    const bool issuer = lane < 4 && warp * 4 + lane < G;
+    const int peer = warp * 4 + lane;
+    auto push_prepare = [&]() {  // before the red barrier: the copies of two blocks ago no longer read their outv
+      if (issuer) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+    };
     auto products = [&](const double2 (&xr)[B]) {
+      push_prepare();
       double val[B][PC];
 #pragma unroll
       for (int i = 0; i < B; ++i)
@@ -1802,25 +1854,28 @@ __global__ void __launch_bounds__(kV3Threads, 1) k_svrg_chain_v3(EpochArgs a) {
 #pragma unroll
         for (int c = 0; c < PC; ++c) red[warp * NV + pm * PC + c] = val[0][c];
     };
-    auto push = [&](int u) {  // entry pairs (16-byte st.async), the 4 warp partials summed in fixed order
+    auto rows_sync = []() { asm volatile("bar.sync 1, %0;" ::"n"(32 * kV3Rows) : "memory"); };
+    // push: the 4 warp partials summed in fixed order into outv, then lanes
+    // 0..3 of each row warp bulk-copy it to 4 peers (16-byte aligned, NV*8 bytes;
+    // entries of a ragged block's missing slices are finite and never summed)
+    auto push = [&](int u) {
       const int par = u & (kRecvSlots - 1);
-      const int np = (bt_of(u) * PC + 1) >> 1;
-      const uint32_t slot = smem_u32(recv + (par * kMaxCluster + g) * NV);
-      const uint32_t rbl = smem_u32(&rbar[par]);
-#pragma unroll 1
-      for (int i = tid; i < (np << lgG); i += 32 * kV3Rows) {
-        const int e = (i >> lgG) * 2, q = i & (G - 1);
-        const double s0 = (red[e] + red[NV + e]) + (red[2 * NV + e] + red[3 * NV + e]);
-        const double s1 = (red[e + 1] + red[NV + e + 1]) + (red[2 * NV + e + 1] + red[3 * NV + e + 1]);
-        st_async_f64x2(mapa(slot, q) + e * 8u, s0, s1, mapa(rbl, q));
+      double* ov = outv + (u & 1) * NV;
+      if (tid < NV) ov[tid] = (red[tid] + red[NV + tid]) + (red[2 * NV + tid] + red[3 * NV + tid]);
+      fence_proxy_async();
+      rows_sync();
+      if (issuer) {
+        dsmem_bulk_copy(mapa(smem_u32(recv + (par * kMaxCluster + g) * NV), peer), smem_u32(ov), NV * 8u,
+                        mapa(smem_u32(&rbar[par]), peer));
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
       }
     };
-    auto rows_sync = []() { asm volatile("bar.sync 1, %0;" ::"n"(32 * kV3Rows) : "memory"); };
     auto update = [&](const double2 (&xr)[B], int t, double rn) {
       if (t & 1)
-        asm volatile("bar.sync 3, %0;" ::"n"(32 * (kV3Rows + 1)) : "memory");
+        asm volatile("bar.sync 3, %0;" ::"n"(32 * (kV3Rows + NRD)) : "memory");
       else
-        asm volatile("bar.sync 2, %0;" ::"n"(32 * (kV3Rows + 1)) : "memory");
+        asm volatile("bar.sync 2, %0;" ::"n"(32 * (kV3Rows + NRD)) : "memory");
+      tick(4);
       const double* cf = coef + (t & 1) * NV;
       double a0[PC], a1[PC];
 #pragma unroll
@@ -1866,15 +1921,20 @@ __global__ void __launch_bounds__(kV3Threads, 1) k_svrg_chain_v3(EpochArgs a) {
     auto step = [&](int t, double2 (&xr)[B], double2 (&xq)[B]) {
       const bool more = t + 1 < nb;
       if (more) {
+        tick(5);
         const int s = wait_stage();
+        tick(0);
         load_rows(stage_at(s), xq);
         if (XREG) {
           __syncwarp();
           if (lane == 0) mbar_arrive(&empty[s]);
         }
         products(xq);
+        tick(1);
         rows_sync();  // red complete (and the previous push's red reads done: they preceded the coef barrier)
+        tick(2);
         push(t + 1);
+        tick(3);
       }
       const double rn = !more ? 1.0 : (t + 1 == nb - 1 ? rho_last : rho_b);
       if (XREG) {
@@ -1901,6 +1961,10 @@ __global__ void __launch_bounds__(kV3Threads, 1) k_svrg_chain_v3(EpochArgs a) {
     } else {
 #pragma unroll 1
       for (int t = 0; t < nb; ++t) step(t, xa, xn);
+    }
+    if (a.dbg && tid == 0) {
+      const int cta = blockIdx.y * gridDim.x + blockIdx.x;
+      for (int kk = 0; kk < 6; ++kk) a.dbg[cta * 8 + kk] = tacc[kk];
     }
     const double beta = -expm1(static_cast<double>(a.m) * log1p(a.rho - 1.0)) / (1.0 - a.rho);
 #pragma unroll
@@ -1965,7 +2029,7 @@ void launch_chain_pc(const EpochArgs& a, const EpochConfig& cfg, cudaStream_t st
   if (cfg.cluster > 8) GAPLRA_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   cudaLaunchConfig_t lc = {};
   lc.gridDim = dim3(cfg.cluster, cfg.groups, 1);
-  lc.blockDim = dim3(v3 ? kV3Threads : kChainThreads + (mode == 4 ? 0 : 32 * kChainProducers), 1, 1);
+  lc.blockDim = dim3(v3 ? v3_threads(PC) : kChainThreads + (mode == 4 ? 0 : 32 * kChainProducers), 1, 1);
   lc.dynamicSmemBytes = smem;
   lc.stream = st;
   cudaLaunchAttribute attr[1];
