@@ -1219,25 +1219,6 @@ int round_pc(int pc) {
 
 }  // namespace
 
-EpochConfig choose_epoch_config(int d_pad, int p) {
-  EpochConfig cfg;
-  cfg.b = kBlock;
-  cfg.cluster = d_pad >= 1024 ? 16 : 8;
-  const int max_clusters = std::max(1, sm_count_dev() / cfg.cluster);
-  cfg.pc = round_pc(static_cast<int>(ceil_div(p, max_clusters)));
-  cfg.rows_per_cta = static_cast<int>(ceil_div(ceil_div(d_pad, cfg.cluster), 4) * 4);
-  const size_t cap = 227 * 1024;
-  for (;;) {
-    cfg.stages = 4;
-    while (cfg.stages > 2 && smem_for(cfg.pc, cfg.rows_per_cta, cfg.stages) > cap) --cfg.stages;
-    if (smem_for(cfg.pc, cfg.rows_per_cta, cfg.stages) <= cap || cfg.pc == 1) break;
-    cfg.pc = round_pc(cfg.pc - 1);
-  }
-  cfg.groups = static_cast<int>(ceil_div(p, cfg.pc));
-  cfg.smem = smem_for(cfg.pc, cfg.rows_per_cta, cfg.stages);
-  return cfg;
-}
-
 int64_t epoch_slab_len(const EpochConfig& cfg) {
   return 2 * kBlock * kBlock + static_cast<int64_t>(kBlock) * cfg.pc * cfg.groups;
 }
@@ -1981,6 +1962,69 @@ __global__ void __launch_bounds__(v3_threads(PC), 1) k_svrg_chain_v3(EpochArgs a
       }
   }
   cluster.sync();
+}
+
+// Clusters of `cluster` one-SM CTAs that can be resident at once (a cluster
+// lives inside one GPC, so this is below SMs / cluster when GPCs are uneven).
+int max_active_clusters(int cluster) {
+  static int cached[17] = {0};
+  if (cluster < 1 || cluster > 16) return 1;
+  if (cached[cluster]) return cached[cluster];
+  auto kern = k_svrg_chain_v3<1, kBlock>;
+  const int smem = 200 * 1024;  // any CTA of the chain takes a whole SM
+  GAPLRA_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  GAPLRA_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3(cluster, 64, 1);
+  lc.blockDim = dim3(v3_threads(1), 1, 1);
+  lc.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cluster;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  lc.attrs = attr;
+  lc.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, kern, &lc) != cudaSuccess || n < 1) {
+    (void)cudaGetLastError();
+    n = std::max(1, sm_count_dev() / cluster);
+  }
+  cached[cluster] = n;
+  return n;
+}
+
+EpochConfig choose_epoch_config(int d_pad, int p) {
+  // Candidate layouts: clusters of 16 or 8 CTAs splitting the d rows, PC RHS
+  // columns per cluster.  Prefer one the warp-specialised chain (v3) runs:
+  // PC <= 3 and <= 256 rows per CTA (C2: 16 x 256 rows, PC 3; C3: 8 x 256,
+  // PC 2); otherwise the largest cluster.  GAPLRA_CLUSTER=8|16 forces the size.
+  static const int env_cluster = getenv("GAPLRA_CLUSTER") ? atoi(getenv("GAPLRA_CLUSTER")) : 0;
+  auto make = [&](int cluster) {
+    EpochConfig cfg;
+    cfg.b = kBlock;
+    cfg.cluster = cluster;
+    const int max_clusters = max_active_clusters(cfg.cluster);
+    cfg.pc = round_pc(static_cast<int>(ceil_div(p, max_clusters)));
+    cfg.rows_per_cta = static_cast<int>(ceil_div(ceil_div(d_pad, cfg.cluster), 4) * 4);
+    const size_t cap = 227 * 1024;
+    for (;;) {
+      cfg.stages = 4;
+      while (cfg.stages > 2 && smem_for(cfg.pc, cfg.rows_per_cta, cfg.stages) > cap) --cfg.stages;
+      if (smem_for(cfg.pc, cfg.rows_per_cta, cfg.stages) <= cap || cfg.pc == 1) break;
+      cfg.pc = round_pc(cfg.pc - 1);
+    }
+    cfg.groups = static_cast<int>(ceil_div(p, cfg.pc));
+    cfg.smem = smem_for(cfg.pc, cfg.rows_per_cta, cfg.stages);
+    return cfg;
+  };
+  if (env_cluster == 8 || env_cluster == 16) return make(env_cluster);
+  const EpochConfig c16 = make(16), c8 = make(8);
+  auto v3_ok = [](const EpochConfig& c) { return c.pc <= 3 && c.rows_per_cta <= 256; };
+  if (d_pad < 1024) return c8;
+  if (v3_ok(c16)) return c16;
+  if (v3_ok(c8)) return c8;
+  return c16;
 }
 
 template <int PC>
