@@ -419,7 +419,12 @@ void epoch_dev(Context& c, Matrix& X, int p, double* W, const double* C, const d
     static const int skip = getenv("GAPLRA_EPOCH_SKIP") ? atoi(getenv("GAPLRA_EPOCH_SKIP")) : 0;
     a.skip = skip;
     DBuf<long long> dbg;
-    if (timing) a.dbg = dbg.ensure(static_cast<size_t>(cfg.cluster) * cfg.groups * 8);
+    if (timing) {
+      a.dbg = dbg.ensure(static_cast<size_t>(cfg.cluster) * cfg.groups * 8);
+      fprintf(stderr, "{\"epoch_layout\": {\"d_pad\": %d, \"p\": %d, \"cluster\": %d, \"pc\": %d, \"groups\": %d, "
+              "\"rows_per_cta\": %d, \"stages\": %d, \"smem\": %zu}}\n", a.d_pad, p, cfg.cluster, cfg.pc, cfg.groups,
+              cfg.rows_per_cta, cfg.stages, cfg.smem);
+    }
     {
       Prof prof(c, p > 1 ? kProfEpoch : kProfEpochP1, col_bytes * m, 4.0 * col_nnz * p * m);
       launch_svrg_epoch_dense(a, cfg, c.st);

@@ -1216,6 +1216,8 @@ int round_pc(int pc) {
   if (pc <= 6) return 6;
   return 8;
 }
+// next smaller supported PC (round_pc(pc - 1) would map 8 back to 8)
+int shrink_pc(int pc) { return pc == 8 ? 6 : (pc == 6 ? 4 : std::max(1, pc - 1)); }
 
 }  // namespace
 
@@ -2012,7 +2014,7 @@ EpochConfig choose_epoch_config(int d_pad, int p) {
       cfg.stages = 4;
       while (cfg.stages > 2 && smem_for(cfg.pc, cfg.rows_per_cta, cfg.stages) > cap) --cfg.stages;
       if (smem_for(cfg.pc, cfg.rows_per_cta, cfg.stages) <= cap || cfg.pc == 1) break;
-      cfg.pc = round_pc(cfg.pc - 1);
+      cfg.pc = shrink_pc(cfg.pc);
     }
     cfg.groups = static_cast<int>(ceil_div(p, cfg.pc));
     cfg.smem = smem_for(cfg.pc, cfg.rows_per_cta, cfg.stages);
