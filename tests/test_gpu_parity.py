@@ -132,6 +132,30 @@ def test_svrg_epoch_lockstep(g, oracle, p):
     assert rel(wd, wo) <= 1e-10
 
 
+@pytest.mark.timeout(120)
+@pytest.mark.parametrize("d,n,p,m", [
+    (4096, 300, 1, 1000),   # 16-CTA clusters x 256 rows, warp-specialised chain, PC = 1
+    (4096, 300, 3, 1000),   # PC = 3, one column group, two reducer warps
+    (4096, 300, 20, 1000),  # C2 layout: 7 groups x PC 3
+    (2048, 300, 32, 1000),  # C3 layout: 8-CTA clusters x 256 rows, 11 groups x PC 3
+    (8192, 200, 1, 500),    # C5 layout, p = 1: 512 rows per CTA (scalar chain)
+    (8192, 200, 64, 500),   # C5 layout: PC 6, two waves of clusters (DMMA chain)
+])
+def test_svrg_epoch_lockstep_layouts(g, oracle, d, n, p, m):
+    """One epoch at the production epoch layouts (m not a multiple of 16: a ragged last block)."""
+    rng = np.random.default_rng(d + p)
+    X = rng.standard_normal((d, n)) / np.sqrt(n)
+    lam = 1.2 * np.linalg.norm(X, 2) ** 2
+    mo = oracle.dense(X)
+    w0 = rng.standard_normal((d, p))
+    _, z, y = oracle.gram_block(mo, w0, want_y=True)
+    eta = 1.0 / (4.0 * (lam + n * oracle.max_col_norm2(mo)))
+    cblk = eta * (z + rng.standard_normal((d, p)))
+    rc, wo, _ = oracle.svrg_epoch(mo, w0, y, cblk, eta, lam, 31, m)
+    wd = g.svrg_epoch(g.DeviceMatrix.dense(X), w0, y, cblk, eta, lam, 31, m)
+    assert rel(wd, wo) <= 1e-10
+
+
 def test_svrg_epoch_sparse_lockstep(g, oracle):
     d, n, p = 120, 500, 4
     cp, ri, v = random_csc(d, n, 8, seed=2)
