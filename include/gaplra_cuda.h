@@ -114,7 +114,8 @@ typedef struct {
  * the algorithmic bytes / flops of those launches.
  * Classes: 0 gram pass X(XᵀW) (p > 1), 1 SVRG epoch chain (p > 1), 2 H = XᵀC
  * pass, 3 index stream, 4 QR (MGS2), 5 anchor epilogue, 6 per-block Gram/T
- * precompute, 7 gram pass (p = 1), 8 SVRG epoch chain (p = 1). */
+ * precompute (TT, M; run beside the previous epoch's chain), 7 gram pass
+ * (p = 1), 8 SVRG epoch chain (p = 1), 9 per-block U coefficients. */
 #define GAPLRA_PROF_CLASSES 12
 typedef struct {
   double ms[GAPLRA_PROF_CLASSES];

@@ -53,7 +53,7 @@ class SiReport(C.Structure):
 
 
 PROF_CLASSES = ["gram", "epoch", "h_pass", "index", "qr", "anchor", "block_gram", "gram_p1", "epoch_p1",
-                "r9", "r10", "r11"]
+                "block_u", "r10", "r11"]
 
 
 class Profile(C.Structure):
@@ -62,7 +62,7 @@ class Profile(C.Structure):
 
     def as_dict(self):
         return {name: {"ms": self.ms[i], "count": int(self.count[i]), "bytes": self.bytes[i],
-                       "flops": self.flops[i]} for i, name in enumerate(PROF_CLASSES[:9])}
+                       "flops": self.flops[i]} for i, name in enumerate(PROF_CLASSES[:10])}
 
 
 _SIGS = {

@@ -162,6 +162,7 @@ enum ProfClass {
   kProfBlockGram,
   kProfGramP1,   // X(Xᵀv) pass, p = 1 (Alg. 3 / tuning)
   kProfEpochP1,  // SVRG epoch chain, p = 1
+  kProfBlockU,   // per-epoch U coefficients of the s-step blocks (needs Y, H)
   kProfClasses
 };
 constexpr int kEpochBlock = 16;  // s-step block (svrg.cu kBlock)
@@ -178,8 +179,24 @@ struct Context {
   gaplra_ledger led{};
   // workspaces
   DBuf<double> gw, ybuf, hbuf, zbuf, cbuf, wbuf, bbuf, sbuf, tbuf, qrs, small, apart, bnorm, scal, tmp, tmat, zcol;
-  DBuf<int32_t> idx;
-  DBuf<unsigned int> rej;
+  DBuf<int32_t> idx, idx2;  // index streams of even / odd epochs
+  DBuf<double> tmat2;        // slab of odd epochs (tmat: even)
+  DBuf<unsigned int> rej, rej2;
+  // Side stream for the next epoch's W-independent precompute (index stream +
+  // k_block_prep), run beside the current epoch's chain on the SMs the chain
+  // leaves idle.  Events order it against the main stream.
+  cudaStream_t aux = nullptr;
+  cudaEvent_t pre_done[2] = {nullptr, nullptr}, chain_done[2] = {nullptr, nullptr};
+  cudaStream_t aux_stream() {
+    if (!aux) {
+      GAPLRA_CUDA_CHECK(cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking));
+      for (int i = 0; i < 2; ++i) {
+        GAPLRA_CUDA_CHECK(cudaEventCreateWithFlags(&pre_done[i], cudaEventDisableTiming));
+        GAPLRA_CUDA_CHECK(cudaEventCreateWithFlags(&chain_done[i], cudaEventDisableTiming));
+      }
+    }
+    return aux;
+  }
   DBuf<int> status;
   double* pin = nullptr;  // pinned host scalars
   int* pin_i = nullptr;
@@ -215,6 +232,14 @@ struct Context {
     if (pin_i) cudaFreeHost(pin_i);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
+    if (aux) {
+      cudaStreamSynchronize(aux);
+      for (int i = 0; i < 2; ++i) {
+        cudaEventDestroy(pre_done[i]);
+        cudaEventDestroy(chain_done[i]);
+      }
+      cudaStreamDestroy(aux);
+    }
     if (own) cudaStreamDestroy(own);
   }
   void sync() {
@@ -234,15 +259,17 @@ struct Prof {
   int cls;
   cudaEvent_t a = nullptr;
   double bytes, flops;
-  Prof(Context& cc, int k, double by, double fl) : c(cc), cls(k), bytes(by), flops(fl) {
+  cudaStream_t s;
+  Prof(Context& cc, int k, double by, double fl, cudaStream_t st = nullptr)
+      : c(cc), cls(k), bytes(by), flops(fl), s(st ? st : cc.st) {
     if (!c.profiling) return;
     a = c.new_event();
-    cudaEventRecord(a, c.st);
+    cudaEventRecord(a, s);
   }
   ~Prof() {
     if (!c.profiling) return;
     cudaEvent_t b = c.new_event();
-    cudaEventRecord(b, c.st);
+    cudaEventRecord(b, s);
     c.pending.push_back({cls, a, b});
     c.prof.count[cls] += 1;
     c.prof.bytes[cls] += bytes;
@@ -368,16 +395,52 @@ SvrgParams resolve(Context& c, Matrix& X, double lambda, const gaplra_svrg_param
   return s;
 }
 
-// One stochastic epoch on device blocks (ld = ldp(p)): W in/out, C, Y given;
-// H = Xᵀ C computed here (dense only).
-void epoch_dev(Context& c, Matrix& X, int p, double* W, const double* C, const double* Y, double eta,
-               double lambda, uint64_t stream_seed, int64_t m) {
-  const int64_t ld = ldp_of(p);
-  int32_t* idx = c.idx.ensure(static_cast<size_t>(m));
+// Dense epochs in two halves.
+//  epoch_pre_dev: the W-independent part — index stream and k_block_prep (TT, M
+//    of every 16-step block) — into the buffers of `parity` on stream `s`;
+//  epoch_run_dev: H = XᵀC, U (k_block_u), the chain, on the main stream.
+// svrg_solve_dev runs epoch e+1's pre on the side stream beside epoch e's chain.
+struct EpochPre {
+  int32_t* idx = nullptr;
+  double* slab = nullptr;
+  EpochConfig cfg{};
+  int64_t m = 0;
+};
+
+EpochPre epoch_pre_dev(Context& c, Matrix& X, int p, double eta, double lambda, uint64_t stream_seed, int64_t m,
+                       int parity, cudaStream_t s) {
+  EpochPre pre;
+  pre.m = m;
+  pre.idx = (parity ? c.idx2 : c.idx).ensure(static_cast<size_t>(m));
   {
-    Prof prof(c, kProfIndex, 4.0 * m, 0.0);
-    launch_index_stream(stream_seed, static_cast<uint64_t>(X.n), m, idx, c.rej.ensure(1), c.st);
+    Prof prof(c, kProfIndex, 4.0 * m, 0.0, s);
+    launch_index_stream(stream_seed, static_cast<uint64_t>(X.n), m, pre.idx, (parity ? c.rej2 : c.rej).ensure(1), s);
   }
+  if (X.kind != 0) return pre;
+  const double col_nnz = static_cast<double>(X.nnz) / X.n;
+  EpochArgs a{};
+  a.X = X.x;
+  a.ldx = X.ld;
+  a.d_pad = static_cast<int>(X.ld);
+  a.n = X.n;
+  a.idx = pre.idx;
+  a.m = m;
+  a.p = p;
+  a.rho = 1.0 - eta * lambda;
+  a.eta_n = eta * static_cast<double>(X.n);
+  pre.cfg = choose_epoch_config(a.d_pad, p);
+  pre.slab = (parity ? c.tmat2 : c.tmat).ensure(epoch_slab_elems(m, pre.cfg));
+  a.slab = pre.slab;
+  a.zcol = c.zcol.ensure(static_cast<size_t>(X.ld));
+  Prof prof(c, kProfBlockGram, 8.0 * X.d * m, 3.0 * kEpochBlock * col_nnz * m, s);
+  launch_block_prep(a, pre.cfg, s);
+  return pre;
+}
+
+void epoch_run_dev(Context& c, Matrix& X, int p, double* W, const double* C, const double* Y, double eta,
+                   double lambda, const EpochPre& pre) {
+  const int64_t ld = ldp_of(p);
+  const int64_t m = pre.m;
   const double col_nnz = static_cast<double>(X.nnz) / X.n;
   const double col_bytes = X.kind == 0 ? 8.0 * X.d : 12.0 * col_nnz;
   const double rho = 1.0 - eta * lambda;
@@ -397,7 +460,7 @@ void epoch_dev(Context& c, Matrix& X, int p, double* W, const double* C, const d
     a.ldx = X.ld;
     a.d_pad = static_cast<int>(X.ld);
     a.n = X.n;
-    a.idx = idx;
+    a.idx = pre.idx;
     a.m = m;
     a.W = W;
     a.C = C;
@@ -408,12 +471,12 @@ void epoch_dev(Context& c, Matrix& X, int p, double* W, const double* C, const d
     a.p = p;
     a.rho = rho;
     a.eta_n = eta_n;
-    const EpochConfig cfg = choose_epoch_config(a.d_pad, p);
-    a.slab = c.tmat.ensure(epoch_slab_elems(m, cfg));
+    const EpochConfig& cfg = pre.cfg;
+    a.slab = pre.slab;
     a.zcol = c.zcol.ensure(static_cast<size_t>(X.ld));
     {
-      Prof prof(c, kProfBlockGram, col_bytes * m, 3.0 * kEpochBlock * col_nnz * m);
-      launch_block_prep(a, cfg, c.st);
+      Prof prof(c, kProfBlockU, 16.0 * m * p, 2.0 * kEpochBlock * m * p);
+      launch_block_u(a, cfg, c.st);
     }
     static const bool timing = getenv("GAPLRA_EPOCH_TIMING") != nullptr;
     static const int skip = getenv("GAPLRA_EPOCH_SKIP") ? atoi(getenv("GAPLRA_EPOCH_SKIP")) : 0;
@@ -454,7 +517,7 @@ void epoch_dev(Context& c, Matrix& X, int p, double* W, const double* C, const d
     a.colptr = X.colptr.p;
     a.rowidx = X.rowidx.p;
     a.val = X.val.p;
-    a.idx = idx;
+    a.idx = pre.idx;
     a.m = m;
     a.W = W;
     a.C = C;
@@ -466,6 +529,14 @@ void epoch_dev(Context& c, Matrix& X, int p, double* W, const double* C, const d
     Prof prof(c, p > 1 ? kProfEpoch : kProfEpochP1, col_bytes * m, 4.0 * col_nnz * p * m);
     launch_svrg_epoch_sparse(a, c.st);
   }
+}
+
+// One stochastic epoch on device blocks (ld = ldp(p)): W in/out, C, Y given;
+// H = Xᵀ C computed here (dense only).  Everything on the main stream.
+void epoch_dev(Context& c, Matrix& X, int p, double* W, const double* C, const double* Y, double eta,
+               double lambda, uint64_t stream_seed, int64_t m) {
+  const EpochPre pre = epoch_pre_dev(c, X, p, eta, lambda, stream_seed, m, 0, c.st);
+  epoch_run_dev(c, X, p, W, C, Y, eta, lambda, pre);
 }
 
 // Block solve (λI − XXᵀ)W = B with W0 = 0; B, W device blocks with ld = ldp(p).
@@ -489,6 +560,20 @@ SvrgResult svrg_solve_dev(Context& c, Matrix& X, double lambda, int p, const dou
   SvrgResult& out = partial ? *partial : local;
   out = SvrgResult{};
   double best = INFINITY;
+  // epoch e+1's index stream + k_block_prep run on the side stream beside
+  // epoch e's chain (dense X); GAPLRA_OVERLAP=0 keeps everything on one stream
+  static const bool overlap = !(getenv("GAPLRA_OVERLAP") && atoi(getenv("GAPLRA_OVERLAP")) == 0);
+  const bool side = overlap && X.kind == 0;
+  EpochPre next;
+  bool have_next = false;
+  struct AuxJoin {  // the main stream never runs ahead of side-stream writes into shared buffers
+    Context& c;
+    bool used = false;
+    ~AuxJoin() {
+      if (used)
+        for (int i = 0; i < 2; ++i) cudaStreamWaitEvent(c.st, c.pre_done[i], 0);
+    }
+  } join{c};
   for (int e = 0;; ++e) {
     const bool zero = e == 0 && !warm;
     if (!zero) gram_block_dev(c, X, p, W, ld, Z, ld, Y, ld);
@@ -503,7 +588,27 @@ SvrgResult svrg_solve_dev(Context& c, Matrix& X, double lambda, int p, const dou
       throw Error(kSolverStalled, "solve_svrg: residual grew above slack x best (epoch " + std::to_string(e) + ")");
     best = std::min(best, r);
     if (e >= prm.cap) throw Error(kSolverStalled, "solve_svrg: epoch cap reached");
-    epoch_dev(c, X, p, W, C, Y, prm.eta, lambda, svrg_stream_seed(prm.root, solve_id, e), prm.m);
+    const int parity = e & 1;
+    EpochPre pre;
+    if (have_next) {
+      pre = next;
+      GAPLRA_CUDA_CHECK(cudaStreamWaitEvent(c.st, c.pre_done[parity], 0));
+    } else {
+      pre = epoch_pre_dev(c, X, p, prm.eta, lambda, svrg_stream_seed(prm.root, solve_id, e), prm.m, parity, c.st);
+    }
+    epoch_run_dev(c, X, p, W, C, Y, prm.eta, lambda, pre);
+    have_next = false;
+    if (side && e + 1 <= prm.cap) {
+      cudaStream_t aux = c.aux_stream();
+      join.used = true;
+      GAPLRA_CUDA_CHECK(cudaEventRecord(c.chain_done[parity], c.st));
+      // buffers of parity e+1 were last read by epoch e−1's chain
+      GAPLRA_CUDA_CHECK(cudaStreamWaitEvent(aux, c.chain_done[parity ^ 1], 0));
+      next = epoch_pre_dev(c, X, p, prm.eta, lambda, svrg_stream_seed(prm.root, solve_id, e + 1), prm.m, parity ^ 1,
+                           aux);
+      GAPLRA_CUDA_CHECK(cudaEventRecord(c.pre_done[parity ^ 1], aux));
+      have_next = true;
+    }
     out.epochs++;
     c.led.epochs++;
     c.led.solver_column_samples += static_cast<uint64_t>(prm.m);

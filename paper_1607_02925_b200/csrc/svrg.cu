@@ -107,7 +107,9 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
 //   T_t   = (I − L_t)⁻¹,  L_jl = ηn ρ^{j−1−l} K_jl
 //   TT_t  = diag(ρ^{b−1−j}) T_t diag(ηn ρ^l)          (coef = TT P̂ + U)
 //   M_t   = TT_t Kx_t                                  (lookahead correction)
-//   U_t   = diag(ρ^{b−1−j}) T_t q,  q_l = ηn((ρ^l β_t + γ_l) H_{i_l} − Y_{i_l})
+//   (U_t = diag(ρ^{b−1−j}) T_t q is formed later by k_block_u: it needs the
+//   epoch's Y and H, the rest depends only on the index stream and X, so
+//   k_block_prep of epoch e+1 runs beside the chain of epoch e)
 // with W = Ŵ + β C tracked lazily (β_t = γ_{tB} = Σ_{k<tB} ρ^k), so C never has
 // to be resident.  Gram by DMMA m8n8k4 fp64, warps split the d rows, fixed
 // order reductions.  Slab per block: [TT | M | U(group 0) | U(group 1) | ...].
@@ -165,7 +167,6 @@ __global__ void __launch_bounds__(kPrepThreads + 32 * kPrepProducers, kPrepCtas)
   __shared__ double Kx[B][B + 1];
   __shared__ double T[B][B + 1];
   __shared__ double TT[B][B + 1];
-  __shared__ double q[B][kMaxP];
   __shared__ double rp[B + 1], gm[B + 1];
   __shared__ __align__(8) uint64_t full[kPrepStages], empty[kPrepStages];
   static_assert(sizeof(red) >= 4 * B * (B + 1) * sizeof(double), "P aliases red");
@@ -230,26 +231,12 @@ __global__ void __launch_bounds__(kPrepThreads + 32 * kPrepProducers, kPrepCtas)
   // -------------------------------------------------------------- consumers
   const int ct = threadIdx.x - 32 * kPrepProducers, cw = warp - kPrepProducers;
   const int fr = lane >> 2, fc = lane & 3;
-  const double one_minus_rho = 1.0 - a.rho;  // exact (Sterbenz) for rho in [0.5, 1]
-  const double lr = log1p(a.rho - 1.0);
   int stage = 0;
   uint32_t phase = 0;
   for (int64_t t = t_begin; t < t_end; t += t_step) {
     const int64_t s0 = t * B;
     const int bt = static_cast<int>(a.m - s0 < B ? a.m - s0 : B);
     const bool has_prev = t > 0;
-    // q_l[c] = ηn((ρ^l β_t + γ_l) H[i_l][c] − Y[i_l][c]) — issued first so the
-    // gathers overlap the Gram loop
-    const double beta = -expm1(static_cast<double>(s0) * lr) / one_minus_rho;
-    for (int e = ct; e < B * a.p; e += kPrepThreads) {
-      const int l = e / a.p, c = e - (e / a.p) * a.p;
-      double v = 0.0;
-      if (l < bt) {
-        const int64_t i = a.idx[s0 + l];
-        v = a.eta_n * (fma(rp[l], beta, gm[l]) * a.H[i * a.ldy + c] - a.Y[i * a.ldy + c]);
-      }
-      q[l][c] = v;
-    }
     double acc[NT][2];
 #pragma unroll
     for (int qq = 0; qq < NT; ++qq) acc[qq][0] = acc[qq][1] = 0.0;
@@ -354,18 +341,6 @@ __global__ void __launch_bounds__(kPrepThreads + 32 * kPrepProducers, kPrepCtas)
 #pragma unroll
         for (int k = 0; k < B; ++k) s = fma(TT[j][k], Kx[k][l], s);
       slab[B * B + l * B + j] = s;
-    }
-    for (int e = ct; e < B * a.groups * a.pc; e += kPrepThreads) {
-      const int grp = e / (B * a.pc), rem = e - grp * (B * a.pc);
-      const int j = rem / a.pc, cc = rem - (rem / a.pc) * a.pc;
-      const int c = grp * a.pc + cc;
-      double s = 0.0;
-      if (j < bt && c < a.p) {
-#pragma unroll
-        for (int l = 0; l < B; ++l) s = fma(T[j][l], q[l][c], s);
-        s *= rp[bt - 1 - j];
-      }
-      slab[2 * B * B + e] = s;
     }
     prep_sync();
   }
@@ -1227,6 +1202,69 @@ int64_t epoch_slab_len(const EpochConfig& cfg) {
 
 size_t epoch_slab_elems(int64_t m, const EpochConfig& cfg) {
   return static_cast<size_t>(ceil_div(m, kBlock)) * epoch_slab_len(cfg);
+}
+
+// U_t[j][c] = ρ^{b−1−j} Σ_l T_jl q_l[c] with q_l = ηn((ρ^l β_t + γ_l) H[i_l][c] − Y[i_l][c]).
+// Since TT_jl = ρ^{b−1−j} T_jl ηn ρ^l:  U_t[j][c] = Σ_l TT_jl q'_l[c],
+// q'_l = (β_t + γ_l / ρ^l) H[i_l][c] − Y[i_l][c] / ρ^l.   One CTA per block.
+constexpr int kBlockUThreads = 128;
+__global__ void __launch_bounds__(kBlockUThreads) k_block_u(EpochArgs a) {
+  constexpr int B = kBlock;
+  __shared__ double q[B][kMaxP];
+  __shared__ double TTs[B * B];
+  __shared__ double rinv[B], gr[B];
+  const int64_t nblocks = (a.m + B - 1) / B;
+  if (threadIdx.x == 0) {
+    double rp = 1.0, gm = 0.0;
+    for (int l = 0; l < B; ++l) {
+      rinv[l] = 1.0 / rp;
+      gr[l] = gm / rp;
+      gm += rp;
+      rp *= a.rho;
+    }
+  }
+  const double one_minus_rho = 1.0 - a.rho;
+  const double lr = log1p(a.rho - 1.0);
+  for (int64_t t = blockIdx.x; t < nblocks; t += gridDim.x) {
+    __syncthreads();
+    const int64_t s0 = t * B;
+    const int bt = static_cast<int>(a.m - s0 < B ? a.m - s0 : B);
+    const double beta = -expm1(static_cast<double>(s0) * lr) / one_minus_rho;
+    double* slab = a.slab + t * a.slab_len;
+    for (int e = threadIdx.x; e < B * B; e += kBlockUThreads) TTs[e] = slab[e];  // transposed: TT[l*B + j]
+    for (int e = threadIdx.x; e < B * a.p; e += kBlockUThreads) {
+      const int l = e / a.p, c = e - (e / a.p) * a.p;
+      double v = 0.0;
+      if (l < bt) {
+        const int64_t i = a.idx[s0 + l];
+        v = fma(beta + gr[l], a.H[i * a.ldy + c], -a.Y[i * a.ldy + c] * rinv[l]);
+      }
+      q[l][c] = v;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < B * a.groups * a.pc; e += kBlockUThreads) {
+      const int grp = e / (B * a.pc), rem = e - grp * (B * a.pc);
+      const int j = rem / a.pc, cc = rem - (rem / a.pc) * a.pc;
+      const int c = grp * a.pc + cc;
+      double s = 0.0;
+      if (j < bt && c < a.p) {
+#pragma unroll
+        for (int l = 0; l < B; ++l) s = fma(TTs[l * B + j], q[l][c], s);
+      }
+      slab[2 * B * B + e] = s;
+    }
+  }
+}
+
+void launch_block_u(const EpochArgs& a, const EpochConfig& cfg, cudaStream_t st) {
+  EpochArgs args = a;
+  args.pc = cfg.pc;
+  args.groups = cfg.groups;
+  args.slab_len = epoch_slab_len(cfg);
+  const int64_t nblocks = ceil_div(a.m, kBlock);
+  const int grid = static_cast<int>(std::min<int64_t>(nblocks, sm_count_dev() * 16));
+  k_block_u<<<grid, kBlockUThreads, 0, st>>>(args);
+  GAPLRA_LAUNCH_CHECK();
 }
 
 void launch_block_prep(const EpochArgs& a, const EpochConfig& cfg, cudaStream_t st) {

@@ -51,8 +51,11 @@ struct EpochConfig {
 EpochConfig choose_epoch_config(int d_pad, int p);
 // doubles of the per-block slabs of an m-step epoch
 size_t epoch_slab_elems(int64_t m, const EpochConfig& cfg);
-// W-independent per-block coefficients (needs X, idx, m, rho, eta_n, d_pad, Y, H, slab)
+// Per-block coefficients that depend only on the index stream and X: TT and M
+// (needs X, ldx, d_pad, idx, m, rho, eta_n, zcol, slab)
 void launch_block_prep(const EpochArgs& a, const EpochConfig& cfg, cudaStream_t st);
+// The epoch-dependent part U (needs idx, m, rho, p, Y, H, ldy and the slab's TT)
+void launch_block_u(const EpochArgs& a, const EpochConfig& cfg, cudaStream_t st);
 void launch_svrg_epoch_dense(const EpochArgs& a, const EpochConfig& cfg, cudaStream_t st);
 void launch_svrg_epoch_sparse(const SparseEpochArgs& a, cudaStream_t st);
 
