@@ -102,21 +102,29 @@ def make_dense_xt(spec: ConfigSpec, device="cuda", chunk_cols=16384):
 
 def make_sparse_csc(spec: ConfigSpec, seed_offset=0, n=None, d=None):
     """C4-style CSC (numpy): 20 distinct sorted uniform rows per column; values
-    = rank-32 signal sum_l u_{i,l} v_{j,l} / sqrt(32) + N(0, noise^2)."""
+    = rank-32 signal sum_l u_{i,l} v_{j,l} / sqrt(32) + N(0, noise^2).
+    Vectorised: draw rows with replacement, redraw the duplicate positions of
+    each sorted column until every column is distinct."""
     n = n or spec.n
     d = d or spec.d
     rng = np.random.default_rng(spec.seed + seed_offset)
     z = spec.nnz_per_col
-    # distinct rows per column: sample with rejection of duplicates, then sort
-    rows = rng.integers(0, d, size=(n, z + 4), dtype=np.int64)
-    out = np.empty((n, z), np.int32)
-    for j in range(n):
-        u = np.unique(rows[j])
-        while u.size < z:
-            u = np.unique(np.concatenate([u, rng.integers(0, d, size=z, dtype=np.int64)]))
-        out[j] = np.sort(rng.permutation(u)[:z])
+    rows = np.sort(rng.integers(0, d, size=(n, z), dtype=np.int64), axis=1)
+    while True:
+        dup = np.zeros_like(rows, dtype=bool)
+        dup[:, 1:] = rows[:, 1:] == rows[:, :-1]
+        k = int(dup.sum())
+        if k == 0:
+            break
+        rows[dup] = rng.integers(0, d, size=k, dtype=np.int64)
+        rows.sort(axis=1)
+    out = rows.astype(np.int32)
     U = rng.standard_normal((d, 32))
-    V = rng.standard_normal((n, 32))
-    vals = np.einsum("jzl,jl->jz", U[out], V) / np.sqrt(32) + spec.noise * rng.standard_normal((n, z))
+    vals = np.empty((n, z))
+    for j0 in range(0, n, 262144):  # chunked: the (cols, z, 32) gather stays small
+        j1 = min(n, j0 + 262144)
+        V = rng.standard_normal((j1 - j0, 32))
+        vals[j0:j1] = np.einsum("jzl,jl->jz", U[out[j0:j1]], V) / np.sqrt(32)
+    vals += spec.noise * rng.standard_normal((n, z))
     colptr = np.arange(n + 1, dtype=np.int64) * z
     return colptr, out.reshape(-1), vals.reshape(-1)

@@ -125,6 +125,7 @@ struct Matrix {
   DBuf<int32_t> rowidx, colidx;
   DBuf<double> val, rval;
   double maxn2 = -1.0, fro2 = -1.0;
+  int max_col_nnz = 0;  // CSC: largest column (sizes the blocked sparse epoch's scratch)
   int device = 0;
   DenseX dense() const {
     DenseX X;
@@ -182,6 +183,8 @@ struct Context {
   DBuf<int32_t> idx, idx2;  // index streams of even / odd epochs
   DBuf<double> tmat2;        // slab of odd epochs (tmat: even)
   DBuf<unsigned int> rej, rej2;
+  DBuf<double> spd;  // blocked sparse epoch: b, u
+  DBuf<int> spi;     // blocked sparse epoch: row lists, pairs, counters
   // Side stream for the next epoch's W-independent precompute (index stream +
   // k_block_prep), run beside the current epoch's chain on the SMs the chain
   // leaves idle.  Events order it against the main stream.
@@ -526,8 +529,19 @@ void epoch_run_dev(Context& c, Matrix& X, int p, double* W, const double* C, con
     a.ldy = ld;
     a.rho = rho;
     a.eta_n = eta_n;
+    static const bool blocked = !(getenv("GAPLRA_SPARSE_BLOCKED") && atoi(getenv("GAPLRA_SPARSE_BLOCKED")) == 0);
     Prof prof(c, p > 1 ? kProfEpoch : kProfEpochP1, col_bytes * m, 4.0 * col_nnz * p * m);
-    launch_svrg_epoch_sparse(a, c.st);
+    if (blocked && sparse_blocked_supported(p) && X.max_col_nnz > 0) {
+      const int bs = sparse_block_steps(X.d, col_nnz, p);
+      double* db = c.spd.ensure(2 * static_cast<size_t>(bs) * p);
+      const size_t ni = sparse_scratch_ints(X.d, bs, X.max_col_nnz);
+      int* ib = c.spi.ensure(ni);
+      // row counts and counters must start at zero (the layout depends on d)
+      GAPLRA_CUDA_CHECK(cudaMemsetAsync(ib, 0, ni * sizeof(int), c.st));
+      launch_svrg_epoch_sparse_blocked(a, bs, X.max_col_nnz, db, ib, c.st);
+    } else {
+      launch_svrg_epoch_sparse(a, c.st);
+    }
   }
 }
 
@@ -1069,6 +1083,7 @@ int gaplra_matrix_csc(gaplra_ctx* ctx, int d, int n, const int64_t* colptr, cons
       }
     m.nnz = nnz;
     m.ld = round4(d);
+    for (int j = 0; j < n; ++j) m.max_col_nnz = std::max(m.max_col_nnz, static_cast<int>(cp[j + 1] - cp[j]));
     auto up = [&](auto& buf, const auto& hv) {
       buf.ensure(hv.size());
       GAPLRA_CUDA_CHECK(cudaMemcpy(buf.p, hv.data(), hv.size() * sizeof(hv[0]), cudaMemcpyHostToDevice));

@@ -58,6 +58,13 @@ void launch_block_prep(const EpochArgs& a, const EpochConfig& cfg, cudaStream_t 
 void launch_block_u(const EpochArgs& a, const EpochConfig& cfg, cudaStream_t st);
 void launch_svrg_epoch_dense(const EpochArgs& a, const EpochConfig& cfg, cudaStream_t st);
 void launch_svrg_epoch_sparse(const SparseEpochArgs& a, cudaStream_t st);
+// Block-parallel sparse epoch (sparse_epoch.cu): steps per block, scratch ints
+// (zeroed by the caller), and the launch (cooperative, one CTA per SM).
+bool sparse_blocked_supported(int p);
+int sparse_block_steps(int d, double col_nnz, int p);
+size_t sparse_scratch_ints(int d, int bs, int max_col_nnz);
+void launch_svrg_epoch_sparse_blocked(const SparseEpochArgs& a, int bs, int max_col_nnz, double* dbuf, int* ibuf,
+                                      cudaStream_t st);
 
 // C = η(Z + B), per-column |λW − Z − B|; out_max = max_c |M_c| / bnorm_c
 // (NaN if any is non-finite).  part needs anchor_parts(d) * 64 doubles.

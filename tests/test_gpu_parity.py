@@ -171,6 +171,27 @@ def test_svrg_epoch_sparse_lockstep(g, oracle):
     assert rel(wd, wo) <= 1e-10
 
 
+@pytest.mark.timeout(120)
+@pytest.mark.parametrize("d,n,z,p,m", [
+    (5000, 20000, 20, 16, 40003),  # C4 density: 157 blocks of 256 steps, rare couplings
+    (300, 2000, 12, 8, 6001),      # dense couplings: deep dependency levels within a block
+    (40, 400, 20, 3, 997),         # row lists overflow: exact serial fallback per block
+])
+def test_svrg_epoch_sparse_blocked_lockstep(g, oracle, d, n, z, p, m):
+    """Block-parallel sparse epoch (sparse_epoch.cu) against the oracle's step-by-step epoch."""
+    cp, ri, v = random_csc(d, n, z, seed=d + p)
+    mo = oracle.csc(d, n, cp, ri, v)
+    rng = np.random.default_rng(d)
+    w0 = rng.standard_normal((d, p))
+    _, zz, y = oracle.gram_block(mo, w0, want_y=True)
+    lam = 1.5 * float(np.sum(v * v))  # ‖X‖_F² ≥ λ₁: a definite shift
+    eta = 1.0 / (4.0 * (lam + n * oracle.max_col_norm2(mo)))
+    cblk = eta * (zz + rng.standard_normal((d, p)))
+    rc, wo, _ = oracle.svrg_epoch(mo, w0, y, cblk, eta, lam, 5, m)
+    wd = g.svrg_epoch(g.DeviceMatrix.csc(d, n, cp, ri, v), w0, y, cblk, eta, lam, 5, m)
+    assert rel(wd, wo) <= 1e-10
+
+
 def test_svrg_solve_matches_oracle_and_direct(g, oracle):
     X, _, sig = planted_dense(60, 300, seed=0)
     lam = 1.05
