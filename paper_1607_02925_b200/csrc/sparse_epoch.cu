@@ -14,9 +14,11 @@
 // step-by-step form).  Per block, one cooperative kernel does
 //   (A) all CTAs: b_j (one warp per step, lane = column) and per-row entry
 //       lists (atomic slot per row, touched-row list);
-//   (B) CTA 0: sort each shared row's entries by step, emit the coupled pairs,
-//       group them by target step in a fixed order, dependency levels by
-//       fixed-point iteration, then u level by level (in shared memory);
+//   (A2) all CTAs: sort each shared row's entries by step, emit the coupled
+//       pairs (key: target, source, entry; value: the K contribution);
+//   (B) CTA 0: group the pairs by target step in a fixed order (counting sort
+//       + per-group insertion sort) and solve u = b + κKu by in-place sweeps
+//       until nothing changes (K is nilpotent), all in shared memory;
 //   (C) all CTAs: one warp per touched row applies its updates in step order
 //       (one write per row: deterministic, no atomics), resets the row slot.
 // A block whose row lists or pair list overflow the fixed capacities is done
@@ -26,6 +28,8 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "svrg.cuh"
@@ -39,8 +43,9 @@ namespace {
 constexpr int kSpThreads = 512;
 constexpr int kSpWarps = kSpThreads / 32;
 constexpr int kRowCap = 16;      // entries of one row within a block
-constexpr int kPairCap = 16384;  // coupled (l, j) contributions within a block
+constexpr int kPairCap = 16384;  // coupled (l, j) contributions within a block (global list)
 constexpr int kSpMaxBs = 1024;
+constexpr int kSpMaxEntries = 8192;  // bs·p: the u tile and the per-thread b registers
 
 struct SpArgs {
   SparseEpochArgs e;
@@ -50,11 +55,19 @@ struct SpArgs {
   int* rowcnt;             // [d], zero between blocks
   int2* rowent;            // [d][kRowCap]  (step j, CSC entry index)
   int* touched;            // [bs * max_col_nnz]
-  int4* pairs;             // [kPairCap]: (target j, source l, entry of j, entry of l)
+  unsigned long long* pkey;  // [kPairCap]: target j << 42 | source l << 32 | entry of l
+  double* pval;              // [kPairCap]: val(entry of j) * val(entry of l)
   int* counters;           // [2][4] per block parity: touched rows, pairs, overflow flag
   double* u_glob;          // [bs][p]
-  int* csr;                // [bs + 1 + kPairCap]: grouped pair indices (global scratch)
+  int spair_cap;           // pairs that fit the shared tile of CTA 0
+  unsigned long long* dbg;  // GAPLRA_EPOCH_TIMING: ns per phase (A, A2, B, C) summed over blocks
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)::"memory");
+  return t;
+}
 
 __device__ __forceinline__ double ldv(const double* p) { return __ldg(p); }
 
@@ -66,8 +79,11 @@ __global__ void __launch_bounds__(kSpThreads, 1) k_sparse_epoch_blocked(SpArgs A
   double* u = smem;                                  // [bs][p]
   double* rp = u + static_cast<size_t>(bs) * p;       // [bs + 1] ρ^j
   double* gm = rp + bs + 1;                           // [bs + 1] γ_j
-  int* lev = reinterpret_cast<int*>(gm + bs + 1);     // [bs]
-  int* cnt = lev + bs;                                // [bs + 1]
+  double* sv = gm + bs + 1;                           // [spair_cap] pair values
+  unsigned long long* sk = reinterpret_cast<unsigned long long*>(sv + A.spair_cap);  // [spair_cap] keys
+  int* lev = reinterpret_cast<int*>(sk + A.spair_cap);  // [bs] scan temporaries / fill cursors
+  int* cnt = lev + bs;                                  // [bs + 1] group bounds
+  int* perm = cnt + bs + 1;                             // [spair_cap] pair indices grouped by target
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int gwarp = blockIdx.x * kSpWarps + warp, nwarps = gridDim.x * kSpWarps;
   if (tid == 0) {
@@ -81,6 +97,14 @@ __global__ void __launch_bounds__(kSpThreads, 1) k_sparse_epoch_blocked(SpArgs A
   __syncthreads();
   const double kappa = a.eta_n / a.rho;
   double al = 1.0, be = 0.0;  // α, β at the block start (identical in every thread)
+  unsigned long long tph[4] = {0, 0, 0, 0}, tlast = gtimer();
+  auto mark = [&](int k) {
+    if (A.dbg && blockIdx.x == 0 && tid == 0) {
+      const unsigned long long now = gtimer();
+      tph[k] += now - tlast;
+      tlast = now;
+    }
+  };
   const int64_t nblk = (a.m + bs - 1) / bs;
   for (int64_t blk = 0; blk < nblk; ++blk) {
     const int64_t s0 = blk * bs;
@@ -123,16 +147,19 @@ __global__ void __launch_bounds__(kSpThreads, 1) k_sparse_epoch_blocked(SpArgs A
       }
     }
     grid.sync();
-    // ---------------------------------------------------------------- (B)
-    if (blockIdx.x == 0) {
-      if (tid < 4) A.counters[((blk + 1) & 1) * 4 + tid] = 0;  // next block's counters
+    mark(0);
+    // --------------------------------------------------------------- (A2)
+    // every CTA: sort the entries of shared rows by step and emit the coupled
+    // pairs with their contribution val_j(row) · val_l(row)
+    {
       const int nt = ctr[0];
-      // sort shared rows by step and emit the coupled pairs
-      for (int k = tid; k < nt; k += kSpThreads) {
+      for (int k = blockIdx.x * kSpThreads + tid; k < nt; k += gridDim.x * kSpThreads) {
         const int row = A.touched[k];
         const int c = min(A.rowcnt[row], kRowCap);
         if (c < 2) continue;
-        int2* ent = A.rowent + static_cast<int64_t>(row) * kRowCap;
+        int2 ent[kRowCap];
+        const int2* src = A.rowent + static_cast<int64_t>(row) * kRowCap;
+        for (int x = 0; x < c; ++x) ent[x] = src[x];
         for (int x = 1; x < c; ++x) {  // insertion sort by step
           const int2 v = ent[x];
           int y = x - 1;
@@ -142,88 +169,129 @@ __global__ void __launch_bounds__(kSpThreads, 1) k_sparse_epoch_blocked(SpArgs A
           }
           ent[y + 1] = v;
         }
-        for (int x = 1; x < c; ++x)
+        int2* dst = A.rowent + static_cast<int64_t>(row) * kRowCap;
+        for (int x = 0; x < c; ++x) dst[x] = ent[x];  // (C) applies the row's updates in step order
+        for (int x = 1; x < c; ++x) {
+          const double vj = ldv(a.val + ent[x].y);
           for (int y = 0; y < x; ++y) {
             const int slot = atomicAdd(&ctr[1], 1);
-            if (slot < kPairCap)
-              A.pairs[slot] = make_int4(ent[x].x, ent[y].x, ent[x].y, ent[y].y);
-            else
+            if (slot < kPairCap) {
+              A.pkey[slot] = (static_cast<unsigned long long>(ent[x].x) << 42) |
+                             (static_cast<unsigned long long>(ent[y].x) << 32) | static_cast<unsigned>(ent[y].y);
+              A.pval[slot] = vj * ldv(a.val + ent[y].y);
+            } else {
               ctr[2] = 1;
+            }
           }
+        }
       }
-      __syncthreads();
-      const bool overflow = ctr[2] != 0;
+    }
+    grid.sync();
+    mark(1);
+    // ---------------------------------------------------------------- (B)
+    if (blockIdx.x == 0) {
+      if (tid < 4) A.counters[((blk + 1) & 1) * 4 + tid] = 0;  // next block's counters
+      const int np = __ldcg(&ctr[1]);
+      const bool overflow = __ldcg(&ctr[2]) != 0 || np > A.spair_cap;
       if (!overflow) {
-        const int np = ctr[1];
-        // group pair indices by target step: counts, exclusive scan, fill, then
-        // sort every group by (source step, entry) — a fixed summation order
+        // pairs into shared memory, grouped by target step (counting sort),
+        // every group sorted by (source step, entry): a fixed summation order
+        for (int k = tid; k < np; k += kSpThreads) {
+          sk[k] = __ldcg(A.pkey + k);
+          sv[k] = __ldcg(A.pval + k);
+        }
         for (int j = tid; j <= bt; j += kSpThreads) cnt[j] = 0;
         __syncthreads();
-        for (int k = tid; k < np; k += kSpThreads) atomicAdd(&cnt[A.pairs[k].x + 1], 1);
+        for (int k = tid; k < np; k += kSpThreads) atomicAdd(&cnt[static_cast<int>(sk[k] >> 42) + 1], 1);
         __syncthreads();
-        if (tid == 0)
-          for (int j = 1; j <= bt; ++j) cnt[j] += cnt[j - 1];
+        // inclusive scan of cnt[1..bt] (bt <= 1024): warp scans + warp totals
+        __shared__ int wsum[kSpWarps];
+        {
+          const int per = (bt + kSpThreads - 1) / kSpThreads;  // 1 or 2 entries per thread
+          const int j0 = 1 + tid * per;
+          int loc = 0;
+          for (int q = 0; q < per; ++q)
+            if (j0 + q <= bt) loc += cnt[j0 + q];
+          int inc = loc;
+          for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += v;
+          }
+          if (lane == 31) wsum[warp] = inc;
+          __syncthreads();
+          int off = 0;
+          for (int w = 0; w < warp; ++w) off += wsum[w];
+          int run = off + inc - loc;
+          for (int q = 0; q < per; ++q)
+            if (j0 + q <= bt) {
+              run += cnt[j0 + q];
+              lev[j0 + q - 1] = run;  // end of group j0+q-1 (temporary)
+            }
+        }
         __syncthreads();
-        int* grp = A.csr;  // [np] pair indices grouped by target
-        for (int j = tid; j < bt; j += kSpThreads) lev[j] = cnt[j];  // fill cursor
+        for (int j = tid; j < bt; j += kSpThreads) cnt[j + 1] = lev[j];
+        if (tid == 0) cnt[0] = 0;
         __syncthreads();
-        for (int k = tid; k < np; k += kSpThreads) grp[atomicAdd(&lev[A.pairs[k].x], 1)] = k;
+        for (int j = tid; j < bt; j += kSpThreads) lev[j] = cnt[j];  // fill cursors
+        __syncthreads();
+        for (int k = tid; k < np; k += kSpThreads) perm[atomicAdd(&lev[static_cast<int>(sk[k] >> 42)], 1)] = k;
         __syncthreads();
         for (int j = tid; j < bt; j += kSpThreads) {
           const int g0 = cnt[j], g1 = cnt[j + 1];
           for (int x = g0 + 1; x < g1; ++x) {
-            const int v = grp[x];
-            const int4 pv = A.pairs[v];
+            const int v = perm[x];
+            const unsigned long long kv = sk[v];
             int y = x - 1;
-            while (y >= g0) {
-              const int4 py = A.pairs[grp[y]];
-              if (py.y < pv.y || (py.y == pv.y && py.w <= pv.w)) break;
-              grp[y + 1] = grp[y];
+            while (y >= g0 && sk[perm[y]] > kv) {
+              perm[y + 1] = perm[y];
               --y;
             }
-            grp[y + 1] = v;
+            perm[y + 1] = v;
           }
-          lev[j] = 0;
         }
         __syncthreads();
-        // dependency levels: lev_j = max(0, max_l lev_l + 1), fixed point from below
-        for (;;) {
-          int changed = 0;
-          for (int j = tid; j < bt; j += kSpThreads) {
-            int L = 0;
-            for (int x = cnt[j]; x < cnt[j + 1]; ++x) L = max(L, lev[A.pairs[grp[x]].y] + 1);
-            if (L != lev[j]) {
-              lev[j] = L;
-              changed = 1;
-            }
-          }
-          if (!__syncthreads_or(changed)) break;
+        // u = b + κ K u by in-place fixed-point sweeps: the coupling is strictly
+        // lower triangular (nilpotent), so the sweeps stop changing after
+        // depth + 1 and the last sweep recomputes every u_j from its final
+        // predecessors in the fixed group order
+        constexpr int kOwn = kSpMaxEntries / kSpThreads;  // (j, c) entries per thread
+        double bown[kOwn];
+        const int ne = bt * p;
+#pragma unroll
+        for (int q = 0; q < kOwn; ++q) {
+          const int e = tid + q * kSpThreads;
+          bown[q] = e < ne ? __ldcg(A.b + e) : 0.0;
+          if (e < ne) u[e] = bown[q];
         }
-        int maxlev = 0;
-        for (int j = tid; j < bt; j += kSpThreads) maxlev = max(maxlev, lev[j]);
-        maxlev = __reduce_max_sync(0xffffffffu, maxlev);
-        __shared__ int wmax[kSpWarps];
-        if (lane == 0) wmax[warp] = maxlev;
         __syncthreads();
-        maxlev = 0;
-        for (int w = 0; w < kSpWarps; ++w) maxlev = max(maxlev, wmax[w]);
-        // solve level by level
-        for (int L = 0; L <= maxlev; ++L) {
-          for (int e = tid; e < bt * p; e += kSpThreads) {
-            const int j = e / p, c = e - j * p;
-            if (lev[j] != L) continue;
-            double acc = 0.0;
-            for (int x = cnt[j]; x < cnt[j + 1]; ++x) {
-              const int4 pv = A.pairs[grp[x]];
-              acc = fma(ldv(a.val + pv.z) * ldv(a.val + pv.w), u[pv.y * p + c], acc);
+        if (np > 0) {
+          for (;;) {
+            int changed = 0;
+#pragma unroll
+            for (int q = 0; q < kOwn; ++q) {
+              const int e = tid + q * kSpThreads;
+              if (e >= ne) break;
+              const int j = e / p, c = e - j * p;
+              const int g0 = cnt[j], g1 = cnt[j + 1];
+              if (g0 == g1) continue;
+              double acc = 0.0;
+              for (int x = g0; x < g1; ++x) {
+                const int k = perm[x];
+                acc = fma(sv[k], u[static_cast<int>((sk[k] >> 32) & 0x3ff) * p + c], acc);
+              }
+              const double nu = fma(kappa, acc, bown[q]);
+              if (nu != u[e]) {
+                u[e] = nu;
+                changed = 1;
+              }
             }
-            u[e] = fma(kappa, acc, __ldcg(A.b + e));
+            if (!__syncthreads_or(changed)) break;
           }
-          __syncthreads();
         }
+        for (int e = tid; e < ne; e += kSpThreads) A.u_glob[e] = u[e];
       } else {
-        // exact serial fallback: step by step with immediate updates (rows of
-        // this block are untouched by (C) below: counters[2] tells it to skip)
+        if (tid == 0) ctr[2] = 1;  // (C) skips the block's row updates
+        // exact serial fallback: step by step with immediate updates
         for (int j = 0; j < bt; ++j) {
           const int i = a.idx[s0 + j];
           const int64_t e0 = a.colptr[i], e1 = a.colptr[i + 1];
@@ -246,12 +314,12 @@ __global__ void __launch_bounds__(kSpThreads, 1) k_sparse_epoch_blocked(SpArgs A
           __syncwarp();
         }
       }
-      for (int e = tid; e < bt * p; e += kSpThreads) A.u_glob[e] = u[e];
     }
     grid.sync();
+    mark(2);
     // ---------------------------------------------------------------- (C)
-    const bool overflow = ctr[2] != 0;
-    const int nt = ctr[0];
+    const bool overflow = __ldcg(&ctr[2]) != 0;
+    const int nt = __ldcg(&ctr[0]);
     for (int k = gwarp; k < nt; k += nwarps) {
       const int row = A.touched[k];
       const int c = min(A.rowcnt[row], kRowCap);
@@ -267,7 +335,10 @@ __global__ void __launch_bounds__(kSpThreads, 1) k_sparse_epoch_blocked(SpArgs A
     al *= rp[bt];
     be = fma(rp[bt], be, gm[bt]);
     grid.sync();
+    mark(3);
   }
+  if (A.dbg && blockIdx.x == 0 && tid == 0)
+    for (int k = 0; k < 4; ++k) A.dbg[k] = tph[k];
   if (blockIdx.x == 0 && tid < 8) A.counters[tid] = 0;  // the last block's counters (all reads were before its sync)
   // W = α Ŵ + β C
   for (int64_t e = static_cast<int64_t>(blockIdx.x) * kSpThreads + tid; e < static_cast<int64_t>(a.d) * p;
@@ -282,9 +353,9 @@ __global__ void __launch_bounds__(kSpThreads, 1) k_sparse_epoch_blocked(SpArgs A
 
 int sparse_block_steps(int d, double col_nnz, int p) {
   // expected coupled pairs in a block of bs steps: (bs·nnz)² / (2d); keep it
-  // near 4096, the shared u tile bs·p doubles within 128 KB
+  // near 4096, the shared u tile bs·p <= kSpMaxEntries doubles
   int bs = kSpMaxBs;
-  while (bs > 32 && ((bs * col_nnz) * (bs * col_nnz) / (2.0 * d) > 4096.0 || bs * p > 16384)) bs /= 2;
+  while (bs > 32 && ((bs * col_nnz) * (bs * col_nnz) / (2.0 * d) > 4096.0 || bs * p > kSpMaxEntries)) bs /= 2;
   return bs;
 }
 
@@ -292,9 +363,8 @@ size_t sparse_scratch_ints(int d, int bs, int max_col_nnz) {
   return static_cast<size_t>(d)                    // rowcnt
          + 2 * static_cast<size_t>(d) * kRowCap      // rowent (int2)
          + static_cast<size_t>(bs) * max_col_nnz     // touched
-         + 4 * static_cast<size_t>(kPairCap)         // pairs (int4)
-         + 8                                         // counters
-         + static_cast<size_t>(kPairCap) + bs + 1;   // grouped pair indices
+         + 4 * static_cast<size_t>(kPairCap)         // pair keys (u64) + values (f64)
+         + 8;                                        // counters
 }
 
 bool sparse_blocked_supported(int p) { return p >= 1 && p <= 32; }
@@ -314,13 +384,26 @@ void launch_svrg_epoch_sparse_blocked(const SparseEpochArgs& a, int bs, int max_
   q += 2 * static_cast<size_t>(a.d) * kRowCap;
   A.touched = q;
   q += static_cast<size_t>(A.bs) * max_col_nnz;
-  A.pairs = reinterpret_cast<int4*>(q);
-  q += 4 * static_cast<size_t>(kPairCap);
+  A.pkey = reinterpret_cast<unsigned long long*>(q);
+  q += 2 * static_cast<size_t>(kPairCap);
+  A.pval = reinterpret_cast<double*>(q);
+  q += 2 * static_cast<size_t>(kPairCap);
   A.counters = q;
   q += 8;
-  A.csr = q;
-  const size_t smem = (static_cast<size_t>(A.bs) * a.p + 2 * (A.bs + 1)) * sizeof(double) +
+  const size_t base = (static_cast<size_t>(A.bs) * a.p + 2 * (A.bs + 1)) * sizeof(double) +
                       (2 * static_cast<size_t>(A.bs) + 1) * sizeof(int);
+  // shared pair tile: a power of two up to 8192 pairs within ~200 KB in total
+  int cap = 8192;
+  while (cap > 256 && base + static_cast<size_t>(cap) * 20 > 200 * 1024) cap >>= 1;
+  A.spair_cap = cap;
+  static const bool timing = getenv("GAPLRA_EPOCH_TIMING") != nullptr;
+  static unsigned long long* dbg = nullptr;
+  A.dbg = nullptr;
+  if (timing) {
+    if (!dbg) GAPLRA_CUDA_CHECK(cudaMalloc(&dbg, 4 * sizeof(unsigned long long)));
+    A.dbg = dbg;
+  }
+  const size_t smem = base + static_cast<size_t>(cap) * 20;
   GAPLRA_CUDA_CHECK(cudaFuncSetAttribute(k_sparse_epoch_blocked, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem)));
   int per_sm = 0;
@@ -333,6 +416,14 @@ void launch_svrg_epoch_sparse_blocked(const SparseEpochArgs& a, int bs, int max_
   GAPLRA_CUDA_CHECK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_sparse_epoch_blocked), dim3(sms),
                                                 dim3(kSpThreads), args, smem, st));
   GAPLRA_LAUNCH_CHECK();
+  if (A.dbg) {
+    unsigned long long h[4];
+    GAPLRA_CUDA_CHECK(cudaMemcpyAsync(h, A.dbg, sizeof(h), cudaMemcpyDeviceToHost, st));
+    GAPLRA_CUDA_CHECK(cudaStreamSynchronize(st));
+    const double nbk = static_cast<double>((a.m + bs - 1) / bs);
+    fprintf(stderr, "{\"sparse_epoch\": {\"bs\": %d, \"blocks\": %.0f, \"us_per_block\": [%.2f, %.2f, %.2f, %.2f]}}\n", bs,
+            nbk, h[0] / nbk / 1e3, h[1] / nbk / 1e3, h[2] / nbk / 1e3, h[3] / nbk / 1e3);
+  }
 }
 
 }  // namespace gaplra_cuda
