@@ -76,12 +76,6 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
-// 16-byte variant: two entries per remote message
-__device__ __forceinline__ void st_async_f64x2(uint32_t remote_addr, double v0, double v1, uint32_t remote_bar) {
-  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(remote_addr),
-               "d"(v0), "d"(v1), "r"(remote_bar)
-               : "memory");
-}
 // Bulk shared::cta -> shared::cluster copy completing on the receiver's mbarrier.
 __device__ __forceinline__ void dsmem_bulk_copy(uint32_t remote_dst, uint32_t local_src, uint32_t bytes,
                                                 uint32_t remote_bar) {
@@ -373,7 +367,7 @@ struct ChainSmem {
 
 // rows_pad ≡ 2 (mod 16) doubles by default (DMMA / scalar phases: fragment
 // loads across 8 slices are conflict-free); PAD16 gives rows_pad ≡ 0 (mod 16)
-// for k_svrg_chain_v2, whose lane-permuted slice loads are then conflict-free.
+// for k_svrg_chain_v3, whose lane-permuted slice loads are then conflict-free.
 template <int PC, int B, bool PAD16 = false>
 __host__ __device__ inline ChainSmem chain_smem(int rows, int stages) {
   ChainSmem s;
@@ -811,261 +805,6 @@ __global__ void __launch_bounds__(kChainThreads + 32 * kChainProducers, 1) k_svr
   cluster.sync();
 }
 
-// ---------------------------------------------------------------------------
-// k_svrg_chain_rr: register-row variant for small PC (<= 4).  Each consumer
-// thread owns R_T rows of the CTA's W slice and keeps them in REGISTERS for
-// the whole epoch.  Per block t:
-//   (b) products X_{B_{t+1}}[j][r] · V[r][c] of the owned rows (independent of
-//       coef_t, so it runs first), a warp reduce-scatter by shuffles, the 8
-//       warp slices summed in fixed order, st.async to every peer;
-//   (a) coef_t = TT Â + M coef_{t−1} + U      (threads (j, c), transposed TT / M)
-//   (c) V ← ρ^{b'} (V + X_{B_t} coef_t) on registers;
-//   (d) wait for the peers' pushes, sum the 16 slots (fixed order).
-// ---------------------------------------------------------------------------
-template <int PC, int B, int RT>
-__global__ void __launch_bounds__(kChainThreads + 32 * kChainProducers, 1) k_svrg_chain_rr(EpochArgs a) {
-  extern __shared__ __align__(128) double sm[];
-  cg::cluster_group cluster = cg::this_cluster();
-  const int G = static_cast<int>(cluster.num_blocks());
-  const int g = static_cast<int>(cluster.block_rank());
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  constexpr int NW = kChainThreads / 32;
-  constexpr int NV = B * PC;                 // dot entries per block (j-major: e = j*PC + c)
-  constexpr int NVP = (NV + 31) / 32 * 32;   // padded to whole 32-entry chunks
-  const int grp = blockIdx.y;
-  const int c0 = grp * PC;
-  const int pc = min(PC, a.p - c0);
-  const ChainSmem L = chain_smem<PC, B>(a.rows_per_cta, a.stages);
-  const int S = L.stages;
-  const int r0 = g * a.rows_per_cta;
-  const int rc = max(0, min(a.rows_per_cta, a.d_pad - r0));
-  const int RP = L.rows_pad;
-  double* recv = sm + L.off_recv;  // [kRecvSlots][kMaxCluster][NV]
-  double* Ahat = sm + L.off_a;
-  double* coef = sm + L.off_coef;
-  double* rprev = sm + L.off_rprev;
-  double* red = sm + L.off_red;    // [NW][NV]
-  uint64_t* full = reinterpret_cast<uint64_t*>(sm + L.off_bar);
-  uint64_t* empty = full + 4;
-  uint64_t* rbar = full + 8;
-  auto stage_at = [&](int s_idx) { return sm + L.off_stage + static_cast<size_t>(s_idx) * L.stage_len; };
-  const int nb = static_cast<int>((a.m + B - 1) / B);
-  const int last_bt = static_cast<int>(a.m - static_cast<int64_t>(nb - 1) * B);
-  auto bt_of = [&](int t) { return t == nb - 1 ? last_bt : B; };
-  double rho_b = 1.0, rho_last = 1.0;  // ρ^B and ρ^{b of the last block}
-  for (int j = 0; j < B; ++j) rho_b *= a.rho;
-  for (int j = 0; j < last_bt; ++j) rho_last *= a.rho;
-
-  if (tid == 0) {
-    for (int s = 0; s < S; ++s) {
-      mbar_init(&full[s], kChainProducers);
-      mbar_init(&empty[s], kChainThreads / 32);  // one arrival per consumer warp
-    }
-    for (int q = 0; q < kRecvSlots; ++q) mbar_init(&rbar[q], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  for (int e = tid; e < NV; e += blockDim.x) rprev[e] = 0.0;
-  cluster.sync();
-
-  if (warp >= NW) {
-    chain_produce<PC, B>(a, warp - NW, lane, nb, last_bt, S, rc, r0, RP, grp, sm + L.off_stage, L.stage_len, full,
-                         empty);
-  } else {
-    // ===== consumers: rows r = tid + k * 256 (k < RT) in registers
-    double v[RT][PC];
-    bool own[RT];
-#pragma unroll
-    for (int k = 0; k < RT; ++k) {
-      const int r = tid + k * kChainThreads;
-      own[k] = r < rc;
-#pragma unroll
-      for (int c = 0; c < PC; ++c)
-        v[k][c] = own[k] && c < pc ? a.W[static_cast<int64_t>(r0 + r) * a.ldw + c0 + c] : 0.0;
-    }
-    int ws = 0;
-    uint32_t wph = 0;
-    auto wait_next = [&]() {
-      mbar_wait(&full[ws], wph);
-      if (++ws == S) {
-        ws = 0;
-        wph ^= 1u;
-      }
-    };
-    auto arm_recv = [&](int u) {
-      mbar_expect_tx(&rbar[u & (kRecvSlots - 1)], static_cast<uint32_t>(G * bt_of(u) * PC * 8));
-    };
-    // products of the owned rows in chunks of 32 entries (e = j*PC + c), each
-    // chunk reduce-scattered over the 32 lanes by recursive halving (1 value
-    // per lane), the 8 warp slices summed in fixed order, st.async to peers
-    auto dots_push = [&](const double* xb, int bt, int u) {
-      const int par = u & (kRecvSlots - 1);
-#pragma unroll
-      for (int ch = 0; ch < NVP / 32; ++ch) {
-        double val[32];
-#pragma unroll
-        for (int i = 0; i < 32; ++i) val[i] = 0.0;
-#pragma unroll
-        for (int k = 0; k < RT; ++k) {
-          if (!own[k]) continue;
-          const int r = tid + k * kChainThreads;
-#pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            const int e = ch * 32 + i;
-            if (e >= NV) break;
-            const int j = e / PC, c = e % PC;
-            if (c == 0 || i == 0) {
-              // one load of x_j[r] per j (the compiler keeps it across c)
-            }
-            val[i] = fma(xb[j * RP + r], v[k][c], val[i]);
-          }
-        }
-        int base = 0;
-#pragma unroll
-        for (int o = 16, n = 32; o >= 1; o >>= 1, n >>= 1) {
-          const bool hi = (lane & o) != 0;
-          const int half = n / 2;
-#pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            if (i >= half) break;
-            const double keep = hi ? val[i + half] : val[i];
-            const double send = hi ? val[i] : val[i + half];
-            val[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
-          }
-          if (hi) base += half;
-        }
-        red[warp * NVP + ch * 32 + base] = val[0];
-      }
-      consumers_sync();
-      const uint32_t slot = smem_u32(recv + (par * kMaxCluster + g) * NV);
-      const uint32_t rbl = smem_u32(&rbar[par]);
-      for (int e = tid; e < bt * PC; e += kChainThreads) {
-        double s = 0.0;
-#pragma unroll
-        for (int w = 0; w < NW; ++w) s += red[w * NVP + e];
-        for (int q = 0; q < G; ++q) st_async_f64(mapa(slot, q) + e * 8u, s, mapa(rbl, q));
-      }
-    };
-    auto recv_sum = [&](int u) {
-      const int par = u & (kRecvSlots - 1);
-      mbar_wait(&rbar[par], static_cast<uint32_t>((u >> 2) & 1));
-      for (int e = tid; e < bt_of(u) * PC; e += kChainThreads) {
-        double s = 0.0;
-        for (int q = 0; q < G; ++q) s += recv[(par * kMaxCluster + q) * NV + e];
-        Ahat[e] = s;
-      }
-    };
-    long long tacc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    long long tp = clock64();
-    auto tick = [&](int k) {
-      if (a.dbg) {
-        long long now;
-        asm volatile("mov.u64 %0, %%clock64;" : "=l"(now)::"memory");
-        tacc[k] += now - tp;
-        tp = now;
-      }
-    };
-    if (nb > 0) {
-      if (tid == 0) arm_recv(0);
-      wait_next();
-      dots_push(stage_at(0), bt_of(0), 0);
-      double rb = 1.0;
-      for (int j = 0; j < bt_of(0); ++j) rb *= a.rho;
-#pragma unroll
-      for (int k = 0; k < RT; ++k)
-#pragma unroll
-        for (int c = 0; c < PC; ++c) v[k][c] *= rb;
-    }
-    int cs = 0;
-    for (int t = 0; t < nb; ++t) {
-      const int bt = bt_of(t);
-      const bool more = t + 1 < nb;
-      const int ns = cs + 1 == S ? 0 : cs + 1;
-      if (tid == 0 && more) arm_recv(t + 1);
-      if (more) wait_next();
-      tick(0);
-      // (b) lookahead dots of block t+1 (needs only V_t, in registers)
-      if (more) dots_push(stage_at(ns), bt_of(t + 1), t + 1);
-      tick(1);
-      // (d) Â_t
-      recv_sum(t);
-      tick(2);
-      consumers_sync();  // Â_t, coef_{t−1} (rprev) visible
-      const double* xb = stage_at(cs);
-      const double* TT = xb + B * RP;
-      const double* M = TT + B * B;
-      const double* Ub = M + B * B;
-      // (a) coef_t
-      for (int e = tid; e < NV; e += kChainThreads) {
-        const int j = e / PC, c = e - (e / PC) * PC;
-        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-        if (j < bt) {
-          s0 = Ub[e];
-#pragma unroll
-          for (int l = 0; l < B; l += 2) {
-            s0 = fma(TT[l * B + j], Ahat[l * PC + c], s0);
-            s1 = fma(TT[(l + 1) * B + j], Ahat[(l + 1) * PC + c], s1);
-            s2 = fma(M[l * B + j], rprev[l * PC + c], s2);
-            s3 = fma(M[(l + 1) * B + j], rprev[(l + 1) * PC + c], s3);
-          }
-        }
-        coef[e] = (s0 + s1) + (s2 + s3);
-      }
-      tick(3);
-      consumers_sync();
-      tick(4);
-      // (c) V ← ρ^{b'} (V + X_B coef)
-      const double rn = !more ? 1.0 : (t + 1 == nb - 1 ? rho_last : rho_b);
-      double cf[B][PC];
-#pragma unroll
-      for (int l = 0; l < B; ++l)
-#pragma unroll
-        for (int c = 0; c < PC; ++c) cf[l][c] = coef[l * PC + c];
-#pragma unroll
-      for (int k = 0; k < RT; ++k) {
-        if (!own[k]) continue;
-        const int r = tid + k * kChainThreads;
-        double w2[PC];
-#pragma unroll
-        for (int c = 0; c < PC; ++c) w2[c] = 0.0;
-#pragma unroll
-        for (int l = 0; l < B; l += 2) {
-          const double x = xb[l * RP + r], x2 = xb[(l + 1) * RP + r];
-#pragma unroll
-          for (int c = 0; c < PC; ++c) {
-            v[k][c] = fma(x, cf[l][c], v[k][c]);
-            w2[c] = fma(x2, cf[l + 1][c], w2[c]);
-          }
-        }
-#pragma unroll
-        for (int c = 0; c < PC; ++c) v[k][c] = (v[k][c] + w2[c]) * rn;
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[cs]);
-      tick(5);
-      for (int e = tid; e < NV; e += kChainThreads) rprev[e] = coef[e];
-      tick(6);
-      cs = ns;
-    }
-    if (a.dbg && tid == 0) {
-      const int cta = blockIdx.y * gridDim.x + blockIdx.x;
-      for (int k = 0; k < 8; ++k) a.dbg[cta * 8 + k] = tacc[k];
-    }
-    const double beta = -expm1(static_cast<double>(a.m) * log1p(a.rho - 1.0)) / (1.0 - a.rho);
-#pragma unroll
-    for (int k = 0; k < RT; ++k) {
-      if (!own[k]) continue;
-      const int r = tid + k * kChainThreads;
-#pragma unroll
-      for (int c = 0; c < PC; ++c)
-        if (c < pc) {
-          const int64_t o = static_cast<int64_t>(r0 + r) * a.ldw + c0 + c;
-          a.W[o] = fma(beta, a.C[o], v[k][c]);
-        }
-    }
-  }
-  cluster.sync();
-}
-
 // Sparse (CSC) epoch, lazy form W = α Ŵ + β C (O(nnz(x_i)) per step).  One
 // warp per group of 32 columns; lane = column; steps strictly sequential.
 __global__ void k_svrg_epoch_sparse(SparseEpochArgs a) {
@@ -1283,359 +1022,6 @@ void launch_block_prep(const EpochArgs& a, const EpochConfig& cfg, cudaStream_t 
   (void)attr;
   k_block_prep<kBlock><<<grid, kPrepThreads + 32 * kPrepProducers, kPrepRingBytes, st>>>(args);
   GAPLRA_LAUNCH_CHECK();
-}
-
-// ---------------------------------------------------------------------------
-// k_svrg_chain_v2: the chain laid out for the SM's 128 B/clk shared-memory
-// datapath and the block's dependency chain.  Thread = row (RT rows per
-// thread): V and the block's X slice rows live in registers, so every slice
-// element crosses the shared-memory port once (TMA write + one LDS).
-// Per block t, two CTA barriers:
-//   (b) load X_{B_{t+1}} rows into registers (kept for (c) of block t+1);
-//       products X_{B_{t+1}}[j][r] V[r][c] summed over the warp by a
-//       select-free recursive halving (lane L orders its products as
-//       j = i XOR (L>>1), so every level keeps the low half and sends the
-//       high half); red[warp][e];  barrier;  every thread sums one
-//       (entry, peer) pair over the 8 warps (fixed tree) and st.async's it
-//   (d) warp 0: wait for Â_t (pushed one block earlier), fixed-order slot sum
-//   (a) warp 0: coef_t = TT_t Â_t + pre_t  (pre_t = M_t coef_{t−1} + U_t was
-//       formed during block t−1);  barrier
-//   (c) V ← ρ^{b'} (V + X_{B_t} coef_t) from the registers of (b);
-//       warp 7 forms pre_{t+1}
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ double sum8_tree(const double* p, int stride) {
-  return ((p[0] + p[stride]) + (p[2 * stride] + p[3 * stride])) +
-         ((p[4 * stride] + p[5 * stride]) + (p[6 * stride] + p[7 * stride]));
-}
-
-// No producer warp: 8 warps (2 per SM sub-partition) leave 255 registers per
-// thread.  Block u's stage is refilled at the start of block u+1 (its last
-// shared-memory reader, warp 0's coef, finished before block u's second
-// barrier) by lanes of warps 4..7, 4 slices each, warp 4 adding the slab part.
-constexpr int kChainV2MaxStages = 6;
-
-// Column index of slice (4 iw + lane) of block u (loaded one block ahead of its
-// use so the copy issue never waits on global memory).
-__device__ __forceinline__ int v2_col(const EpochArgs& a, int u, int nb, int iw, int lane) {
-  const int64_t s = static_cast<int64_t>(u) * 16 + iw * 4 + lane;
-  return (u < nb && lane < 4 && s < a.m) ? __ldg(a.idx + s) : 0;
-}
-
-template <int PC, int B>
-__device__ __forceinline__ void v2_issue(const EpochArgs& a, int u, int nb, int last_bt, int rc, int r0, int RP,
-                                         int grp, double* st, uint64_t* fb, int iw, int lane, int col) {
-  const int bt = u == nb - 1 ? last_bt : B;
-  const int j0 = iw * 4;
-  const int mine = rc > 0 && !(a.skip & 8) ? max(0, min(4, bt - j0)) : 0;  // skip & 8: timing ablation
-  fence_proxy_async();  // generic-proxy reads of the stage (ordered by the CTA barrier) before the async writes
-  if (lane == 0) mbar_expect_tx(fb, static_cast<uint32_t>(mine * rc + (iw == 0 ? 2 * B * B + B * PC : 0)) * 8u);
-  __syncwarp();
-  if (lane < mine) {
-    const int j = j0 + lane;
-    tma_load_1d(st + j * RP, a.X + static_cast<int64_t>(col) * a.ldx + r0, rc * 8u, fb);
-  }
-  if (iw == 0 && lane == 31) {
-    const double* slab = a.slab + static_cast<int64_t>(u) * a.slab_len;
-    tma_load_1d(st + B * RP, slab, 2 * B * B * 8u, fb);
-    tma_load_1d(st + B * RP + 2 * B * B, slab + 2 * B * B + static_cast<size_t>(grp) * B * PC, B * PC * 8u, fb);
-  }
-}
-
-template <int PC, int B, int RT>
-__global__ void __launch_bounds__(kChainThreads, 1) k_svrg_chain_v2(EpochArgs a) {
-  static_assert(B == 16, "lane permutation j = i ^ (lane >> 1) covers 16 slices");
-  extern __shared__ __align__(128) double sm[];
-  cg::cluster_group cluster = cg::this_cluster();
-  const int G = static_cast<int>(cluster.num_blocks());
-  const int lgG = G == 16 ? 4 : (G == 8 ? 3 : (G == 4 ? 2 : (G == 2 ? 1 : 0)));
-  const int g = static_cast<int>(cluster.block_rank());
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  constexpr int NW = kChainThreads / 32;
-  static_assert(NW == 8, "sum8_tree");
-  constexpr int NV = B * PC;  // entries per block (j-major: e = j*PC + c)
-  const int grp = blockIdx.y;
-  const int c0 = grp * PC;
-  const int pc = min(PC, a.p - c0);
-  const ChainSmem L = chain_smem<PC, B, true>(a.rows_per_cta, a.stages);
-  static_assert(NW * NV <= kChainThreads / 32 * (B / 8) * 64, "red fits");
-  const int S = L.stages;
-  const int r0 = g * a.rows_per_cta;
-  const int rc = max(0, min(a.rows_per_cta, a.d_pad - r0));
-  const int RP = L.rows_pad;
-  double* recv = sm + L.off_recv;  // [kRecvSlots][kMaxCluster][NV]
-  double* Ahat = sm + L.off_a;
-  double* coef = sm + L.off_coef;
-  double* pre = sm + L.off_rprev;
-  double* red = sm + L.off_red;  // [NW][NV]
-  uint64_t* full = reinterpret_cast<uint64_t*>(sm + L.off_bar);  // [S <= 8]
-  uint64_t* rbar = full + 8;
-  auto stage_at = [&](int s_idx) { return sm + L.off_stage + static_cast<size_t>(s_idx) * L.stage_len; };
-  const int nb = static_cast<int>((a.m + B - 1) / B);
-  const int last_bt = static_cast<int>(a.m - static_cast<int64_t>(nb - 1) * B);
-  auto bt_of = [&](int t) { return t == nb - 1 ? last_bt : B; };
-  double rho_b = 1.0, rho_last = 1.0;
-  for (int j = 0; j < B; ++j) rho_b *= a.rho;
-  for (int j = 0; j < last_bt; ++j) rho_last *= a.rho;
-  // slices j >= bt of a ragged last block are never written: zero the stage
-  // ring once so that those rows read as 0
-#pragma unroll 1
-  for (size_t e = tid; e < L.off_v; e += blockDim.x) sm[e] = 0.0;
-
-  if (tid == 0) {
-    for (int s = 0; s < S; ++s) mbar_init(&full[s], 4);
-    for (int q = 0; q < kRecvSlots; ++q) mbar_init(&rbar[q], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  int ncol = 0;  // column index for the next refill (block S, then S+1, ...)
-  if (warp >= 4) {  // first S blocks
-    fence_proxy_async();
-    for (int u = 0; u < S && u < nb; ++u)
-      v2_issue<PC, B>(a, u, nb, last_bt, rc, r0, RP, grp, stage_at(u), &full[u], warp - 4, lane,
-                      v2_col(a, u, nb, warp - 4, lane));
-    ncol = v2_col(a, S, nb, warp - 4, lane);
-  }
-  cluster.sync();
-
-  {
-    const int pm = lane >> 1;  // product order j = i ^ pm
-    double v[RT][PC];
-    bool own[RT];
-#pragma unroll
-    for (int k = 0; k < RT; ++k) {
-      const int r = tid + k * kChainThreads;
-      own[k] = r < rc;
-#pragma unroll
-      for (int c = 0; c < PC; ++c)
-        v[k][c] = own[k] && c < pc ? a.W[static_cast<int64_t>(r0 + r) * a.ldw + c0 + c] : 0.0;
-    }
-    int ws = 0;
-    uint32_t wph = 0;
-    auto wait_next = [&]() {
-      mbar_wait(&full[ws], wph);
-      if (++ws == S) {
-        ws = 0;
-        wph ^= 1u;
-      }
-    };
-    // entries travel in pairs (16-byte st.async): a peer sends ceil(nv/2) pairs
-    auto arm_recv = [&](int u) {
-      mbar_expect_tx(&rbar[u & (kRecvSlots - 1)], static_cast<uint32_t>(G * ((bt_of(u) * PC + 1) & ~1) * 8));
-    };
-    // X slice rows of one block, lane-permuted: xr[k][i] = X_B[i ^ pm][row k]
-    double xa[RT][B], xn[RT][B];
-    auto load_rows = [&](const double* xb, double (&xr)[RT][B]) {
-#pragma unroll
-      for (int k = 0; k < RT; ++k) {
-        const double* col = xb + tid + k * kChainThreads;
-#pragma unroll
-        for (int i = 0; i < B; ++i) xr[k][i] = own[k] ? col[(i ^ pm) * RP] : 0.0;
-      }
-    };
-    // (b) products of the loaded rows with V, select-free warp halving, red
-    auto products = [&](const double (&xr)[RT][B]) {
-      double val[B][PC];
-#pragma unroll
-      for (int i = 0; i < B; ++i)
-#pragma unroll
-        for (int c = 0; c < PC; ++c) {
-          double s = 0.0;
-#pragma unroll
-          for (int k = 0; k < RT; ++k) s = fma(xr[k][i], v[k][c], s);
-          val[i][c] = s;
-        }
-#pragma unroll
-      for (int o = 16, n = B / 2; o >= 2; o >>= 1, n >>= 1)
-#pragma unroll
-        for (int i = 0; i < n; ++i)
-#pragma unroll
-          for (int c = 0; c < PC; ++c) val[i][c] += __shfl_xor_sync(0xffffffffu, val[i + n][c], o);
-#pragma unroll
-      for (int c = 0; c < PC; ++c) val[0][c] += __shfl_xor_sync(0xffffffffu, val[0][c], 1);
-      // lane L now holds the warp total of j = L >> 1
-      if (!(lane & 1))
-#pragma unroll
-        for (int c = 0; c < PC; ++c) red[warp * NV + pm * PC + c] = val[0][c];
-    };
-    // every thread: (entry, peer) pairs, the 8 warp partials summed in a fixed tree
-    auto push = [&](int u) {
-      const int par = u & (kRecvSlots - 1);
-      const int nv = bt_of(u) * PC;
-      const uint32_t slot = smem_u32(recv + (par * kMaxCluster + g) * NV);
-      const uint32_t rbl = smem_u32(&rbar[par]);
-      const int np = (nv + 1) >> 1;
-#pragma unroll 1
-      for (int i = tid; i < (np << lgG); i += kChainThreads) {
-        const int e = (i >> lgG) * 2, q = i & (G - 1);
-        st_async_f64x2(mapa(slot, q) + e * 8u, sum8_tree(red + e, NV), sum8_tree(red + e + 1, NV), mapa(rbl, q));
-      }
-    };
-    long long tacc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    long long tp;
-    asm volatile("mov.u64 %0, %%clock64;" : "=l"(tp)::"memory");
-    auto tick = [&](int k) {
-      if (a.dbg) {
-        long long now;
-        asm volatile("mov.u64 %0, %%clock64;" : "=l"(now)::"memory");
-        tacc[k] += now - tp;
-        tp = now;
-      }
-    };
-    // (c) V ← ρ^{b'} (V + X_B coef) with the lane-permuted rows: coef read at j = i ^ pm
-    auto update = [&](const double (&xr)[RT][B], int bt, double rn) {
-      double cf[B][PC];
-#pragma unroll
-      for (int i = 0; i < B; ++i)
-#pragma unroll
-        for (int c = 0; c < PC; ++c) cf[i][c] = coef[(i ^ pm) * PC + c];
-      (void)bt;  // coef rows j >= bt are 0 and so are the slice rows
-#pragma unroll
-      for (int k = 0; k < RT; ++k) {
-        double w2[PC];
-#pragma unroll
-        for (int c = 0; c < PC; ++c) w2[c] = 0.0;
-#pragma unroll
-        for (int i = 0; i < B; i += 2)
-#pragma unroll
-          for (int c = 0; c < PC; ++c) {
-            v[k][c] = fma(xr[k][i], cf[i][c], v[k][c]);
-            w2[c] = fma(xr[k][i + 1], cf[i + 1][c], w2[c]);
-          }
-#pragma unroll
-        for (int c = 0; c < PC; ++c) v[k][c] = own[k] ? (v[k][c] + w2[c]) * rn : 0.0;
-      }
-    };
-    auto step = [&](int t, int& cs, double (&xcur)[RT][B], double (&xnext)[RT][B]) {
-      const int bt = bt_of(t);
-      const bool more = t + 1 < nb;
-      const int ns = cs + 1 == S ? 0 : cs + 1;
-      if (tid == 0 && more) arm_recv(t + 1);
-      // refill block t−1's stage with block t−1+S
-      if (warp >= 4 && t >= 1 && t - 1 + S < nb) {
-        const int ps = cs == 0 ? S - 1 : cs - 1;
-        v2_issue<PC, B>(a, t - 1 + S, nb, last_bt, rc, r0, RP, grp, stage_at(ps), &full[ps], warp - 4, lane, ncol);
-        ncol = v2_col(a, t + S, nb, warp - 4, lane);
-      }
-      tick(0);
-      if (more) wait_next();
-      tick(7);
-      if (more) {
-        load_rows(stage_at(ns), xnext);
-        products(xnext);
-      }
-      tick(1);
-      consumers_sync();  // red complete; pre_t visible; coef reads of block t−1 done
-      tick(2);
-      if (more) push(t + 1);
-      tick(3);
-      const double* xb = stage_at(cs);
-      if (warp == 0) {
-        // (d) Â_t
-        const int par = t & (kRecvSlots - 1);
-        mbar_wait(&rbar[par], static_cast<uint32_t>((t >> 2) & 1));
-        const int nv = bt * PC;
-        for (int e = lane; e < NV; e += 32) {
-          double s = 0.0;
-          if (e < nv) {
-            const double* sl = recv + par * kMaxCluster * NV + e;
-            double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-#pragma unroll 1
-            for (int q = 0; q < G; q += 4) {
-              s0 += sl[q * NV];
-              s1 += sl[(q + 1) * NV];
-              s2 += sl[(q + 2) * NV];
-              s3 += sl[(q + 3) * NV];
-            }
-            s = (s0 + s1) + (s2 + s3);
-          }
-          Ahat[e] = s;
-        }
-        __syncwarp();
-        // (a) coef_t = TT_t Â_t + pre_t   (TT stored transposed: TT[l*B + j])
-        const double* TT = xb + B * RP;
-        for (int e = lane; e < NV; e += 32) {
-          const int j = e / PC, c = e - (e / PC) * PC;
-          double s0 = pre[e], s1 = 0.0, s2 = 0.0, s3 = 0.0;
-#pragma unroll
-          for (int l = 0; l < B; l += 4) {
-            s0 = fma(TT[l * B + j], Ahat[l * PC + c], s0);
-            s1 = fma(TT[(l + 1) * B + j], Ahat[(l + 1) * PC + c], s1);
-            s2 = fma(TT[(l + 2) * B + j], Ahat[(l + 2) * PC + c], s2);
-            s3 = fma(TT[(l + 3) * B + j], Ahat[(l + 3) * PC + c], s3);
-          }
-          coef[e] = (s0 + s1) + (s2 + s3);
-        }
-      }
-      tick(4);
-      consumers_sync();  // coef_t visible
-      tick(5);
-      const double rn = !more ? 1.0 : (t + 1 == nb - 1 ? rho_last : rho_b);
-      update(xcur, bt, rn);
-      // pre_{t+1} = M_{t+1} coef_t + U_{t+1}   (M stored transposed: M[l*B + j])
-      if (warp == NW - 1 && more) {
-        const double* M = stage_at(ns) + B * RP + B * B;
-        const double* Ub = M + B * B;
-        for (int e = lane; e < NV; e += 32) {
-          const int j = e / PC, c = e - (e / PC) * PC;
-          double s0 = Ub[e], s1 = 0.0, s2 = 0.0, s3 = 0.0;
-#pragma unroll
-          for (int l = 0; l < B; l += 4) {
-            s0 = fma(M[l * B + j], coef[l * PC + c], s0);
-            s1 = fma(M[(l + 1) * B + j], coef[(l + 1) * PC + c], s1);
-            s2 = fma(M[(l + 2) * B + j], coef[(l + 2) * PC + c], s2);
-            s3 = fma(M[(l + 3) * B + j], coef[(l + 3) * PC + c], s3);
-          }
-          pre[e] = (s0 + s1) + (s2 + s3);
-        }
-      }
-      tick(6);
-      cs = ns;
-    };
-    int cs = 0;
-    if (nb > 0) {  // Â_0 = X_{B_0}ᵀ Ŵ_0, then V_0 = ρ^{b_0} Ŵ_0, pre_0 = U_0
-      if (tid == 0) arm_recv(0);
-      wait_next();
-      load_rows(stage_at(0), xa);
-      products(xa);
-      consumers_sync();
-      push(0);
-      double rb = 1.0;
-      for (int j = 0; j < bt_of(0); ++j) rb *= a.rho;
-#pragma unroll
-      for (int k = 0; k < RT; ++k)
-#pragma unroll
-        for (int c = 0; c < PC; ++c) v[k][c] *= rb;
-      if (warp == NW - 1) {
-        const double* Ub = stage_at(0) + B * RP + 2 * B * B;
-        for (int e = lane; e < NV; e += 32) pre[e] = Ub[e];
-      }
-    }
-#pragma unroll 1
-    for (int t = 0; t < nb; ++t) {
-      step(t, cs, xa, xn);
-#pragma unroll
-      for (int k = 0; k < RT; ++k)
-#pragma unroll
-        for (int i = 0; i < B; ++i) xa[k][i] = xn[k][i];
-    }
-    if (a.dbg && tid == 0) {
-      const int cta = blockIdx.y * gridDim.x + blockIdx.x;
-      for (int k = 0; k < 8; ++k) a.dbg[cta * 8 + k] = tacc[k];
-    }
-    const double beta = -expm1(static_cast<double>(a.m) * log1p(a.rho - 1.0)) / (1.0 - a.rho);
-#pragma unroll
-    for (int k = 0; k < RT; ++k) {
-      if (!own[k]) continue;
-      const int r = tid + k * kChainThreads;
-#pragma unroll
-      for (int c = 0; c < PC; ++c)
-        if (c < pc) {
-          const int64_t o = static_cast<int64_t>(r0 + r) * a.ldw + c0 + c;
-          a.W[o] = fma(beta, a.C[o], v[k][c]);
-        }
-    }
-  }
-  cluster.sync();
 }
 
 // ---------------------------------------------------------------------------
@@ -2069,26 +1455,18 @@ EpochConfig choose_epoch_config(int d_pad, int p) {
 
 template <int PC>
 void launch_chain_pc(const EpochArgs& a, const EpochConfig& cfg, cudaStream_t st) {
-  // 0: auto (warp-specialised v3 where it fits: PC <= 3 and <= 256 rows per
-  // CTA; else scalar smem phases for PC <= 2, DMMA phases above), 1: DMMA,
-  // 2: scalar smem, 3: register-row, 4: register-row v2, 5: v3.
-  // Measured r01 on C2 (ms per epoch, p = 1 / p = 20 at PC = 3):
-  // v3 9.97 / 18.95; scalar 19.1 / 29.4; DMMA 25.1 / 28.0.
+  // GAPLRA_CHAIN_MODE: 0 auto (the warp-specialised v3 where it fits: PC <= 3
+  // and <= 256 rows per CTA; else scalar smem phases for PC <= 2, DMMA phases
+  // above), 1 DMMA, 2 scalar smem, 3 v3.  Measured r01 on C2 (ms per epoch,
+  // p = 1 / p = 20 at PC = 3): v3 9.9 / 17.6; scalar 19.1 / 29.4; DMMA 25.1 / 28.0.
   static const int env_mode = getenv("GAPLRA_CHAIN_MODE") ? atoi(getenv("GAPLRA_CHAIN_MODE")) : 0;
   const bool v3_fits = PC <= 3 && cfg.rows_per_cta <= 2 * 32 * kV3Rows;
-  const int mode = env_mode ? env_mode : (v3_fits ? 5 : (PC <= 2 ? 2 : 1));
+  const int mode = env_mode ? env_mode : (v3_fits ? 3 : (PC <= 2 ? 2 : 1));
+  const bool v3 = mode == 3 && v3_fits;
   auto kern = mode == 1 ? k_svrg_chain<PC, kBlock, false> : k_svrg_chain<PC, kBlock, true>;
-  if constexpr (PC <= 4) {
-    if (mode == 3) kern = cfg.rows_per_cta <= kChainThreads ? k_svrg_chain_rr<PC, kBlock, 1> : k_svrg_chain_rr<PC, kBlock, 2>;
-  }
   if constexpr (PC <= 3) {
-    if (mode == 4)
-      kern = cfg.rows_per_cta <= kChainThreads ? k_svrg_chain_v2<PC, kBlock, 1> : k_svrg_chain_v2<PC, kBlock, 2>;
+    if (v3) kern = k_svrg_chain_v3<PC, kBlock>;
   }
-  if constexpr (PC <= 3) {
-    if (mode == 5 && cfg.rows_per_cta <= 2 * 32 * kV3Rows) kern = k_svrg_chain_v3<PC, kBlock>;
-  }
-  const bool v3 = mode == 5 && PC <= 3 && cfg.rows_per_cta <= 2 * 32 * kV3Rows;
   int stages = cfg.stages;
   size_t smem = cfg.smem;
   if (v3) {  // pitch ≡ 0 (mod 16) layout, at most 4 stages (barrier slots)
@@ -2100,20 +1478,11 @@ void launch_chain_pc(const EpochArgs& a, const EpochConfig& cfg, cudaStream_t st
       }
     smem = chain_smem<PC, kBlock, true>(cfg.rows_per_cta, stages).total;
   }
-  if (mode == 4) {  // v2: no empty barriers, deeper ring where shared memory allows
-    stages = 2;
-    for (int sN = kChainV2MaxStages; sN > 2; --sN)
-      if (chain_smem<PC, kBlock, true>(cfg.rows_per_cta, sN).total <= 227 * 1024) {
-        stages = sN;
-        break;
-      }
-    smem = chain_smem<PC, kBlock, true>(cfg.rows_per_cta, stages).total;
-  }
   GAPLRA_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   if (cfg.cluster > 8) GAPLRA_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   cudaLaunchConfig_t lc = {};
   lc.gridDim = dim3(cfg.cluster, cfg.groups, 1);
-  lc.blockDim = dim3(v3 ? v3_threads(PC) : kChainThreads + (mode == 4 ? 0 : 32 * kChainProducers), 1, 1);
+  lc.blockDim = dim3(v3 ? v3_threads(PC) : kChainThreads + 32 * kChainProducers, 1, 1);
   lc.dynamicSmemBytes = smem;
   lc.stream = st;
   cudaLaunchAttribute attr[1];
