@@ -1046,11 +1046,16 @@ constexpr int kV3Producers = 2;  // producer warps
 // 2818 of 2900 cycles per block)
 __host__ __device__ constexpr int v3_reducers(int pc) { return pc >= 2 ? 2 : 1; }
 __host__ __device__ constexpr int v3_threads(int pc) { return 32 * (kV3Rows + v3_reducers(pc) + kV3Producers); }
+// layouts the warp-specialised chain runs: 256 rows per CTA (H = 1, PC <= 3) or
+// 512 rows (H = 2, PC = 1: only there do three 512-row stages fit beside the
+// receive slots; with two, the stage re-read by the update would stall the ring)
+inline bool v3_supports(int pc, int rows) { return pc <= 3 && (rows <= 256 || (rows <= 512 && pc == 1)); }
 
-template <int PC, int B>
+// H: 256-row halves per row thread (rows 2·tid + {0,1} + 256·h): 256·H rows per CTA.
+template <int PC, int B, int H = 1>
 __global__ void __launch_bounds__(v3_threads(PC), 1) k_svrg_chain_v3(EpochArgs a) {
   static_assert(B == 16, "lane permutation j = i ^ (lane >> 1) covers 16 slices");
-  constexpr bool XREG = PC == 1;  // update from the products' registers (else re-read the stage)
+  constexpr bool XREG = PC == 1 && H == 1;  // update from the products' registers (else re-read the stage)
   extern __shared__ __align__(128) double sm[];
   cg::cluster_group cluster = cg::this_cluster();
   const int G = static_cast<int>(cluster.num_blocks());
@@ -1214,13 +1219,19 @@ __global__ void __launch_bounds__(v3_threads(PC), 1) k_svrg_chain_v3(EpochArgs a
     }
   } else {  // --------------------------------------------------------------- rows
     const int pm = lane >> 1;  // product order j = i ^ pm
-    const int ra = 2 * tid;    // rows ra, ra + 1
-    const bool own0 = ra < rc, own1 = ra + 1 < rc;
-    double v0[PC], v1[PC];
+    const int ra = 2 * tid;    // rows ra + 256 h, ra + 1 + 256 h
+    bool own0[H], own1[H];
+    double v0[H][PC], v1[H][PC];
 #pragma unroll
-    for (int c = 0; c < PC; ++c) {
-      v0[c] = own0 && c < pc ? a.W[static_cast<int64_t>(r0 + ra) * a.ldw + c0 + c] : 0.0;
-      v1[c] = own1 && c < pc ? a.W[static_cast<int64_t>(r0 + ra + 1) * a.ldw + c0 + c] : 0.0;
+    for (int h = 0; h < H; ++h) {
+      const int rh = ra + 256 * h;
+      own0[h] = rh < rc;
+      own1[h] = rh + 1 < rc;
+#pragma unroll
+      for (int c = 0; c < PC; ++c) {
+        v0[h][c] = own0[h] && c < pc ? a.W[static_cast<int64_t>(r0 + rh) * a.ldw + c0 + c] : 0.0;
+        v1[h][c] = own1[h] && c < pc ? a.W[static_cast<int64_t>(r0 + rh + 1) * a.ldw + c0 + c] : 0.0;
+      }
     }
     int ws = 0;
     uint32_t wph = 0;
@@ -1233,22 +1244,30 @@ __global__ void __launch_bounds__(v3_threads(PC), 1) k_svrg_chain_v3(EpochArgs a
       }
       return s;
     };
-    auto load_rows = [&](const double* xb, double2 (&xr)[B]) {
+    auto load_rows = [&](const double* xb, double2 (&xr)[H][B]) {
 #pragma unroll
-      for (int i = 0; i < B; ++i) xr[i] = *reinterpret_cast<const double2*>(xb + (i ^ pm) * RP + ra);
+      for (int h = 0; h < H; ++h)
+#pragma unroll
+        for (int i = 0; i < B; ++i)
+          xr[h][i] = *reinterpret_cast<const double2*>(xb + (i ^ pm) * RP + ra + 256 * h);
     };
     const bool issuer = lane < 4 && warp * 4 + lane < G;
     const int peer = warp * 4 + lane;
     auto push_prepare = [&]() {  // before the red barrier: the copies of two blocks ago no longer read their outv
       if (issuer) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
     };
-    auto products = [&](const double2 (&xr)[B]) {
+    auto products = [&](const double2 (&xr)[H][B]) {
       push_prepare();
       double val[B][PC];
 #pragma unroll
       for (int i = 0; i < B; ++i)
 #pragma unroll
-        for (int c = 0; c < PC; ++c) val[i][c] = fma(xr[i].x, v0[c], xr[i].y * v1[c]);
+        for (int c = 0; c < PC; ++c) {
+          double sv = fma(xr[0][i].x, v0[0][c], xr[0][i].y * v1[0][c]);
+#pragma unroll
+          for (int h = 1; h < H; ++h) sv = fma(xr[h][i].x, v0[h][c], fma(xr[h][i].y, v1[h][c], sv));
+          val[i][c] = sv;
+        }
 #pragma unroll
       for (int o = 16, n = B / 2; o >= 2; o >>= 1, n >>= 1)
 #pragma unroll
@@ -1277,33 +1296,36 @@ __global__ void __launch_bounds__(v3_threads(PC), 1) k_svrg_chain_v3(EpochArgs a
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
       }
     };
-    auto update = [&](const double2 (&xr)[B], int t, double rn) {
+    auto update = [&](const double2 (&xr)[H][B], int t, double rn) {
       if (t & 1)
         asm volatile("bar.sync 3, %0;" ::"n"(32 * (kV3Rows + NRD)) : "memory");
       else
         asm volatile("bar.sync 2, %0;" ::"n"(32 * (kV3Rows + NRD)) : "memory");
       tick(4);
       const double* cf = coef + (t & 1) * NV;
-      double a0[PC], a1[PC];
 #pragma unroll
-      for (int c = 0; c < PC; ++c) a0[c] = a1[c] = 0.0;
+      for (int h = 0; h < H; ++h) {
+        double a0[PC], a1[PC];
 #pragma unroll
-      for (int i = 0; i < B; i += 2)
+        for (int c = 0; c < PC; ++c) a0[c] = a1[c] = 0.0;
+#pragma unroll
+        for (int i = 0; i < B; i += 2)
+#pragma unroll
+          for (int c = 0; c < PC; ++c) {
+            const double k0 = cf[(i ^ pm) * PC + c], k1 = cf[((i + 1) ^ pm) * PC + c];
+            v0[h][c] = fma(xr[h][i].x, k0, v0[h][c]);
+            v1[h][c] = fma(xr[h][i].y, k0, v1[h][c]);
+            a0[c] = fma(xr[h][i + 1].x, k1, a0[c]);
+            a1[c] = fma(xr[h][i + 1].y, k1, a1[c]);
+          }
 #pragma unroll
         for (int c = 0; c < PC; ++c) {
-          const double k0 = cf[(i ^ pm) * PC + c], k1 = cf[((i + 1) ^ pm) * PC + c];
-          v0[c] = fma(xr[i].x, k0, v0[c]);
-          v1[c] = fma(xr[i].y, k0, v1[c]);
-          a0[c] = fma(xr[i + 1].x, k1, a0[c]);
-          a1[c] = fma(xr[i + 1].y, k1, a1[c]);
+          v0[h][c] = own0[h] ? (v0[h][c] + a0[c]) * rn : 0.0;
+          v1[h][c] = own1[h] ? (v1[h][c] + a1[c]) * rn : 0.0;
         }
-#pragma unroll
-      for (int c = 0; c < PC; ++c) {
-        v0[c] = own0 ? (v0[c] + a0[c]) * rn : 0.0;
-        v1[c] = own1 ? (v1[c] + a1[c]) * rn : 0.0;
       }
     };
-    double2 xa[B], xn[B];
+    double2 xa[H][B], xn[H][B];
     if (nb > 0) {  // Â_0 = X_{B_0}ᵀ Ŵ_0, then V_0 = ρ^{b_0} Ŵ_0
       const int s = wait_stage();
       load_rows(stage_at(s), xa);
@@ -1319,13 +1341,15 @@ __global__ void __launch_bounds__(v3_threads(PC), 1) k_svrg_chain_v3(EpochArgs a
       double rb = 1.0;
       for (int j = 0; j < bt_of(0); ++j) rb *= a.rho;
 #pragma unroll
-      for (int c = 0; c < PC; ++c) {
-        v0[c] *= rb;
-        v1[c] *= rb;
-      }
+      for (int h = 0; h < H; ++h)
+#pragma unroll
+        for (int c = 0; c < PC; ++c) {
+          v0[h][c] *= rb;
+          v1[h][c] *= rb;
+        }
     }
     // block t: products of t+1 (stage ns) then the update of t
-    auto step = [&](int t, double2 (&xr)[B], double2 (&xq)[B]) {
+    auto step = [&](int t, double2 (&xr)[H][B], double2 (&xq)[H][B]) {
       const bool more = t + 1 < nb;
       if (more) {
         tick(5);
@@ -1348,7 +1372,7 @@ __global__ void __launch_bounds__(v3_threads(PC), 1) k_svrg_chain_v3(EpochArgs a
         update(xr, t, rn);
       } else {
         const int cs = t % S;
-        double2 xt[B];
+        double2 xt[H][B];
         load_rows(stage_at(cs), xt);
         update(xt, t, rn);
         __syncwarp();
@@ -1375,17 +1399,20 @@ __global__ void __launch_bounds__(v3_threads(PC), 1) k_svrg_chain_v3(EpochArgs a
     }
     const double beta = -expm1(static_cast<double>(a.m) * log1p(a.rho - 1.0)) / (1.0 - a.rho);
 #pragma unroll
-    for (int c = 0; c < PC; ++c)
-      if (c < pc) {
-        if (own0) {
-          const int64_t o = static_cast<int64_t>(r0 + ra) * a.ldw + c0 + c;
-          a.W[o] = fma(beta, a.C[o], v0[c]);
+    for (int h = 0; h < H; ++h)
+#pragma unroll
+      for (int c = 0; c < PC; ++c)
+        if (c < pc) {
+          const int rh = ra + 256 * h;
+          if (own0[h]) {
+            const int64_t o = static_cast<int64_t>(r0 + rh) * a.ldw + c0 + c;
+            a.W[o] = fma(beta, a.C[o], v0[h][c]);
+          }
+          if (own1[h]) {
+            const int64_t o = static_cast<int64_t>(r0 + rh + 1) * a.ldw + c0 + c;
+            a.W[o] = fma(beta, a.C[o], v1[h][c]);
+          }
         }
-        if (own1) {
-          const int64_t o = static_cast<int64_t>(r0 + ra + 1) * a.ldw + c0 + c;
-          a.W[o] = fma(beta, a.C[o], v1[c]);
-        }
-      }
   }
   cluster.sync();
 }
@@ -1446,7 +1473,7 @@ EpochConfig choose_epoch_config(int d_pad, int p) {
   };
   if (env_cluster == 8 || env_cluster == 16) return make(env_cluster);
   const EpochConfig c16 = make(16), c8 = make(8);
-  auto v3_ok = [](const EpochConfig& c) { return c.pc <= 3 && c.rows_per_cta <= 256; };
+  auto v3_ok = [](const EpochConfig& c) { return v3_supports(c.pc, c.rows_per_cta); };
   if (d_pad < 1024) return c8;
   if (v3_ok(c16)) return c16;
   if (v3_ok(c8)) return c8;
@@ -1460,12 +1487,15 @@ void launch_chain_pc(const EpochArgs& a, const EpochConfig& cfg, cudaStream_t st
   // above), 1 DMMA, 2 scalar smem, 3 v3.  Measured r01 on C2 (ms per epoch,
   // p = 1 / p = 20 at PC = 3): v3 9.9 / 17.6; scalar 19.1 / 29.4; DMMA 25.1 / 28.0.
   static const int env_mode = getenv("GAPLRA_CHAIN_MODE") ? atoi(getenv("GAPLRA_CHAIN_MODE")) : 0;
-  const bool v3_fits = PC <= 3 && cfg.rows_per_cta <= 2 * 32 * kV3Rows;
+  const bool v3_fits = v3_supports(PC, cfg.rows_per_cta);
   const int mode = env_mode ? env_mode : (v3_fits ? 3 : (PC <= 2 ? 2 : 1));
   const bool v3 = mode == 3 && v3_fits;
   auto kern = mode == 1 ? k_svrg_chain<PC, kBlock, false> : k_svrg_chain<PC, kBlock, true>;
   if constexpr (PC <= 3) {
-    if (v3) kern = k_svrg_chain_v3<PC, kBlock>;
+    if (v3) kern = k_svrg_chain_v3<PC, kBlock, 1>;
+  }
+  if constexpr (PC == 1) {
+    if (v3 && cfg.rows_per_cta > 256) kern = k_svrg_chain_v3<1, kBlock, 2>;
   }
   int stages = cfg.stages;
   size_t smem = cfg.smem;
