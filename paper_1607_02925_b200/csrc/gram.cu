@@ -183,6 +183,16 @@ __device__ __forceinline__ void mma884(double& c0, double& c1, double a, double 
       : "d"(a), "d"(b));
 }
 
+// 8-byte global -> shared copy without register staging (LDGSTS); src_bytes = 0
+// writes zeros.  Committed per stage, waited before the stage is read.
+__device__ __forceinline__ void cp_async8(double* dst, const double* src, bool valid) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(dst))),
+               "l"(src), "r"(valid ? 8 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
 // smem pitch (doubles) for a KC x (8*NT) B-operand tile: ≡ 8 (mod 16) keeps the
 // 4 rows x 8 columns of an m8n8k4 B fragment on distinct bank pairs.
 template <int NT>
@@ -228,15 +238,18 @@ __global__ void __launch_bounds__(kMmaThreads) k_xtw_mma(const double* __restric
     live[mt] = col < n;
     xc[mt] = X + static_cast<int64_t>(live[mt] ? col : 0) * ldx + 4 * tq;
   }
-  auto stage_w = [&](int buf, int rbase) {
+  auto stage_w = [&](int buf, int rbase) {  // asynchronous: no register round trip
     for (int e = threadIdx.x; e < kKC * 8 * NT; e += kMmaThreads) {
       const int rr = e / (8 * NT), c = e - rr * (8 * NT);
       const int r = rbase + rr;
-      Ws[buf][rr * BP + c] = (c < pc && r < r1) ? __ldg(W + static_cast<int64_t>(r) * ldw + c) : 0.0;
+      const bool ok = c < pc && r < r1;
+      cp_async8(&Ws[buf][rr * BP + c], W + (ok ? static_cast<int64_t>(r) * ldw + c : 0), ok);
     }
+    cp_async_commit();
   };
   int buf = 0;
   if (r0 < r1) stage_w(0, r0);
+  cp_async_wait_all();
   __syncthreads();
   for (int rb = r0; rb < r1; rb += kKC) {
     if (rb + kKC < r1) stage_w(buf ^ 1, rb + kKC);
@@ -270,6 +283,7 @@ __global__ void __launch_bounds__(kMmaThreads) k_xtw_mma(const double* __restric
           for (int nt = 0; nt < NT; ++nt) mma884(acc[mt][nt][0], acc[mt][nt][1], av[kb][mt][u], bfr[nt]);
       }
     }
+    cp_async_wait_all();
     __syncthreads();
     buf ^= 1;
   }
@@ -321,15 +335,18 @@ __global__ void __launch_bounds__(kMmaThreads) k_xy_mma(const double* __restrict
   const bool live0 = rbase + 2 * gq + 1 < rows_total, live1 = rbase + 16 + 2 * gq + 1 < rows_total;
   const double* xr0 = X + (live0 ? rbase + 2 * gq : 0);
   const double* xr1 = X + (live1 ? rbase + 16 + 2 * gq : 0);
-  auto stage_y = [&](int buf, int jb) {
+  auto stage_y = [&](int buf, int jb) {  // asynchronous: no register round trip
     for (int e = threadIdx.x; e < kKC * 8 * NT; e += kMmaThreads) {
       const int jj = e / (8 * NT), c = e - jj * (8 * NT);
       const int j = jb + jj;
-      Ys[buf][jj * BP + c] = (c < pc && j < j1) ? __ldg(Y + static_cast<int64_t>(j) * ldy + c) : 0.0;
+      const bool ok = c < pc && j < j1;
+      cp_async8(&Ys[buf][jj * BP + c], Y + (ok ? static_cast<int64_t>(j) * ldy + c : 0), ok);
     }
+    cp_async_commit();
   };
   int buf = 0;
   if (j0 < j1) stage_y(0, j0);
+  cp_async_wait_all();
   __syncthreads();
   for (int jb = j0; jb < j1; jb += kKC) {
     if (jb + kKC < j1) stage_y(buf ^ 1, jb + kKC);
@@ -359,6 +376,7 @@ __global__ void __launch_bounds__(kMmaThreads) k_xy_mma(const double* __restrict
         }
       }
     }
+    cp_async_wait_all();
     __syncthreads();
     buf ^= 1;
   }

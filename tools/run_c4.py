@@ -41,6 +41,8 @@ spec_s = time.time() - t
 tot = float(np.sum(v * v))
 delta = 2.0 / 3.0 * (lam[spec.k - 1] - lam[spec.p])
 mu = math.sqrt(tot / max(tot - lam[: spec.k].sum(), 1e-300))
+print(json.dumps({"spectrum_s": spec_s, "lambda_top": lam[: spec.p + 2].tolist(), "delta": delta, "mu": mu}),
+      flush=True)
 cfg = g.SIConfig(k=spec.k, p=spec.p, eps=spec.eps, mu=mu, delta=delta, seed=spec.seed)
 ctx.enable_profiling(True)
 ctx.reset_profile()
