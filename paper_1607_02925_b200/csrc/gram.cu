@@ -6,10 +6,17 @@
 // share one layout and no transposes happen at the boundary.
 #include "gram.cuh"
 
+#include <cooperative_groups.h>
+
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
+#include <map>
+#include <vector>
 
 namespace gaplra_cuda {
+
+namespace cg = cooperative_groups;
 
 namespace {
 
@@ -591,6 +598,632 @@ struct XyRun {
 };
 
 // ---------------------------------------------------------------------------
+// Single-pass Z = X (Xᵀ W) (and Y = Xᵀ W), X read from HBM once (north star
+// item 2).
+//
+// One thread-block cluster of G CTAs splits the d rows (R = 256 or 128 rows per
+// CTA); W's row slice stays in shared memory and Z's row slice in registers for
+// the whole pass, so only X streams.  The clusters take 16-column tiles of X
+// round-robin.  Warp roles per CTA:
+//   producer  one cp.async.bulk per column slice into a 2-4 stage ring
+//   8 compute A  Ŷ_g = X_tile[rows g]ᵀ W[rows g]  (DMMA m8n8k4; warp = m-tile x
+//                K quarter), partials to a double-buffered shared slab
+//             B  Z[rows g] += X_tile[rows g] · Y_tile  (DMMA, accumulators in
+//                registers; the tile's X fragments are re-read from L2 one
+//                iteration ahead, so the stage is freed right after A)
+//   2 exchange RS: fixed-order sum of the K quarters, entry chunk q st.async'd
+//                to CTA q (complete_tx on q's mbarrier); AG: q sums the G
+//                chunks in rank order, writes them to Y and st.async's them to
+//                every CTA
+// Compute iteration t runs A(t+2) | B(t) while the exchange warps run RS(t+2)
+// and AG(t+1), so each DSMEM exchange has a whole iteration to land.  Every
+// reduction has a fixed order, so the pass is bitwise run-to-run stable.  The
+// cluster partials of Z are summed in cluster order by k_sum_splits.
+// Shared-memory pitches (doubles): X slices XP = R + 4 (XP/2 ≡ 2 mod 8), W rows
+// BP = 8NT + 2 (≡ 2 mod 8), Y_tile rows YP = 8NT + 4; with the column
+// permutation perm(gq) in phase A the fragment loads are bank-conflict free.
+// Measured (GAPLRA_GRAM_TIMING, tools/gram_probe.py): at d = 4096 only seven
+// 16-CTA clusters are resident (112 of 148 SMs) and a tile costs ~5300 cycles at
+// p = 20 (DMMA issue 57 % of peak on the active SMs) — slower than the two-pass
+// kernels there, faster at d <= 1024, where it is the default (plan()).
+// ---------------------------------------------------------------------------
+namespace fused {
+
+constexpr int kNB = 16;  // columns of X per tile
+constexpr int kWarps = 8;  // compute (DMMA) warps
+constexpr int kXch = 2;    // exchange warps: reduce-scatter / all-gather over DSMEM
+constexpr int kThreads = 32 * (kWarps + kXch + 1);  // + one producer warp
+
+__host__ __device__ constexpr int bp(int nt) { return 8 * nt + 2; }
+__host__ __device__ constexpr int yp(int nt) { return 8 * nt + 4; }  // ≡ 4 or 12 (mod 16)
+constexpr int kSlots = 3;     // exchange slots: tiles t, t+1, t+2 in flight
+constexpr int kRedParts = 4;  // phase A: warp = (m-tile, K quarter)
+
+struct Layout {
+  int xp, stage, off_w, off_red, off_rs, off_yt, off_ys, off_bar, ch;
+  size_t bytes;
+};
+__host__ __device__ inline Layout layout(int nt, int r, int g, int stages) {
+  Layout L;
+  L.xp = r + 4;
+  L.stage = kNB * L.xp;
+  L.ch = kNB * 8 * nt / g;
+  L.off_w = stages * L.stage;
+  L.off_red = L.off_w + r * bp(nt);
+  L.off_rs = L.off_red + 2 * kRedParts * kNB * 8 * nt;
+  L.off_yt = L.off_rs + kSlots * g * L.ch;
+  L.off_ys = L.off_yt + kSlots * kNB * yp(nt);
+  L.off_bar = L.off_ys + L.ch;
+  L.bytes = static_cast<size_t>(L.off_bar + 24) * sizeof(double);
+  return L;
+}
+
+__device__ __forceinline__ uint32_t su32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void bar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(count));
+}
+__device__ __forceinline__ void bar_expect(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ void bar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "W_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra W_%=;\n\t}" ::"r"(su32(b)),
+      "r"(parity)
+      : "memory");
+}
+// producer-side wait: back off instead of spinning (the producers run ahead)
+__device__ __forceinline__ void bar_wait_backoff(uint64_t* b, uint32_t parity) {
+  for (;;) {
+    uint32_t done;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(su32(b)), "r"(parity)
+        : "memory");
+    if (done) return;
+    __nanosleep(64);
+  }
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   su32(dst)),
+               "l"(src), "r"(bytes), "r"(su32(b))
+               : "memory");
+}
+__device__ __forceinline__ uint32_t peer_addr(uint32_t local, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local), "r"(rank));
+  return r;
+}
+// 16-byte remote store completing 16 transaction bytes on the peer's mbarrier
+__device__ __forceinline__ void st_async2(uint32_t raddr, double2 v, uint32_t rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.b64 [%0], {%1, %2}, [%3];" ::"r"(raddr),
+               "l"(__double_as_longlong(v.x)), "l"(__double_as_longlong(v.y)), "r"(rbar)
+               : "memory");
+}
+__device__ __forceinline__ void compute_sync() { asm volatile("bar.sync 1, %0;" ::"n"(32 * kWarps) : "memory"); }
+
+struct Args {
+  const double* X;
+  int64_t ldx;
+  int n, rows_total;
+  const double* W;
+  int64_t ldw;
+  int pc;
+  double* Y;
+  int64_t ldy;
+  double* Z;  // Z (one cluster) or part + cluster * zstride (ld = pc)
+  int64_t ldz;
+  size_t zstride;
+  int stages;
+  long long* dbg;  // GAPLRA_GRAM_TIMING: per-CTA cycle counters (thread 0), else null
+};
+
+template <int NT, int R>
+__global__ void __launch_bounds__(kThreads, 1) k_gram_fused(Args a) {
+  constexpr int RW = R / kWarps;  // rows per compute warp
+  constexpr int NC8 = 8 * NT, BP = bp(NT), YP = yp(NT);
+  constexpr int NP = kNB * NC8 / 2;              // entry pairs of a tile's Ŷ
+  constexpr int PER = (NP + 32 * kXch - 1) / (32 * kXch);  // pairs per exchange thread
+  static_assert(RW % 16 == 0, "phase B takes 16-row groups");
+  extern __shared__ __align__(128) double sm[];
+  cg::cluster_group cluster = cg::this_cluster();
+  const int G = static_cast<int>(cluster.num_blocks());
+  const int g = static_cast<int>(cluster.block_rank());
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int gq = lane >> 2, tq = lane & 3;
+  const int S = a.stages;
+  const Layout L = layout(NT, R, G, S);
+  const int XP = L.xp, CH = L.ch;
+  double* Ws = sm + L.off_w;
+  double* red = sm + L.off_red;  // [2][kRedParts][kNB][NC8]
+  double* rs = sm + L.off_rs;    // [kSlots][G][CH]
+  double* yt = sm + L.off_yt;    // [kSlots][kNB][YP]
+  double* ysum = sm + L.off_ys;  // [CH]
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + L.off_bar);
+  uint64_t* empty = full + 4;
+  uint64_t* rsb = full + 8;        // [kSlots]
+  uint64_t* agb = full + 11;       // [kSlots]
+  uint64_t* red_full = full + 14;  // [2]
+  uint64_t* red_empty = full + 16; // [2]
+  const int r0 = g * R;
+  const int rc = max(0, min(R, a.rows_total - r0));
+  const int ncl = gridDim.y, ci = blockIdx.y;
+  const int T = static_cast<int>((a.n + kNB - 1) / kNB);
+  const int Tl = ci < T ? (T - 1 - ci) / ncl + 1 : 0;
+  auto tile_col0 = [&](int lt) { return (ci + lt * ncl) * kNB; };
+  // GAPLRA_GRAM_TIMING: wait cycles of lane 0 of the first warp of each role
+  long long tw[4] = {0, 0, 0, 0};
+  const bool rec = a.dbg && lane == 0 && (warp == 0 || warp == kWarps || warp == kWarps + kXch);
+  auto timed_wait = [&](int k, uint64_t* b, uint32_t par) {
+    const long long t = rec ? clock64() : 0;
+    bar_wait(b, par);
+    if (rec) tw[k] += clock64() - t;
+  };
+
+  for (int e = tid; e < L.off_bar; e += blockDim.x) sm[e] = 0.0;
+  __syncthreads();
+  for (int e = tid; e < rc * a.pc; e += blockDim.x) {
+    const int r = e / a.pc, c = e - (e / a.pc) * a.pc;
+    Ws[r * BP + c] = a.W[static_cast<int64_t>(r0 + r) * a.ldw + c];
+  }
+  if (tid == 0) {
+    for (int s = 0; s < 4; ++s) {
+      bar_init(&full[s], 1);
+      bar_init(&empty[s], kWarps);
+    }
+    for (int s = 0; s < kSlots; ++s) {
+      bar_init(&rsb[s], 1);
+      bar_init(&agb[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      bar_init(&red_full[s], 32 * kWarps);
+      bar_init(&red_empty[s], 32 * kXch);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int s = 0; s < kSlots && s < Tl; ++s) {
+      bar_expect(&rsb[s], static_cast<uint32_t>(G * CH * 8));
+      bar_expect(&agb[s], static_cast<uint32_t>(kNB * NC8 * 8));
+    }
+  }
+  cluster.sync();
+
+  if (warp >= kWarps + kXch) {  // ----------------------------------------- producer
+    if (lane == 0) {
+      for (int lt = 0; lt < Tl; ++lt) {
+        const int s = lt % S;
+        const long long tb = rec ? clock64() : 0;
+        if (lt >= S) bar_wait_backoff(&empty[s], static_cast<uint32_t>(((lt / S) & 1) ^ 1));
+        if (rec) tw[0] += clock64() - tb;
+        const int j0 = tile_col0(lt);
+        const int nv = min(kNB, a.n - j0);
+        bar_expect(&full[s], static_cast<uint32_t>(nv * rc * 8));
+        double* dst = sm + s * L.stage;
+        for (int c = 0; c < nv; ++c)
+          bulk_g2s(dst + c * XP, a.X + static_cast<int64_t>(j0 + c) * a.ldx + r0, static_cast<uint32_t>(rc * 8),
+                   &full[s]);
+      }
+    }
+  } else if (warp >= kWarps) {  // ------------------------------------------ exchange
+    const int xt = tid - 32 * kWarps;
+    // fixed per-thread targets: RS pair i -> CTA q = 2i / CH; AG send k -> (pair k % (CH/2), CTA k / (CH/2))
+    uint32_t rs_addr[PER], rs_bar[PER], ag_addr[PER], ag_bar[PER];
+    int ag_pair[PER];
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+      const int i = min(xt + 32 * kXch * j, NP - 1);
+      const int e = 2 * i, q = e / CH, off = e - q * CH;
+      rs_addr[j] = peer_addr(su32(rs) + (g * CH + off) * 8u, q);
+      rs_bar[j] = peer_addr(su32(&rsb[0]), q);
+      const int half = CH / 2;
+      const int pr = i % half, qa = i / half;
+      const int ea = g * CH + 2 * pr, col = ea / NC8, rhs = ea - col * NC8;
+      ag_pair[j] = pr;
+      ag_addr[j] = peer_addr(su32(yt) + (col * YP + rhs) * 8u, qa);
+      ag_bar[j] = peer_addr(su32(&agb[0]), qa);
+    }
+    auto xch_sync = []() { asm volatile("bar.sync 2, %0;" ::"n"(32 * kXch) : "memory"); };
+    auto rs_step = [&](int t) {  // fixed-order sum of the K quarters, reduce-scatter
+      const int b = t & 1;
+      timed_wait(0, &red_full[b], static_cast<uint32_t>((t >> 1) & 1));
+      const double* rb = red + b * kRedParts * kNB * NC8;
+      const int slot = t % kSlots;
+#pragma unroll
+      for (int j = 0; j < PER; ++j) {
+        const int i = xt + 32 * kXch * j;
+        if (i < NP) {
+          double2 v = *reinterpret_cast<const double2*>(rb + 2 * i);
+#pragma unroll
+          for (int w = 1; w < kRedParts; ++w) {
+            const double2 u = *reinterpret_cast<const double2*>(rb + w * kNB * NC8 + 2 * i);
+            v.x += u.x;
+            v.y += u.y;
+          }
+          st_async2(rs_addr[j] + slot * G * CH * 8u, v, rs_bar[j] + slot * 8u);
+        }
+      }
+      bar_arrive(&red_empty[b]);
+    };
+    auto ag_step = [&](int t) {  // owner sum in rank order, all-gather, Y to HBM
+      const int slot = t % kSlots;
+      timed_wait(1, &rsb[slot], static_cast<uint32_t>((t / kSlots) & 1));
+      if (xt == 0 && t + kSlots < Tl) bar_expect(&rsb[slot], static_cast<uint32_t>(G * CH * 8));
+      const double* rsl = rs + slot * G * CH;
+      xch_sync();  // the previous step's ysum reads are done
+      const int j0 = tile_col0(t);
+      for (int pr = xt; pr < CH / 2; pr += 32 * kXch) {
+        double2 v = *reinterpret_cast<const double2*>(rsl + 2 * pr);
+#pragma unroll
+        for (int s2 = 1; s2 < 16; ++s2) {
+          if (s2 < G) {
+            const double2 u = *reinterpret_cast<const double2*>(rsl + s2 * CH + 2 * pr);
+            v.x += u.x;
+            v.y += u.y;
+          }
+        }
+        *reinterpret_cast<double2*>(ysum + 2 * pr) = v;
+        const int e = g * CH + 2 * pr, col = e / NC8, rhs = e - col * NC8;
+        if (j0 + col < a.n) {
+          double* yo = a.Y + static_cast<int64_t>(j0 + col) * a.ldy + rhs;
+          if (rhs + 1 < a.pc) {
+            yo[0] = v.x;
+            yo[1] = v.y;
+          } else if (rhs < a.pc) {
+            yo[0] = v.x;
+          }
+        }
+      }
+      xch_sync();
+#pragma unroll
+      for (int j = 0; j < PER; ++j)
+        if (xt + 32 * kXch * j < NP)
+          st_async2(ag_addr[j] + slot * kNB * YP * 8u, *reinterpret_cast<const double2*>(ysum + 2 * ag_pair[j]),
+                    ag_bar[j] + slot * 8u);
+    };
+#pragma unroll 1
+    for (int t = 0; t <= Tl; ++t) {
+      if (t < Tl) rs_step(t);
+      if (t >= 1) ag_step(t - 1);
+    }
+  } else {  // ---------------------------------------------------------------- compute
+    const int perm = ((gq & 1) << 1) | ((gq >> 1) & 1) | (gq & 4);  // 0 2 1 3 4 6 5 7
+    double accz[RW / 16][2][NT][2];
+#pragma unroll
+    for (int h = 0; h < RW / 16; ++h)
+#pragma unroll
+      for (int e = 0; e < 2; ++e)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) accz[h][e][nt][0] = accz[h][e][nt][1] = 0.0;
+
+    // phase A: warp w takes m-tile w / 4 (8 of the 16 columns) and the K
+    // quarter w % 4 of the CTA's rows; the exchange warps sum the quarters
+    auto phase_a = [&](int lt) {
+      constexpr int RQ = R / kRedParts;
+      const int mt = warp / kRedParts, kq = warp % kRedParts;
+      const int s = lt % S;
+      timed_wait(0, &full[s], static_cast<uint32_t>((lt / S) & 1));
+      const double* xs = sm + s * L.stage + (mt * 8 + perm) * XP + kq * RQ + 2 * tq;
+      const double* wsb = Ws + (kq * RQ + 2 * tq) * BP + gq;
+      // NACC independent accumulator sets (summed in order at the end): the
+      // DMMA latency (~120 cycles) would otherwise serialise the K loop
+      constexpr int NACC = NT == 1 ? 4 : 2;
+      double acc[NACC][NT][2];
+#pragma unroll
+      for (int q = 0; q < NACC; ++q)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) acc[q][nt][0] = acc[q][nt][1] = 0.0;
+#pragma unroll
+      for (int kb = 0; kb < RQ / 8; ++kb) {
+        const double2 av = *reinterpret_cast<const double2*>(xs + 8 * kb);
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int q = (2 * kb + u) % NACC;
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt)
+            mma884(acc[q][nt][0], acc[q][nt][1], u ? av.y : av.x, wsb[(8 * kb + u) * BP + nt * 8]);
+        }
+      }
+#pragma unroll
+      for (int q = 1; q < NACC; ++q)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          acc[0][nt][0] += acc[q][nt][0];
+          acc[0][nt][1] += acc[q][nt][1];
+        }
+      __syncwarp();
+      if (lane == 0) bar_arrive(&empty[s]);  // phase B re-reads the tile from L2, not from the stage
+      const int b = lt & 1;
+      if (lt >= 2) timed_wait(1, &red_empty[b], static_cast<uint32_t>(((lt >> 1) & 1) ^ 1));
+      double* rb = red + b * kRedParts * kNB * NC8;
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+        *reinterpret_cast<double2*>(rb + (kq * kNB + mt * 8 + perm) * NC8 + nt * 8 + 2 * tq) =
+            make_double2(acc[0][nt][0], acc[0][nt][1]);
+      bar_arrive(&red_full[b]);
+    };
+
+    // phase B operands: the tile's X fragments, re-read from L2 (the tile left
+    // HBM two iterations earlier) into registers one iteration ahead of use,
+    // so the shared-memory stage is free as soon as phase A has read it
+    const int rbase = warp * RW + 2 * gq;
+    auto load_b = [&](int lt, double2 (&xb)[RW / 16][kNB / 4]) {
+      const int j0 = tile_col0(lt);
+#pragma unroll
+      for (int ks = 0; ks < kNB / 4; ++ks) {
+        const int j = j0 + 4 * ks + tq;
+#pragma unroll
+        for (int h = 0; h < RW / 16; ++h) {
+          const int row = rbase + 16 * h;
+          xb[h][ks] = (j < a.n && row < rc) ? ldg2(a.X + static_cast<int64_t>(j) * a.ldx + r0 + row)
+                                            : make_double2(0.0, 0.0);
+        }
+      }
+    };
+    auto phase_b = [&](int lt, const double2 (&xb)[RW / 16][kNB / 4]) {
+      const int slot = lt % kSlots;
+      timed_wait(2, &agb[slot], static_cast<uint32_t>((lt / kSlots) & 1));
+      if (tid == 0 && lt + kSlots < Tl) bar_expect(&agb[slot], static_cast<uint32_t>(kNB * NC8 * 8));
+      const double* ys = yt + slot * kNB * YP;
+      const int nv = min(kNB, a.n - tile_col0(lt));
+#pragma unroll
+      for (int ks = 0; ks < kNB / 4; ++ks) {
+        const int k = 4 * ks + tq;
+        double bv[NT];
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) bv[nt] = k < nv ? ys[k * YP + nt * 8 + gq] : 0.0;
+#pragma unroll
+        for (int h = 0; h < RW / 16; ++h) {
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) {
+            mma884(accz[h][0][nt][0], accz[h][0][nt][1], xb[h][ks].x, bv[nt]);
+            mma884(accz[h][1][nt][0], accz[h][1][nt][1], xb[h][ks].y, bv[nt]);
+          }
+        }
+      }
+    };
+
+    // software pipeline: compute iteration t runs A(t+2) then B(t); the
+    // exchange warps run RS(t+2) and AG(t+1) meanwhile, so each exchange has
+    // a whole iteration to land.  Slot reuse is safe with 3 slots: a peer
+    // sends RS(t+3) / AG(t+3) only after this CTA's RS(t+3), which follows
+    // the B(t) of every compute warp.
+    long long t0 = clock64();
+    if (Tl > 0) phase_a(0);
+    if (Tl > 1) phase_a(1);
+    if constexpr (NT <= 2) {
+      // light DMMA work per tile: prefetch phase B's operands two tiles ahead
+      double2 xa[RW / 16][kNB / 4], xc[RW / 16][kNB / 4];
+      if (Tl > 0) load_b(0, xa);
+      if (Tl > 1) load_b(1, xc);
+#pragma unroll 1
+      for (int lt = 0; lt < Tl; lt += 2) {
+        if (lt + 2 < Tl) phase_a(lt + 2);
+        phase_b(lt, xa);
+        if (lt + 2 < Tl) load_b(lt + 2, xa);
+        if (lt + 1 < Tl) {
+          if (lt + 3 < Tl) phase_a(lt + 3);
+          phase_b(lt + 1, xc);
+          if (lt + 3 < Tl) load_b(lt + 3, xc);
+        }
+      }
+    } else {
+      double2 xb[RW / 16][kNB / 4];
+#pragma unroll 1
+      for (int lt = 0; lt < Tl; ++lt) {
+        load_b(lt, xb);
+        if (lt + 2 < Tl) phase_a(lt + 2);
+        phase_b(lt, xb);
+      }
+    }
+    if (a.dbg && tid == 0) {
+      const int cta = blockIdx.y * gridDim.x + blockIdx.x;
+      a.dbg[cta * 12 + 0] = clock64() - t0;
+      a.dbg[cta * 12 + 10] = Tl;
+    }
+#pragma unroll
+    for (int h = 0; h < RW / 16; ++h)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int row = warp * RW + 16 * h + 2 * gq + e;
+        if (row >= rc) continue;
+        double* zo = a.Z + ci * a.zstride + static_cast<int64_t>(r0 + row) * a.ldz;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          const int c = nt * 8 + 2 * tq;
+          if (c + 1 < a.pc) {
+            zo[c] = accz[h][e][nt][0];
+            zo[c + 1] = accz[h][e][nt][1];
+          } else if (c < a.pc) {
+            zo[c] = accz[h][e][nt][0];
+          }
+        }
+      }
+  }
+  if (rec) {
+    const int cta = blockIdx.y * gridDim.x + blockIdx.x;
+    const int base = warp == 0 ? 1 : (warp == kWarps ? 4 : 7);
+    for (int k = 0; k < 3; ++k) a.dbg[cta * 12 + base + k] = tw[k];
+  }
+  cluster.sync();  // no CTA leaves while a peer may still st.async into it
+}
+
+struct Plan {
+  int r = 0, g = 0, stages = 0, ncl = 0;
+  size_t smem = 0;
+};
+
+template <int NT, int R>
+int max_clusters(int G, size_t smem) {
+  auto kern = k_gram_fused<NT, R>;
+  GAPLRA_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  GAPLRA_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3(G, 64, 1);
+  lc.blockDim = dim3(kThreads, 1, 1);
+  lc.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = G;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  lc.attrs = attr;
+  lc.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, kern, &lc) != cudaSuccess || n < 1) {
+    (void)cudaGetLastError();
+    n = std::max(1, sm_count() / G);
+  }
+  return n;
+}
+
+template <int NT, int R>
+int max_clusters_cached(int G, size_t smem) {
+  static std::map<std::pair<int, size_t>, int> cache;
+  int& c = cache[{G, smem}];
+  if (!c) c = max_clusters<NT, R>(G, smem);
+  return c;
+}
+
+constexpr size_t kSmemCap = 227 * 1024;
+
+// Layout for one <= 32-column chunk; g = 0 when the fused pass does not apply.
+Plan plan(const DenseX& X, int pc) {
+  Plan pl;
+  // GAPLRA_GRAM_FUSED: 0 never, 2 wherever the layout fits, 1 (default) where
+  // it measured faster than the two-pass kernels: d <= 1024 (C1: p = 10 0.042
+  // vs 0.072 ms, p = 1 0.032 vs 0.062 ms).  At d = 4096 only seven 16-CTA
+  // clusters fit (112 SMs) and the per-tile exchange costs more than the
+  // second read of X saves (C2 p = 20: 2.4 vs 1.8 ms; p = 1: 1.2 vs 1.13 ms).
+  static const int mode = getenv("GAPLRA_GRAM_FUSED") ? atoi(getenv("GAPLRA_GRAM_FUSED")) : 1;
+  if (!mode || (mode == 1 && X.ld > 1024)) return pl;
+  const int nt = (pc + 7) / 8;
+  const int64_t ld = X.ld;
+  // prefer 256 rows per CTA (fewer exchange bytes per X byte), then 128, and
+  // four X stages (A(t+2) and B(t) hold two, one prefetches) over three
+  int r = 0, gp = 0, stages = 0;
+  for (int want = 4; want >= 2 && !r; --want)  // the ring holds only the tile phase A reads
+    for (int rr : {256, 128}) {
+      if (rr == 256 && ld <= 1024) continue;  // small d: keep clusters small
+      int g = 1;
+      while (g < ceil_div(ld, rr)) g <<= 1;
+      if (g > 16 || layout(nt, rr, g, want).bytes > kSmemCap) continue;
+      r = rr;
+      gp = g;
+      stages = want;
+      break;
+    }
+  if (!r) return pl;
+  pl.r = r;
+  pl.g = gp;
+  pl.stages = stages;
+  pl.smem = layout(nt, r, gp, stages).bytes;
+  return pl;
+}
+
+template <int NT, int R>
+void launch_chunk(const DenseX& X, const double* W, int64_t ldw, int pc, double* Y, int64_t ldy, double* Z,
+                  int64_t ldz, GramWork& work, cudaStream_t st, const Plan& pl) {
+  const int T = static_cast<int>(ceil_div(X.n, kNB));
+  const int ncl = std::max(1, std::min(max_clusters_cached<NT, R>(pl.g, pl.smem), T));
+  Args args;
+  args.X = X.x;
+  args.ldx = X.ld;
+  args.n = X.n;
+  args.rows_total = static_cast<int>(X.ld);
+  args.W = W;
+  args.ldw = ldw;
+  args.pc = pc;
+  args.Y = Y;
+  args.ldy = ldy;
+  args.stages = pl.stages;
+  args.dbg = nullptr;
+  static const bool timing = getenv("GAPLRA_GRAM_TIMING") != nullptr;
+  static long long* dbg_buf = nullptr;
+  const int nctas = pl.g * ncl;
+  if (timing) {
+    if (!dbg_buf) GAPLRA_CUDA_CHECK(cudaMalloc(&dbg_buf, 12 * sizeof(long long) * 16 * 64));
+    args.dbg = dbg_buf;
+  }
+  const size_t stride = static_cast<size_t>(X.ld) * pc;
+  if (ncl == 1) {
+    args.Z = Z;
+    args.ldz = ldz;
+    args.zstride = 0;
+  } else {
+    if (work.part_elems < stride * ncl) throw Error(kContractViolation, "gram_fused: workspace too small");
+    args.Z = work.part;
+    args.ldz = pc;
+    args.zstride = stride;
+  }
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3(pl.g, ncl, 1);
+  lc.blockDim = dim3(kThreads, 1, 1);
+  lc.dynamicSmemBytes = pl.smem;
+  lc.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = pl.g;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  lc.attrs = attr;
+  lc.numAttrs = 1;
+  auto kern = k_gram_fused<NT, R>;
+  GAPLRA_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(pl.smem)));
+  GAPLRA_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  static const bool dbg = getenv("GAPLRA_GRAM_DEBUG") != nullptr;
+  if (dbg)
+    fprintf(stderr, "gram_fused: ld %lld n %d pc %d -> R %d G %d stages %d smem %zu clusters %d\n",
+            static_cast<long long>(X.ld), X.n, pc, pl.r, pl.g, pl.stages, pl.smem, ncl);
+  GAPLRA_CUDA_CHECK(cudaLaunchKernelEx(&lc, kern, args));
+  GAPLRA_LAUNCH_CHECK();
+  if (timing) {  // cycles per tile, averaged over CTAs: wait X, wait RS, wait AG, compute_sync, rest
+    std::vector<long long> h(static_cast<size_t>(nctas) * 12);
+    GAPLRA_CUDA_CHECK(cudaMemcpyAsync(h.data(), dbg_buf, h.size() * sizeof(long long), cudaMemcpyDeviceToHost, st));
+    GAPLRA_CUDA_CHECK(cudaStreamSynchronize(st));
+    double v[10] = {}, tiles = 0;
+    for (int c = 0; c < nctas; ++c) {
+      for (int k = 0; k < 10; ++k) v[k] += h[c * 12 + k];
+      tiles += h[c * 12 + 10];
+    }
+    for (double& x : v) x /= tiles;
+    fprintf(stderr,
+            "gram_fused timing (cycles/tile): total %.0f | compute wait X %.0f red_empty %.0f AG %.0f | exchange "
+            "wait red_full %.0f RS %.0f | producer wait empty %.0f\n",
+            v[0], v[1], v[2], v[3], v[4], v[5], v[7]);
+  }
+  if (ncl > 1) {
+    k_sum_splits<<<sm_count() * 4, 256, 0, st>>>(work.part, ncl, stride, static_cast<int>(X.ld), pc, pc, Z, ldz);
+    GAPLRA_LAUNCH_CHECK();
+  }
+}
+
+int clusters_for(const DenseX& X, int pc, const Plan& pl) {
+  const int T = static_cast<int>(ceil_div(X.n, kNB));
+  int c = 0;
+  switch ((pc + 7) / 8 * 1000 + pl.r) {
+    case 1128: c = max_clusters_cached<1, 128>(pl.g, pl.smem); break;
+    case 1256: c = max_clusters_cached<1, 256>(pl.g, pl.smem); break;
+    case 2128: c = max_clusters_cached<2, 128>(pl.g, pl.smem); break;
+    case 2256: c = max_clusters_cached<2, 256>(pl.g, pl.smem); break;
+    case 3128: c = max_clusters_cached<3, 128>(pl.g, pl.smem); break;
+    case 3256: c = max_clusters_cached<3, 256>(pl.g, pl.smem); break;
+    case 4128: c = max_clusters_cached<4, 128>(pl.g, pl.smem); break;
+    default: c = max_clusters_cached<4, 256>(pl.g, pl.smem); break;
+  }
+  return std::max(1, std::min(c, T));
+}
+
+}  // namespace fused
+
+// ---------------------------------------------------------------------------
 // Sparse (CSC for Xᵀ W, CSR for X Y): one thread per output row of Y / Z.
 // ---------------------------------------------------------------------------
 template <int NC>
@@ -696,6 +1329,11 @@ size_t gram_work_elems(const DenseX& X, int p) {
   size_t need = 0;
   for (int c0 = 0; c0 < p; c0 += 32) {
     const int pc = std::min(32, p - c0);
+    const fused::Plan fp = fused::plan(X, pc);
+    if (fp.g) {  // (the two-pass needs below still apply: H = Xᵀ C runs launch_xtw alone)
+      const int ncl = fused::clusters_for(X, pc, fp);
+      if (ncl > 1) need = std::max(need, static_cast<size_t>(ncl) * X.ld * pc);
+    }
     if (use_mma(pc)) {
       const MmaPlan m = mma_plan(X);
       if (m.rs > 1) need = std::max(need, static_cast<size_t>(m.rs) * X.n * pc);
@@ -708,6 +1346,34 @@ size_t gram_work_elems(const DenseX& X, int p) {
     if (b.s > 1) need = std::max(need, static_cast<size_t>(b.s) * X.ld * pc);
   }
   return need;
+}
+
+bool gram_fused_applies(const DenseX& X, int p) {
+  for (int c0 = 0; c0 < p; c0 += 32)
+    if (!fused::plan(X, std::min(32, p - c0)).g) return false;
+  return true;
+}
+
+void launch_gram_fused(const DenseX& X, const double* W, int64_t ldw, int p, double* Y, int64_t ldy, double* Z,
+                       int64_t ldz, GramWork& work, cudaStream_t st) {
+  for (int c0 = 0; c0 < p; c0 += 32) {
+    const int pc = std::min(32, p - c0);
+    const fused::Plan pl = fused::plan(X, pc);
+    if (!pl.g) throw Error(kContractViolation, "gram_fused: layout does not apply");
+    const double* w = W + c0;
+    double* y = Y + c0;
+    double* z = Z + c0;
+    switch ((pc + 7) / 8 * 1000 + pl.r) {
+      case 1128: fused::launch_chunk<1, 128>(X, w, ldw, pc, y, ldy, z, ldz, work, st, pl); break;
+      case 1256: fused::launch_chunk<1, 256>(X, w, ldw, pc, y, ldy, z, ldz, work, st, pl); break;
+      case 2128: fused::launch_chunk<2, 128>(X, w, ldw, pc, y, ldy, z, ldz, work, st, pl); break;
+      case 2256: fused::launch_chunk<2, 256>(X, w, ldw, pc, y, ldy, z, ldz, work, st, pl); break;
+      case 3128: fused::launch_chunk<3, 128>(X, w, ldw, pc, y, ldy, z, ldz, work, st, pl); break;
+      case 3256: fused::launch_chunk<3, 256>(X, w, ldw, pc, y, ldy, z, ldz, work, st, pl); break;
+      case 4128: fused::launch_chunk<4, 128>(X, w, ldw, pc, y, ldy, z, ldz, work, st, pl); break;
+      default: fused::launch_chunk<4, 256>(X, w, ldw, pc, y, ldy, z, ldz, work, st, pl); break;
+    }
+  }
 }
 
 void launch_xtw(const DenseX& X, const double* W, int64_t ldw, int p, double* Y, int64_t ldy, GramWork& work,

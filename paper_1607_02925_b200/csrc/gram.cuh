@@ -49,6 +49,13 @@ void launch_xtw(const DenseX& X, const double* W, int64_t ldw, int p, double* Y,
 void launch_xy(const DenseX& X, const double* Y, int64_t ldy, int p, double* Z, int64_t ldz,
                GramWork& work, cudaStream_t st);
 
+// Single-pass Z = X (Xᵀ W) and Y = Xᵀ W (X read once; cluster row split, W and
+// Z resident on chip).  Fits when X.ld <= 16 * 256 and is the default where it
+// measured faster (d <= 1024); gram_fused_applies says.
+bool gram_fused_applies(const DenseX& X, int p);
+void launch_gram_fused(const DenseX& X, const double* W, int64_t ldw, int p, double* Y, int64_t ldy, double* Z,
+                       int64_t ldz, GramWork& work, cudaStream_t st);
+
 void launch_xtw_sparse(const SparseX& X, const double* W, int64_t ldw, int p, double* Y,
                        int64_t ldy, cudaStream_t st);
 void launch_xy_sparse(const SparseX& X, const double* Y, int64_t ldy, int p, double* Z,

@@ -334,8 +334,12 @@ void gram_block_dev(Context& c, const Matrix& X, int p, const double* W, int64_t
     GramWork w;
     w.part_elems = gram_work_elems(D, p);
     w.part = w.part_elems ? c.gw.ensure(w.part_elems) : nullptr;
-    launch_xtw(D, W, ldw, p, Y, ldy, w, c.st);
-    launch_xy(D, Y, ldy, p, Z, ldz, w, c.st);
+    if (gram_fused_applies(D, p)) {  // one pass over X (d <= 4096)
+      launch_gram_fused(D, W, ldw, p, Y, ldy, Z, ldz, w, c.st);
+    } else {
+      launch_xtw(D, W, ldw, p, Y, ldy, w, c.st);
+      launch_xy(D, Y, ldy, p, Z, ldz, w, c.st);
+    }
   } else {
     const SparseX S = X.sparse();
     launch_xtw_sparse(S, W, ldw, p, Y, ldy, c.st);

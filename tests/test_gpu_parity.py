@@ -50,6 +50,50 @@ def test_gram_block_dense(g, oracle, p):
     assert np.abs(y - yo).max() <= 1e-13 * np.linalg.norm(X, 2) * np.abs(W).max() * np.sqrt(d)
 
 
+@pytest.mark.parametrize("d,n,p", [(4096, 3001, 20), (4096, 5, 1), (4096, 1000, 33), (2048, 4099, 32), (1000, 1601, 10),
+                                   (1000, 777, 64), (300, 16, 2), (8192, 300, 3)])
+def test_gram_block_layouts(g, d, n, p):
+    # every single-pass layout (16- / 8- / 4-CTA clusters, 256 / 128 rows per
+    # CTA, ragged last tile, several clusters, 32-column chunks) and the
+    # two-pass fallback (d = 8192) against a float64 numpy product
+    rng = np.random.default_rng(d + n + p)
+    X = rng.standard_normal((d, n))
+    W = rng.standard_normal((d, p))
+    z, y = g.gram_block(g.DeviceMatrix.dense(X), W, want_y=True)
+    yr = X.T @ W
+    zr = X @ yr
+    scale = np.linalg.norm(X, 2) ** 2 * np.abs(W).max()
+    assert np.abs(z - zr).max() <= 1e-13 * scale
+    assert np.abs(y - yr).max() <= 1e-13 * np.linalg.norm(X, 2) * np.abs(W).max() * np.sqrt(d)
+
+
+def test_gram_block_fused_forced_layouts(tmp_path):
+    # the single-pass kernel is the default only for d <= 1024; force it
+    # (GAPLRA_GRAM_FUSED=2, read once per process) for the 16- and 8-CTA
+    # cluster layouts in a child process
+    import os
+    import subprocess
+    import sys
+    code = """
+import sys, numpy as np
+sys.path.insert(0, %r)
+import paper_1607_02925_b200 as g
+for d, n, p in [(4096, 3001, 20), (4096, 37, 1), (2048, 4099, 32), (4096, 999, 33)]:
+    rng = np.random.default_rng(d + n + p)
+    X = rng.standard_normal((d, n)); W = rng.standard_normal((d, p))
+    z, y = g.gram_block(g.DeviceMatrix.dense(X), W, want_y=True)
+    yr = X.T @ W; zr = X @ yr
+    s = np.linalg.norm(X, 2)
+    assert np.abs(z - zr).max() <= 1e-13 * s * s * np.abs(W).max(), (d, n, p)
+    assert np.abs(y - yr).max() <= 1e-13 * s * np.abs(W).max() * np.sqrt(d), (d, n, p)
+    assert np.array_equal(z, g.gram_block(g.DeviceMatrix.dense(X), W)), (d, n, p)
+print("ok")
+""" % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, GAPLRA_GRAM_FUSED="2")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
 def test_gram_block_deterministic(g):
     rng = np.random.default_rng(1)
     X = rng.standard_normal((512, 4096))
