@@ -27,6 +27,9 @@
  * gaplra_restricted_projection         restricted_projection
  * gaplra_shift_invert                  Alg. 7 ShiftedInverse branch on I = {1..k}
  *                                      (SPEC.md:505-516,546-549 / PAPER.md:341-351)
+ * gaplra_cg_solve                      solve_cg / inverse_operator(cg)
+ * gaplra_error_report                  error_report
+ * gaplra_principal_angles              principal_angles
  */
 #ifndef GAPLRA_CUDA_H
 #define GAPLRA_CUDA_H
@@ -94,6 +97,7 @@ typedef struct {
   int epoch_cap;
   double monotone_slack;
   double lambda1_hint; /* with an explicit lambda: upper estimate of lambda_1 (0: none) */
+  int backend;         /* inverse_operator backend: 0 svrg, 1 cg */
 } gaplra_si_config;
 
 typedef struct {
@@ -177,6 +181,20 @@ GAPLRA_API int gaplra_tune_shift(gaplra_ctx* ctx, const gaplra_matrix* x, double
                       int64_t* solve_counter, gaplra_si_report* rep);
 GAPLRA_API int gaplra_restricted_projection(gaplra_ctx* ctx, const gaplra_matrix* x, int p, const double* s, int k,
                                  double* w, double* ritz);
+/* solve_cg: block CG on (lambda I - X Xᵀ) W = B from W = 0,
+ * per-column recurrences, stop when max_c |r_c|/|b_c| <= tol; max_iter <= 0:
+ * d + 10.  IndefiniteShift on nonpositive curvature. */
+GAPLRA_API int gaplra_cg_solve(gaplra_ctx* ctx, const gaplra_matrix* x, double lambda, int p, const double* b,
+                               double* w, double tol, int max_iter, int* iterations, double* history, int hist_cap,
+                               int* hist_len);
+/* error_report: |X - W Wᵀ X|_F exactly (|X|_F^2 - |WᵀX|_F^2)
+ * and the spectral norm by `iters` power iterations (seeded start). */
+GAPLRA_API int gaplra_error_report(gaplra_ctx* ctx, const gaplra_matrix* x, int k, const double* w, int iters,
+                                   uint64_t seed, double* frob, double* spec);
+/* principal_angles: cosines (descending) between span(U),
+ * U d x k orthonormal, and span(S), S d x p full column rank. */
+GAPLRA_API int gaplra_principal_angles(gaplra_ctx* ctx, int d, int k, const double* u, int p, const double* s,
+                                       double* cosines);
 GAPLRA_API int gaplra_shift_invert(gaplra_ctx* ctx, const gaplra_matrix* x, const gaplra_si_config* cfg, double* w,
                         double* ritz, double* s, gaplra_si_report* rep);
 

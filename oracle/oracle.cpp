@@ -527,6 +527,91 @@ struct InverseOp : BlockOp {
   }
 };
 
+// solve_cg: block CG on (lambda I - X X^T) W = B, one
+// independent recurrence per column, all columns stepped together.  Pinned:
+// W0 = 0 (or the warm guess, R0 = B - D W0), stop before an iteration when
+// max_c |r_c| / |b_c| <= tol, IndefiniteShift when p_c^T D p_c <= 0 for a
+// column with r_c != 0, a column with r_c = 0 is frozen (alpha = beta = 0),
+// cap = max_iter > 0 ? max_iter : d + 10 iterations -> SolverStalled.
+// Dots are sequential row sums; D p = lambda p - X (X^T p) is one gram_block.
+struct CgResult {
+  int iterations = 0;
+  std::vector<double> history;
+};
+
+CgResult cg_solve(const Mat& x, double lambda, const Block& b, Block& w, double tol, int max_iter,
+                  orc_ledger* led, int nthreads, const Block* guess = nullptr) {
+  const int d = x.d(), p = b.p;
+  const int cap = max_iter > 0 ? max_iter : d + 10;
+  auto coldot = [&](const Block& u, const Block& v, int c) {
+    double acc = 0.0;
+    for (int i = 0; i < d; ++i) acc += u.at(i, c) * v.at(i, c);
+    return acc;
+  };
+  std::vector<double> bnorm(p), rr(p), pq(p), alpha(p), beta(p);
+  for (int c = 0; c < p; ++c) bnorm[c] = std::sqrt(coldot(b, b, c));
+  Block r = b, z, q(d, p);
+  if (guess) {
+    w = *guess;
+    gram_block(x, w, z, nullptr, nthreads);
+    if (led) led->gram_applies += p;
+    for (int c = 0; c < p; ++c)
+      for (int i = 0; i < d; ++i) r.at(i, c) = b.at(i, c) - (lambda * w.at(i, c) - z.at(i, c));
+  } else {
+    w = Block(d, p);
+  }
+  Block pd = r;
+  for (int c = 0; c < p; ++c) rr[c] = coldot(r, r, c);
+  CgResult res;
+  for (int it = 0;; ++it) {
+    double worst = 0.0;
+    for (int c = 0; c < p; ++c) worst = std::max(worst, std::sqrt(rr[c]) / (bnorm[c] > 0.0 ? bnorm[c] : 1.0));
+    res.history.push_back(worst);
+    if (!std::isfinite(worst)) throw Status(ORC_SOLVER_STALLED);
+    if (worst <= tol) break;
+    if (it >= cap) throw Status(ORC_SOLVER_STALLED);
+    gram_block(x, pd, z, nullptr, nthreads);
+    if (led) led->gram_applies += p;
+    for (int c = 0; c < p; ++c)
+      for (int i = 0; i < d; ++i) q.at(i, c) = lambda * pd.at(i, c) - z.at(i, c);
+    for (int c = 0; c < p; ++c) {
+      pq[c] = coldot(pd, q, c);
+      if (rr[c] > 0.0 && !(pq[c] > 0.0)) throw Status(ORC_INDEFINITE_SHIFT);
+      alpha[c] = rr[c] > 0.0 ? rr[c] / pq[c] : 0.0;
+    }
+    for (int c = 0; c < p; ++c)
+      for (int i = 0; i < d; ++i) {
+        w.at(i, c) += alpha[c] * pd.at(i, c);
+        r.at(i, c) -= alpha[c] * q.at(i, c);
+      }
+    for (int c = 0; c < p; ++c) {
+      const double rn = coldot(r, r, c);
+      beta[c] = rr[c] > 0.0 ? rn / rr[c] : 0.0;
+      rr[c] = rn;
+    }
+    for (int c = 0; c < p; ++c)
+      for (int i = 0; i < d; ++i) pd.at(i, c) = r.at(i, c) + beta[c] * pd.at(i, c);
+    res.iterations++;
+  }
+  if (led) led->linear_solves++;
+  return res;
+}
+
+// inverse_operator(cg, lambda) (backend = cg)
+struct CgOp : BlockOp {
+  Mat x;
+  double lambda, tol;
+  int max_iter;
+  orc_ledger* led;
+  int nthreads;
+  CgOp(const Mat& xx, double lam, double t, int mi, orc_ledger* l, int nt)
+      : x(xx), lambda(lam), tol(t), max_iter(mi), led(l), nthreads(nt) {}
+  void apply(const Block& in, Block& out, const Block* guess = nullptr) override {
+    cg_solve(x, lambda, in, out, tol, max_iter, led, nthreads, guess);
+    if (led) led->operator_applies += in.p;
+  }
+};
+
 // G = Aᵀ B (p x q, row-major), sequential row sums
 std::vector<double> gram_ab(const Block& a, const Block& b) {
   std::vector<double> g(static_cast<size_t>(a.p) * b.p, 0.0);
@@ -683,7 +768,9 @@ void tune_shift(const Mat& x, double delta, const orc_si_config* cfg, int64_t* s
     if (t > 0) hint = 2.0 * lambda - prev_lambda;
     prm.lambda1_hint = hint;
     InverseOp dinv(x, lambda, prm, solve_counter, &rep->ledger, nthreads);
-    const double est = estimate_top(dinv, d, 1.0 / 9.0, derive_seed(cfg->seed, kTagEstD + t),
+    CgOp dcg(x, lambda, cfg->tol_tune, 0, &rep->ledger, nthreads);
+    BlockOp& op = cfg->backend == 1 ? static_cast<BlockOp&>(dcg) : static_cast<BlockOp&>(dinv);
+    const double est = estimate_top(op, d, 1.0 / 9.0, derive_seed(cfg->seed, kTagEstD + t),
                                     cfg->rq_tol, nullptr, &rep->ledger);
     const double inv = 1.0 / std::max(est, 1e-300);
     if (rep->tune_steps < 64) {
@@ -920,8 +1007,10 @@ int orc_shift_invert(const orc_mat* x, const orc_si_config* cfg, double* w, doub
     orc_svrg_params prm = make_prm(cfg, cfg->tol_solve);
     prm.lambda1_hint = rep->lambda1_hint;
     InverseOp dinv(m, rep->lambda, prm, &solves, &rep->ledger, nthreads);
+    CgOp dcg(m, rep->lambda, cfg->tol_solve, 0, &rep->ledger, nthreads);
+    BlockOp& op = cfg->backend == 1 ? static_cast<BlockOp&>(dcg) : static_cast<BlockOp&>(dinv);
     rep->outer_cap = outer_cap(cfg, x->d);
-    Block s = subspace_iterate(dinv, x->d, cfg->p, rep->outer_cap, derive_seed(cfg->seed, kTagSubspace),
+    Block s = subspace_iterate(op, x->d, cfg->p, rep->outer_cap, derive_seed(cfg->seed, kTagSubspace),
                                cfg->conv_tol, &rep->outer_iterations, &rep->ledger);
     Block wb;
     std::vector<double> r;
@@ -958,6 +1047,106 @@ double orc_sin_theta(int d, int k, const double* u, int q, const double* qm) {
   std::vector<double> vals(k), vecs(static_cast<size_t>(k) * k);
   jacobi(k, h.data(), vals.data(), vecs.data());
   return std::sqrt(std::max(vals[0], 0.0));
+}
+
+int orc_cg_solve(const orc_mat* x, double lambda, int p, const double* b, double* w, double tol, int max_iter,
+                 int* iterations, double* history, int hist_cap, int* hist_len, int nthreads) {
+  if (!valid(x) || p < 1 || !(tol > 0.0)) return ORC_CONTRACT_VIOLATION;
+  return guarded([&] {
+    Block bb = Block::from_rowmajor(x->d, p, b), wb;
+    CgResult r;
+    try {
+      r = cg_solve(Mat(x), lambda, bb, wb, tol, max_iter, nullptr, nthreads);
+    } catch (...) {
+      if (iterations) *iterations = -1;
+      throw;
+    }
+    wb.to_rowmajor(w);
+    if (iterations) *iterations = r.iterations;
+    if (hist_len) {
+      *hist_len = static_cast<int>(r.history.size());
+      for (int i = 0; i < std::min(hist_cap, *hist_len); ++i) history[i] = r.history[i];
+    }
+  });
+}
+
+// error_report: frobenius = sqrt(max(0, |X|_F^2 - |W^T X|_F^2))
+// (sequential sums: column j of X^T W is spmv_transpose of column c of W);
+// spectral = power method on P X X^T P, P = I - W W^T: v0 = P g / |P g| with
+// g = gaussian_init(d, 1, derive_seed(seed, "errs")), then `iters` times
+// z = P X X^T v, theta = v^T z, v = z / |z|; spectral = sqrt(max(theta, 0)).
+int orc_error_report(const orc_mat* x, int k, const double* w, int iters, uint64_t seed, double* frob,
+                     double* spec) {
+  if (!valid(x) || k < 0 || k > x->d) return ORC_CONTRACT_VIOLATION;
+  return guarded([&] {
+    Mat m(x);
+    const int d = x->d, n = x->n;
+    double fx = 0.0;
+    for (int j = 0; j < n; ++j) fx += m.column_norm_squared(j);
+    Block wb = Block::from_rowmajor(d, k, w);
+    std::vector<double> yc(n);
+    double fy = 0.0;
+    for (int c = 0; c < k; ++c) {
+      m.spmv_transpose(wb.col(c), yc.data());
+      for (int j = 0; j < n; ++j) fy += yc[j] * yc[j];
+    }
+    *frob = std::sqrt(std::max(fx - fy, 0.0));
+    auto project = [&](std::vector<double>& v) {
+      for (int c = 0; c < k; ++c) {
+        double a = 0.0;
+        for (int i = 0; i < d; ++i) a += wb.at(i, c) * v[i];
+        for (int i = 0; i < d; ++i) v[i] -= a * wb.at(i, c);
+      }
+    };
+    auto normalize = [&](std::vector<double>& v) {
+      double a = 0.0;
+      for (int i = 0; i < d; ++i) a += v[i] * v[i];
+      a = std::sqrt(a);
+      if (a > 0.0)
+        for (int i = 0; i < d; ++i) v[i] /= a;
+      return a;
+    };
+    constexpr uint64_t kTagErr = 0x65727273ull;  // "errs"
+    Block g = gaussian_init(d, 1, derive_seed(seed, kTagErr));
+    std::vector<double> v(g.a.begin(), g.a.end()), t(n), z(d);
+    project(v);
+    double theta = 0.0;
+    if (normalize(v) > 0.0) {
+      for (int it = 0; it < iters; ++it) {
+        m.spmv_transpose(v.data(), t.data());
+        m.spmv(t.data(), z.data());
+        project(z);
+        theta = 0.0;
+        for (int i = 0; i < d; ++i) theta += v[i] * z[i];
+        v = z;
+        if (normalize(v) == 0.0) break;
+      }
+    }
+    *spec = std::sqrt(std::max(theta, 0.0));
+  });
+}
+
+// principal_angles: Q = qr_orthonormalize(S); G = U^T Q
+// (k x p, sequential sums); cosines = sqrt(clamp(eig(G G^T), 0, 1)), descending
+// (jacobi_eigh order), one per column of U.
+int orc_principal_angles(int d, int k, const double* u, int p, const double* s, double* cosines) {
+  if (k < 1 || p < 1 || k > d || p > d) return ORC_CONTRACT_VIOLATION;
+  return guarded([&] {
+    Block q = Block::from_rowmajor(d, p, s);
+    qr_inplace(q);
+    Block ub = Block::from_rowmajor(d, k, u);
+    const std::vector<double> g = gram_ab(ub, q);  // k x p
+    std::vector<double> h(static_cast<size_t>(k) * k, 0.0);
+    for (int a = 0; a < k; ++a)
+      for (int b = 0; b < k; ++b) {
+        double acc = 0.0;
+        for (int j = 0; j < p; ++j) acc += g[static_cast<size_t>(a) * p + j] * g[static_cast<size_t>(b) * p + j];
+        h[static_cast<size_t>(a) * k + b] = acc;
+      }
+    std::vector<double> vals(k), vecs(static_cast<size_t>(k) * k);
+    jacobi(k, h.data(), vals.data(), vecs.data());
+    for (int a = 0; a < k; ++a) cosines[a] = std::sqrt(std::min(std::max(vals[a], 0.0), 1.0));
+  });
 }
 
 }  // extern "C"

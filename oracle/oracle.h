@@ -12,7 +12,8 @@
  *     with every unpinned choice pinned here and in DESIGN.md §2: solve_svrg
  *     (SPEC.md:327-335,362-365), inverse_operator (:345-353), subspace_iterate
  *     (:234-242), estimate_eigenvalues (:254-262), restricted_projection
- *     (:244-252), tune_shift (:423-431).
+ *     (:244-252), tune_shift (:423-431), solve_cg (:317-325),
+ *     error_report (:528-536), principal_angles (:181-189).
  *
  * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / reference
  * arm may load this library, and only as the checker or the timed CPU
@@ -86,6 +87,7 @@ typedef struct {
   int epoch_cap;      /* 0: spec cap                                       */
   double monotone_slack;
   double lambda1_hint; /* with an explicit lambda: upper estimate of lambda_1 (0: none) */
+  int backend;         /* inverse_operator backend: 0 svrg, 1 cg */
 } orc_si_config;
 
 typedef struct {
@@ -147,6 +149,13 @@ int orc_shift_invert(const orc_mat* x, const orc_si_config* cfg, double* w_rowma
 
 /* sin of the largest principal angle between range(U) (d x k, orthonormal)
  * and range(Q) (d x q, orthonormal), computed as |(I - QQ^T)U|_2. */
+int orc_cg_solve(const orc_mat* x, double lambda, int p, const double* b_rowmajor, double* w_rowmajor,
+                 double tol, int max_iter, int* iterations, double* history, int hist_cap, int* hist_len,
+                 int nthreads);
+int orc_error_report(const orc_mat* x, int k, const double* w_rowmajor, int iters, uint64_t seed, double* frob,
+                     double* spec);
+int orc_principal_angles(int d, int k, const double* u_rowmajor, int p, const double* s_rowmajor,
+                         double* cosines);
 double orc_sin_theta(int d, int k, const double* u_rowmajor, int q, const double* q_rowmajor);
 
 #ifdef __cplusplus

@@ -8,7 +8,8 @@ from .gaplra import (  # noqa: F401
     NoPreconditioningNeeded, OutOfMemory, RankDeficient, ShiftInvertResult, ShiftOutOfRange, ShiftState,
     ShiftTuningStalled, SIConfig, SolverReport, SolverStalled, SymmetricEigen, default_context, estimate_top,
     gaussian_init, gram_apply, gram_block, index_stream, jacobi_eigh, orthonormality_defect, qr_orthonormalize,
-    restricted_projection, shift_invert, solve_svrg, svrg_epoch, tune_shift,
+    restricted_projection, shift_invert, solve_svrg, svrg_epoch, tune_shift, solve_cg, error_report,
+    principal_angles,
 )
 
 __version__ = "0.1.0"

@@ -40,7 +40,8 @@ class SiConfig(C.Structure):
                 ("delta", C.c_double), ("lambda_", C.c_double), ("seed", C.c_uint64),
                 ("tol_solve", C.c_double), ("tol_tune", C.c_double), ("conv_tol", C.c_double),
                 ("rq_tol", C.c_double), ("max_outer", C.c_int), ("force", C.c_int),
-                ("epoch_cap", C.c_int), ("monotone_slack", C.c_double), ("lambda1_hint", C.c_double)]
+                ("epoch_cap", C.c_int), ("monotone_slack", C.c_double), ("lambda1_hint", C.c_double),
+                ("backend", C.c_int)]
 
 
 class SiReport(C.Structure):
@@ -104,6 +105,10 @@ _SIGS = {
     "gaplra_restricted_projection": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, _dp, C.c_int, _dp, _dp]),
     "gaplra_shift_invert": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(SiConfig), _dp, _dp, _dp,
                                       C.POINTER(SiReport)]),
+    "gaplra_cg_solve": (C.c_int, [C.c_void_p, C.c_void_p, C.c_double, C.c_int, _dp, _dp, C.c_double, C.c_int,
+                                  _ip, _dp, C.c_int, _ip]),
+    "gaplra_error_report": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, _dp, C.c_int, C.c_uint64, _dp, _dp]),
+    "gaplra_principal_angles": (C.c_int, [C.c_void_p, C.c_int, C.c_int, _dp, C.c_int, _dp, _dp]),
 }
 
 

@@ -292,6 +292,79 @@ __global__ void k_frob2_part(const double* __restrict__ A, int64_t lda, int d, i
   if (threadIdx.x == 0) part[blockIdx.x] = s;
 }
 
+// part[blk][c] = sum over the block's rows of A[r][c] B[r][c]: thread (c, sub)
+// strides the rows by nsub, then a fixed-order shared-memory sum over sub.
+__global__ void k_col_dots_part(const double* __restrict__ A, int64_t lda, const double* __restrict__ B, int64_t ldb,
+                                int d, int p, int rows_per, double* __restrict__ part) {
+  __shared__ double red[256];
+  const int nsub = blockDim.x / p;
+  const int c = threadIdx.x % p, sub = threadIdx.x / p;
+  const int r0 = blockIdx.x * rows_per, r1 = min(r0 + rows_per, d);
+  double s = 0.0;
+  if (sub < nsub)
+    for (int r = r0 + sub; r < r1; r += nsub) s = fma(A[static_cast<int64_t>(r) * lda + c], B[static_cast<int64_t>(r) * ldb + c], s);
+  red[threadIdx.x] = s;
+  __syncthreads();
+  if (threadIdx.x < p) {
+    double t = 0.0;
+    for (int q = 0; q < nsub; ++q) t += red[q * p + threadIdx.x];
+    part[static_cast<int64_t>(blockIdx.x) * p + threadIdx.x] = t;
+  }
+}
+
+// CG pieces (runtime.cu cg_solve_dev; oracle.cpp cg_solve)
+__global__ void k_cg_dq(const double* __restrict__ P, const double* __restrict__ Zg, double lambda,
+                        double* __restrict__ Q, int64_t ld, int d, int p) {
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < static_cast<int64_t>(d) * p;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t i = e / p, o = i * ld + (e - i * p);
+    Q[o] = lambda * P[o] - Zg[o];
+  }
+}
+// alpha = rr / pq (0 for a frozen column), status[0] = 1 on nonpositive curvature
+__global__ void k_cg_alpha(const double* __restrict__ rr, const double* __restrict__ pq, int p,
+                           double* __restrict__ alpha, int* __restrict__ status) {
+  const int c = threadIdx.x;
+  if (c >= p) return;
+  const bool live = rr[c] > 0.0;
+  if (live && !(pq[c] > 0.0)) status[0] = 1;
+  alpha[c] = live ? rr[c] / pq[c] : 0.0;
+}
+__global__ void k_cg_xr(const double* __restrict__ alpha, const double* __restrict__ P, const double* __restrict__ Q,
+                        double* __restrict__ W, double* __restrict__ R, int64_t ld, int d, int p) {
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < static_cast<int64_t>(d) * p;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t i = e / p;
+    const int c = static_cast<int>(e - i * p);
+    const int64_t o = i * ld + c;
+    W[o] += alpha[c] * P[o];
+    R[o] -= alpha[c] * Q[o];
+  }
+}
+// beta = rr_new / rr (0 for a frozen column); P = R + beta P
+__global__ void k_cg_dir(const double* __restrict__ rr, const double* __restrict__ rr_new, const double* __restrict__ R,
+                         double* __restrict__ P, int64_t ld, int d, int p) {
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < static_cast<int64_t>(d) * p;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t i = e / p;
+    const int c = static_cast<int>(e - i * p);
+    const double beta = rr[c] > 0.0 ? rr_new[c] / rr[c] : 0.0;
+    const int64_t o = i * ld + c;
+    P[o] = R[o] + beta * P[o];
+  }
+}
+// v *= 1 / sqrt(*s2) when *s2 > 0
+__global__ void k_scale_inv_sqrt(double* __restrict__ v, int64_t ld, int d, int p, const double* __restrict__ s2) {
+  const double s = *s2;
+  if (!(s > 0.0)) return;
+  const double inv = 1.0 / sqrt(s);
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < static_cast<int64_t>(d) * p;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t i = e / p;
+    v[i * ld + (e - i * p)] *= inv;
+  }
+}
+
 }  // namespace
 
 void launch_qr_mgs2(double* Y, int64_t ldy, int d, int p, double* colmajor_scratch, int* status,
@@ -354,6 +427,42 @@ void launch_frob2(const double* A, int64_t lda, int d, int p, double* part, doub
   k_frob2_part<<<parts, 256, 0, st>>>(A, lda, d, p, rows_per, part);
   GAPLRA_LAUNCH_CHECK();
   k_sum_parts<<<1, 32, 0, st>>>(part, parts, 1, out);
+  GAPLRA_LAUNCH_CHECK();
+}
+
+void launch_col_dots(const double* A, int64_t lda, const double* B, int64_t ldb, int d, int p, double* part,
+                     double* out, cudaStream_t st) {
+  const int parts = small_gram_parts(d);
+  const int rows_per = static_cast<int>(ceil_div(d, parts));
+  k_col_dots_part<<<parts, 256, 0, st>>>(A, lda, B, ldb, d, p, rows_per, part);
+  GAPLRA_LAUNCH_CHECK();
+  k_sum_parts<<<1, 64, 0, st>>>(part, parts, p, out);
+  GAPLRA_LAUNCH_CHECK();
+}
+
+static int ew_grid(int64_t n) { return static_cast<int>(std::min<int64_t>(ceil_div(n, 256), 148 * 8)); }
+
+void launch_cg_dq(const double* P, const double* Zg, double lambda, double* Q, int64_t ld, int d, int p,
+                  cudaStream_t st) {
+  k_cg_dq<<<ew_grid(static_cast<int64_t>(d) * p), 256, 0, st>>>(P, Zg, lambda, Q, ld, d, p);
+  GAPLRA_LAUNCH_CHECK();
+}
+void launch_cg_alpha(const double* rr, const double* pq, int p, double* alpha, int* status, cudaStream_t st) {
+  k_cg_alpha<<<1, 64, 0, st>>>(rr, pq, p, alpha, status);
+  GAPLRA_LAUNCH_CHECK();
+}
+void launch_cg_xr(const double* alpha, const double* P, const double* Q, double* W, double* R, int64_t ld, int d,
+                  int p, cudaStream_t st) {
+  k_cg_xr<<<ew_grid(static_cast<int64_t>(d) * p), 256, 0, st>>>(alpha, P, Q, W, R, ld, d, p);
+  GAPLRA_LAUNCH_CHECK();
+}
+void launch_cg_dir(const double* rr, const double* rr_new, const double* R, double* P, int64_t ld, int d, int p,
+                   cudaStream_t st) {
+  k_cg_dir<<<ew_grid(static_cast<int64_t>(d) * p), 256, 0, st>>>(rr, rr_new, R, P, ld, d, p);
+  GAPLRA_LAUNCH_CHECK();
+}
+void launch_scale_inv_sqrt(double* v, int64_t ld, int d, int p, const double* s2, cudaStream_t st) {
+  k_scale_inv_sqrt<<<ew_grid(static_cast<int64_t>(d) * p), 256, 0, st>>>(v, ld, d, p, s2);
   GAPLRA_LAUNCH_CHECK();
 }
 

@@ -24,4 +24,20 @@ void launch_small_mul(const double* A, int64_t lda, int pa, const double* U, int
 // out[0] = |A|_F^2 over d rows x p columns (deterministic); part: small_gram_parts(d) doubles.
 void launch_frob2(const double* A, int64_t lda, int d, int p, double* part, double* out, cudaStream_t st);
 
+// out[c] = sum_r A[r][c] B[r][c] (p <= 64; deterministic); part: small_gram_parts(d) * p doubles.
+void launch_col_dots(const double* A, int64_t lda, const double* B, int64_t ldb, int d, int p, double* part,
+                     double* out, cudaStream_t st);
+// Block CG pieces on row-major d x p blocks with leading dimension ld:
+//   Q = lambda P - Zg;  alpha = rr / pq (status[0] = 1 on pq <= 0 with rr > 0);
+//   W += alpha P, R -= alpha Q;  P = R + (rr_new / rr) P.
+void launch_cg_dq(const double* P, const double* Zg, double lambda, double* Q, int64_t ld, int d, int p,
+                  cudaStream_t st);
+void launch_cg_alpha(const double* rr, const double* pq, int p, double* alpha, int* status, cudaStream_t st);
+void launch_cg_xr(const double* alpha, const double* P, const double* Q, double* W, double* R, int64_t ld, int d,
+                  int p, cudaStream_t st);
+void launch_cg_dir(const double* rr, const double* rr_new, const double* R, double* P, int64_t ld, int d, int p,
+                   cudaStream_t st);
+// v *= 1 / sqrt(*s2) when *s2 > 0 (device scalar)
+void launch_scale_inv_sqrt(double* v, int64_t ld, int d, int p, const double* s2, cudaStream_t st);
+
 }  // namespace gaplra_cuda

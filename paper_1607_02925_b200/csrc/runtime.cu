@@ -672,6 +672,104 @@ struct InverseOp : Op {
   }
 };
 
+// solve_cg, the pinned block form of oracle.cpp cg_solve:
+// one CG recurrence per column, all columns stepped together; W0 = 0 or the
+// warm guess (R0 = B - D W0); stop before an iteration when max_c |r_c|/|b_c|
+// <= tol; IndefiniteShift on p_cᵀ D p_c <= 0 with r_c != 0; frozen columns
+// (r_c = 0) take alpha = beta = 0; cap = max_iter > 0 ? max_iter : d + 10.
+// Per iteration: one X·(XᵀP) pass, six small kernels, one read of the p
+// residual norms (the stopping test).
+struct CgResult {
+  int iterations = 0;
+  std::vector<double> history;
+};
+
+CgResult cg_solve_dev(Context& c, Matrix& X, double lambda, int p, const double* B, double* W, double tol,
+                      int max_iter, bool warm, CgResult* partial = nullptr) {
+  if (p < 1 || p > 64) throw Error(kContractViolation, "solve_cg: need 1 <= p <= 64");
+  if (!(tol > 0.0)) throw Error(kContractViolation, "solve_cg: tol must be > 0");
+  const int d = X.d;
+  const int64_t ld = ldp_of(p), dp = X.d_pad();
+  const size_t blk = static_cast<size_t>(dp) * ld;
+  const int cap = max_iter > 0 ? max_iter : d + 10;
+  DBuf<double> rb, pb, qb, zb, vb;
+  double* R = rb.ensure(blk);
+  double* P = pb.ensure(blk);
+  double* Q = qb.ensure(blk);
+  double* Zg = zb.ensure(blk);
+  double* v = vb.ensure(5 * 64);
+  double *rr = v, *rr_new = v + 64, *pq = v + 128, *alpha = v + 192, *bn2 = v + 256;
+  double* part = c.tmp.ensure(static_cast<size_t>(small_gram_parts(d)) * 64 + 8);
+  int* status = c.status.ensure(2);
+  GAPLRA_CUDA_CHECK(cudaMemsetAsync(status, 0, 2 * sizeof(int), c.st));
+  launch_col_dots(B, ld, B, ld, d, p, part, bn2, c.st);
+  std::vector<double> bnorm(p);
+  GAPLRA_CUDA_CHECK(cudaMemcpyAsync(c.pin, bn2, p * sizeof(double), cudaMemcpyDeviceToHost, c.st));
+  c.sync();
+  for (int k = 0; k < p; ++k) bnorm[k] = std::sqrt(c.pin[k]);
+  if (warm) {  // R = B - D W0: Q = lambda W0 - X Xᵀ W0, then R = 1 * B - Q
+    gram_block_dev(c, X, p, W, ld, Zg, ld, nullptr, 0);
+    launch_cg_dq(W, Zg, lambda, Q, ld, d, p, c.st);
+    launch_cg_dq(B, Q, 1.0, R, ld, d, p, c.st);
+  } else {
+    GAPLRA_CUDA_CHECK(cudaMemsetAsync(W, 0, blk * sizeof(double), c.st));
+    GAPLRA_CUDA_CHECK(cudaMemcpyAsync(R, B, blk * sizeof(double), cudaMemcpyDeviceToDevice, c.st));
+  }
+  GAPLRA_CUDA_CHECK(cudaMemcpyAsync(P, R, blk * sizeof(double), cudaMemcpyDeviceToDevice, c.st));
+  launch_col_dots(R, ld, R, ld, d, p, part, rr, c.st);
+  CgResult out;
+  auto residual = [&](const double* rrd) {
+    GAPLRA_CUDA_CHECK(cudaMemcpyAsync(c.pin, rrd, p * sizeof(double), cudaMemcpyDeviceToHost, c.st));
+    GAPLRA_CUDA_CHECK(cudaMemcpyAsync(c.pin_i, status, sizeof(int), cudaMemcpyDeviceToHost, c.st));
+    c.sync();
+    double worst = 0.0;
+    for (int k = 0; k < p; ++k) {
+      const double rk = std::sqrt(c.pin[k]) / (bnorm[k] > 0.0 ? bnorm[k] : 1.0);
+      worst = std::isfinite(rk) ? std::max(worst, rk) : rk;
+    }
+    return worst;
+  };
+  try {
+    for (int it = 0;; ++it) {
+      const double r = residual(rr);
+      if (c.pin_i[0]) throw Error(kIndefiniteShift, "solve_cg: nonpositive curvature pᵀ(lambda I - X Xᵀ)p <= 0");
+      out.history.push_back(r);
+      if (!std::isfinite(r)) throw Error(kSolverStalled, "solve_cg: non-finite residual");
+      if (r <= tol) break;
+      if (it >= cap) throw Error(kSolverStalled, "solve_cg: iteration cap reached");
+      gram_block_dev(c, X, p, P, ld, Zg, ld, nullptr, 0);
+      launch_cg_dq(P, Zg, lambda, Q, ld, d, p, c.st);
+      launch_col_dots(P, ld, Q, ld, d, p, part, pq, c.st);
+      launch_cg_alpha(rr, pq, p, alpha, status, c.st);
+      launch_cg_xr(alpha, P, Q, W, R, ld, d, p, c.st);
+      launch_col_dots(R, ld, R, ld, d, p, part, rr_new, c.st);
+      launch_cg_dir(rr, rr_new, R, P, ld, d, p, c.st);
+      GAPLRA_CUDA_CHECK(cudaMemcpyAsync(rr, rr_new, p * sizeof(double), cudaMemcpyDeviceToDevice, c.st));
+      out.iterations++;
+    }
+  } catch (...) {
+    if (partial) *partial = out;
+    throw;
+  }
+  c.led.linear_solves++;
+  return out;
+}
+
+// inverse_operator(cg, lambda)
+struct CgOp : Op {
+  Context& c;
+  Matrix& X;
+  double lambda, tol;
+  CgOp(Context& cc, Matrix& xx, double lam, double t) : c(cc), X(xx), lambda(lam), tol(t) {}
+  void apply(const double* in, double* out, int p, const double* guess = nullptr) override {
+    if (guess)
+      GAPLRA_CUDA_CHECK(cudaMemcpyAsync(out, guess, static_cast<size_t>(X.d_pad()) * ldp_of(p) * sizeof(double),
+                                        cudaMemcpyDeviceToDevice, c.st));
+    cg_solve_dev(c, X, lambda, p, in, out, tol, 0, guess != nullptr);
+    c.led.operator_applies += p;
+  }
+};
+
 // S0 = QR(gaussian_init(d, p, seed)), redraw once with seed + 1.
 void orth_init(Context& c, int d, int64_t dp, int p, uint64_t seed, double* S) {
   const int64_t ld = ldp_of(p);
@@ -811,7 +909,9 @@ void tune_shift_dev(Context& c, Matrix& X, double delta, const gaplra_si_config&
     if (t > 0) hint = 2.0 * lambda - prev_lambda;
     prm.lambda1_hint = hint;
     InverseOp dinv(c, X, lambda, prm, counter);
-    const double est = estimate_top_dev(c, dinv, d, dp, 1.0 / 9.0, derive_seed(cfg.seed, kTagEstD + t), cfg.rq_tol,
+    CgOp dcg(c, X, lambda, cfg.tol_tune);
+    Op& op = cfg.backend == 1 ? static_cast<Op&>(dcg) : static_cast<Op&>(dinv);
+    const double est = estimate_top_dev(c, op, d, dp, 1.0 / 9.0, derive_seed(cfg.seed, kTagEstD + t), cfg.rq_tol,
                                         nullptr);
     const double inv = 1.0 / std::max(est, 1e-300);
     if (rep.tune_steps < 64) {
@@ -849,6 +949,90 @@ void restricted_projection_dev(Context& c, Matrix& X, const double* S, int p, in
   launch_small_mul(S, ld, p, vecs, p, k, d, 0.0, 1.0, W, ldp_of(k), c.st);
   GAPLRA_CUDA_CHECK(cudaMemcpyAsync(ritz_host, vals, k * sizeof(double), cudaMemcpyDeviceToHost, c.st));
   c.sync();
+}
+
+// error_report, the pinned form of oracle.cpp
+// orc_error_report: frobenius = sqrt(max(0, |X|_F^2 - |XᵀW|_F^2)) (one Xᵀ W
+// pass); spectral = power method on P X Xᵀ P (P = I - W Wᵀ) from
+// P g / |P g|, g = gaussian_init(d, 1, derive_seed(seed, "errs")), `iters`
+// gram passes at p = 1.
+constexpr uint64_t kTagErr = 0x65727273ull;  // "errs"
+
+void error_report_dev(Context& c, Matrix& X, int k, const double* W, int iters, uint64_t seed, double* frob,
+                      double* spec) {
+  const int d = X.d;
+  const int64_t dp = X.d_pad(), ldk = ldp_of(k);
+  col_norms(c, X);
+  double fy = 0.0;
+  double* out = c.scal.ensure(8) + 5;
+  if (k > 0) {
+    const int64_t ldy = ldk;
+    double* Y = c.ybuf.ensure(static_cast<size_t>(X.n) * ldy);
+    if (X.kind == 0) {
+      const DenseX D = X.dense();
+      GramWork w;
+      w.part_elems = gram_work_elems(D, k);
+      w.part = w.part_elems ? c.gw.ensure(w.part_elems) : nullptr;
+      launch_xtw(D, W, ldk, k, Y, ldy, w, c.st);
+    } else {
+      launch_xtw_sparse(X.sparse(), W, ldk, k, Y, ldy, c.st);
+    }
+    double* part = c.tmp.ensure(static_cast<size_t>(small_gram_parts(X.n)) + 8);
+    launch_frob2(Y, ldy, X.n, k, part, out, c.st);
+    fy = c.read_scalar(out);
+  }
+  *frob = std::sqrt(std::max(X.fro2 - fy, 0.0));
+  DBuf<double> vb, zb;
+  double* v = vb.ensure(static_cast<size_t>(dp));
+  double* z = zb.ensure(static_cast<size_t>(dp));
+  double* G = c.small.ensure(static_cast<size_t>(64) * 64 * 4 + 8);
+  double* part = c.tmp.ensure(static_cast<size_t>(small_gram_parts(d)) * 64 * 64 + 8);
+  std::vector<double> h(static_cast<size_t>(dp), 0.0);
+  gaussian_init_host(d, 1, derive_seed(seed, kTagErr), h.data(), 1);
+  GAPLRA_CUDA_CHECK(cudaMemcpyAsync(v, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice, c.st));
+  auto project = [&](double* u) {  // u -= W (Wᵀ u)
+    if (k == 0) return;
+    launch_small_gram(W, ldk, k, u, 1, 1, d, part, G, c.st);
+    launch_small_mul(W, ldk, k, G, 1, 1, d, 1.0, -1.0, u, 1, c.st);
+  };
+  auto normalize = [&](double* u) {
+    launch_frob2(u, 1, d, 1, part, out, c.st);
+    launch_scale_inv_sqrt(u, 1, d, 1, out, c.st);
+    return c.read_scalar(out);
+  };
+  project(v);
+  double theta = 0.0;
+  if (normalize(v) > 0.0) {
+    for (int it = 0; it < iters; ++it) {
+      gram_block_dev(c, X, 1, v, 1, z, 1, nullptr, 0);
+      project(z);
+      launch_small_gram(v, 1, 1, z, 1, 1, d, part, out + 1, c.st);
+      theta = c.read_scalar(out + 1);
+      std::swap(v, z);
+      if (normalize(v) == 0.0) break;
+    }
+  }
+  *spec = std::sqrt(std::max(theta, 0.0));
+}
+
+// principal_angles, oracle.cpp orc_principal_angles:
+// Q = qr_orthonormalize(S), Gᵀ = Qᵀ U (p x k), H = G Gᵀ, Jacobi, cos = sqrt(clamp).
+void principal_angles_dev(Context& c, int d, int k, const double* U, int p, double* S, double* cos_host) {
+  const int64_t ldu = ldp_of(k), lds = ldp_of(p);
+  if (k < 1 || p < 1 || k > 64 || p > 64 || k > d || p > d)
+    throw Error(kContractViolation, "principal_angles: need 1 <= k, p <= min(d, 64)");
+  qr_dev(c, S, lds, d, p, /*count=*/false);
+  double* G = c.small.ensure(static_cast<size_t>(64) * 64 * 4 + 8);
+  double* H = G + 64 * 64;
+  double* part = c.tmp.ensure(static_cast<size_t>(small_gram_parts(std::max(d, p))) * 64 * 64 + 8);
+  launch_small_gram(S, lds, p, U, ldu, k, d, part, G, c.st);  // Gᵀ: p x k, ld = k
+  launch_small_gram(G, k, k, G, k, k, p, part, H, c.st);      // H = G Gᵀ: k x k
+  DBuf<double> vv;
+  double* vals = vv.ensure(static_cast<size_t>(k) + static_cast<size_t>(k) * k);
+  launch_jacobi(H, k, vals, vals + k, c.st);
+  GAPLRA_CUDA_CHECK(cudaMemcpyAsync(c.pin, vals, k * sizeof(double), cudaMemcpyDeviceToHost, c.st));
+  c.sync();
+  for (int a = 0; a < k; ++a) cos_host[a] = std::sqrt(std::min(std::max(c.pin[a], 0.0), 1.0));
 }
 
 int outer_cap(const gaplra_si_config& cfg, int d) {
@@ -1368,8 +1552,10 @@ int gaplra_shift_invert(gaplra_ctx* ctx, const gaplra_matrix* x, const gaplra_si
       gaplra_svrg_params prm = prm_from(*cfg, cfg->tol_solve);
       prm.lambda1_hint = rep->lambda1_hint;
       InverseOp dinv(c, X, rep->lambda, prm, &solves);
+      CgOp dcg(c, X, rep->lambda, cfg->tol_solve);
+      Op& op = cfg->backend == 1 ? static_cast<Op&>(dcg) : static_cast<Op&>(dinv);
       rep->outer_cap = outer_cap(*cfg, X.d);
-      rep->outer_iterations = subspace_iterate_dev(c, dinv, X.d, dp, p, rep->outer_cap,
+      rep->outer_iterations = subspace_iterate_dev(c, op, X.d, dp, p, rep->outer_cap,
                                                    derive_seed(cfg->seed, kTagSubspace), cfg->conv_tol, S);
     }
     double* W = wb.ensure(static_cast<size_t>(dp) * ldp_of(k));
@@ -1388,6 +1574,71 @@ int gaplra_shift_invert(gaplra_ctx* ctx, const gaplra_matrix* x, const gaplra_si
     L.solver_column_samples = c.led.solver_column_samples - before.solver_column_samples;
     L.epochs = c.led.epochs - before.epochs;
     L.outer_iterations = c.led.outer_iterations - before.outer_iterations;
+  });
+}
+
+int gaplra_cg_solve(gaplra_ctx* ctx, const gaplra_matrix* x, double lambda, int p, const double* b, double* w,
+                    double tol, int max_iter, int* iterations, double* history, int hist_cap, int* hist_len) {
+  if (!ctx || !x) return GAPLRA_CONTRACT_VIOLATION;
+  return guard(ctx, [&] {
+    require(p >= 1 && p <= 64 && b && w && tol > 0.0, "solve_cg: bad arguments");
+    require(all_finite(b, static_cast<size_t>(x->m.d) * p), "solve_cg: non-finite right-hand side");
+    Context& c = ctx->c;
+    Matrix& X = const_cast<gaplra_matrix*>(x)->m;
+    const int64_t ld = ldp_of(p), dp = X.d_pad();
+    DBuf<double> bd, wd;
+    bd.ensure(static_cast<size_t>(dp) * ld);
+    wd.ensure(static_cast<size_t>(dp) * ld);
+    GAPLRA_CUDA_CHECK(cudaMemsetAsync(bd.p, 0, static_cast<size_t>(dp) * ld * sizeof(double), c.st));
+    upload_block(c, b, X.d, p, bd.p, ld);
+    CgResult r;
+    auto report = [&] {
+      if (iterations) *iterations = r.iterations;
+      if (hist_len) *hist_len = static_cast<int>(r.history.size());
+      if (history)
+        for (int i = 0; i < std::min<int>(hist_cap, static_cast<int>(r.history.size())); ++i) history[i] = r.history[i];
+    };
+    try {
+      r = cg_solve_dev(c, X, lambda, p, bd.p, wd.p, tol, max_iter, false, &r);
+    } catch (...) {
+      report();
+      throw;
+    }
+    download_block(c, wd.p, ld, X.d, p, w);
+    c.sync();
+    report();
+  });
+}
+
+int gaplra_error_report(gaplra_ctx* ctx, const gaplra_matrix* x, int k, const double* w, int iters, uint64_t seed,
+                        double* frob, double* spec) {
+  if (!ctx || !x || !frob || !spec) return GAPLRA_CONTRACT_VIOLATION;
+  return guard(ctx, [&] {
+    Context& c = ctx->c;
+    Matrix& X = const_cast<gaplra_matrix*>(x)->m;
+    require(k >= 0 && k <= 64 && k <= X.d && (k == 0 || w) && iters >= 0, "error_report: bad arguments");
+    const int64_t ldk = ldp_of(std::max(k, 1)), dp = X.d_pad();
+    DBuf<double> wd;
+    wd.ensure(static_cast<size_t>(dp) * ldk);
+    GAPLRA_CUDA_CHECK(cudaMemsetAsync(wd.p, 0, static_cast<size_t>(dp) * ldk * sizeof(double), c.st));
+    if (k > 0) upload_block(c, w, X.d, k, wd.p, ldk);
+    error_report_dev(c, X, k, wd.p, iters, seed, frob, spec);
+  });
+}
+
+int gaplra_principal_angles(gaplra_ctx* ctx, int d, int k, const double* u, int p, const double* s, double* cosines) {
+  if (!ctx || !u || !s || !cosines) return GAPLRA_CONTRACT_VIOLATION;
+  return guard(ctx, [&] {
+    Context& c = ctx->c;
+    const int64_t dp = round4(d);
+    DBuf<double> ud, sd;
+    ud.ensure(static_cast<size_t>(dp) * ldp_of(k));
+    sd.ensure(static_cast<size_t>(dp) * ldp_of(p));
+    GAPLRA_CUDA_CHECK(cudaMemsetAsync(ud.p, 0, static_cast<size_t>(dp) * ldp_of(k) * sizeof(double), c.st));
+    GAPLRA_CUDA_CHECK(cudaMemsetAsync(sd.p, 0, static_cast<size_t>(dp) * ldp_of(p) * sizeof(double), c.st));
+    upload_block(c, u, d, k, ud.p, ldp_of(k));
+    upload_block(c, s, d, p, sd.p, ldp_of(p));
+    principal_angles_dev(c, d, k, ud.p, p, sd.p, cosines);
   });
 }
 

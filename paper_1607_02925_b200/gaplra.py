@@ -349,6 +349,48 @@ def solve_svrg(x: DeviceMatrix, lam: float, b: np.ndarray, tol: float, seed: int
     return SolverReport(w, ep.value, ep.value * m, history[-1] if history else float("nan"), history)
 
 
+def solve_cg(x: DeviceMatrix, lam: float, b: np.ndarray, tol: float, max_iter: int = 0) -> SolverReport:
+    """Block CG solve of (λI − XXᵀ)W = B; column_samples = 0
+    and `epochs` counts CG iterations."""
+    b = _f64(b)
+    if b.ndim == 1:
+        b = b[:, None]
+    p = b.shape[1]
+    w = np.zeros_like(b)
+    it, hl = C.c_int(0), C.c_int(0)
+    hist = np.zeros(8192)
+    rc = x.ctx.lib.gaplra_cg_solve(x.ctx.h, x.h, lam, p, _p(b), _p(w), tol, max_iter, C.byref(it), _p(hist), 8192,
+                                   C.byref(hl))
+    history = hist[:hl.value].tolist()
+    x.ctx.check(rc, history)
+    return SolverReport(w, it.value, 0, history[-1] if history else float("nan"), history)
+
+
+def error_report(x: DeviceMatrix, w: np.ndarray, iters: int = 20, seed: int = 0):
+    """error_report (SPEC.md:528-536): (‖X − WWᵀX‖_F, power-method ‖X − WWᵀX‖₂)."""
+    w = _f64(w)
+    if w.ndim == 1:
+        w = w[:, None]
+    if w.shape[0] != x.d:
+        raise ContractViolation("error_report: W must be d x k")
+    fr, sp = C.c_double(), C.c_double()
+    x.ctx.check(x.ctx.lib.gaplra_error_report(x.ctx.h, x.h, w.shape[1], _p(w), iters, seed, C.byref(fr),
+                                              C.byref(sp)))
+    return fr.value, sp.value
+
+
+def principal_angles(u: np.ndarray, s: np.ndarray, ctx: Context | None = None) -> np.ndarray:
+    """principal_angles: cosines, descending, between span(U)
+    (d x k orthonormal) and span(S) (d x p, full column rank)."""
+    ctx = ctx or default_context()
+    u, s = _f64(u), _f64(s)
+    if u.shape[0] != s.shape[0]:
+        raise ContractViolation("principal_angles: U and S need the same number of rows")
+    cos = np.zeros(u.shape[1])
+    ctx.check(ctx.lib.gaplra_principal_angles(ctx.h, u.shape[0], u.shape[1], _p(u), s.shape[1], _p(s), _p(cos)))
+    return cos
+
+
 def estimate_top(x: DeviceMatrix, eps_prime: float, seed: int, *, inverse: bool = False, lam: float = 0.0,
                  rq_tol: float = 1e-3, tol: float = 1e-6, svrg_seed: int = 0, solve_counter: int = 0,
                  lambda1_hint: float = 0.0):
@@ -380,11 +422,14 @@ class SIConfig:
     epoch_cap: int = 0
     monotone_slack: float = 10.0
     lambda1_hint: float = 0.0
+    backend: str = "svrg"  # inverse_operator backend: "svrg" | "cg"
 
     def native(self) -> N.SiConfig:
+        if self.backend not in ("svrg", "cg"):
+            raise ContractViolation(f"unknown solver backend {self.backend!r} (svrg | cg)")
         return N.SiConfig(self.k, self.p, self.eps, self.mu, self.delta, self.lam, self.seed, self.tol_solve,
                           self.tol_tune, self.conv_tol, self.rq_tol, self.max_outer, int(self.force),
-                          self.epoch_cap, self.monotone_slack, self.lambda1_hint)
+                          self.epoch_cap, self.monotone_slack, self.lambda1_hint, int(self.backend == "cg"))
 
 
 @dataclass

@@ -46,7 +46,8 @@ class OrcSiConfig(C.Structure):
                 ("delta", C.c_double), ("lambda_", C.c_double), ("seed", C.c_uint64),
                 ("tol_solve", C.c_double), ("tol_tune", C.c_double), ("conv_tol", C.c_double),
                 ("rq_tol", C.c_double), ("max_outer", C.c_int), ("force", C.c_int),
-                ("epoch_cap", C.c_int), ("monotone_slack", C.c_double), ("lambda1_hint", C.c_double)]
+                ("epoch_cap", C.c_int), ("monotone_slack", C.c_double), ("lambda1_hint", C.c_double),
+                ("backend", C.c_int)]
 
 
 class OrcSiReport(C.Structure):
@@ -201,6 +202,28 @@ class Oracle:
                                      C.byref(rep), self.nthreads)
         return rc, rep
 
+    def cg_solve(self, m, lam, b, tol, max_iter=0):
+        b = c64(b)
+        w = np.zeros_like(b)
+        it, hl = C.c_int(0), C.c_int(0)
+        hist = np.zeros(8192)
+        rc = self.lib.orc_cg_solve(C.byref(m), C.c_double(lam), b.shape[1], _ptr(b), _ptr(w), C.c_double(tol),
+                                   max_iter, C.byref(it), _ptr(hist), 8192, C.byref(hl), self.nthreads)
+        return rc, w, it.value, hist[:hl.value]
+
+    def error_report(self, m, w, iters=20, seed=0):
+        w = c64(w)
+        fr, sp = C.c_double(), C.c_double()
+        rc = self.lib.orc_error_report(C.byref(m), w.shape[1], _ptr(w), iters, C.c_uint64(seed), C.byref(fr),
+                                       C.byref(sp))
+        return rc, fr.value, sp.value
+
+    def principal_angles(self, u, s):
+        u, s = c64(u), c64(s)
+        cos = np.zeros(u.shape[1])
+        rc = self.lib.orc_principal_angles(u.shape[0], u.shape[1], _ptr(u), s.shape[1], _ptr(s), _ptr(cos))
+        return rc, cos
+
     def sin_theta(self, u, q):
         u, q = c64(u), c64(q)
         return float(self.lib.orc_sin_theta(u.shape[0], u.shape[1], _ptr(u), q.shape[1], _ptr(q)))
@@ -279,6 +302,6 @@ class Reference:
 
 def default_si_config(k, p, *, eps=1e-8, mu=1.0, delta=0.0, lam=0.0, seed=0, tol_solve=1e-10,
                       tol_tune=1e-6, conv_tol=1e-9, rq_tol=1e-3, max_outer=0, force=0,
-                      epoch_cap=0, slack=10.0, hint=0.0):
+                      epoch_cap=0, slack=10.0, hint=0.0, backend=0):
     return OrcSiConfig(k, p, eps, mu, delta, lam, seed, tol_solve, tol_tune, conv_tol, rq_tol,
-                       max_outer, force, epoch_cap, slack, hint)
+                       max_outer, force, epoch_cap, slack, hint, backend)

@@ -7,6 +7,7 @@ FMA)."""
 import numpy as np
 import pytest
 
+from oracle_lib import default_si_config
 from problems import csc_to_dense, planted_dense, random_csc
 
 pytestmark = pytest.mark.gpu
@@ -308,3 +309,74 @@ def test_shift_invert_sparse(g, oracle):
     assert oracle.sin_theta(wo, res.W) <= 1e-8
     assert np.allclose(res.ritz, ro, rtol=1e-10)
     assert np.allclose(res.ritz, ev[:k], rtol=1e-9)
+
+
+# ---- solve_cg / error_report / principal_angles ----
+@pytest.mark.parametrize("p", [1, 5, 20])
+def test_cg_solve_matches_oracle_and_direct(g, oracle, p):
+    X, _, sig = planted_dense(300, 900, seed=p)
+    lam = sig[0] ** 2 * 1.02
+    b = np.random.default_rng(p).standard_normal((300, p))
+    r = g.solve_cg(g.DeviceMatrix.dense(X), lam, b, 1e-11)
+    rc, wo, it, _ = oracle.cg_solve(oracle.dense(X), lam, b, 1e-11)
+    assert rc == 0
+    assert abs(r.epochs - it) <= 1
+    assert rel(r.solution, wo) <= 1e-9
+    assert rel(r.solution, np.linalg.solve(lam * np.eye(300) - X @ X.T, b)) <= 1e-9
+
+
+def test_cg_solve_sparse_identity_and_indefinite(g):
+    # D = I -> one iteration; lambda < lambda_1 -> IndefiniteShift
+    b = np.random.default_rng(0).standard_normal((9, 2))
+    r = g.solve_cg(g.DeviceMatrix.dense(np.zeros((9, 4))), 1.0, b, 1e-12)
+    assert r.epochs == 1 and np.allclose(r.solution, b, atol=1e-15)
+    X, U, sig = planted_dense(40, 80, seed=4)
+    with pytest.raises(g.IndefiniteShift):
+        g.solve_cg(g.DeviceMatrix.dense(X), 0.5 * sig[0] ** 2, U[:, :1] + 0.01, 1e-10)
+
+
+def test_error_report_matches_oracle(g, oracle):
+    X, U, sig = planted_dense(256, 700, seed=9, noise=1e-2)
+    W, _ = np.linalg.qr(U[:, :4] + 1e-3 * np.random.default_rng(1).standard_normal((256, 4)))
+    fd, sd = g.error_report(g.DeviceMatrix.dense(X), W, iters=30, seed=3)
+    rc, fo, so = oracle.error_report(oracle.dense(X), W, iters=30, seed=3)
+    assert rc == 0
+    assert abs(fd - fo) <= 1e-12 * np.linalg.norm(X)
+    assert abs(sd - so) <= 1e-10 * so
+    assert abs(fd - np.linalg.norm(X - W @ (W.T @ X))) <= 1e-12 * np.linalg.norm(X)
+    cp, ri, v = random_csc(200, 500, 7, seed=2)
+    Xs = csc_to_dense(200, 500, cp, ri, v)
+    Ws, _ = np.linalg.qr(np.random.default_rng(2).standard_normal((200, 3)))
+    fd, sd = g.error_report(g.DeviceMatrix.csc(200, 500, cp, ri, v), Ws, iters=25, seed=5)
+    rc, fo, so = oracle.error_report(oracle.csc(200, 500, cp, ri, v), Ws, iters=25, seed=5)
+    assert abs(fd - fo) <= 1e-12 * np.linalg.norm(Xs) and abs(sd - so) <= 1e-10 * so
+
+
+def test_principal_angles_matches_oracle(g, oracle):
+    rng = np.random.default_rng(11)
+    U, _ = np.linalg.qr(rng.standard_normal((500, 6)))
+    S = U @ rng.standard_normal((6, 10)) + 1e-3 * rng.standard_normal((500, 10))
+    cd = g.principal_angles(U, S)
+    rc, co = oracle.principal_angles(U, S)
+    assert rc == 0 and np.allclose(cd, co, atol=1e-13)
+    Q, _ = np.linalg.qr(S)
+    assert np.allclose(cd, np.linalg.svd(U.T @ Q, compute_uv=False), atol=1e-13)
+
+
+def test_shift_invert_cg_backend(g, oracle):
+    # inverse_operator(cg) in the pipeline: device vs oracle, and against the
+    # svrg backend (Frobenius error within 1e-6 relative)
+    X, U, sig = planted_dense(200, 1000, k=4, p=8, seed=12, noise=1e-3)
+    lam = sig[0] ** 2 + 0.05
+    x = g.DeviceMatrix.dense(X)
+    kw = dict(k=4, p=8, lam=lam, seed=2, max_outer=80, lambda1_hint=sig[0] ** 2)
+    rc_ = g.shift_invert(x, g.SIConfig(backend="cg", **kw))
+    rs_ = g.shift_invert(x, g.SIConfig(**kw))
+    rc, wo, ro, _, rep = oracle.shift_invert(
+        oracle.dense(X), default_si_config(4, 8, lam=lam, seed=2, max_outer=80, hint=sig[0] ** 2, backend=1))
+    assert rc == 0
+    assert oracle.sin_theta(rc_.W, wo) <= 1e-8
+    assert np.allclose(rc_.ritz, ro, rtol=1e-10)
+    fc = g.error_report(x, rc_.W)[0]
+    fs = g.error_report(x, rs_.W)[0]
+    assert abs(fc - fs) <= 1e-6 * fs
