@@ -527,6 +527,26 @@ struct InverseOp : BlockOp {
   }
 };
 
+// project_out (linear_operator.cpp:66-81): one-pass CGS, all coefficients
+// first, then subtracted in basis order; per column of a block.
+void project_out_block(const Block& basis, Block& v) {
+  const int m = basis.p, d = basis.d;
+  if (m == 0) return;
+  std::vector<double> coeffs(m);
+  for (int c = 0; c < v.p; ++c) {
+    for (int j = 0; j < m; ++j) {
+      double acc = 0.0;
+      for (int i = 0; i < d; ++i) acc += basis.at(i, j) * v.at(i, c);
+      coeffs[j] = acc;
+    }
+    for (int j = 0; j < m; ++j) {
+      const double cj = coeffs[j];
+      if (cj == 0.0) continue;
+      for (int i = 0; i < d; ++i) v.at(i, c) -= cj * basis.at(i, j);
+    }
+  }
+}
+
 // solve_cg: block CG on (lambda I - X X^T) W = B, one
 // independent recurrence per column, all columns stepped together.  Pinned:
 // W0 = 0 (or the warm guess, R0 = B - D W0), stop before an iteration when
@@ -539,8 +559,11 @@ struct CgResult {
   std::vector<double> history;
 };
 
+// With a deflation basis U the system is lambda I - P X Xᵀ P (P = I - U Uᵀ;
+// SPEC.md:114, Alg. 7's X_{-(s-1)}): for iterates in range(P) that is
+// p -> lambda p - P (X Xᵀ p), i.e. one project_out after each gram pass.
 CgResult cg_solve(const Mat& x, double lambda, const Block& b, Block& w, double tol, int max_iter,
-                  orc_ledger* led, int nthreads, const Block* guess = nullptr) {
+                  orc_ledger* led, int nthreads, const Block* guess = nullptr, const Block* basis = nullptr) {
   const int d = x.d(), p = b.p;
   const int cap = max_iter > 0 ? max_iter : d + 10;
   auto coldot = [&](const Block& u, const Block& v, int c) {
@@ -554,6 +577,7 @@ CgResult cg_solve(const Mat& x, double lambda, const Block& b, Block& w, double 
   if (guess) {
     w = *guess;
     gram_block(x, w, z, nullptr, nthreads);
+    if (basis) project_out_block(*basis, z);
     if (led) led->gram_applies += p;
     for (int c = 0; c < p; ++c)
       for (int i = 0; i < d; ++i) r.at(i, c) = b.at(i, c) - (lambda * w.at(i, c) - z.at(i, c));
@@ -571,6 +595,7 @@ CgResult cg_solve(const Mat& x, double lambda, const Block& b, Block& w, double 
     if (worst <= tol) break;
     if (it >= cap) throw Status(ORC_SOLVER_STALLED);
     gram_block(x, pd, z, nullptr, nthreads);
+    if (basis) project_out_block(*basis, z);
     if (led) led->gram_applies += p;
     for (int c = 0; c < p; ++c)
       for (int i = 0; i < d; ++i) q.at(i, c) = lambda * pd.at(i, c) - z.at(i, c);
@@ -604,10 +629,11 @@ struct CgOp : BlockOp {
   int max_iter;
   orc_ledger* led;
   int nthreads;
-  CgOp(const Mat& xx, double lam, double t, int mi, orc_ledger* l, int nt)
-      : x(xx), lambda(lam), tol(t), max_iter(mi), led(l), nthreads(nt) {}
+  const Block* basis;  // deflated system (nullptr: none)
+  CgOp(const Mat& xx, double lam, double t, int mi, orc_ledger* l, int nt, const Block* u = nullptr)
+      : x(xx), lambda(lam), tol(t), max_iter(mi), led(l), nthreads(nt), basis(u && u->p > 0 ? u : nullptr) {}
   void apply(const Block& in, Block& out, const Block* guess = nullptr) override {
-    cg_solve(x, lambda, in, out, tol, max_iter, led, nthreads, guess);
+    cg_solve(x, lambda, in, out, tol, max_iter, led, nthreads, guess, basis);
     if (led) led->operator_applies += in.p;
   }
 };
@@ -733,6 +759,77 @@ double estimate_top(BlockOp& op, int d, double eps_prime, uint64_t seed, double 
   return theta;
 }
 
+// DeflatedOperator::apply (linear_operator.cpp:56-64) on a block: P C P with
+// P = I - basis basisᵀ; for an inverse operator this is inverse_operator's
+// "apply(v) = P solve(lambda, P v)".
+struct DeflatedOp : BlockOp {
+  BlockOp& base;
+  const Block& basis;
+  DeflatedOp(BlockOp& b, const Block& u) : base(b), basis(u) {}
+  void apply(const Block& in, Block& out, const Block* guess = nullptr) override {
+    Block work = in;
+    project_out_block(basis, work);
+    base.apply(work, out, guess);
+    project_out_block(basis, out);
+  }
+};
+
+// Alg. 3 for any k: subspace iteration on k columns, the
+// estimates are the Ritz values (eigenvalues of Sᵀ C S = z_iᵀ C z_i for the
+// Ritz vectors z_i, descending), early stop when every one changes by
+// <= rq_tol relative.  For k = 1 this is estimate_top.
+std::vector<double> estimate_eigs(BlockOp& op, int d, int k, double eps_prime, uint64_t seed, double rq_tol,
+                                  int* iters, orc_ledger* led) {
+  const int L = static_cast<int>(std::ceil(4.0 / eps_prime * std::log(d / eps_prime)));
+  Block s = orth_init(d, k, seed);
+  Block y, guess;
+  bool have_guess = false;
+  std::vector<double> prev(k, 0.0), theta(k, 0.0), vecs(static_cast<size_t>(k) * k);
+  int it = 0;
+  for (int l = 1; l <= L + 1; ++l) {
+    op.apply(s, y, have_guess ? &guess : nullptr);
+    it = l;
+    std::vector<double> h = gram_ab(s, y);
+    for (int a = 0; a < k; ++a)
+      for (int b = a + 1; b < k; ++b) {
+        const double m = 0.5 * (h[static_cast<size_t>(a) * k + b] + h[static_cast<size_t>(b) * k + a]);
+        h[static_cast<size_t>(a) * k + b] = h[static_cast<size_t>(b) * k + a] = m;
+      }
+    jacobi(k, h.data(), theta.data(), vecs.data());
+    bool stop = l > 1;
+    for (int a = 0; a < k && stop; ++a) stop = std::fabs(theta[a] - prev[a]) <= rq_tol * std::fabs(theta[a]);
+    if (stop || l == L + 1) break;
+    Block q = y;
+    qr_inplace(q);
+    if (led) led->qr_factorizations++;
+    guess = warm_guess(q, y, gram_ab(s, q));
+    have_guess = true;
+    s = q;
+    prev = theta;
+  }
+  if (iters) *iters = it;
+  return theta;
+}
+
+// Alg. 4: smallest global q in {s..s+count-2} with
+// est[q+1] <= est[q] (1 - p^-2); -1 when none (est[i] = lambda_hat_{s+i}).
+int detect_multiplicative_gap(const double* est, int count, int s, int p) {
+  const double f = 1.0 - 1.0 / (static_cast<double>(p) * p);
+  for (int i = 0; i + 1 < count; ++i)
+    if (est[i + 1] <= est[i] * f) return s + i;
+  return -1;
+}
+
+// Alg. 5: requires inv[0] = lambda~_s^-1 in [delta/27,
+// delta/5] (Eq. 5) else ShiftOutOfRange; q = min{i : inv_{i+1} - inv_i >=
+// 5 delta / 9} over the consecutive estimates, else k.
+int detect_additive_gap(const double* inv, int count, int s, int k, double delta) {
+  if (count < 1 || !(inv[0] >= delta / 27.0 && inv[0] <= delta / 5.0)) throw Status(ORC_SHIFT_OUT_OF_RANGE);
+  for (int i = 0; i + 1 < count; ++i)
+    if (inv[i + 1] - inv[i] >= 5.0 * delta / 9.0) return s + i;
+  return k;
+}
+
 orc_svrg_params make_prm(const orc_si_config* cfg, double tol) {
   orc_svrg_params prm;
   prm.eta = 0.0;
@@ -748,9 +845,12 @@ orc_svrg_params make_prm(const orc_si_config* cfg, double tol) {
 // tune_shift — Alg. 6 with the window
 // [Delta/27, Delta/5] and estimate -> test -> update order.
 void tune_shift(const Mat& x, double delta, const orc_si_config* cfg, int64_t* solve_counter,
-                orc_si_report* rep, int nthreads) {
+                orc_si_report* rep, int nthreads, const Block* basis = nullptr) {
   const int d = x.d();
-  GramOp a(x, &rep->ledger, nthreads);
+  const Block none(d, 0);
+  const Block& u = basis ? *basis : none;
+  GramOp a0(x, &rep->ledger, nthreads);
+  DeflatedOp a(a0, u);  // A_{-(s-1)} (Alg. 6 on the deflated matrix)
   const double l1 = estimate_top(a, d, 0.25, derive_seed(cfg->seed, kTagEstA), cfg->rq_tol,
                                  nullptr, &rep->ledger);
   rep->lambda1_hat = l1;
@@ -768,8 +868,11 @@ void tune_shift(const Mat& x, double delta, const orc_si_config* cfg, int64_t* s
     if (t > 0) hint = 2.0 * lambda - prev_lambda;
     prm.lambda1_hint = hint;
     InverseOp dinv(x, lambda, prm, solve_counter, &rep->ledger, nthreads);
-    CgOp dcg(x, lambda, cfg->tol_tune, 0, &rep->ledger, nthreads);
-    BlockOp& op = cfg->backend == 1 ? static_cast<BlockOp&>(dcg) : static_cast<BlockOp&>(dinv);
+    CgOp dcg(x, lambda, cfg->tol_tune, 0, &rep->ledger, nthreads, &u);
+    // a deflated shifted system is solved by CG (the SVRG epoch samples the
+    // undeflated columns of X)
+    const bool cg = cfg->backend == 1 || u.p > 0;
+    DeflatedOp op(cg ? static_cast<BlockOp&>(dcg) : static_cast<BlockOp&>(dinv), u);
     const double est = estimate_top(op, d, 1.0 / 9.0, derive_seed(cfg->seed, kTagEstD + t),
                                     cfg->rq_tol, nullptr, &rep->ledger);
     const double inv = 1.0 / std::max(est, 1e-300);
@@ -816,6 +919,124 @@ void restricted_projection(const Mat& x, const Block& s, int k, Block& w, std::v
       for (int j = 0; j < k; ++j) w.at(i, j) += a * vecs[static_cast<size_t>(kk) * p + j];
     }
   ritz.assign(vals.begin(), vals.begin() + k);
+}
+
+// deflation_basis_extend: project the new block against the
+// current basis (project_out), QR it, append; RankDeficient -> DegenerateProgress
+// (reported as ORC_RANK_DEFICIENT).
+Block basis_extend(const Block& cur, const Block& nb) {
+  Block q = nb;
+  project_out_block(cur, q);
+  qr_inplace(q);
+  Block out(cur.d, cur.p + q.p);
+  std::copy(cur.a.begin(), cur.a.end(), out.a.begin());
+  std::copy(q.a.begin(), q.a.end(), out.a.begin() + cur.a.size());
+  return out;
+}
+
+// approximate — Alg. 7 with every SPEC
+// design decision: eps_int = eps / (3 mu k d); per interval {s..k} on the
+// deflated A_{-(s-1)}: Alg. 3 at eps' = 1/(9p^2) -> Alg. 4; a multiplicative
+// gap q gives PlainPower on {s..q} (width q-s+1, L = ceil(4 p^4 ln(kd/eps_int)));
+// otherwise Alg. 6 tune_shift, Alg. 3 on D_{-(s-1)} at eps' = 1/(9p) -> Alg. 5
+// -> ShiftedInverse on {s..q} with width q-s+1 (q < k) or p-s+1 (q = k) and
+// L = ceil(4 k ln(kd/eps_int)).  NoPreconditioningNeeded from tune_shift
+// (lambda_hat_s < 3 delta) routes the interval to PlainPower with width
+// p-s+1 and q = k (plain power converges there without a shift).  Every
+// subspace iteration stops early at conv_tol and is capped at max_outer when
+// > 0.  Seeds: interval j uses derive_seed(seed, "intv" + j) as its root.
+// Final: restricted_projection(A, basis (d x p), k).
+constexpr uint64_t kTagInterval = 0x696e7476ull;  // "intv"
+
+void approximate(const Mat& x, const orc_si_config* cfg, Block& w, std::vector<double>& ritz, orc_ap_report* rep,
+                 int nthreads) {
+  const int d = x.d(), k = cfg->k, p = cfg->p;
+  const double eps_int = cfg->eps / (3.0 * std::max(cfg->mu, 1.0) * k * d);
+  const double lg = std::log(k * static_cast<double>(d) / eps_int);
+  auto capped = [&](double L) {
+    const int l = static_cast<int>(std::min(std::ceil(L), 1e9));
+    return cfg->max_outer > 0 ? std::min(l, cfg->max_outer) : l;
+  };
+  Block basis(d, 0);
+  int64_t solves = 0;
+  int s = 1;
+  for (int j = 0; s <= k; ++j) {
+    if (j >= k) throw Status(ORC_RANK_DEFICIENT);  // DegenerateProgress
+    orc_si_config cj = *cfg;
+    cj.seed = derive_seed(cfg->seed, kTagInterval + static_cast<uint64_t>(j));
+    GramOp a0(x, &rep->ledger, nthreads);
+    DeflatedOp a(a0, basis);
+    const int cnt = k - s + 1;
+    const std::vector<double> est = estimate_eigs(a, d, cnt, 1.0 / (9.0 * p * p), derive_seed(cj.seed, kTagEstA),
+                                                  cfg->rq_tol, nullptr, &rep->ledger);
+    int q = detect_multiplicative_gap(est.data(), cnt, s, p);
+    int strategy = 0, width = 0, iters = 0;
+    double shift = 0.0;
+    Block S;
+    auto plain = [&](int wdt) {
+      strategy = 0;
+      width = wdt;
+      S = subspace_iterate(a, d, wdt, capped(4.0 * std::pow(static_cast<double>(p), 4) * lg),
+                           derive_seed(cj.seed, kTagSubspace), cfg->conv_tol, &iters, &rep->ledger);
+    };
+    if (q >= 0) {
+      plain(q - s + 1);
+    } else {
+      orc_si_report tr;
+      std::memset(&tr, 0, sizeof(tr));
+      bool shifted = true;
+      try {
+        tune_shift(x, cfg->delta, &cj, &solves, &tr, nthreads, &basis);
+      } catch (const Status& e) {
+        if (e.code != ORC_NO_PRECONDITIONING_NEEDED) throw;
+        shifted = false;
+      }
+      auto add = [&](const orc_ledger& l) {
+        rep->ledger.gram_applies += l.gram_applies;
+        rep->ledger.operator_applies += l.operator_applies;
+        rep->ledger.qr_factorizations += l.qr_factorizations;
+        rep->ledger.linear_solves += l.linear_solves;
+        rep->ledger.solver_column_samples += l.solver_column_samples;
+        rep->ledger.epochs += l.epochs;
+        rep->ledger.outer_iterations += l.outer_iterations;
+      };
+      add(tr.ledger);
+      if (!shifted) {
+        q = k;
+        plain(p - s + 1);
+      } else {
+        shift = tr.lambda;
+        orc_svrg_params prm = make_prm(&cj, cfg->tol_solve);
+        prm.lambda1_hint = tr.lambda1_hint;
+        InverseOp dinv(x, shift, prm, &solves, &rep->ledger, nthreads);
+        CgOp dcg(x, shift, cfg->tol_solve, 0, &rep->ledger, nthreads, &basis);
+        const bool cg = cfg->backend == 1 || basis.p > 0;
+        DeflatedOp dd(cg ? static_cast<BlockOp&>(dcg) : static_cast<BlockOp&>(dinv), basis);
+        const std::vector<double> dest = estimate_eigs(dd, d, cnt, 1.0 / (9.0 * p), derive_seed(cj.seed, kTagEstD),
+                                                       cfg->rq_tol, nullptr, &rep->ledger);
+        std::vector<double> inv(cnt);
+        for (int i = 0; i < cnt; ++i) inv[i] = 1.0 / std::max(dest[i], 1e-300);
+        q = detect_additive_gap(inv.data(), cnt, s, k, cfg->delta);
+        strategy = 1;
+        width = q < k ? q - s + 1 : p - s + 1;
+        S = subspace_iterate(dd, d, width, capped(4.0 * k * lg), derive_seed(cj.seed, kTagSubspace), cfg->conv_tol,
+                             &iters, &rep->ledger);
+      }
+    }
+    basis = basis_extend(basis, S);
+    if (rep->n_intervals < 64) {
+      const int t = rep->n_intervals;
+      rep->s[t] = s;
+      rep->q[t] = q;
+      rep->strategy[t] = strategy;
+      rep->width[t] = width;
+      rep->iterations[t] = iters;
+      rep->shift[t] = shift;
+    }
+    rep->n_intervals++;
+    s = q + 1;
+  }
+  restricted_projection(x, basis, k, w, ritz, &rep->ledger, nthreads);
 }
 
 int outer_cap(const orc_si_config* cfg, int d) {
@@ -1047,6 +1268,47 @@ double orc_sin_theta(int d, int k, const double* u, int q, const double* qm) {
   std::vector<double> vals(k), vecs(static_cast<size_t>(k) * k);
   jacobi(k, h.data(), vals.data(), vecs.data());
   return std::sqrt(std::max(vals[0], 0.0));
+}
+
+int orc_detect_multiplicative_gap(const double* est, int count, int s, int p) {
+  return detect_multiplicative_gap(est, count, s, p);
+}
+
+int orc_detect_additive_gap(const double* inv, int count, int s, int k, double delta, int* q) {
+  return guarded([&] { *q = detect_additive_gap(inv, count, s, k, delta); });
+}
+
+int orc_estimate_eigenvalues(const orc_mat* x, int inverse, double lambda, int k, double eps_prime, uint64_t seed,
+                             double rq_tol, const orc_svrg_params* prm, double* values, int* iterations,
+                             int nthreads) {
+  if (!valid(x) || k < 1 || k > x->d || !(eps_prime > 0.0 && eps_prime < 1.0)) return ORC_CONTRACT_VIOLATION;
+  return guarded([&] {
+    Mat m(x);
+    int64_t sc = 0;
+    std::vector<double> v;
+    if (inverse) {
+      InverseOp op(m, lambda, *prm, &sc, nullptr, nthreads);
+      v = estimate_eigs(op, x->d, k, eps_prime, seed, rq_tol, iterations, nullptr);
+    } else {
+      GramOp op(m, nullptr, nthreads);
+      v = estimate_eigs(op, x->d, k, eps_prime, seed, rq_tol, iterations, nullptr);
+    }
+    std::copy(v.begin(), v.end(), values);
+  });
+}
+
+int orc_approximate(const orc_mat* x, const orc_si_config* cfg, double* w, double* ritz, orc_ap_report* rep,
+                    int nthreads) {
+  if (!valid(x) || !cfg || cfg->k < 1 || cfg->p <= cfg->k || cfg->p >= x->d || !(cfg->delta > 0.0))
+    return ORC_CONTRACT_VIOLATION;
+  std::memset(rep, 0, sizeof(*rep));
+  return guarded([&] {
+    Block wb;
+    std::vector<double> r;
+    approximate(Mat(x), cfg, wb, r, rep, nthreads);
+    wb.to_rowmajor(w);
+    std::copy(r.begin(), r.end(), ritz);
+  });
 }
 
 int orc_cg_solve(const orc_mat* x, double lambda, int p, const double* b, double* w, double tol, int max_iter,

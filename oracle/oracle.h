@@ -13,7 +13,8 @@
  *     (SPEC.md:327-335,362-365), inverse_operator (:345-353), subspace_iterate
  *     (:234-242), estimate_eigenvalues (:254-262), restricted_projection
  *     (:244-252), tune_shift (:423-431), solve_cg (:317-325),
- *     error_report (:528-536), principal_angles (:181-189).
+ *     error_report (:528-536), principal_angles (:181-189), Alg. 4/5 gap
+ *     detection (:403-421), approximate = Alg. 7 (:505-551).
  *
  * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / reference
  * arm may load this library, and only as the checker or the timed CPU
@@ -102,6 +103,15 @@ typedef struct {
   orc_ledger ledger;
 } orc_si_report;
 
+/* Executed partition plan of approximate (Alg. 7): per interval {s..q}, the
+ * branch (0 PlainPower, 1 ShiftedInverse), block width, iterations, shift. */
+typedef struct {
+  int n_intervals;
+  int s[64], q[64], strategy[64], width[64], iterations[64];
+  double shift[64];
+  orc_ledger ledger;
+} orc_ap_report;
+
 /* ---- primitives (bit-exact restatements) ---- */
 uint64_t orc_derive_seed(uint64_t root, uint64_t tag);
 void orc_next_u64(uint64_t seed, int64_t count, uint64_t* out);
@@ -149,6 +159,13 @@ int orc_shift_invert(const orc_mat* x, const orc_si_config* cfg, double* w_rowma
 
 /* sin of the largest principal angle between range(U) (d x k, orthonormal)
  * and range(Q) (d x q, orthonormal), computed as |(I - QQ^T)U|_2. */
+int orc_detect_multiplicative_gap(const double* est, int count, int s, int p);
+int orc_detect_additive_gap(const double* inv, int count, int s, int k, double delta, int* q);
+int orc_estimate_eigenvalues(const orc_mat* x, int inverse, double lambda, int k, double eps_prime, uint64_t seed,
+                             double rq_tol, const orc_svrg_params* prm, double* values, int* iterations,
+                             int nthreads);
+int orc_approximate(const orc_mat* x, const orc_si_config* cfg, double* w_rowmajor, double* ritz,
+                    orc_ap_report* rep, int nthreads);
 int orc_cg_solve(const orc_mat* x, double lambda, int p, const double* b_rowmajor, double* w_rowmajor,
                  double tol, int max_iter, int* iterations, double* history, int hist_cap, int* hist_len,
                  int nthreads);

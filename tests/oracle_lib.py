@@ -57,6 +57,17 @@ class OrcSiReport(C.Structure):
                 ("outer_iterations", C.c_int), ("outer_cap", C.c_int), ("ledger", OrcLedger)]
 
 
+class OrcApReport(C.Structure):
+    _fields_ = [("n_intervals", C.c_int), ("s", C.c_int * 64), ("q", C.c_int * 64), ("strategy", C.c_int * 64),
+                ("width", C.c_int * 64), ("iterations", C.c_int * 64), ("shift", C.c_double * 64),
+                ("ledger", OrcLedger)]
+
+    def plan(self):
+        n = min(self.n_intervals, 64)
+        return [dict(s=self.s[i], q=self.q[i], strategy=("PlainPower", "ShiftedInverse")[self.strategy[i]],
+                     width=self.width[i], iterations=self.iterations[i], shift=self.shift[i]) for i in range(n)]
+
+
 def build_oracle(ref: bool | None = None) -> None:
     """Compile oracle/liboracle.so (and oracle/_ref when /root/reference exists)."""
     subprocess.run(["make", "-s", "-C", str(ROOT / "oracle"), "liboracle.so"], check=True)
@@ -201,6 +212,34 @@ class Oracle:
         rc = self.lib.orc_tune_shift(C.byref(m), C.c_double(delta), C.byref(cfg), C.byref(sc),
                                      C.byref(rep), self.nthreads)
         return rc, rep
+
+    def detect_multiplicative_gap(self, est, s, p):
+        est = np.ascontiguousarray(est, dtype=np.float64)
+        q = self.lib.orc_detect_multiplicative_gap(_ptr(est), len(est), s, p)
+        return None if q < 0 else q
+
+    def detect_additive_gap(self, inv, s, k, delta):
+        inv = np.ascontiguousarray(inv, dtype=np.float64)
+        q = C.c_int(0)
+        rc = self.lib.orc_detect_additive_gap(_ptr(inv), len(inv), s, k, C.c_double(delta), C.byref(q))
+        return rc, q.value
+
+    def estimate_eigenvalues(self, m, k, eps_prime, seed, *, inverse=False, lam=0.0, rq_tol=1e-3, tol=1e-6,
+                             svrg_seed=0, hint=0.0):
+        prm = OrcSvrgParams(0.0, 0, tol, 0, 10.0, svrg_seed, hint)
+        vals = np.zeros(k)
+        it = C.c_int(0)
+        rc = self.lib.orc_estimate_eigenvalues(C.byref(m), int(inverse), C.c_double(lam), k, C.c_double(eps_prime),
+                                               C.c_uint64(seed), C.c_double(rq_tol), C.byref(prm), _ptr(vals),
+                                               C.byref(it), self.nthreads)
+        return rc, vals, it.value
+
+    def approximate(self, m, cfg):
+        w = np.zeros((m.d, cfg.k))
+        ritz = np.zeros(cfg.k)
+        rep = OrcApReport()
+        rc = self.lib.orc_approximate(C.byref(m), C.byref(cfg), _ptr(w), _ptr(ritz), C.byref(rep), self.nthreads)
+        return rc, w, ritz, rep
 
     def cg_solve(self, m, lam, b, tol, max_iter=0):
         b = c64(b)
