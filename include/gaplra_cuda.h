@@ -27,6 +27,9 @@
  * gaplra_restricted_projection         restricted_projection
  * gaplra_shift_invert                  Alg. 7 ShiftedInverse branch on I = {1..k}
  *                                      (SPEC.md:505-516,546-549 / PAPER.md:341-351)
+ * gaplra_detect_*_gap                  Alg. 4 / Alg. 5
+ * gaplra_estimate_eigenvalues          estimate_eigenvalues, any k
+ * gaplra_approximate                   approximate = Alg. 7
  * gaplra_cg_solve                      solve_cg / inverse_operator(cg)
  * gaplra_error_report                  error_report
  * gaplra_principal_angles              principal_angles
@@ -114,6 +117,17 @@ typedef struct {
   double ms_tune, ms_subspace, ms_rayleigh_ritz, ms_total;
 } gaplra_si_report;
 
+/* Executed partition plan of gaplra_approximate (Alg. 7):
+ * per interval {s..q}: strategy 0 PlainPower / 1 ShiftedInverse, block width,
+ * subspace iterations, shift (0 for PlainPower). */
+typedef struct {
+  int n_intervals;
+  int s[64], q[64], strategy[64], width[64], iterations[64];
+  double shift[64];
+  gaplra_ledger ledger;
+  double ms_total;
+} gaplra_ap_report;
+
 /* Live per-kernel-class device time (CUDA events on the context stream) and
  * the algorithmic bytes / flops of those launches.
  * Classes: 0 gram pass X(XᵀW) (p > 1), 1 SVRG epoch chain (p > 1), 2 H = XᵀC
@@ -195,6 +209,21 @@ GAPLRA_API int gaplra_error_report(gaplra_ctx* ctx, const gaplra_matrix* x, int 
  * U d x k orthonormal, and span(S), S d x p full column rank. */
 GAPLRA_API int gaplra_principal_angles(gaplra_ctx* ctx, int d, int k, const double* u, int p, const double* s,
                                        double* cosines);
+/* Alg. 4 detect_multiplicative_gap: est[i] = lambda_hat_{s+i};
+ * *q = smallest global q with est_{q+1} <= est_q (1 - p^-2), or -1. */
+GAPLRA_API int gaplra_detect_multiplicative_gap(const double* est, int count, int s, int p, int* q);
+/* Alg. 5 detect_additive_gap: inv[i] = lambda~_{s+i}^-1;
+ * GAPLRA_SHIFT_OUT_OF_RANGE unless inv[0] in [delta/27, delta/5]. */
+GAPLRA_API int gaplra_detect_additive_gap(gaplra_ctx* ctx, const double* inv, int count, int s, int k, double delta,
+                                          int* q);
+/* estimate_eigenvalues (Alg. 3) for k <= 64 on A = X Xᵀ or D⁻¹. */
+GAPLRA_API int gaplra_estimate_eigenvalues(gaplra_ctx* ctx, const gaplra_matrix* x, int inverse, double lambda, int k,
+                                           double eps_prime, uint64_t seed, double rq_tol,
+                                           const gaplra_svrg_params* prm, double* values, int* iterations);
+/* approximate (Alg. 7) with the caller's gap budget cfg->delta:
+ * W (d x k row-major), top-k Ritz values, the executed partition plan. */
+GAPLRA_API int gaplra_approximate(gaplra_ctx* ctx, const gaplra_matrix* x, const gaplra_si_config* cfg, double* w,
+                                  double* ritz, gaplra_ap_report* rep);
 GAPLRA_API int gaplra_shift_invert(gaplra_ctx* ctx, const gaplra_matrix* x, const gaplra_si_config* cfg, double* w,
                         double* ritz, double* s, gaplra_si_report* rep);
 

@@ -57,6 +57,12 @@ PROF_CLASSES = ["gram", "epoch", "h_pass", "index", "qr", "anchor", "block_gram"
                 "block_u", "r10", "r11"]
 
 
+class ApReport(C.Structure):
+    _fields_ = [("n_intervals", C.c_int), ("s", C.c_int * 64), ("q", C.c_int * 64), ("strategy", C.c_int * 64),
+                ("width", C.c_int * 64), ("iterations", C.c_int * 64), ("shift", C.c_double * 64),
+                ("ledger", Ledger), ("ms_total", C.c_double)]
+
+
 class Profile(C.Structure):
     _fields_ = [("ms", C.c_double * 12), ("count", C.c_uint64 * 12), ("bytes", C.c_double * 12),
                 ("flops", C.c_double * 12)]
@@ -105,6 +111,11 @@ _SIGS = {
     "gaplra_restricted_projection": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, _dp, C.c_int, _dp, _dp]),
     "gaplra_shift_invert": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(SiConfig), _dp, _dp, _dp,
                                       C.POINTER(SiReport)]),
+    "gaplra_detect_multiplicative_gap": (C.c_int, [_dp, C.c_int, C.c_int, C.c_int, _ip]),
+    "gaplra_detect_additive_gap": (C.c_int, [C.c_void_p, _dp, C.c_int, C.c_int, C.c_int, C.c_double, _ip]),
+    "gaplra_estimate_eigenvalues": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_double, C.c_int, C.c_double,
+                                              C.c_uint64, C.c_double, C.POINTER(SvrgParams), _dp, _ip]),
+    "gaplra_approximate": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(SiConfig), _dp, _dp, C.POINTER(ApReport)]),
     "gaplra_cg_solve": (C.c_int, [C.c_void_p, C.c_void_p, C.c_double, C.c_int, _dp, _dp, C.c_double, C.c_int,
                                   _ip, _dp, C.c_int, _ip]),
     "gaplra_error_report": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, _dp, C.c_int, C.c_uint64, _dp, _dp]),

@@ -365,6 +365,17 @@ __global__ void k_scale_inv_sqrt(double* __restrict__ v, int64_t ld, int d, int 
   }
 }
 
+// H = (H + Hᵀ) / 2 in place (k x k row-major), the oracle's expression 0.5 * (h_ab + h_ba)
+__global__ void k_symmetrize(double* __restrict__ H, int k) {
+  for (int e = threadIdx.x; e < k * k; e += blockDim.x) {
+    const int a = e / k, b = e - (e / k) * k;
+    if (b <= a) continue;
+    const double m = 0.5 * (H[a * k + b] + H[b * k + a]);
+    H[a * k + b] = m;
+    H[b * k + a] = m;
+  }
+}
+
 }  // namespace
 
 void launch_qr_mgs2(double* Y, int64_t ldy, int d, int p, double* colmajor_scratch, int* status,
@@ -463,6 +474,12 @@ void launch_cg_dir(const double* rr, const double* rr_new, const double* R, doub
 }
 void launch_scale_inv_sqrt(double* v, int64_t ld, int d, int p, const double* s2, cudaStream_t st) {
   k_scale_inv_sqrt<<<ew_grid(static_cast<int64_t>(d) * p), 256, 0, st>>>(v, ld, d, p, s2);
+  GAPLRA_LAUNCH_CHECK();
+}
+
+void launch_symmetrize(double* H, int k, cudaStream_t st) {
+  if (k < 2) return;
+  k_symmetrize<<<1, 256, 0, st>>>(H, k);
   GAPLRA_LAUNCH_CHECK();
 }
 

@@ -684,8 +684,22 @@ struct CgResult {
   std::vector<double> history;
 };
 
+// P u = u - U (Uᵀ u) for a row-major d x p device block (project_out,
+// linear_operator.cpp:66-81: all coefficients first, then one subtraction);
+// U: d_pad x ldp(m) row-major, m <= 64.
+void project_out_dev(Context& c, const double* U, int m, double* v, int64_t ldv, int d, int p) {
+  if (m <= 0) return;
+  double* G = c.small.ensure(static_cast<size_t>(64) * 64 * 4 + 8) + 3 * 64 * 64;
+  double* part = c.tmp.ensure(static_cast<size_t>(small_gram_parts(d)) * 64 * 64 + 8);
+  launch_small_gram(U, ldp_of(m), m, v, ldv, p, d, part, G, c.st);  // m x p coefficients
+  launch_small_mul(U, ldp_of(m), m, G, p, p, d, 1.0, -1.0, v, ldv, c.st);
+}
+
+// With a deflation basis U (m columns) the system is lambda I - P X Xᵀ P,
+// P = I - U Uᵀ (Alg. 7's X_{-(s-1)}); for iterates in range(P)
+// that is one project_out after each gram pass (oracle.cpp cg_solve).
 CgResult cg_solve_dev(Context& c, Matrix& X, double lambda, int p, const double* B, double* W, double tol,
-                      int max_iter, bool warm, CgResult* partial = nullptr) {
+                      int max_iter, bool warm, CgResult* partial = nullptr, const double* U = nullptr, int m = 0) {
   if (p < 1 || p > 64) throw Error(kContractViolation, "solve_cg: need 1 <= p <= 64");
   if (!(tol > 0.0)) throw Error(kContractViolation, "solve_cg: tol must be > 0");
   const int d = X.d;
@@ -709,6 +723,7 @@ CgResult cg_solve_dev(Context& c, Matrix& X, double lambda, int p, const double*
   for (int k = 0; k < p; ++k) bnorm[k] = std::sqrt(c.pin[k]);
   if (warm) {  // R = B - D W0: Q = lambda W0 - X Xᵀ W0, then R = 1 * B - Q
     gram_block_dev(c, X, p, W, ld, Zg, ld, nullptr, 0);
+    project_out_dev(c, U, m, Zg, ld, d, p);
     launch_cg_dq(W, Zg, lambda, Q, ld, d, p, c.st);
     launch_cg_dq(B, Q, 1.0, R, ld, d, p, c.st);
   } else {
@@ -738,6 +753,7 @@ CgResult cg_solve_dev(Context& c, Matrix& X, double lambda, int p, const double*
       if (r <= tol) break;
       if (it >= cap) throw Error(kSolverStalled, "solve_cg: iteration cap reached");
       gram_block_dev(c, X, p, P, ld, Zg, ld, nullptr, 0);
+      project_out_dev(c, U, m, Zg, ld, d, p);
       launch_cg_dq(P, Zg, lambda, Q, ld, d, p, c.st);
       launch_col_dots(P, ld, Q, ld, d, p, part, pq, c.st);
       launch_cg_alpha(rr, pq, p, alpha, status, c.st);
@@ -760,13 +776,41 @@ struct CgOp : Op {
   Context& c;
   Matrix& X;
   double lambda, tol;
-  CgOp(Context& cc, Matrix& xx, double lam, double t) : c(cc), X(xx), lambda(lam), tol(t) {}
+  const double* U;  // deflated system (m = 0: none)
+  int m;
+  CgOp(Context& cc, Matrix& xx, double lam, double t, const double* u = nullptr, int mm = 0)
+      : c(cc), X(xx), lambda(lam), tol(t), U(u), m(mm) {}
   void apply(const double* in, double* out, int p, const double* guess = nullptr) override {
     if (guess)
       GAPLRA_CUDA_CHECK(cudaMemcpyAsync(out, guess, static_cast<size_t>(X.d_pad()) * ldp_of(p) * sizeof(double),
                                         cudaMemcpyDeviceToDevice, c.st));
-    cg_solve_dev(c, X, lambda, p, in, out, tol, 0, guess != nullptr);
+    cg_solve_dev(c, X, lambda, p, in, out, tol, 0, guess != nullptr, nullptr, U, m);
     c.led.operator_applies += p;
+  }
+};
+
+// DeflatedOperator::apply (linear_operator.cpp:56-64) on device blocks: P C P.
+struct DeflatedOp : Op {
+  Context& c;
+  Op& base;
+  const double* U;
+  int m, d;
+  int64_t dp;
+  DBuf<double> work;
+  DeflatedOp(Context& cc, Op& b, const double* u, int mm, int dd, int64_t dpp)
+      : c(cc), base(b), U(u), m(mm), d(dd), dp(dpp) {}
+  void apply(const double* in, double* out, int p, const double* guess = nullptr) override {
+    if (m <= 0) {
+      base.apply(in, out, p, guess);
+      return;
+    }
+    const int64_t ld = ldp_of(p);
+    double* w = work.ensure(static_cast<size_t>(dp) * ld);
+    GAPLRA_CUDA_CHECK(cudaMemcpyAsync(w, in, static_cast<size_t>(dp) * ld * sizeof(double), cudaMemcpyDeviceToDevice,
+                                      c.st));
+    project_out_dev(c, U, m, w, ld, d, p);
+    base.apply(w, out, p, guess);
+    project_out_dev(c, U, m, out, ld, d, p);
   }
 };
 
@@ -875,6 +919,68 @@ double estimate_top_dev(Context& c, Op& op, int d, int64_t dp, double eps_prime,
   return theta;
 }
 
+// Alg. 3 for any k (oracle.cpp estimate_eigs): Ritz values of the k-column
+// iterate (H = Sᵀ C S symmetrised, Jacobi), descending; early stop when
+// every value changes by <= rq_tol relative; k = 1 is estimate_top_dev.
+std::vector<double> estimate_eigs_dev(Context& c, Op& op, int d, int64_t dp, int k, double eps_prime, uint64_t seed,
+                                      double rq_tol, int* iters) {
+  if (k < 1 || k > 64) throw Error(kContractViolation, "estimate_eigenvalues: need 1 <= k <= 64");
+  const int L = static_cast<int>(std::ceil(4.0 / eps_prime * std::log(d / eps_prime)));
+  const int64_t ld = ldp_of(k);
+  const size_t blk = static_cast<size_t>(dp) * ld;
+  DBuf<double> s, y, q, gs, hb;
+  double* S = s.ensure(blk);
+  double* Yb = y.ensure(blk);
+  double* Q = q.ensure(blk);
+  double* guess = gs.ensure(blk);
+  double* H = hb.ensure(static_cast<size_t>(k) * k + k + static_cast<size_t>(k) * k);
+  double* vals = H + k * k;
+  double* vecs = vals + k;
+  orth_init(c, d, dp, k, seed, S);
+  double* G = c.small.ensure(static_cast<size_t>(64) * 64 * 4 + 8);
+  double* part = c.tmp.ensure(static_cast<size_t>(small_gram_parts(d)) * 64 * 64 + 8);
+  std::vector<double> theta(k, 0.0), prev(k, 0.0);
+  bool have_guess = false;
+  int it = 0;
+  for (int l = 1; l <= L + 1; ++l) {
+    op.apply(S, Yb, k, have_guess ? guess : nullptr);
+    it = l;
+    launch_small_gram(S, ld, k, Yb, ld, k, d, part, H, c.st);
+    launch_symmetrize(H, k, c.st);
+    launch_jacobi(H, k, vals, vecs, c.st);
+    GAPLRA_CUDA_CHECK(cudaMemcpyAsync(c.pin, vals, k * sizeof(double), cudaMemcpyDeviceToHost, c.st));
+    c.sync();
+    for (int a = 0; a < k; ++a) theta[a] = c.pin[a];
+    bool stop = l > 1;
+    for (int a = 0; a < k && stop; ++a) stop = std::fabs(theta[a] - prev[a]) <= rq_tol * std::fabs(theta[a]);
+    if (stop || l == L + 1) break;
+    GAPLRA_CUDA_CHECK(cudaMemcpyAsync(Q, Yb, blk * sizeof(double), cudaMemcpyDeviceToDevice, c.st));
+    qr_dev(c, Q, ld, d, k);
+    launch_small_gram(S, ld, k, Q, ld, k, d, part, G, c.st);  // G = S_oldᵀ Q
+    warm_guess_dev(c, Q, Yb, d, k, guess);
+    have_guess = true;
+    std::swap(S, Q);
+    prev = theta;
+  }
+  if (iters) *iters = it;
+  return theta;
+}
+
+// Alg. 4 / Alg. 5 (oracle.cpp detect_multiplicative_gap / detect_additive_gap)
+int detect_multiplicative_gap_host(const double* est, int count, int s, int p) {
+  const double f = 1.0 - 1.0 / (static_cast<double>(p) * p);
+  for (int i = 0; i + 1 < count; ++i)
+    if (est[i + 1] <= est[i] * f) return s + i;
+  return -1;
+}
+int detect_additive_gap_host(const double* inv, int count, int s, int k, double delta) {
+  if (count < 1 || !(inv[0] >= delta / 27.0 && inv[0] <= delta / 5.0))
+    throw Error(kShiftOutOfRange, "detect_additive_gap: inverse estimate outside [delta/27, delta/5] (Eq. 5)");
+  for (int i = 0; i + 1 < count; ++i)
+    if (inv[i + 1] - inv[i] >= 5.0 * delta / 9.0) return s + i;
+  return k;
+}
+
 gaplra_svrg_params prm_from(const gaplra_si_config& cfg, double tol) {
   gaplra_svrg_params p{};
   p.eta = 0.0;
@@ -888,11 +994,12 @@ gaplra_svrg_params prm_from(const gaplra_si_config& cfg, double tol) {
 }
 
 void tune_shift_dev(Context& c, Matrix& X, double delta, const gaplra_si_config& cfg, int64_t* counter,
-                    gaplra_si_report& rep) {
+                    gaplra_si_report& rep, const double* U = nullptr, int m = 0) {
   if (!(delta > 0.0)) throw Error(kContractViolation, "tune_shift: delta must be > 0");
   const int d = X.d;
   const int64_t dp = X.d_pad();
-  GramOp a(c, X);
+  GramOp a0(c, X);
+  DeflatedOp a(c, a0, U, m, d, dp);  // A_{-(s-1)}
   const double l1 = estimate_top_dev(c, a, d, dp, 0.25, derive_seed(cfg.seed, kTagEstA), cfg.rq_tol, nullptr);
   rep.lambda1_hat = l1;
   rep.tune_steps = 0;
@@ -909,8 +1016,9 @@ void tune_shift_dev(Context& c, Matrix& X, double delta, const gaplra_si_config&
     if (t > 0) hint = 2.0 * lambda - prev_lambda;
     prm.lambda1_hint = hint;
     InverseOp dinv(c, X, lambda, prm, counter);
-    CgOp dcg(c, X, lambda, cfg.tol_tune);
-    Op& op = cfg.backend == 1 ? static_cast<Op&>(dcg) : static_cast<Op&>(dinv);
+    CgOp dcg(c, X, lambda, cfg.tol_tune, U, m);
+    // a deflated shifted system is solved by CG (oracle.cpp tune_shift)
+    DeflatedOp op(c, cfg.backend == 1 || m > 0 ? static_cast<Op&>(dcg) : static_cast<Op&>(dinv), U, m, d, dp);
     const double est = estimate_top_dev(c, op, d, dp, 1.0 / 9.0, derive_seed(cfg.seed, kTagEstD + t), cfg.rq_tol,
                                         nullptr);
     const double inv = 1.0 / std::max(est, 1e-300);
@@ -1033,6 +1141,119 @@ void principal_angles_dev(Context& c, int d, int k, const double* U, int p, doub
   GAPLRA_CUDA_CHECK(cudaMemcpyAsync(c.pin, vals, k * sizeof(double), cudaMemcpyDeviceToHost, c.st));
   c.sync();
   for (int a = 0; a < k; ++a) cos_host[a] = std::sqrt(std::min(std::max(c.pin[a], 0.0), 1.0));
+}
+
+// approximate — Alg. 7, the device form of oracle.cpp
+// approximate with the same pins: per interval {s..k} on A_{-(s-1)}, Alg. 3 at
+// eps' = 1/(9p^2) -> Alg. 4; a multiplicative gap q gives PlainPower on
+// {s..q} (width q-s+1, L = ceil(4 p^4 ln(kd/eps_int))); otherwise tune_shift
+// on the deflated operators, Alg. 3 on D_{-(s-1)} at eps' = 1/(9p) -> Alg. 5
+// -> ShiftedInverse (width q-s+1 or p-s+1 at q = k, L = ceil(4 k ln(kd/eps_int)));
+// NoPreconditioningNeeded -> PlainPower with width p-s+1, q = k.  Deflated
+// shifted systems are solved by CG; the first interval's by the configured
+// backend.  Finally restricted_projection(A, basis, k).
+constexpr uint64_t kTagInterval = 0x696e7476ull;  // "intv"
+
+void approximate_dev(Context& c, Matrix& X, const gaplra_si_config& cfg, double* W, double* ritz_host,
+                     gaplra_ap_report& rep) {
+  const int d = X.d, k = cfg.k, p = cfg.p;
+  const int64_t dp = X.d_pad();
+  if (k < 1 || p <= k || p >= d || p > 64) throw Error(kContractViolation, "approximate: need 1 <= k < p < d, p <= 64");
+  if (!(cfg.delta > 0.0)) throw Error(kContractViolation, "approximate: gap budget delta must be > 0");
+  const double eps_int = cfg.eps / (3.0 * std::max(cfg.mu, 1.0) * k * d);
+  const double lg = std::log(k * static_cast<double>(d) / eps_int);
+  auto capped = [&](double L) {
+    const int l = static_cast<int>(std::min(std::ceil(L), 1e9));
+    return cfg.max_outer > 0 ? std::min(l, cfg.max_outer) : l;
+  };
+  DBuf<double> ubs[2], sb;
+  int cur = 0;
+  double* U = nullptr;
+  int m = 0;
+  int64_t solves = 0;
+  int s = 1;
+  for (int j = 0; s <= k; ++j) {
+    if (j >= k) throw Error(kRankDeficient, "approximate: no progress (DegenerateProgress)");
+    gaplra_si_config cj = cfg;
+    cj.seed = derive_seed(cfg.seed, kTagInterval + static_cast<uint64_t>(j));
+    GramOp a0(c, X);
+    DeflatedOp a(c, a0, U, m, d, dp);
+    const int cnt = k - s + 1;
+    const std::vector<double> est =
+        estimate_eigs_dev(c, a, d, dp, cnt, 1.0 / (9.0 * p * p), derive_seed(cj.seed, kTagEstA), cfg.rq_tol, nullptr);
+    int q = detect_multiplicative_gap_host(est.data(), cnt, s, p);
+    int strategy = 0, width = 0, iters = 0;
+    double shift = 0.0;
+    double* S = nullptr;
+    auto plain = [&](int wdt) {
+      strategy = 0;
+      width = wdt;
+      S = sb.ensure(static_cast<size_t>(dp) * ldp_of(wdt));
+      iters = subspace_iterate_dev(c, a, d, dp, wdt, capped(4.0 * std::pow(static_cast<double>(p), 4) * lg),
+                                   derive_seed(cj.seed, kTagSubspace), cfg.conv_tol, S);
+    };
+    if (q >= 0) {
+      plain(q - s + 1);
+    } else {
+      gaplra_si_report tr;
+      std::memset(&tr, 0, sizeof(tr));
+      bool shifted = true;
+      try {
+        tune_shift_dev(c, X, cfg.delta, cj, &solves, tr, U, m);
+      } catch (const Error& e) {
+        if (e.code != kNoPreconditioningNeeded) throw;
+        shifted = false;
+      }
+      if (!shifted) {
+        q = k;
+        plain(p - s + 1);
+      } else {
+        shift = tr.lambda;
+        gaplra_svrg_params prm = prm_from(cj, cfg.tol_solve);
+        prm.lambda1_hint = tr.lambda1_hint;
+        InverseOp dinv(c, X, shift, prm, &solves);
+        CgOp dcg(c, X, shift, cfg.tol_solve, U, m);
+        DeflatedOp dd(c, cfg.backend == 1 || m > 0 ? static_cast<Op&>(dcg) : static_cast<Op&>(dinv), U, m, d, dp);
+        const std::vector<double> dest = estimate_eigs_dev(c, dd, d, dp, cnt, 1.0 / (9.0 * p),
+                                                           derive_seed(cj.seed, kTagEstD), cfg.rq_tol, nullptr);
+        std::vector<double> inv(cnt);
+        for (int i = 0; i < cnt; ++i) inv[i] = 1.0 / std::max(dest[i], 1e-300);
+        q = detect_additive_gap_host(inv.data(), cnt, s, k, cfg.delta);
+        strategy = 1;
+        width = q < k ? q - s + 1 : p - s + 1;
+        S = sb.ensure(static_cast<size_t>(dp) * ldp_of(width));
+        iters = subspace_iterate_dev(c, dd, d, dp, width, capped(4.0 * k * lg), derive_seed(cj.seed, kTagSubspace),
+                                     cfg.conv_tol, S);
+      }
+    }
+    // deflation_basis_extend (oracle.cpp basis_extend): project, QR, append
+    project_out_dev(c, U, m, S, ldp_of(width), d, width);
+    qr_dev(c, S, ldp_of(width), d, width, /*count=*/false);
+    const int m2 = m + width;
+    if (m2 > 64) throw Error(kContractViolation, "approximate: basis wider than 64 columns");
+    double* U2 = ubs[cur ^ 1].ensure(static_cast<size_t>(dp) * ldp_of(m2));
+    GAPLRA_CUDA_CHECK(cudaMemsetAsync(U2, 0, static_cast<size_t>(dp) * ldp_of(m2) * sizeof(double), c.st));
+    if (m > 0)
+      GAPLRA_CUDA_CHECK(cudaMemcpy2DAsync(U2, ldp_of(m2) * sizeof(double), U, ldp_of(m) * sizeof(double),
+                                          m * sizeof(double), d, cudaMemcpyDeviceToDevice, c.st));
+    GAPLRA_CUDA_CHECK(cudaMemcpy2DAsync(U2 + m, ldp_of(m2) * sizeof(double), S, ldp_of(width) * sizeof(double),
+                                        width * sizeof(double), d, cudaMemcpyDeviceToDevice, c.st));
+    cur ^= 1;
+    U = U2;
+    m = m2;
+    if (rep.n_intervals < 64) {
+      const int t = rep.n_intervals;
+      rep.s[t] = s;
+      rep.q[t] = q;
+      rep.strategy[t] = strategy;
+      rep.width[t] = width;
+      rep.iterations[t] = iters;
+      rep.shift[t] = shift;
+    }
+    rep.n_intervals++;
+    s = q + 1;
+  }
+  restricted_projection_dev(c, X, U, m, k, W, ritz_host);
 }
 
 int outer_cap(const gaplra_si_config& cfg, int d) {
@@ -1639,6 +1860,64 @@ int gaplra_principal_angles(gaplra_ctx* ctx, int d, int k, const double* u, int 
     upload_block(c, u, d, k, ud.p, ldp_of(k));
     upload_block(c, s, d, p, sd.p, ldp_of(p));
     principal_angles_dev(c, d, k, ud.p, p, sd.p, cosines);
+  });
+}
+
+int gaplra_detect_multiplicative_gap(const double* est, int count, int s, int p, int* q) {
+  if (!est || !q || count < 1 || p < 1) return GAPLRA_CONTRACT_VIOLATION;
+  *q = detect_multiplicative_gap_host(est, count, s, p);
+  return GAPLRA_OK;
+}
+
+int gaplra_detect_additive_gap(gaplra_ctx* ctx, const double* inv, int count, int s, int k, double delta, int* q) {
+  if (!inv || !q) return GAPLRA_CONTRACT_VIOLATION;
+  return guard(ctx, [&] { *q = detect_additive_gap_host(inv, count, s, k, delta); });
+}
+
+int gaplra_estimate_eigenvalues(gaplra_ctx* ctx, const gaplra_matrix* x, int inverse, double lambda, int k,
+                                double eps_prime, uint64_t seed, double rq_tol, const gaplra_svrg_params* prm,
+                                double* values, int* iterations) {
+  if (!ctx || !x || !values) return GAPLRA_CONTRACT_VIOLATION;
+  return guard(ctx, [&] {
+    require(eps_prime > 0.0 && eps_prime < 1.0 && k >= 1 && k <= 64 && (!inverse || prm),
+            "estimate_eigenvalues: bad arguments");
+    Context& c = ctx->c;
+    Matrix& X = const_cast<gaplra_matrix*>(x)->m;
+    int64_t sc = 0;
+    std::vector<double> v;
+    if (inverse) {
+      InverseOp op(c, X, lambda, *prm, &sc);
+      v = estimate_eigs_dev(c, op, X.d, X.d_pad(), k, eps_prime, seed, rq_tol, iterations);
+    } else {
+      GramOp op(c, X);
+      v = estimate_eigs_dev(c, op, X.d, X.d_pad(), k, eps_prime, seed, rq_tol, iterations);
+    }
+    std::copy(v.begin(), v.end(), values);
+  });
+}
+
+int gaplra_approximate(gaplra_ctx* ctx, const gaplra_matrix* x, const gaplra_si_config* cfg, double* w, double* ritz,
+                       gaplra_ap_report* rep) {
+  if (!ctx || !x || !cfg || !w || !ritz || !rep) return GAPLRA_CONTRACT_VIOLATION;
+  std::memset(rep, 0, sizeof(*rep));
+  return guard(ctx, [&] {
+    Context& c = ctx->c;
+    Matrix& X = const_cast<gaplra_matrix*>(x)->m;
+    const gaplra_ledger before = c.led;
+    Timer total(c, &rep->ms_total);
+    DBuf<double> wb;
+    double* W = wb.ensure(static_cast<size_t>(X.d_pad()) * ldp_of(cfg->k));
+    approximate_dev(c, X, *cfg, W, ritz, *rep);
+    download_block(c, W, ldp_of(cfg->k), X.d, cfg->k, w);
+    c.sync();
+    gaplra_ledger& L = rep->ledger;
+    L.gram_applies = c.led.gram_applies - before.gram_applies;
+    L.operator_applies = c.led.operator_applies - before.operator_applies;
+    L.qr_factorizations = c.led.qr_factorizations - before.qr_factorizations;
+    L.linear_solves = c.led.linear_solves - before.linear_solves;
+    L.solver_column_samples = c.led.solver_column_samples - before.solver_column_samples;
+    L.epochs = c.led.epochs - before.epochs;
+    L.outer_iterations = c.led.outer_iterations - before.outer_iterations;
   });
 }
 

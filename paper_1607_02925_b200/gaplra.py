@@ -391,6 +391,67 @@ def principal_angles(u: np.ndarray, s: np.ndarray, ctx: Context | None = None) -
     return cos
 
 
+def detect_multiplicative_gap(estimates, s: int, p: int):
+    """Alg. 4: estimates = λ̂_s, λ̂_{s+1}, ...; the smallest
+    global q with λ̂_{q+1} <= λ̂_q (1 − p⁻²), or None."""
+    est = np.ascontiguousarray(estimates, dtype=np.float64)
+    q = C.c_int(0)
+    rc = N.load().gaplra_detect_multiplicative_gap(_p(est), len(est), s, p, C.byref(q))
+    if rc != GAPLRA_OK:
+        raise ContractViolation("detect_multiplicative_gap: bad arguments")
+    return None if q.value < 0 else q.value
+
+
+def detect_additive_gap(inv_estimates, s: int, k: int, delta: float, ctx: Context | None = None) -> int:
+    """Alg. 5 (SPEC.md:413-421): inv_estimates = λ̃_s⁻¹, ...; q = min J or k;
+    ShiftOutOfRange unless λ̃_s⁻¹ ∈ [Δ/27, Δ/5]."""
+    ctx = ctx or default_context()
+    inv = np.ascontiguousarray(inv_estimates, dtype=np.float64)
+    q = C.c_int(0)
+    ctx.check(ctx.lib.gaplra_detect_additive_gap(ctx.h, _p(inv), len(inv), s, k, delta, C.byref(q)))
+    return q.value
+
+
+def estimate_eigenvalues(x: DeviceMatrix, k: int, eps_prime: float, seed: int, *, inverse: bool = False,
+                         lam: float = 0.0, rq_tol: float = 1e-3, tol: float = 1e-6, svrg_seed: int = 0,
+                         lambda1_hint: float = 0.0):
+    """Alg. 3 for any k: descending estimates of the top-k
+    eigenvalues of A = XXᵀ (or of D⁻¹ with inverse=True) and the iterations."""
+    prm = N.SvrgParams(0.0, 0, tol, 0, 10.0, svrg_seed, lambda1_hint)
+    vals = np.zeros(k)
+    it = C.c_int()
+    x.ctx.check(x.ctx.lib.gaplra_estimate_eigenvalues(x.ctx.h, x.h, int(inverse), lam, k, eps_prime, seed, rq_tol,
+                                                      C.byref(prm), _p(vals), C.byref(it)))
+    return vals, it.value
+
+
+@dataclass
+class RankKProjection:
+    """W (d x k orthonormal), Ritz values, errors, executed plan."""
+    W: np.ndarray
+    ritz: np.ndarray
+    frobenius_error: float
+    spectral_error: float
+    plan: list
+    ledger: dict
+    ms: float
+
+
+def approximate(x: DeviceMatrix, cfg: SIConfig, error_iters: int = 20) -> RankKProjection:
+    """Alg. 7: adaptive partition into PlainPower /
+    ShiftedInverse intervals with deflation, then Alg. 2 on the concatenated
+    basis.  cfg.delta is the gap budget (Δ <= λ_k − λ_{p+1} <= 2Δ)."""
+    w = np.zeros((x.d, cfg.k))
+    ritz = np.zeros(cfg.k)
+    rep = N.ApReport()
+    x.ctx.check(x.ctx.lib.gaplra_approximate(x.ctx.h, x.h, C.byref(cfg.native()), _p(w), _p(ritz), C.byref(rep)))
+    plan = [dict(s=rep.s[i], q=rep.q[i], strategy=("PlainPower", "ShiftedInverse")[rep.strategy[i]],
+                 width=rep.width[i], iterations=rep.iterations[i], shift=rep.shift[i])
+            for i in range(min(rep.n_intervals, 64))]
+    fr, sp = error_report(x, w, iters=error_iters, seed=cfg.seed)
+    return RankKProjection(w, ritz, fr, sp, plan, rep.ledger.as_dict(), rep.ms_total)
+
+
 def estimate_top(x: DeviceMatrix, eps_prime: float, seed: int, *, inverse: bool = False, lam: float = 0.0,
                  rq_tol: float = 1e-3, tol: float = 1e-6, svrg_seed: int = 0, solve_counter: int = 0,
                  lambda1_hint: float = 0.0):

@@ -380,3 +380,69 @@ def test_shift_invert_cg_backend(g, oracle):
     fc = g.error_report(x, rc_.W)[0]
     fs = g.error_report(x, rs_.W)[0]
     assert abs(fc - fs) <= 1e-6 * fs
+
+
+# ---- Alg. 3 (k > 1), Alg. 4 / 5, Alg. 7 adaptive driver ----
+def test_gap_detection_kats_device(g):
+    assert g.detect_multiplicative_gap([4.0, 3.0, 2.99], 1, 2) == 1
+    assert g.detect_multiplicative_gap([2.0, 2.0, 2.0], 1, 3) is None
+    assert g.detect_multiplicative_gap([9.0, 8.9, 4.0], 4, 3) == 5
+    assert g.detect_additive_gap([0.1, 0.2, 1.0], 2, 4, 1.0) == 3
+    assert g.detect_additive_gap([0.1, 0.2, 0.3], 2, 4, 1.0) == 4
+    with pytest.raises(g.ShiftOutOfRange):
+        g.detect_additive_gap([0.5, 0.6], 1, 2, 1.0)
+
+
+@pytest.mark.parametrize("k", [1, 3, 8])
+def test_estimate_eigenvalues_matches_oracle(g, oracle, k):
+    X, _, sig = planted_dense(200, 500, k=4, p=10, seed=20 + k, noise=1e-3)
+    vd, itd = g.estimate_eigenvalues(g.DeviceMatrix.dense(X), k, 1 / 9, 7)
+    rc, vo, ito = oracle.estimate_eigenvalues(oracle.dense(X), k, 1 / 9, 7)
+    assert rc == 0 and abs(itd - ito) <= 1
+    if itd == ito:
+        assert np.allclose(vd, vo, rtol=1e-10)
+    lam = np.linalg.eigvalsh(X @ X.T)[::-1][:k]
+    assert np.all(vd >= (1 - 1 / 9) * lam - 1e-12) and np.all(vd <= lam / (1 - 1 / 9) + 1e-12)
+
+
+def _check_approximate(g, oracle, X, cfg_kw, ocfg):
+    x = g.DeviceMatrix.dense(X)
+    res = g.approximate(x, g.SIConfig(**cfg_kw))
+    rc, wo, ro, rep = oracle.approximate(oracle.dense(X), ocfg)
+    assert rc == 0
+    assert [(iv["s"], iv["q"], iv["strategy"], iv["width"]) for iv in res.plan] == \
+        [(iv["s"], iv["q"], iv["strategy"], iv["width"]) for iv in rep.plan()]
+    assert oracle.sin_theta(res.W, wo) <= 1e-7
+    assert np.allclose(res.ritz, ro, rtol=1e-9)
+    return res
+
+
+def test_approximate_diag_device(g, oracle):
+    X = np.diag([5.0, 4.0, 3.0, 2.0, 1.0])
+    res = _check_approximate(g, oracle, X, dict(k=2, p=4, eps=1e-3, delta=10.0, seed=1),
+                             default_si_config(2, 4, eps=1e-3, delta=10.0, seed=1))
+    assert res.frobenius_error <= (1 + 1e-3) * np.sqrt(14.0)
+
+
+def test_approximate_shifted_inverse_device(g, oracle):
+    sig = np.concatenate([[10.0, 9.99, 9.98, 5.0, 1.0], 0.5 / np.arange(1, 31)])
+    X, U, _ = planted_dense(60, 80, sigma=sig, seed=11)
+    gap = sig[2] ** 2 - sig[6] ** 2
+    res = _check_approximate(g, oracle, X, dict(k=3, p=6, eps=1e-4, delta=gap / 1.5, seed=3, force=True,
+                                                max_outer=400),
+                             default_si_config(3, 6, eps=1e-4, delta=gap / 1.5, seed=3, force=1, max_outer=400))
+    assert any(iv["strategy"] == "ShiftedInverse" and iv["s"] == 1 and iv["q"] >= 3 for iv in res.plan)
+    assert res.frobenius_error <= (1 + 1e-4) * np.sqrt(np.sum(sig[3:] ** 2))
+
+
+def test_approximate_deflated_intervals_device(g, oracle):
+    # a multiplicative gap after index 1 and a small-gap tail: PlainPower {1}
+    # then a deflated interval (CG on the deflated shifted system)
+    sig = np.concatenate([[6.0, 3.0, 2.99, 2.98], 0.3 / np.arange(1, 41)])
+    X, U, _ = planted_dense(80, 120, sigma=sig, seed=13)
+    gap = sig[3] ** 2 - sig[6] ** 2
+    res = _check_approximate(g, oracle, X, dict(k=4, p=7, eps=1e-4, delta=gap / 1.5, seed=4, force=True,
+                                                max_outer=600),
+                             default_si_config(4, 7, eps=1e-4, delta=gap / 1.5, seed=4, force=1, max_outer=600))
+    assert len(res.plan) >= 2 and res.plan[0]["strategy"] == "PlainPower"
+    assert res.frobenius_error <= (1 + 1e-4) * np.sqrt(np.sum(sig[4:] ** 2))
