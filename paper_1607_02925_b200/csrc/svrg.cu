@@ -1417,6 +1417,368 @@ __global__ void __launch_bounds__(v3_threads(PC), 1) k_svrg_chain_v3(EpochArgs a
   cluster.sync();
 }
 
+// ---------------------------------------------------------------------------
+// k_svrg_chain_v4: the chain on the FP64 tensor path for PC = 8 right-hand
+// sides per cluster (C2: 3 clusters instead of 7 x PC 3).  Same algebra,
+// lookahead and slab as v3; the products and the update are DMMA m8n8k4 in
+// the transposed form, with Vᵀ (8 columns x the warp's 64 rows) kept as the
+// update's C fragments in registers:
+//   update    Vᵀ += coefᵀ X_Bᵀ   M = column, N = rows (8 per tile), K = slices
+//   products  Âᵀ = Vᵀ X_B        M = column, N = slices, K = rows; the A
+//             fragment of k-step (tile, u) is element u of the tile's C
+//             fragment (lane tq <-> row 8 tile + 2 tq + u), so V never leaves
+//             the registers
+// Slice pitch RP ≡ 4 (mod 16) doubles: the update's LDS.64 B fragments and the
+// products' LDS.128 (rows 2tq, 2tq+1, slices permuted 0 2 1 3 4 6 5 7) are
+// bank-conflict free; coef is stored [slice][12].  Warps: 4 rows (64 rows
+// each), 4 reducers (one Â / coef entry per lane), 1 pusher (sums the row
+// warps' partials, bulk-copies Â_{t+1} to the 16 peers), 2 producers.
+// ---------------------------------------------------------------------------
+namespace v4 {
+constexpr int PC = 8, B = 16, NV = B * PC;
+constexpr int kRows = 8, kRed = 4, kProd = 2;
+constexpr int kRW = 256 / kRows, kTiles = kRW / 8;  // rows and 8-row tiles per row warp
+constexpr int kThreads = 32 * (kRows + kRed + 1 + kProd);
+constexpr int CP = 12;  // coef pitch (doubles)
+
+struct Smem {
+  int rp, stages;
+  size_t stage_len, off_recv, off_red, off_outv, off_cf, off_ahat, off_pre, off_bar, total;
+};
+__host__ __device__ inline Smem smem(int rows, int stages) {
+  Smem L;
+  (void)rows;  // the 4 row warps always span 256 rows (pad rows are zero)
+  L.rp = 256 + 4;
+  L.stages = stages;
+  L.stage_len = static_cast<size_t>(B) * L.rp + 2 * B * B + B * PC;
+  size_t o = L.stage_len * stages;
+  L.off_recv = o;
+  o += static_cast<size_t>(kRecvSlots) * kMaxCluster * NV;
+  L.off_red = o;
+  o += 2 * kRows * NV;
+  L.off_outv = o;
+  o += 2 * NV;
+  L.off_cf = o;
+  o += 2 * B * CP;
+  L.off_ahat = o;
+  o += NV;
+  L.off_pre = o;
+  o += NV;
+  L.off_bar = o;
+  o += 16;
+  L.total = o * sizeof(double);
+  return L;
+}
+}  // namespace v4
+
+__global__ void __launch_bounds__(v4::kThreads, 1) k_svrg_chain_v4(EpochArgs a) {
+  using namespace v4;
+  extern __shared__ __align__(128) double sm[];
+  cg::cluster_group cluster = cg::this_cluster();
+  const int G = static_cast<int>(cluster.num_blocks());
+  const int g = static_cast<int>(cluster.block_rank());
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int gq = lane >> 2, tq = lane & 3;
+  const int grp = blockIdx.y;
+  const int c0 = grp * PC;
+  const int pc = min(PC, a.p - c0);
+  const Smem L = smem(a.rows_per_cta, a.stages);
+  const int S = L.stages, RP = L.rp;
+  const int r0 = g * a.rows_per_cta;
+  const int rc = max(0, min(a.rows_per_cta, a.d_pad - r0));
+  double* recv = sm + L.off_recv;  // [kRecvSlots][kMaxCluster][NV]
+  double* red = sm + L.off_red;    // [2][kRows][NV]
+  double* outv = sm + L.off_outv;  // [2][NV]
+  double* cfb = sm + L.off_cf;     // [2][B][CP]
+  double* Ahat = sm + L.off_ahat;  // [NV]
+  double* pre = sm + L.off_pre;    // [NV]
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + L.off_bar);  // [S <= 4]
+  uint64_t* empty = full + 4;                                     // [S]
+  uint64_t* rbar = full + 8;                                      // [kRecvSlots]
+  auto stage_at = [&](int s_idx) { return sm + static_cast<size_t>(s_idx) * L.stage_len; };
+  const int nb = static_cast<int>((a.m + B - 1) / B);
+  const int last_bt = static_cast<int>(a.m - static_cast<int64_t>(nb - 1) * B);
+  auto bt_of = [&](int t) { return t == nb - 1 ? last_bt : B; };
+  double rho_b = 1.0, rho_last = 1.0;
+  for (int j = 0; j < B; ++j) rho_b *= a.rho;
+  for (int j = 0; j < last_bt; ++j) rho_last *= a.rho;
+#pragma unroll 1
+  for (size_t e = tid; e < L.off_recv; e += blockDim.x) sm[e] = 0.0;  // pad rows / unwritten slices read as 0
+  for (int e = tid; e < 2 * B * CP; e += blockDim.x) cfb[e] = 0.0;
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], kProd);
+      mbar_init(&empty[s], kRows + kRed);
+    }
+    for (int q = 0; q < kRecvSlots; ++q) mbar_init(&rbar[q], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  cluster.sync();
+  // GAPLRA_EPOCH_TIMING: cycles per block; rows (tid 0): 0 wait stage, 1 products,
+  // 2 wait coef, 3 update; reducer (warp 4 lane 0): 4 wait Â, 5 reduce + coef,
+  // 6 pre; pusher (lane 0): 7 wait red + push
+  long long tacc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long tp = clock64();
+  auto tick = [&](int kk) {
+    if (a.dbg) {
+      long long now;
+      asm volatile("mov.u64 %0, %%clock64;" : "=l"(now)::"memory");
+      tacc[kk] += now - tp;
+      tp = now;
+    }
+  };
+  auto bar_red_arrive = [](int u) {  // rows -> pusher, red(u) written (barrier 5 / 6 by parity)
+    if (u & 1)
+      asm volatile("bar.arrive 6, %0;" ::"n"(32 * (kRows + 1)) : "memory");
+    else
+      asm volatile("bar.arrive 5, %0;" ::"n"(32 * (kRows + 1)) : "memory");
+  };
+
+  if (warp >= kRows + kRed + 1) {  // ------------------------------------------ producers
+    chain_produce<PC, B, kProd>(a, warp - kRows - kRed - 1, lane, nb, last_bt, S, rc, r0, RP, grp, sm,
+                                L.stage_len, full, empty);
+  } else if (warp == kRows + kRed) {  // ---------------------------------------- pusher
+    // Â_u partials of the 4 row warps -> fixed-order sum -> outv[u & 1] ->
+    // one bulk copy per peer (lane q -> peer q).  The rows cannot arrive for
+    // u + 2 on this barrier before this warp's sync for u: products(u + 2)
+    // follows update(u), which needs Â_u from every peer, including this one.
+    for (int u = 0; u < nb; ++u) {
+      tick(7);
+      if (u & 1)
+        asm volatile("bar.sync 6, %0;" ::"n"(32 * (kRows + 1)) : "memory");
+      else
+        asm volatile("bar.sync 5, %0;" ::"n"(32 * (kRows + 1)) : "memory");
+      if (lane < G) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+      __syncwarp();
+      const double* rb = red + (u & 1) * kRows * NV;
+      double* ov = outv + (u & 1) * NV;
+#pragma unroll
+      for (int q = 0; q < NV / 32; ++q) {
+        const int e = q * 32 + lane;
+        double sum = 0.0;
+#pragma unroll
+        for (int w = 0; w < kRows; w += 2) sum += rb[w * NV + e] + rb[(w + 1) * NV + e];
+        ov[e] = sum;
+      }
+      fence_proxy_async();
+      __syncwarp();
+      if (lane < G) {
+        const int par = u & (kRecvSlots - 1);
+        dsmem_bulk_copy(mapa(smem_u32(recv + (par * kMaxCluster + g) * NV), lane), smem_u32(ov), NV * 8u,
+                        mapa(smem_u32(&rbar[par]), lane));
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+    }
+    if (lane < G) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    tick(7);
+    if (a.dbg && lane == 0) a.dbg[(blockIdx.y * gridDim.x + blockIdx.x) * 8 + 7] = tacc[7];
+  } else if (warp >= kRows) {  // --------------------------------------------- reducers
+    const int rw = warp - kRows;
+    const int e = rw * 32 + lane;  // this lane's entry (j, c) = (e / PC, e % PC)
+    const int j = e / PC, c = e - (e / PC) * PC;
+    auto red_sync = []() { asm volatile("bar.sync 4, %0;" ::"n"(32 * kRed) : "memory"); };
+    auto arm = [&](int u) {
+      if (rw == 0 && lane == 0)
+        mbar_expect_tx(&rbar[u & (kRecvSlots - 1)], static_cast<uint32_t>(G * NV * 8));
+    };
+    if (nb > 0) {
+      arm(0);
+      mbar_wait(&full[0], 0);
+      pre[e] = stage_at(0)[B * RP + 2 * B * B + e];
+    }
+    int cs = 0;
+    uint32_t cph = 0;
+#pragma unroll 1
+    for (int t = 0; t < nb; ++t) {
+      const bool more = t + 1 < nb;
+      const int ns = cs + 1 == S ? 0 : cs + 1;
+      const uint32_t nph = ns == 0 ? cph ^ 1u : cph;
+      if (more) arm(t + 1);
+      const int par = t & (kRecvSlots - 1);
+      tick(6);
+      mbar_wait(&rbar[par], static_cast<uint32_t>((t >> 2) & 1));
+      tick(4);
+      double sacc = 0.0;
+      if (e < bt_of(t) * PC) {
+        const double* sl = recv + par * kMaxCluster * NV + e;
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll 1
+        for (int q = 0; q < G; q += 4) {
+          s0 += sl[q * NV];
+          s1 += sl[(q + 1) * NV];
+          s2 += sl[(q + 2) * NV];
+          s3 += sl[(q + 3) * NV];
+        }
+        sacc = (s0 + s1) + (s2 + s3);
+      }
+      Ahat[e] = sacc;
+      red_sync();  // Â_t complete
+      const double* TT = stage_at(cs) + B * RP;
+      double* cf = cfb + (t & 1) * B * CP;
+      {
+        double s0 = pre[e], s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+        for (int l = 0; l < B; l += 4) {
+          s0 = fma(TT[l * B + j], Ahat[l * PC + c], s0);
+          s1 = fma(TT[(l + 1) * B + j], Ahat[(l + 1) * PC + c], s1);
+          s2 = fma(TT[(l + 2) * B + j], Ahat[(l + 2) * PC + c], s2);
+          s3 = fma(TT[(l + 3) * B + j], Ahat[(l + 3) * PC + c], s3);
+        }
+        cf[j * CP + c] = (s0 + s1) + (s2 + s3);
+      }
+      if (t & 1)
+        asm volatile("bar.arrive 3, %0;" ::"n"(32 * (kRows + kRed)) : "memory");
+      else
+        asm volatile("bar.arrive 2, %0;" ::"n"(32 * (kRows + kRed)) : "memory");
+      tick(5);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[cs]);  // TT_t was the reducers' last use of stage t
+      if (more) {  // pre_{t+1} = M_{t+1} coef_t + U_{t+1}
+        red_sync();  // coef_t complete; Â reads done
+        mbar_wait(&full[ns], nph);
+        const double* M = stage_at(ns) + B * RP + B * B;
+        const double* Ub = M + B * B;
+        double s0 = Ub[e], s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+        for (int l = 0; l < B; l += 4) {
+          s0 = fma(M[l * B + j], cf[l * CP + c], s0);
+          s1 = fma(M[(l + 1) * B + j], cf[(l + 1) * CP + c], s1);
+          s2 = fma(M[(l + 2) * B + j], cf[(l + 2) * CP + c], s2);
+          s3 = fma(M[(l + 3) * B + j], cf[(l + 3) * CP + c], s3);
+        }
+        pre[e] = (s0 + s1) + (s2 + s3);
+      }
+      cs = ns;
+      cph = nph;
+    }
+    tick(6);
+    if (a.dbg && warp == kRows && lane == 0)
+      for (int kk = 4; kk < 7; ++kk) a.dbg[(blockIdx.y * gridDim.x + blockIdx.x) * 8 + kk] = tacc[kk];
+  } else {  // --------------------------------------------------------------- rows
+    const int perm = ((gq & 1) << 1) | ((gq >> 1) & 1) | (gq & 4);  // 0 2 1 3 4 6 5 7
+    const int rw0 = warp * kRW;  // this warp's first row (of the CTA's slice)
+    double v[kTiles][2];          // Vᵀ C fragments: column gq, rows rw0 + 8 tile + 2 tq + {0, 1}
+#pragma unroll
+    for (int tl = 0; tl < kTiles; ++tl)
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int r = rw0 + 8 * tl + 2 * tq + u;
+        v[tl][u] = (r < rc && gq < pc) ? a.W[static_cast<int64_t>(r0 + r) * a.ldw + c0 + gq] : 0.0;
+      }
+    int ws = 0;
+    uint32_t wph = 0;
+    auto wait_stage = [&]() {
+      mbar_wait(&full[ws], wph);
+      const int s = ws;
+      if (++ws == S) {
+        ws = 0;
+        wph ^= 1u;
+      }
+      return s;
+    };
+    // Âᵀ partial over the warp's 64 rows: 2 slice tiles, K = 16 k-steps
+    auto products = [&](const double* xb, int u_blk) {
+      double acc[2][2][2];  // [slice tile][chain][elem]
+#pragma unroll
+      for (int n2 = 0; n2 < 2; ++n2)
+#pragma unroll
+        for (int ch = 0; ch < 2; ++ch) acc[n2][ch][0] = acc[n2][ch][1] = 0.0;
+#pragma unroll
+      for (int tl = 0; tl < kTiles; ++tl) {
+        double2 xv[2];
+#pragma unroll
+        for (int n2 = 0; n2 < 2; ++n2)
+          xv[n2] = *reinterpret_cast<const double2*>(xb + (8 * n2 + perm) * RP + rw0 + 8 * tl + 2 * tq);
+#pragma unroll
+        for (int n2 = 0; n2 < 2; ++n2) {
+          dmma(acc[n2][tl & 1][0], acc[n2][tl & 1][1], v[tl][0], xv[n2].x);
+          dmma(acc[n2][tl & 1][0], acc[n2][tl & 1][1], v[tl][1], xv[n2].y);
+        }
+      }
+      // C fragment (column gq, slices 8 n2 + perm(2 tq), 8 n2 + perm(2 tq + 1)) -> red(u_blk) in [j PC + c]
+      double* rb = red + (u_blk & 1) * kRows * NV + warp * NV;
+      const int pa = ((2 * tq) & 1) << 1 | (((2 * tq) >> 1) & 1) | ((2 * tq) & 4);
+      const int pb = ((2 * tq + 1) & 1) << 1 | (((2 * tq + 1) >> 1) & 1) | ((2 * tq + 1) & 4);
+#pragma unroll
+      for (int n2 = 0; n2 < 2; ++n2) {
+        rb[(8 * n2 + pa) * PC + gq] = acc[n2][0][0] + acc[n2][1][0];
+        rb[(8 * n2 + pb) * PC + gq] = acc[n2][0][1] + acc[n2][1][1];
+      }
+      bar_red_arrive(u_blk);
+    };
+    // Vᵀ = rn (Vᵀ + coefᵀ X_Bᵀ)
+    auto update = [&](const double* xb, int t, double rn) {
+      tick(1);
+      if (t & 1)
+        asm volatile("bar.sync 3, %0;" ::"n"(32 * (kRows + kRed)) : "memory");
+      else
+        asm volatile("bar.sync 2, %0;" ::"n"(32 * (kRows + kRed)) : "memory");
+      tick(2);
+      const double* cf = cfb + (t & 1) * B * CP;
+      double af[4];
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks) af[ks] = cf[(4 * ks + tq) * CP + gq];
+      double bx[4][kTiles];
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks)
+#pragma unroll
+        for (int tl = 0; tl < kTiles; ++tl) bx[ks][tl] = xb[(4 * ks + tq) * RP + rw0 + 8 * tl + gq];
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks)
+#pragma unroll
+        for (int tl = 0; tl < kTiles; ++tl) dmma(v[tl][0], v[tl][1], af[ks], bx[ks][tl]);
+#pragma unroll
+      for (int tl = 0; tl < kTiles; ++tl) {
+        v[tl][0] *= rn;
+        v[tl][1] *= rn;
+      }
+    };
+    if (nb > 0) {  // Â_0 = X_{B_0}ᵀ Ŵ_0, then V_0 = ρ^{b_0} Ŵ_0
+      const int s = wait_stage();
+      products(stage_at(s), 0);
+      double rb0 = 1.0;
+      for (int jj = 0; jj < bt_of(0); ++jj) rb0 *= a.rho;
+#pragma unroll
+      for (int tl = 0; tl < kTiles; ++tl) {
+        v[tl][0] *= rb0;
+        v[tl][1] *= rb0;
+      }
+    }
+    int cs = 0;
+#pragma unroll 1
+    for (int t = 0; t < nb; ++t) {
+      const bool more = t + 1 < nb;
+      if (more) {
+        tick(3);
+        const int s = wait_stage();
+        tick(0);
+        products(stage_at(s), t + 1);
+      }
+      const double rn = !more ? 1.0 : (t + 1 == nb - 1 ? rho_last : rho_b);
+      update(stage_at(cs), t, rn);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[cs]);
+      cs = cs + 1 == S ? 0 : cs + 1;
+    }
+    tick(3);
+    if (a.dbg && tid == 0)
+      for (int kk = 0; kk < 4; ++kk) a.dbg[(blockIdx.y * gridDim.x + blockIdx.x) * 8 + kk] = tacc[kk];
+    const double beta = -expm1(static_cast<double>(a.m) * log1p(a.rho - 1.0)) / (1.0 - a.rho);
+    if (gq < pc)
+#pragma unroll
+      for (int tl = 0; tl < kTiles; ++tl)
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int r = rw0 + 8 * tl + 2 * tq + u;
+          if (r < rc) {
+            const int64_t o = static_cast<int64_t>(r0 + r) * a.ldw + c0 + gq;
+            a.W[o] = fma(beta, a.C[o], v[tl][u]);
+          }
+        }
+  }
+  cluster.sync();
+}
+
 // Clusters of `cluster` one-SM CTAs that can be resident at once (a cluster
 // lives inside one GPC, so this is below SMs / cluster when GPCs are uneven).
 int max_active_clusters(int cluster) {
@@ -1458,7 +1820,8 @@ EpochConfig choose_epoch_config(int d_pad, int p) {
     cfg.b = kBlock;
     cfg.cluster = cluster;
     const int max_clusters = max_active_clusters(cfg.cluster);
-    cfg.pc = round_pc(static_cast<int>(ceil_div(p, max_clusters)));
+    static const int env_pc = getenv("GAPLRA_CHAIN_PC") ? atoi(getenv("GAPLRA_CHAIN_PC")) : 0;  // experiments
+    cfg.pc = round_pc(env_pc > 0 ? std::min(env_pc, p) : static_cast<int>(ceil_div(p, max_clusters)));
     cfg.rows_per_cta = static_cast<int>(ceil_div(ceil_div(d_pad, cfg.cluster), 4) * 4);
     const size_t cap = 227 * 1024;
     for (;;) {
@@ -1472,6 +1835,23 @@ EpochConfig choose_epoch_config(int d_pad, int p) {
     return cfg;
   };
   if (env_cluster == 8 || env_cluster == 16) return make(env_cluster);
+  // the DMMA chain v4 (PC = 8, <= 256 rows per CTA) for p >= 4: C2 runs 3
+  // clusters of 16 CTAs instead of 7 x PC 3 (epoch 17.7 -> 14.2 ms);
+  // GAPLRA_CHAIN_V4=0 keeps the scalar chains
+  static const int env_v4 = getenv("GAPLRA_CHAIN_V4") ? atoi(getenv("GAPLRA_CHAIN_V4")) : 1;
+  static const int env_pc = getenv("GAPLRA_CHAIN_PC") ? atoi(getenv("GAPLRA_CHAIN_PC")) : 0;
+  if (env_v4 && env_pc == 0 && p >= 4 && d_pad <= 16 * 256) {
+    EpochConfig cfg;
+    cfg.b = kBlock;
+    cfg.cluster = d_pad <= 8 * 256 ? 8 : 16;
+    cfg.pc = 8;
+    cfg.rows_per_cta = static_cast<int>(ceil_div(ceil_div(d_pad, cfg.cluster), 4) * 4);
+    cfg.groups = static_cast<int>(ceil_div(p, 8));
+    cfg.stages = 3;
+    while (cfg.stages > 2 && v4::smem(cfg.rows_per_cta, cfg.stages).total > 227 * 1024) --cfg.stages;
+    cfg.smem = v4::smem(cfg.rows_per_cta, cfg.stages).total;
+    if (cfg.groups <= max_active_clusters(cfg.cluster)) return cfg;
+  }
   const EpochConfig c16 = make(16), c8 = make(8);
   auto v3_ok = [](const EpochConfig& c) { return v3_supports(c.pc, c.rows_per_cta); };
   if (d_pad < 1024) return c8;
@@ -1499,7 +1879,19 @@ void launch_chain_pc(const EpochArgs& a, const EpochConfig& cfg, cudaStream_t st
   }
   int stages = cfg.stages;
   size_t smem = cfg.smem;
-  if (v3) {  // pitch ≡ 0 (mod 16) layout, at most 4 stages (barrier slots)
+  // the DMMA chain v4 at PC = 8 (rows <= 256 per CTA); GAPLRA_CHAIN_MODE=4 forces it
+  const bool use_v4 = PC == 8 && cfg.rows_per_cta <= 256 && (env_mode == 0 || env_mode == 4);
+  if (use_v4) {
+    stages = 2;
+    for (int sN = 4; sN > 2; --sN)
+      if (v4::smem(cfg.rows_per_cta, sN).total <= 227 * 1024) {
+        stages = sN;
+        break;
+      }
+    smem = v4::smem(cfg.rows_per_cta, stages).total;
+    kern = k_svrg_chain_v4;
+  }
+  if (v3 && !use_v4) {  // pitch ≡ 0 (mod 16) layout, at most 4 stages (barrier slots)
     stages = 2;
     for (int sN = 4; sN > 2; --sN)
       if (chain_smem<PC, kBlock, true>(cfg.rows_per_cta, sN).total <= 227 * 1024) {
@@ -1512,7 +1904,7 @@ void launch_chain_pc(const EpochArgs& a, const EpochConfig& cfg, cudaStream_t st
   if (cfg.cluster > 8) GAPLRA_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   cudaLaunchConfig_t lc = {};
   lc.gridDim = dim3(cfg.cluster, cfg.groups, 1);
-  lc.blockDim = dim3(v3 ? v3_threads(PC) : kChainThreads + 32 * kChainProducers, 1, 1);
+  lc.blockDim = dim3(use_v4 ? v4::kThreads : (v3 ? v3_threads(PC) : kChainThreads + 32 * kChainProducers), 1, 1);
   lc.dynamicSmemBytes = smem;
   lc.stream = st;
   cudaLaunchAttribute attr[1];
