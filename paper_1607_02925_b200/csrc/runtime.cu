@@ -488,6 +488,8 @@ void epoch_run_dev(Context& c, Matrix& X, int p, double* W, const double* C, con
     static const bool timing = getenv("GAPLRA_EPOCH_TIMING") != nullptr;
     static const int skip = getenv("GAPLRA_EPOCH_SKIP") ? atoi(getenv("GAPLRA_EPOCH_SKIP")) : 0;
     a.skip = skip;
+    static const int prefetch = getenv("GAPLRA_CHAIN_PREFETCH") ? atoi(getenv("GAPLRA_CHAIN_PREFETCH")) : 0;
+    a.prefetch = prefetch;
     DBuf<long long> dbg;
     if (timing) {
       a.dbg = dbg.ensure(static_cast<size_t>(cfg.cluster) * cfg.groups * 8);

@@ -418,6 +418,7 @@ __device__ __forceinline__ void consumers_sync() { asm volatile("bar.sync 1, %0;
 // turn), so kChainProducers warps share the columns.
 constexpr int kChainProducers = 4;
 
+
 template <int PC, int B, int NP = kChainProducers>
 __device__ __forceinline__ void chain_produce(const EpochArgs& a, int pw, int lane, int nb, int last_bt, int S, int rc,
                                               int r0, int RP, int grp, double* stages, size_t stage_len,
@@ -441,6 +442,19 @@ __device__ __forceinline__ void chain_produce(const EpochArgs& a, int pw, int la
       const int j = j0 + lane;
       tma_load_1d(st + j * RP, a.X + static_cast<int64_t>(__ldg(a.idx + static_cast<int64_t>(t) * B + j)) * a.ldx + r0,
                   rc * 8u, &full[s]);
+    }
+    // L2 prefetch of the same slices a.prefetch blocks ahead: the index
+    // stream is known for the whole epoch, so the ring's TMA loads hit L2
+    // instead of paying the DRAM latency with only S blocks in flight
+    if (a.prefetch > 0 && t + a.prefetch < nb && rc > 0 && lane < CPP) {
+      const int64_t tp = t + a.prefetch;
+      const int btp = tp == nb - 1 ? last_bt : B;
+      const int j = j0 + lane;
+      if (j < btp) {
+        const double* src = a.X + static_cast<int64_t>(__ldg(a.idx + tp * B + j)) * a.ldx + r0;
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(static_cast<uint32_t>(rc * 8u))
+                     : "memory");
+      }
     }
     if (pw == 0 && lane == 31) {
       const double* slab = a.slab + static_cast<int64_t>(t) * a.slab_len;
@@ -1045,7 +1059,9 @@ constexpr int kV3Producers = 2;  // producer warps
 // (they split the entries; measured p = 20 / PC = 3: one reducer warp was busy
 // 2818 of 2900 cycles per block)
 __host__ __device__ constexpr int v3_reducers(int pc) { return pc >= 2 ? 2 : 1; }
-__host__ __device__ constexpr int v3_threads(int pc) { return 32 * (kV3Rows + v3_reducers(pc) + kV3Producers); }
+// + one push warp: sums the row warps' partials and bulk-copies Â_{t+1} to the
+// peers, so the rows go straight from products(t+1) to update(t)
+__host__ __device__ constexpr int v3_threads(int pc) { return 32 * (kV3Rows + v3_reducers(pc) + 1 + kV3Producers); }
 // layouts the warp-specialised chain runs: 256 rows per CTA (H = 1, PC <= 3) or
 // 512 rows (H = 2, PC = 1: only there do three 512-row stages fit beside the
 // receive slots; with two, the stage re-read by the update would stall the ring)
@@ -1069,14 +1085,14 @@ __global__ void __launch_bounds__(v3_threads(PC), 1) k_svrg_chain_v3(EpochArgs a
   const int c0 = grp * PC;
   const int pc = min(PC, a.p - c0);
   const ChainSmem L = chain_smem<PC, B, true>(a.rows_per_cta, a.stages);
-  static_assert(kV3Rows * NV + 6 * NV <= kChainThreads / 32 * (B / 8) * 64, "red + coef + ahat + pre + outv fit");
+  static_assert(2 * kV3Rows * NV + 6 * NV <= kChainThreads / 32 * (B / 8) * 64, "red[2] + coef + ahat + pre + outv fit");
   const int S = L.stages;
   const int r0 = g * a.rows_per_cta;
   const int rc = max(0, min(a.rows_per_cta, a.d_pad - r0));
   const int RP = L.rows_pad;
   double* recv = sm + L.off_recv;  // [kRecvSlots][kMaxCluster][NV]
-  double* red = sm + L.off_red;    // [kV3Rows][NV]
-  double* coef = red + kV3Rows * NV;  // [2][NV]
+  double* red = sm + L.off_red;    // [2][kV3Rows][NV] (block parity)
+  double* coef = red + 2 * kV3Rows * NV;  // [2][NV]
   double* Ahat = coef + 2 * NV;       // [NV]
   double* pre = Ahat + NV;            // [NV]
   double* outv = pre + NV;            // [2][NV] this CTA's summed partials, bulk-copied to every peer
@@ -1114,9 +1130,34 @@ __global__ void __launch_bounds__(v3_threads(PC), 1) k_svrg_chain_v3(EpochArgs a
     }
   };
 
-  if (warp >= kV3Rows + NRD) {  // ----------------------------------------- producers
-    chain_produce<PC, B, kV3Producers>(a, warp - kV3Rows - NRD, lane, nb, last_bt, S, rc, r0, RP, grp,
+  if (warp >= kV3Rows + NRD + 1) {  // ------------------------------------- producers
+    chain_produce<PC, B, kV3Producers>(a, warp - kV3Rows - NRD - 1, lane, nb, last_bt, S, rc, r0, RP, grp,
                                        sm + L.off_stage, L.stage_len, full, empty);
+  } else if (warp == kV3Rows + NRD) {  // ---------------------------------- pusher
+    // Â_u: wait for the rows' red(u) (named barrier 5 / 6 by parity; the rows
+    // cannot arrive for u + 2 first, since products(u + 2) follows update(u),
+    // which needs Â_u from every peer, this one included), fixed-order sum of
+    // the 4 warp partials into outv[u & 1], one bulk copy per peer
+    for (int u = 0; u < nb; ++u) {
+      if (u & 1)
+        asm volatile("bar.sync 6, %0;" ::"n"(32 * (kV3Rows + 1)) : "memory");
+      else
+        asm volatile("bar.sync 5, %0;" ::"n"(32 * (kV3Rows + 1)) : "memory");
+      if (lane < G) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+      __syncwarp();
+      const double* rb = red + (u & 1) * kV3Rows * NV;
+      double* ov = outv + (u & 1) * NV;
+      for (int e = lane; e < NV; e += 32) ov[e] = (rb[e] + rb[NV + e]) + (rb[2 * NV + e] + rb[3 * NV + e]);
+      fence_proxy_async();
+      __syncwarp();
+      if (lane < G) {
+        const int par = u & (kRecvSlots - 1);
+        dsmem_bulk_copy(mapa(smem_u32(recv + (par * kMaxCluster + g) * NV), lane), smem_u32(ov), NV * 8u,
+                        mapa(smem_u32(&rbar[par]), lane));
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+    }
+    if (lane < G) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   } else if (warp >= kV3Rows) {  // ------------------------------------------ reducers
     const int rw = warp - kV3Rows;
     const int me = rw * EPW + lane;  // this lane's entry
@@ -1251,13 +1292,7 @@ __global__ void __launch_bounds__(v3_threads(PC), 1) k_svrg_chain_v3(EpochArgs a
         for (int i = 0; i < B; ++i)
           xr[h][i] = *reinterpret_cast<const double2*>(xb + (i ^ pm) * RP + ra + 256 * h);
     };
-    const bool issuer = lane < 4 && warp * 4 + lane < G;
-    const int peer = warp * 4 + lane;
-    auto push_prepare = [&]() {  // before the red barrier: the copies of two blocks ago no longer read their outv
-      if (issuer) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-    };
-    auto products = [&](const double2 (&xr)[H][B]) {
-      push_prepare();
+    auto products = [&](const double2 (&xr)[H][B], int u) {
       double val[B][PC];
 #pragma unroll
       for (int i = 0; i < B; ++i)
@@ -1276,25 +1311,14 @@ __global__ void __launch_bounds__(v3_threads(PC), 1) k_svrg_chain_v3(EpochArgs a
           for (int c = 0; c < PC; ++c) val[i][c] += __shfl_xor_sync(0xffffffffu, val[i + n][c], o);
 #pragma unroll
       for (int c = 0; c < PC; ++c) val[0][c] += __shfl_xor_sync(0xffffffffu, val[0][c], 1);
+      double* rb = red + (u & 1) * kV3Rows * NV;
       if (!(lane & 1))
 #pragma unroll
-        for (int c = 0; c < PC; ++c) red[warp * NV + pm * PC + c] = val[0][c];
-    };
-    auto rows_sync = []() { asm volatile("bar.sync 1, %0;" ::"n"(32 * kV3Rows) : "memory"); };
-    // push: the 4 warp partials summed in fixed order into outv, then lanes
-    // 0..3 of each row warp bulk-copy it to 4 peers (16-byte aligned, NV*8 bytes;
-    // entries of a ragged block's missing slices are finite and never summed)
-    auto push = [&](int u) {
-      const int par = u & (kRecvSlots - 1);
-      double* ov = outv + (u & 1) * NV;
-      if (tid < NV) ov[tid] = (red[tid] + red[NV + tid]) + (red[2 * NV + tid] + red[3 * NV + tid]);
-      fence_proxy_async();
-      rows_sync();
-      if (issuer) {
-        dsmem_bulk_copy(mapa(smem_u32(recv + (par * kMaxCluster + g) * NV), peer), smem_u32(ov), NV * 8u,
-                        mapa(smem_u32(&rbar[par]), peer));
-        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-      }
+        for (int c = 0; c < PC; ++c) rb[warp * NV + pm * PC + c] = val[0][c];
+      if (u & 1)  // red(u) complete for the pusher (barrier 5 / 6 by parity)
+        asm volatile("bar.arrive 6, %0;" ::"n"(32 * (kV3Rows + 1)) : "memory");
+      else
+        asm volatile("bar.arrive 5, %0;" ::"n"(32 * (kV3Rows + 1)) : "memory");
     };
     auto update = [&](const double2 (&xr)[H][B], int t, double rn) {
       if (t & 1)
@@ -1335,9 +1359,7 @@ __global__ void __launch_bounds__(v3_threads(PC), 1) k_svrg_chain_v3(EpochArgs a
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
       }
-      products(xa);
-      rows_sync();
-      push(0);
+      products(xa, 0);
       double rb = 1.0;
       for (int j = 0; j < bt_of(0); ++j) rb *= a.rho;
 #pragma unroll
@@ -1360,12 +1382,8 @@ __global__ void __launch_bounds__(v3_threads(PC), 1) k_svrg_chain_v3(EpochArgs a
           __syncwarp();
           if (lane == 0) mbar_arrive(&empty[s]);
         }
-        products(xq);
+        products(xq, t + 1);
         tick(1);
-        rows_sync();  // red complete (and the previous push's red reads done: they preceded the coef barrier)
-        tick(2);
-        push(t + 1);
-        tick(3);
       }
       const double rn = !more ? 1.0 : (t + 1 == nb - 1 ? rho_last : rho_b);
       if (XREG) {

@@ -26,6 +26,7 @@ struct EpochArgs {
   int rows_per_cta, stages, pc, groups;
   long long* dbg;  // optional per-CTA phase cycle counters (8 per CTA)
   int skip;        // debug ablation mask: 1 coef, 2 dots, 4 update (results invalid)
+  int prefetch;    // chain producers: L2-prefetch the slices this many blocks ahead (0: off)
 };
 
 struct SparseEpochArgs {
