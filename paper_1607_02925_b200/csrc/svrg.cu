@@ -392,7 +392,7 @@ __host__ __device__ inline ChainSmem chain_smem(int rows, int stages) {
   s.off_red = o;
   o += (kChainThreads / 32) * (B / 8) * 64;
   s.off_bar = o;
-  o += 12;
+  o += 20;  // full[8] | empty[8] | rbar[4]
   s.total = o * sizeof(double);
   return s;
 }
@@ -1097,8 +1097,8 @@ __global__ void __launch_bounds__(v3_threads(PC), 1) k_svrg_chain_v3(EpochArgs a
   double* pre = Ahat + NV;            // [NV]
   double* outv = pre + NV;            // [2][NV] this CTA's summed partials, bulk-copied to every peer
   uint64_t* full = reinterpret_cast<uint64_t*>(sm + L.off_bar);  // [S <= 4]
-  uint64_t* empty = full + 4;                                     // [S]
-  uint64_t* rbar = full + 8;                                      // [kRecvSlots]
+  uint64_t* empty = full + 8;                                     // [S <= 8]
+  uint64_t* rbar = full + 16;                                      // [kRecvSlots]
   auto stage_at = [&](int s_idx) { return sm + L.off_stage + static_cast<size_t>(s_idx) * L.stage_len; };
   const int nb = static_cast<int>((a.m + B - 1) / B);
   const int last_bt = static_cast<int>(a.m - static_cast<int64_t>(nb - 1) * B);
@@ -1909,9 +1909,10 @@ void launch_chain_pc(const EpochArgs& a, const EpochConfig& cfg, cudaStream_t st
     smem = v4::smem(cfg.rows_per_cta, stages).total;
     kern = k_svrg_chain_v4;
   }
-  if (v3 && !use_v4) {  // pitch ≡ 0 (mod 16) layout, at most 4 stages (barrier slots)
+  if (v3 && !use_v4) {  // pitch ≡ 0 (mod 16) layout; up to GAPLRA_CHAIN_STAGES (<= 8) stages as fit
+    static const int max_st = getenv("GAPLRA_CHAIN_STAGES") ? std::min(8, atoi(getenv("GAPLRA_CHAIN_STAGES"))) : 4;
     stages = 2;
-    for (int sN = 4; sN > 2; --sN)
+    for (int sN = max_st; sN > 2; --sN)
       if (chain_smem<PC, kBlock, true>(cfg.rows_per_cta, sN).total <= 227 * 1024) {
         stages = sN;
         break;
