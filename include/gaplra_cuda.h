@@ -59,7 +59,8 @@ typedef enum {
   GAPLRA_SHIFT_TUNING_STALLED = 6,     /* gaplra::ShiftTuningStalled (errors.hpp:73) */
   GAPLRA_NO_PRECONDITIONING_NEEDED = 7,/* SPEC.md:425 signal */
   GAPLRA_DEVICE_ERROR = 8,
-  GAPLRA_OUT_OF_MEMORY = 9
+  GAPLRA_OUT_OF_MEMORY = 9,
+  GAPLRA_NO_USABLE_GAP = 10            /* find_gap_budget */
 } gaplra_status;
 
 typedef struct gaplra_ctx gaplra_ctx;
@@ -126,6 +127,7 @@ typedef struct {
   double shift[64];
   gaplra_ledger ledger;
   double ms_total;
+  double delta; /* the gap budget used (supplied, or find_gap_budget's) */
 } gaplra_ap_report;
 
 /* Live per-kernel-class device time (CUDA events on the context stream) and
@@ -222,6 +224,11 @@ GAPLRA_API int gaplra_estimate_eigenvalues(gaplra_ctx* ctx, const gaplra_matrix*
                                            const gaplra_svrg_params* prm, double* values, int* iterations);
 /* approximate (Alg. 7) with the caller's gap budget cfg->delta:
  * W (d x k row-major), top-k Ritz values, the executed partition plan. */
+/* find_gap_budget: delta from Alg. 3 estimates of lambda_k and
+ * lambda_{p+1} at eps' = 1/100; GAPLRA_NO_USABLE_GAP without a gap. */
+GAPLRA_API int gaplra_find_gap_budget(gaplra_ctx* ctx, const gaplra_matrix* x, int k, int p, uint64_t seed,
+                                      double rq_tol, double* delta);
+/* cfg->delta <= 0: the gap budget comes from gaplra_find_gap_budget. */
 GAPLRA_API int gaplra_approximate(gaplra_ctx* ctx, const gaplra_matrix* x, const gaplra_si_config* cfg, double* w,
                                   double* ritz, gaplra_ap_report* rep);
 GAPLRA_API int gaplra_shift_invert(gaplra_ctx* ctx, const gaplra_matrix* x, const gaplra_si_config* cfg, double* w,

@@ -947,6 +947,22 @@ Block basis_extend(const Block& cur, const Block& nb) {
 // > 0.  Seeds: interval j uses derive_seed(seed, "intv" + j) as its root.
 // Final: restricted_projection(A, basis (d x p), k).
 constexpr uint64_t kTagInterval = 0x696e7476ull;  // "intv"
+constexpr uint64_t kTagGapBudget = 0x67617062ull;  // "gapb"
+
+// find_gap_budget (procedure pinned here):
+// Alg. 3 on A with p + 1 columns at eps' = 1/100 (seed derive_seed(seed,
+// "gapb")), Delta0 = lambda_hat_k - lambda_hat_{p+1}; NoUsableGap when
+// Delta0 <= 1e-14 lambda_hat_1; Delta = Delta0 / 1.5 (the contract Delta <=
+// lambda_k - lambda_{p+1} <= 2 Delta then holds while the two estimates are
+// within the +-1/3 band of the true gap).
+double find_gap_budget(const Mat& x, int k, int p, uint64_t seed, double rq_tol, orc_ledger* led, int nthreads) {
+  GramOp a(x, led, nthreads);
+  const std::vector<double> est = estimate_eigs(a, x.d(), p + 1, 0.01, derive_seed(seed, kTagGapBudget), rq_tol,
+                                                nullptr, led);
+  const double d0 = est[k - 1] - est[p];
+  if (!(d0 > 1e-14 * est[0])) throw Status(ORC_NO_USABLE_GAP);
+  return d0 / 1.5;
+}
 
 void approximate(const Mat& x, const orc_si_config* cfg, Block& w, std::vector<double>& ritz, orc_ap_report* rep,
                  int nthreads) {
@@ -957,6 +973,10 @@ void approximate(const Mat& x, const orc_si_config* cfg, Block& w, std::vector<d
     const int l = static_cast<int>(std::min(std::ceil(L), 1e9));
     return cfg->max_outer > 0 ? std::min(l, cfg->max_outer) : l;
   };
+  orc_si_config c2 = *cfg;
+  if (!(c2.delta > 0.0)) c2.delta = find_gap_budget(x, k, p, cfg->seed, cfg->rq_tol, &rep->ledger, nthreads);
+  rep->delta = c2.delta;
+  cfg = &c2;
   Block basis(d, 0);
   int64_t solves = 0;
   int s = 1;
@@ -1297,10 +1317,14 @@ int orc_estimate_eigenvalues(const orc_mat* x, int inverse, double lambda, int k
   });
 }
 
+int orc_find_gap_budget(const orc_mat* x, int k, int p, uint64_t seed, double rq_tol, double* delta, int nthreads) {
+  if (!valid(x) || k < 1 || p <= k || p + 1 > x->d || !delta) return ORC_CONTRACT_VIOLATION;
+  return guarded([&] { *delta = find_gap_budget(Mat(x), k, p, seed, rq_tol, nullptr, nthreads); });
+}
+
 int orc_approximate(const orc_mat* x, const orc_si_config* cfg, double* w, double* ritz, orc_ap_report* rep,
                     int nthreads) {
-  if (!valid(x) || !cfg || cfg->k < 1 || cfg->p <= cfg->k || cfg->p >= x->d || !(cfg->delta > 0.0))
-    return ORC_CONTRACT_VIOLATION;
+  if (!valid(x) || !cfg || cfg->k < 1 || cfg->p <= cfg->k || cfg->p >= x->d) return ORC_CONTRACT_VIOLATION;
   std::memset(rep, 0, sizeof(*rep));
   return guarded([&] {
     Block wb;

@@ -38,7 +38,8 @@ enum {
   ORC_SOLVER_STALLED = 4,
   ORC_SHIFT_OUT_OF_RANGE = 5,
   ORC_SHIFT_TUNING_STALLED = 6,
-  ORC_NO_PRECONDITIONING_NEEDED = 7
+  ORC_NO_PRECONDITIONING_NEEDED = 7,
+  ORC_NO_USABLE_GAP = 10 /* find_gap_budget */
 };
 
 /* X in R^{d x n}: kind 0 = dense column-major (ld = d), kind 1 = CSC
@@ -110,6 +111,7 @@ typedef struct {
   int s[64], q[64], strategy[64], width[64], iterations[64];
   double shift[64];
   orc_ledger ledger;
+  double delta; /* the gap budget used (supplied, or find_gap_budget's) */
 } orc_ap_report;
 
 /* ---- primitives (bit-exact restatements) ---- */
@@ -164,6 +166,7 @@ int orc_detect_additive_gap(const double* inv, int count, int s, int k, double d
 int orc_estimate_eigenvalues(const orc_mat* x, int inverse, double lambda, int k, double eps_prime, uint64_t seed,
                              double rq_tol, const orc_svrg_params* prm, double* values, int* iterations,
                              int nthreads);
+int orc_find_gap_budget(const orc_mat* x, int k, int p, uint64_t seed, double rq_tol, double* delta, int nthreads);
 int orc_approximate(const orc_mat* x, const orc_si_config* cfg, double* w_rowmajor, double* ritz,
                     orc_ap_report* rep, int nthreads);
 int orc_cg_solve(const orc_mat* x, double lambda, int p, const double* b_rowmajor, double* w_rowmajor,

@@ -60,7 +60,7 @@ PROF_CLASSES = ["gram", "epoch", "h_pass", "index", "qr", "anchor", "block_gram"
 class ApReport(C.Structure):
     _fields_ = [("n_intervals", C.c_int), ("s", C.c_int * 64), ("q", C.c_int * 64), ("strategy", C.c_int * 64),
                 ("width", C.c_int * 64), ("iterations", C.c_int * 64), ("shift", C.c_double * 64),
-                ("ledger", Ledger), ("ms_total", C.c_double)]
+                ("ledger", Ledger), ("ms_total", C.c_double), ("delta", C.c_double)]
 
 
 class Profile(C.Structure):
@@ -115,6 +115,7 @@ _SIGS = {
     "gaplra_detect_additive_gap": (C.c_int, [C.c_void_p, _dp, C.c_int, C.c_int, C.c_int, C.c_double, _ip]),
     "gaplra_estimate_eigenvalues": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_double, C.c_int, C.c_double,
                                               C.c_uint64, C.c_double, C.POINTER(SvrgParams), _dp, _ip]),
+    "gaplra_find_gap_budget": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_uint64, C.c_double, _dp]),
     "gaplra_approximate": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(SiConfig), _dp, _dp, C.POINTER(ApReport)]),
     "gaplra_cg_solve": (C.c_int, [C.c_void_p, C.c_void_p, C.c_double, C.c_int, _dp, _dp, C.c_double, C.c_int,
                                   _ip, _dp, C.c_int, _ip]),

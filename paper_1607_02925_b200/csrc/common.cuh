@@ -21,6 +21,7 @@ enum Status : int {
   kNoPreconditioningNeeded = 7,
   kDeviceError = 8,
   kOutOfMemory = 9,
+  kNoUsableGap = 10,
 };
 
 struct Error : std::runtime_error {

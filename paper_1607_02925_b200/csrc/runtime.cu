@@ -1155,13 +1155,30 @@ void principal_angles_dev(Context& c, int d, int k, const double* U, int p, doub
 // shifted systems are solved by CG; the first interval's by the configured
 // backend.  Finally restricted_projection(A, basis, k).
 constexpr uint64_t kTagInterval = 0x696e7476ull;  // "intv"
+constexpr uint64_t kTagGapBudget = 0x67617062ull;  // "gapb"
+
+// find_gap_budget (oracle.cpp find_gap_budget): Alg. 3 on A with p + 1 columns
+// at eps' = 1/100, Delta0 = lambda_hat_k - lambda_hat_{p+1}, Delta = Delta0 / 1.5.
+double find_gap_budget_dev(Context& c, Matrix& X, int k, int p, uint64_t seed, double rq_tol) {
+  if (k < 1 || p <= k || p + 1 > 64 || p + 1 > X.d)
+    throw Error(kContractViolation, "find_gap_budget: need 1 <= k < p, p + 1 <= min(d, 64)");
+  GramOp a(c, X);
+  const std::vector<double> est =
+      estimate_eigs_dev(c, a, X.d, X.d_pad(), p + 1, 0.01, derive_seed(seed, kTagGapBudget), rq_tol, nullptr);
+  const double d0 = est[k - 1] - est[p];
+  if (!(d0 > 1e-14 * est[0])) throw Error(kNoUsableGap, "find_gap_budget: no gap between lambda_k and lambda_{p+1}");
+  return d0 / 1.5;
+}
 
 void approximate_dev(Context& c, Matrix& X, const gaplra_si_config& cfg, double* W, double* ritz_host,
                      gaplra_ap_report& rep) {
   const int d = X.d, k = cfg.k, p = cfg.p;
   const int64_t dp = X.d_pad();
   if (k < 1 || p <= k || p >= d || p > 64) throw Error(kContractViolation, "approximate: need 1 <= k < p < d, p <= 64");
-  if (!(cfg.delta > 0.0)) throw Error(kContractViolation, "approximate: gap budget delta must be > 0");
+  gaplra_si_config cfg_d = cfg;
+  if (!(cfg_d.delta > 0.0)) cfg_d.delta = find_gap_budget_dev(c, X, k, p, cfg.seed, cfg.rq_tol);
+  rep.delta = cfg_d.delta;
+  const gaplra_si_config& cfgd = cfg_d;
   const double eps_int = cfg.eps / (3.0 * std::max(cfg.mu, 1.0) * k * d);
   const double lg = std::log(k * static_cast<double>(d) / eps_int);
   auto capped = [&](double L) {
@@ -1201,7 +1218,7 @@ void approximate_dev(Context& c, Matrix& X, const gaplra_si_config& cfg, double*
       std::memset(&tr, 0, sizeof(tr));
       bool shifted = true;
       try {
-        tune_shift_dev(c, X, cfg.delta, cj, &solves, tr, U, m);
+        tune_shift_dev(c, X, cfgd.delta, cj, &solves, tr, U, m);
       } catch (const Error& e) {
         if (e.code != kNoPreconditioningNeeded) throw;
         shifted = false;
@@ -1220,7 +1237,7 @@ void approximate_dev(Context& c, Matrix& X, const gaplra_si_config& cfg, double*
                                                            derive_seed(cj.seed, kTagEstD), cfg.rq_tol, nullptr);
         std::vector<double> inv(cnt);
         for (int i = 0; i < cnt; ++i) inv[i] = 1.0 / std::max(dest[i], 1e-300);
-        q = detect_additive_gap_host(inv.data(), cnt, s, k, cfg.delta);
+        q = detect_additive_gap_host(inv.data(), cnt, s, k, cfgd.delta);
         strategy = 1;
         width = q < k ? q - s + 1 : p - s + 1;
         S = sb.ensure(static_cast<size_t>(dp) * ldp_of(width));
@@ -1921,6 +1938,12 @@ int gaplra_approximate(gaplra_ctx* ctx, const gaplra_matrix* x, const gaplra_si_
     L.epochs = c.led.epochs - before.epochs;
     L.outer_iterations = c.led.outer_iterations - before.outer_iterations;
   });
+}
+
+int gaplra_find_gap_budget(gaplra_ctx* ctx, const gaplra_matrix* x, int k, int p, uint64_t seed, double rq_tol,
+                           double* delta) {
+  if (!ctx || !x || !delta) return GAPLRA_CONTRACT_VIOLATION;
+  return guard(ctx, [&] { *delta = find_gap_budget_dev(ctx->c, const_cast<gaplra_matrix*>(x)->m, k, p, seed, rq_tol); });
 }
 
 }  // extern "C"

@@ -63,6 +63,10 @@ class NoPreconditioningNeeded(Error):
     """tune_shift's guard signal."""
 
 
+class NoUsableGap(Error):
+    """find_gap_budget found no gap above the floor."""
+
+
 class DeviceError(Error):
     pass
 
@@ -72,7 +76,7 @@ class OutOfMemory(DeviceError):
 
 
 _CODES = {1: ContractViolation, 3: IndefiniteShift, 5: ShiftOutOfRange, 7: NoPreconditioningNeeded,
-          8: DeviceError, 9: OutOfMemory}
+          8: DeviceError, 9: OutOfMemory, 10: NoUsableGap}
 
 
 def _f64(a, shape=None):
@@ -435,12 +439,22 @@ class RankKProjection:
     plan: list
     ledger: dict
     ms: float
+    delta: float = 0.0  # the gap budget used
+
+
+def find_gap_budget(x: DeviceMatrix, k: int, p: int, seed: int = 0, rq_tol: float = 1e-3) -> float:
+    """find_gap_budget: Δ from Alg. 3 estimates of λ_k and
+    λ_{p+1} at ε′ = 1/100; NoUsableGap without a gap."""
+    delta = C.c_double()
+    x.ctx.check(x.ctx.lib.gaplra_find_gap_budget(x.ctx.h, x.h, k, p, seed, rq_tol, C.byref(delta)))
+    return delta.value
 
 
 def approximate(x: DeviceMatrix, cfg: SIConfig, error_iters: int = 20) -> RankKProjection:
     """Alg. 7: adaptive partition into PlainPower /
     ShiftedInverse intervals with deflation, then Alg. 2 on the concatenated
-    basis.  cfg.delta is the gap budget (Δ <= λ_k − λ_{p+1} <= 2Δ)."""
+    basis.  cfg.delta is the gap budget (Δ <= λ_k − λ_{p+1} <= 2Δ); with
+    cfg.delta <= 0 it comes from find_gap_budget."""
     w = np.zeros((x.d, cfg.k))
     ritz = np.zeros(cfg.k)
     rep = N.ApReport()
@@ -449,7 +463,7 @@ def approximate(x: DeviceMatrix, cfg: SIConfig, error_iters: int = 20) -> RankKP
                  width=rep.width[i], iterations=rep.iterations[i], shift=rep.shift[i])
             for i in range(min(rep.n_intervals, 64))]
     fr, sp = error_report(x, w, iters=error_iters, seed=cfg.seed)
-    return RankKProjection(w, ritz, fr, sp, plan, rep.ledger.as_dict(), rep.ms_total)
+    return RankKProjection(w, ritz, fr, sp, plan, rep.ledger.as_dict(), rep.ms_total, rep.delta)
 
 
 def estimate_top(x: DeviceMatrix, eps_prime: float, seed: int, *, inverse: bool = False, lam: float = 0.0,

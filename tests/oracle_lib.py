@@ -60,7 +60,7 @@ class OrcSiReport(C.Structure):
 class OrcApReport(C.Structure):
     _fields_ = [("n_intervals", C.c_int), ("s", C.c_int * 64), ("q", C.c_int * 64), ("strategy", C.c_int * 64),
                 ("width", C.c_int * 64), ("iterations", C.c_int * 64), ("shift", C.c_double * 64),
-                ("ledger", OrcLedger)]
+                ("ledger", OrcLedger), ("delta", C.c_double)]
 
     def plan(self):
         n = min(self.n_intervals, 64)
@@ -233,6 +233,12 @@ class Oracle:
                                                C.c_uint64(seed), C.c_double(rq_tol), C.byref(prm), _ptr(vals),
                                                C.byref(it), self.nthreads)
         return rc, vals, it.value
+
+    def find_gap_budget(self, m, k, p, seed=0, rq_tol=1e-3):
+        delta = C.c_double()
+        rc = self.lib.orc_find_gap_budget(C.byref(m), k, p, C.c_uint64(seed), C.c_double(rq_tol), C.byref(delta),
+                                          self.nthreads)
+        return rc, delta.value
 
     def approximate(self, m, cfg):
         w = np.zeros((m.d, cfg.k))

@@ -446,3 +446,21 @@ def test_approximate_deflated_intervals_device(g, oracle):
                              default_si_config(4, 7, eps=1e-4, delta=gap / 1.5, seed=4, force=1, max_outer=600))
     assert len(res.plan) >= 2 and res.plan[0]["strategy"] == "PlainPower"
     assert res.frobenius_error <= (1 + 1e-4) * np.sqrt(np.sum(sig[4:] ** 2))
+
+
+def test_find_gap_budget_device(g, oracle):
+    X, U, sig = planted_dense(300, 800, k=5, p=10, seed=21, noise=1e-3)
+    dd = g.find_gap_budget(g.DeviceMatrix.dense(X), 5, 10, seed=4)
+    rc, do = oracle.find_gap_budget(oracle.dense(X), 5, 10, seed=4)
+    assert rc == 0 and abs(dd - do) <= 1e-9 * do
+    lam = sig ** 2
+    assert dd <= lam[4] - lam[10] <= 2 * dd
+    with pytest.raises(g.NoUsableGap):
+        g.find_gap_budget(g.DeviceMatrix.dense(np.diag(np.sqrt([3.0, 2.0] + [1.0] * 8))), 3, 6, seed=1)
+
+
+def test_approximate_auto_delta_device(g, oracle):
+    X = np.diag([5.0, 4.0, 3.0, 2.0, 1.0])
+    res = _check_approximate(g, oracle, X, dict(k=2, p=3, eps=1e-3, delta=0.0, seed=1),
+                             default_si_config(2, 3, eps=1e-3, delta=0.0, seed=1))
+    assert 6.0 <= res.delta <= 12.0
