@@ -83,3 +83,23 @@ def test_missing_library_fails_loudly(tmp_path):
 
     with pytest.raises(ImportError):
         N.load(tmp_path / "nope.so")
+
+
+def test_binary_x_roundtrip(tmp_path):
+    # binary X + JSON spectrum sidecar (host side, no GPU)
+    from paper_1607_02925_b200 import xio
+    from problems import planted_dense, random_csc
+
+    X, _, sig = planted_dense(37, 53, seed=3)
+    side = xio.save_dense(tmp_path / "x.bin", X, sigma=sig.tolist(), k=3, p=6, seed=3)
+    Y, s2 = xio.load_dense(tmp_path / "x.bin")
+    assert np.array_equal(X, Y) and s2["sha256"] == side["sha256"] and s2["sigma"] == sig.tolist()
+    cp, ri, v = random_csc(40, 30, 5, seed=1)
+    xio.save_csc(tmp_path / "c.bin", 40, 30, cp, ri, v, note="csc")
+    (d, n, cp2, ri2, v2), _ = xio.load_csc(tmp_path / "c.bin")
+    assert (d, n) == (40, 30) and np.array_equal(cp, cp2) and np.array_equal(ri, ri2) and np.array_equal(v, v2)
+    raw = bytearray((tmp_path / "x.bin").read_bytes())
+    raw[8] ^= 1
+    (tmp_path / "x.bin").write_bytes(bytes(raw))
+    with pytest.raises(ValueError):
+        xio.load_dense(tmp_path / "x.bin")

@@ -464,3 +464,15 @@ def test_approximate_auto_delta_device(g, oracle):
     res = _check_approximate(g, oracle, X, dict(k=2, p=3, eps=1e-3, delta=0.0, seed=1),
                              default_si_config(2, 3, eps=1e-3, delta=0.0, seed=1))
     assert 6.0 <= res.delta <= 12.0
+
+
+def test_binary_x_to_device(g, tmp_path):
+    # streamed binary X -> HBM (column chunks), same gram pass as the in-memory upload
+    from paper_1607_02925_b200 import xio
+
+    X, _, sig = planted_dense(301, 777, seed=5)
+    xio.save_dense(tmp_path / "x.bin", X, sigma=sig.tolist())
+    x, side = xio.load_dense_device(tmp_path / "x.bin")
+    W = np.random.default_rng(0).standard_normal((301, 7))
+    assert np.array_equal(g.gram_block(x, W), g.gram_block(g.DeviceMatrix.dense(X), W))
+    assert side["sigma"] == sig.tolist()
