@@ -181,8 +181,10 @@ def test_svrg_epoch_lockstep(g, oracle, p):
 @pytest.mark.parametrize("d,n,p,m", [
     (4096, 300, 1, 1000),   # 16-CTA clusters x 256 rows, warp-specialised chain, PC = 1
     (4096, 300, 3, 1000),   # PC = 3, one column group, two reducer warps
-    (4096, 300, 20, 1000),  # C2 layout: 7 groups x PC 3
-    (2048, 300, 32, 1000),  # C3 layout: 8-CTA clusters x 256 rows, 11 groups x PC 3
+    (4096, 300, 20, 1000),  # C2 layout: tensor-core chain v4, 3 groups x PC 8 (last group 4 columns)
+    (2048, 300, 32, 1000),  # C3 layout: v4 on 8-CTA clusters x 256 rows, 4 groups
+    (4096, 300, 13, 1000),  # v4, ragged last group (5 columns)
+    (1000, 300, 10, 1000),  # C1 layout: v4 on 8-CTA clusters x 128 rows (half the row warps idle)
     (8192, 200, 1, 500),    # C5 layout, p = 1: 512 rows per CTA (scalar chain)
     (8192, 200, 64, 500),   # C5 layout: PC 6, two waves of clusters (DMMA chain)
 ])
