@@ -1858,7 +1858,9 @@ EpochConfig choose_epoch_config(int d_pad, int p) {
   // GAPLRA_CHAIN_V4=0 keeps the scalar chains
   static const int env_v4 = getenv("GAPLRA_CHAIN_V4") ? atoi(getenv("GAPLRA_CHAIN_V4")) : 1;
   static const int env_pc = getenv("GAPLRA_CHAIN_PC") ? atoi(getenv("GAPLRA_CHAIN_PC")) : 0;
-  if (env_v4 && env_pc == 0 && p >= 4 && d_pad <= 16 * 256) {
+  // (d <= 1024 keeps v3: with <= 128 rows per CTA half of v4's row warps idle;
+  // C1 measured 0.31 s with v4 against 0.28 s)
+  if (env_v4 && env_pc == 0 && p >= 4 && d_pad > 1024 && d_pad <= 16 * 256) {
     EpochConfig cfg;
     cfg.b = kBlock;
     cfg.cluster = d_pad <= 8 * 256 ? 8 : 16;

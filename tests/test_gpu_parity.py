@@ -184,7 +184,7 @@ def test_svrg_epoch_lockstep(g, oracle, p):
     (4096, 300, 20, 1000),  # C2 layout: tensor-core chain v4, 3 groups x PC 8 (last group 4 columns)
     (2048, 300, 32, 1000),  # C3 layout: v4 on 8-CTA clusters x 256 rows, 4 groups
     (4096, 300, 13, 1000),  # v4, ragged last group (5 columns)
-    (1000, 300, 10, 1000),  # C1 layout: v4 on 8-CTA clusters x 128 rows (half the row warps idle)
+    (1000, 300, 10, 1000),  # C1 layout (v3: d <= 1024)
     (8192, 200, 1, 500),    # C5 layout, p = 1: 512 rows per CTA (scalar chain)
     (8192, 200, 64, 500),   # C5 layout: PC 6, two waves of clusters (DMMA chain)
 ])
