@@ -28,6 +28,13 @@
 
 namespace cg = cooperative_groups;
 
+#ifndef V3_PROD1
+#define V3_PROD1 2
+#endif
+#ifndef V3_SLEEP
+#define V3_SLEEP 128
+#endif
+
 namespace gaplra_cuda {
 
 namespace {
@@ -67,7 +74,7 @@ __device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity
         : "r"(smem_u32(bar)), "r"(parity)
         : "memory");
     if (done) return;
-    __nanosleep(128);
+    __nanosleep(V3_SLEEP);
   }
 }
 __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
@@ -1054,14 +1061,16 @@ void launch_block_prep(const EpochArgs& a, const EpochConfig& cfg, cudaStream_t 
 // reducer can never arrive twice on one barrier phase.
 // ---------------------------------------------------------------------------
 constexpr int kV3Rows = 4;       // row warps
-constexpr int kV3Producers = 2;  // producer warps
+// producer warps: 4 at PC = 1 (each issues its lanes' bulk copies one after
+// another, so more warps raise the feed; PC > 1 needs the registers)
+__host__ __device__ constexpr int v3_producers(int pc) { return pc == 1 ? V3_PROD1 : 2; }
 // reducer warps: 2 once the block has more than 32 entries per column group
 // (they split the entries; measured p = 20 / PC = 3: one reducer warp was busy
 // 2818 of 2900 cycles per block)
 __host__ __device__ constexpr int v3_reducers(int pc) { return pc >= 2 ? 2 : 1; }
 // + one push warp: sums the row warps' partials and bulk-copies Â_{t+1} to the
 // peers, so the rows go straight from products(t+1) to update(t)
-__host__ __device__ constexpr int v3_threads(int pc) { return 32 * (kV3Rows + v3_reducers(pc) + 1 + kV3Producers); }
+__host__ __device__ constexpr int v3_threads(int pc) { return 32 * (kV3Rows + v3_reducers(pc) + 1 + v3_producers(pc)); }
 // layouts the warp-specialised chain runs: 256 rows per CTA (H = 1, PC <= 3) or
 // 512 rows (H = 2, PC = 1: only there do three 512-row stages fit beside the
 // receive slots; with two, the stage re-read by the update would stall the ring)
@@ -1110,7 +1119,7 @@ __global__ void __launch_bounds__(v3_threads(PC), 1) k_svrg_chain_v3(EpochArgs a
   for (size_t e = tid; e < L.off_v; e += blockDim.x) sm[e] = 0.0;  // pad rows / unwritten slices read as 0
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
-      mbar_init(&full[s], kV3Producers);
+      mbar_init(&full[s], v3_producers(PC));
       mbar_init(&empty[s], kV3Rows + NRD);
     }
     for (int q = 0; q < kRecvSlots; ++q) mbar_init(&rbar[q], 1);
@@ -1131,7 +1140,7 @@ __global__ void __launch_bounds__(v3_threads(PC), 1) k_svrg_chain_v3(EpochArgs a
   };
 
   if (warp >= kV3Rows + NRD + 1) {  // ------------------------------------- producers
-    chain_produce<PC, B, kV3Producers>(a, warp - kV3Rows - NRD - 1, lane, nb, last_bt, S, rc, r0, RP, grp,
+    chain_produce<PC, B, v3_producers(PC)>(a, warp - kV3Rows - NRD - 1, lane, nb, last_bt, S, rc, r0, RP, grp,
                                        sm + L.off_stage, L.stage_len, full, empty);
   } else if (warp == kV3Rows + NRD) {  // ---------------------------------- pusher
     // Â_u: wait for the rows' red(u) (named barrier 5 / 6 by parity; the rows
