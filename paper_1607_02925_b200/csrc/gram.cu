@@ -1224,6 +1224,198 @@ int clusters_for(const DenseX& X, int pc, const Plan& pl) {
 }  // namespace fused
 
 // ---------------------------------------------------------------------------
+// Z = X Y with X streamed through shared memory by a TMA producer warp
+// (cp.async.bulk column slices into a 3-6 stage ring, the 16 Y rows of the
+// tile in the same stage) and 8 DMMA warps — the single-pass kernel's phase B
+// without the cluster exchange.  CTA = 256 rows x a column range; the Z row
+// slice accumulates in registers; column splits write partials summed in
+// order by k_sum_splits.  Replaces k_xy_mma (X loaded straight into registers:
+// DRAM latency exposed at every 64-column chunk, long_scoreboard the top stall).
+// ---------------------------------------------------------------------------
+namespace xyt {
+
+constexpr int kNB = 16, kWarps = 8, kThreads = 32 * (kWarps + 1), kR = 256, kXP = kR + 4;
+
+struct Args {
+  const double* X;
+  int64_t ldx;
+  int n, rows_total;
+  const double* Y;
+  int64_t ldy;
+  int pc;
+  double* Z;
+  int64_t ldz;
+  size_t zstride;
+  int cols_per_split, stages;
+};
+
+__host__ __device__ inline int stage_len(int64_t ldy) { return kNB * kXP + static_cast<int>(kNB * ldy); }
+__host__ __device__ inline size_t smem_bytes(int64_t ldy, int stages) {
+  return (static_cast<size_t>(stage_len(ldy)) * stages + 16) * sizeof(double);
+}
+
+template <int NT>
+__global__ void __launch_bounds__(kThreads, 1) k_xy_tma(Args a) {
+  using namespace fused;
+  extern __shared__ __align__(128) double sm[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int gq = lane >> 2, tq = lane & 3;
+  const int S = a.stages, SL = stage_len(a.ldy);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + static_cast<size_t>(SL) * S);
+  uint64_t* empty = full + 8;
+  const int r0 = blockIdx.x * kR;
+  const int rc = max(0, min(kR, a.rows_total - r0));
+  const int j0 = blockIdx.y * a.cols_per_split;
+  const int j1 = min(j0 + a.cols_per_split, a.n);
+  const int T = j1 > j0 ? (j1 - j0 + kNB - 1) / kNB : 0;
+  for (size_t e = tid; e < static_cast<size_t>(SL) * S; e += blockDim.x) sm[e] = 0.0;
+  if (tid == 0) {
+    for (int q = 0; q < S; ++q) {
+      bar_init(&full[q], 1);
+      bar_init(&empty[q], kWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == kWarps) {  // ------------------------------------------------- producer
+    if (lane == 0)
+      for (int lt = 0; lt < T; ++lt) {
+        const int q = lt % S;
+        if (lt >= S) bar_wait_backoff(&empty[q], static_cast<uint32_t>(((lt / S) & 1) ^ 1));
+        const int j = j0 + lt * kNB;
+        const int nv = min(kNB, j1 - j);
+        bar_expect(&full[q], static_cast<uint32_t>(nv * (rc + a.ldy) * 8));
+        double* st = sm + static_cast<size_t>(q) * SL;
+        for (int c = 0; c < nv; ++c)
+          bulk_g2s(st + c * kXP, a.X + static_cast<int64_t>(j + c) * a.ldx + r0, static_cast<uint32_t>(rc * 8),
+                   &full[q]);
+        bulk_g2s(st + kNB * kXP, a.Y + static_cast<int64_t>(j) * a.ldy, static_cast<uint32_t>(nv * a.ldy * 8), &full[q]);
+      }
+    return;
+  }
+  double acc[2][2][NT][2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int e = 0; e < 2; ++e)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) acc[h][e][nt][0] = acc[h][e][nt][1] = 0.0;
+  const int rw = warp * 32 + 2 * gq;
+#pragma unroll 1
+  for (int lt = 0; lt < T; ++lt) {
+    const int q = lt % S;
+    bar_wait(&full[q], static_cast<uint32_t>((lt / S) & 1));
+    const double* xs = sm + static_cast<size_t>(q) * SL;
+    const double* ys = xs + kNB * kXP;
+    const int nv = min(kNB, j1 - (j0 + lt * kNB));
+#pragma unroll
+    for (int ks = 0; ks < kNB / 4; ++ks) {
+      const int k = 4 * ks + tq;
+      double b[NT];
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        const int c = nt * 8 + gq;
+        b[nt] = (k < nv && c < a.pc) ? ys[k * a.ldy + c] : 0.0;
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const double2 x2 = *reinterpret_cast<const double2*>(xs + k * kXP + rw + 16 * h);
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          mma884(acc[h][0][nt][0], acc[h][0][nt][1], x2.x, b[nt]);
+          mma884(acc[h][1][nt][0], acc[h][1][nt][1], x2.y, b[nt]);
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) bar_arrive(&empty[q]);
+  }
+  double* zb = a.Z + blockIdx.y * a.zstride;
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int row = warp * 32 + 16 * h + 2 * gq + e;
+      if (row >= rc) continue;
+      double* zo = zb + static_cast<int64_t>(r0 + row) * a.ldz;
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        const int c = nt * 8 + 2 * tq;
+        if (c + 1 < a.pc) {
+          zo[c] = acc[h][e][nt][0];
+          zo[c + 1] = acc[h][e][nt][1];
+        } else if (c < a.pc) {
+          zo[c] = acc[h][e][nt][0];
+        }
+      }
+    }
+}
+
+struct Plan {
+  int splits = 0, cols_per_split = 0, stages = 0;
+  size_t smem = 0;
+};
+
+inline Plan plan(const DenseX& X, int64_t ldy) {
+  Plan pl;
+  const int row_blocks = static_cast<int>(ceil_div(X.ld, kR));
+  int s = std::max(1, sm_count() / row_blocks);
+  pl.cols_per_split = static_cast<int>(ceil_div(ceil_div(X.n, s), kNB) * kNB);
+  pl.splits = static_cast<int>(ceil_div(X.n, pl.cols_per_split));
+  pl.stages = 6;
+  while (pl.stages > 2 && smem_bytes(ldy, pl.stages) > 227 * 1024) --pl.stages;
+  pl.smem = smem_bytes(ldy, pl.stages);
+  return pl;
+}
+
+template <int NT>
+void launch(const DenseX& X, const double* Y, int64_t ldy, int pc, double* Z, int64_t ldz, GramWork& work,
+            cudaStream_t st) {
+  const Plan pl = plan(X, ldy);
+  Args a;
+  a.X = X.x;
+  a.ldx = X.ld;
+  a.n = X.n;
+  a.rows_total = static_cast<int>(X.ld);
+  a.Y = Y;
+  a.ldy = ldy;
+  a.pc = pc;
+  a.cols_per_split = pl.cols_per_split;
+  a.stages = pl.stages;
+  const size_t stride = static_cast<size_t>(X.ld) * pc;
+  if (pl.splits == 1) {
+    a.Z = Z;
+    a.ldz = ldz;
+    a.zstride = 0;
+  } else {
+    if (work.part_elems < stride * pl.splits) throw Error(kContractViolation, "xy_tma: workspace too small");
+    a.Z = work.part;
+    a.ldz = pc;
+    a.zstride = stride;
+  }
+  static bool attr = false;
+  if (!attr) {
+    GAPLRA_CUDA_CHECK(cudaFuncSetAttribute(k_xy_tma<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    attr = true;
+  }
+  dim3 grid(static_cast<unsigned>(ceil_div(X.ld, kR)), pl.splits);
+  k_xy_tma<NT><<<grid, kThreads, pl.smem, st>>>(a);
+  GAPLRA_LAUNCH_CHECK();
+  if (pl.splits > 1) {
+    k_sum_splits<<<sm_count() * 4, 256, 0, st>>>(work.part, pl.splits, stride, static_cast<int>(X.ld), pc, pc, Z, ldz);
+    GAPLRA_LAUNCH_CHECK();
+  }
+}
+
+// applies to pc >= 2 with an even Y leading dimension (16-byte bulk copies of Y rows)
+inline bool applies(int pc, int64_t ldy) {
+  static const int mode = getenv("GAPLRA_XY_TMA") ? atoi(getenv("GAPLRA_XY_TMA")) : 1;
+  return mode != 0 && pc >= 2 && ldy % 2 == 0;
+}
+
+}  // namespace xyt
+
+// ---------------------------------------------------------------------------
 // Sparse (CSC for Xᵀ W, CSR for X Y): one thread per output row of Y / Z.
 // ---------------------------------------------------------------------------
 template <int NC>
@@ -1325,10 +1517,17 @@ __global__ void k_sum_max(const double* __restrict__ v, int n, double* __restric
 
 }  // namespace
 
+// the row-major block leading dimension the runtime uses (ldp_of: p rounded to even, 1 for p = 1)
+static int64_t ldp_even(int p) { return p == 1 ? 1 : (p + 1) / 2 * 2; }
+
 size_t gram_work_elems(const DenseX& X, int p) {
   size_t need = 0;
   for (int c0 = 0; c0 < p; c0 += 32) {
     const int pc = std::min(32, p - c0);
+    if (xyt::applies(pc, ldp_even(p))) {
+      const xyt::Plan xp = xyt::plan(X, ldp_even(p));
+      if (xp.splits > 1) need = std::max(need, static_cast<size_t>(xp.splits) * X.ld * pc);
+    }
     const fused::Plan fp = fused::plan(X, pc);
     if (fp.g) {  // (the two-pass needs below still apply: H = Xᵀ C runs launch_xtw alone)
       const int ncl = fused::clusters_for(X, pc, fp);
@@ -1398,6 +1597,15 @@ void launch_xy(const DenseX& X, const double* Y, int64_t ldy, int p, double* Z, 
                cudaStream_t st) {
   for (int c0 = 0; c0 < p; c0 += 32) {
     const int pc = std::min(32, p - c0);
+    if (p <= 32 && xyt::applies(pc, ldy)) {  // (chunks of a wider block would need a strided Y copy)
+      switch ((pc + 7) / 8) {
+        case 1: xyt::launch<1>(X, Y + c0, ldy, pc, Z + c0, ldz, work, st); break;
+        case 2: xyt::launch<2>(X, Y + c0, ldy, pc, Z + c0, ldz, work, st); break;
+        case 3: xyt::launch<3>(X, Y + c0, ldy, pc, Z + c0, ldz, work, st); break;
+        default: xyt::launch<4>(X, Y + c0, ldy, pc, Z + c0, ldz, work, st); break;
+      }
+      continue;
+    }
     if (use_mma(pc)) {
       const MmaPlan m = mma_plan(X);
       switch ((pc + 7) / 8) {
