@@ -1414,164 +1414,6 @@ inline bool applies(int pc, int64_t ldy) {
 }
 
 
-// Y = Xᵀ W the same way: CTA = 256 rows x a column range, W's row slice
-// resident in shared memory, X tiles through the TMA ring; warp = (8-column
-// m-tile, 64-row K quarter) as in the single-pass kernel's phase A, the four
-// quarters summed in fixed order, then one partial Y tile per row block
-// (row-block partials summed in order by k_sum_splits).
-template <int NT>
-__global__ void __launch_bounds__(kThreads, 1) k_xtw_tma(Args a) {
-  using namespace fused;
-  constexpr int NC8 = 8 * NT, BP = bp(NT), RQ = kR / 4;
-  extern __shared__ __align__(128) double sm[];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int gq = lane >> 2, tq = lane & 3;
-  const int S = a.stages, SL = kNB * kXP;
-  double* Ws = sm + static_cast<size_t>(SL) * S;  // [kR][BP]
-  double* red = Ws + kR * BP;                      // [4][kNB][NC8]
-  uint64_t* full = reinterpret_cast<uint64_t*>(red + 4 * kNB * NC8);
-  uint64_t* empty = full + 8;
-  const int r0 = blockIdx.x * kR;
-  const int rc = max(0, min(kR, a.rows_total - r0));
-  const int j0 = blockIdx.y * a.cols_per_split;
-  const int j1 = min(j0 + a.cols_per_split, a.n);
-  const int T = j1 > j0 ? (j1 - j0 + kNB - 1) / kNB : 0;
-  for (size_t e = tid; e < static_cast<size_t>(SL) * S + kR * BP; e += blockDim.x) sm[e] = 0.0;
-  __syncthreads();
-  for (int e = tid; e < rc * a.pc; e += blockDim.x) {  // W rows (a.Y / a.ldy carry W / ldw here)
-    const int r = e / a.pc, c = e - (e / a.pc) * a.pc;
-    Ws[r * BP + c] = a.Y[static_cast<int64_t>(r0 + r) * a.ldy + c];
-  }
-  if (tid == 0) {
-    for (int q = 0; q < S; ++q) {
-      bar_init(&full[q], 1);
-      bar_init(&empty[q], kWarps);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  if (warp == kWarps) {  // ------------------------------------------------- producer
-    if (lane == 0)
-      for (int lt = 0; lt < T; ++lt) {
-        const int q = lt % S;
-        if (lt >= S) bar_wait_backoff(&empty[q], static_cast<uint32_t>(((lt / S) & 1) ^ 1));
-        const int j = j0 + lt * kNB;
-        const int nv = min(kNB, j1 - j);
-        bar_expect(&full[q], static_cast<uint32_t>(nv * rc * 8));
-        double* st = sm + static_cast<size_t>(q) * SL;
-        for (int c = 0; c < nv; ++c)
-          bulk_g2s(st + c * kXP, a.X + static_cast<int64_t>(j + c) * a.ldx + r0, static_cast<uint32_t>(rc * 8),
-                   &full[q]);
-      }
-    return;
-  }
-  const int perm = ((gq & 1) << 1) | ((gq >> 1) & 1) | (gq & 4);  // 0 2 1 3 4 6 5 7
-  const int mt = warp / 4, kq = warp % 4;
-  double* out = a.Z + blockIdx.x * a.zstride;  // partial Y (n x ldz) of this row block
-#pragma unroll 1
-  for (int lt = 0; lt < T; ++lt) {
-    const int q = lt % S;
-    bar_wait(&full[q], static_cast<uint32_t>((lt / S) & 1));
-    const double* xs = sm + static_cast<size_t>(q) * SL + (mt * 8 + perm) * kXP + kq * RQ + 2 * tq;
-    const double* wsb = Ws + (kq * RQ + 2 * tq) * BP + gq;
-    double acc[2][NT][2];
-#pragma unroll
-    for (int ch = 0; ch < 2; ++ch)
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt) acc[ch][nt][0] = acc[ch][nt][1] = 0.0;
-#pragma unroll
-    for (int kb = 0; kb < RQ / 8; ++kb) {
-      const double2 av = *reinterpret_cast<const double2*>(xs + 8 * kb);
-#pragma unroll
-      for (int u = 0; u < 2; ++u)
-#pragma unroll
-        for (int nt = 0; nt < NT; ++nt)
-          mma884(acc[u][nt][0], acc[u][nt][1], u ? av.y : av.x, wsb[(8 * kb + u) * BP + nt * 8]);
-    }
-    __syncwarp();
-    if (lane == 0) bar_arrive(&empty[q]);
-    asm volatile("bar.sync 1, %0;" ::"n"(32 * kWarps) : "memory");  // previous tile's red reads done
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt)
-      *reinterpret_cast<double2*>(red + (kq * kNB + mt * 8 + perm) * NC8 + nt * 8 + 2 * tq) =
-          make_double2(acc[0][nt][0] + acc[1][nt][0], acc[0][nt][1] + acc[1][nt][1]);
-    asm volatile("bar.sync 1, %0;" ::"n"(32 * kWarps) : "memory");
-    const int j = j0 + lt * kNB;
-    const int nv = min(kNB, j1 - j);
-    for (int e = tid; e < kNB * a.pc; e += 32 * kWarps) {
-      const int col = e / a.pc, c = e - (e / a.pc) * a.pc;
-      if (col >= nv) continue;
-      const int o = col * NC8 + c;
-      out[static_cast<int64_t>(j + col) * a.ldz + c] = (red[o] + red[kNB * NC8 + o]) +
-                                                       (red[2 * kNB * NC8 + o] + red[3 * kNB * NC8 + o]);
-    }
-  }
-}
-
-inline size_t xtw_smem_bytes(int nt, int stages) {
-  return (static_cast<size_t>(kNB * kXP) * stages + kR * fused::bp(nt) + 4 * kNB * 8 * nt + 16) * sizeof(double);
-}
-
-inline Plan xtw_plan(const DenseX& X, int nt) {
-  Plan pl;
-  const int row_blocks = static_cast<int>(ceil_div(X.ld, kR));
-  int s = std::max(1, sm_count() / row_blocks);
-  pl.cols_per_split = static_cast<int>(ceil_div(ceil_div(X.n, s), kNB) * kNB);
-  pl.splits = static_cast<int>(ceil_div(X.n, pl.cols_per_split));
-  pl.stages = 6;
-  while (pl.stages > 2 && xtw_smem_bytes(nt, pl.stages) > 227 * 1024) --pl.stages;
-  pl.smem = xtw_smem_bytes(nt, pl.stages);
-  return pl;
-}
-
-template <int NT>
-void launch_xtw(const DenseX& X, const double* W, int64_t ldw, int pc, double* Y, int64_t ldy, GramWork& work,
-                cudaStream_t st) {
-  const Plan pl = xtw_plan(X, NT);
-  const int row_blocks = static_cast<int>(ceil_div(X.ld, kR));
-  Args a;
-  a.X = X.x;
-  a.ldx = X.ld;
-  a.n = X.n;
-  a.rows_total = static_cast<int>(X.ld);
-  a.Y = W;
-  a.ldy = ldw;
-  a.pc = pc;
-  a.cols_per_split = pl.cols_per_split;
-  a.stages = pl.stages;
-  const size_t stride = static_cast<size_t>(X.n) * pc;
-  if (row_blocks == 1) {
-    a.Z = Y;
-    a.ldz = ldy;
-    a.zstride = 0;
-  } else {
-    if (work.part_elems < stride * row_blocks) throw Error(kContractViolation, "xtw_tma: workspace too small");
-    a.Z = work.part;
-    a.ldz = pc;
-    a.zstride = stride;
-  }
-  static bool attr = false;
-  if (!attr) {
-    GAPLRA_CUDA_CHECK(cudaFuncSetAttribute(k_xtw_tma<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    attr = true;
-  }
-  dim3 grid(static_cast<unsigned>(row_blocks), pl.splits);
-  k_xtw_tma<NT><<<grid, kThreads, pl.smem, st>>>(a);
-  GAPLRA_LAUNCH_CHECK();
-  if (row_blocks > 1) {
-    k_sum_splits<<<sm_count() * 4, 256, 0, st>>>(work.part, row_blocks, stride, X.n, pc, pc, Y, ldy);
-    GAPLRA_LAUNCH_CHECK();
-  }
-}
-
-// off by default: the 16 row-block partials (2 x 256 MB at C2) and the per-tile
-// quarter sums make it slower than k_xtw_mma (C2 p = 20: 1.05 vs 0.86 ms);
-// GAPLRA_XTW_TMA=1 enables it
-inline bool xtw_applies(int pc) {
-  static const int mode = getenv("GAPLRA_XTW_TMA") ? atoi(getenv("GAPLRA_XTW_TMA")) : 0;
-  return mode != 0 && pc >= 3;
-}
-
 }  // namespace xyt
 
 // ---------------------------------------------------------------------------
@@ -1683,7 +1525,6 @@ size_t gram_work_elems(const DenseX& X, int p) {
   size_t need = 0;
   for (int c0 = 0; c0 < p; c0 += 32) {
     const int pc = std::min(32, p - c0);
-    if (xyt::xtw_applies(pc)) need = std::max(need, static_cast<size_t>(ceil_div(X.ld, xyt::kR)) * X.n * pc);
     if (xyt::applies(pc, ldp_even(p))) {
       const xyt::Plan xp = xyt::plan(X, ldp_even(p));
       if (xp.splits > 1) need = std::max(need, static_cast<size_t>(xp.splits) * X.ld * pc);
@@ -1739,15 +1580,7 @@ void launch_xtw(const DenseX& X, const double* W, int64_t ldw, int p, double* Y,
                 cudaStream_t st) {
   for (int c0 = 0; c0 < p; c0 += 32) {
     const int pc = std::min(32, p - c0);
-    if (xyt::xtw_applies(pc)) {
-      switch ((pc + 7) / 8) {
-        case 1: xyt::launch_xtw<1>(X, W + c0, ldw, pc, Y + c0, ldy, work, st); break;
-        case 2: xyt::launch_xtw<2>(X, W + c0, ldw, pc, Y + c0, ldy, work, st); break;
-        case 3: xyt::launch_xtw<3>(X, W + c0, ldw, pc, Y + c0, ldy, work, st); break;
-        default: xyt::launch_xtw<4>(X, W + c0, ldw, pc, Y + c0, ldy, work, st); break;
-      }
-      continue;
-    }
+
     if (use_mma(pc)) {
       const MmaPlan m = mma_plan(X);
       switch ((pc + 7) / 8) {
