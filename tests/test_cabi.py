@@ -38,13 +38,15 @@ def test_struct_layouts_match_header(tmp_path):
 
     src = tmp_path / "sz.c"
     src.write_text('#include "gaplra_cuda.h"\n#include <stdio.h>\n#include <stddef.h>\nint main(){printf("%zu %zu %zu %zu '
-                   '%zu %zu\\n", sizeof(gaplra_svrg_params), sizeof(gaplra_ledger), sizeof(gaplra_si_config), '
-                   'sizeof(gaplra_si_report), sizeof(gaplra_profile), offsetof(gaplra_si_report, ms_total));}\n')
+                   '%zu %zu %zu %zu %zu\\n", sizeof(gaplra_svrg_params), sizeof(gaplra_ledger), sizeof(gaplra_si_config), '
+                   'sizeof(gaplra_si_report), sizeof(gaplra_profile), offsetof(gaplra_si_report, ms_total), '
+                   'sizeof(gaplra_ap_report), offsetof(gaplra_ap_report, delta), offsetof(gaplra_si_config, backend));}\n')
     exe = tmp_path / "sz"
     subprocess.run(["gcc", "-I", str(ROOT / "include"), str(src), "-o", str(exe)], check=True)
     got = [int(v) for v in subprocess.run([str(exe)], capture_output=True, text=True).stdout.split()]
     want = [C.sizeof(N.SvrgParams), C.sizeof(N.Ledger), C.sizeof(N.SiConfig), C.sizeof(N.SiReport),
-            C.sizeof(N.Profile), N.SiReport.ms_total.offset]
+            C.sizeof(N.Profile), N.SiReport.ms_total.offset, C.sizeof(N.ApReport), N.ApReport.delta.offset,
+            N.SiConfig.backend.offset]
     assert got == want
 
 
