@@ -30,6 +30,7 @@
  * gaplra_detect_*_gap                  Alg. 4 / Alg. 5
  * gaplra_estimate_eigenvalues          estimate_eigenvalues, any k
  * gaplra_approximate                   approximate = Alg. 7
+ * gaplra_accsvrg_solve                 solve_accelerated_svrg
  * gaplra_cg_solve                      solve_cg / inverse_operator(cg)
  * gaplra_error_report                  error_report
  * gaplra_principal_angles              principal_angles
@@ -101,7 +102,7 @@ typedef struct {
   int epoch_cap;
   double monotone_slack;
   double lambda1_hint; /* with an explicit lambda: upper estimate of lambda_1 (0: none) */
-  int backend;         /* inverse_operator backend: 0 svrg, 1 cg */
+  int backend;         /* inverse_operator backend: 0 svrg, 1 cg, 2 accsvrg */
 } gaplra_si_config;
 
 typedef struct {
@@ -200,6 +201,11 @@ GAPLRA_API int gaplra_restricted_projection(gaplra_ctx* ctx, const gaplra_matrix
 /* solve_cg: block CG on (lambda I - X Xᵀ) W = B from W = 0,
  * per-column recurrences, stop when max_c |r_c|/|b_c| <= tol; max_iter <= 0:
  * d + 10.  IndefiniteShift on nonpositive curvature. */
+/* solve_accelerated_svrg: Catalyst outer loop around block
+ * SVRG (kappa = sqrt(h (lambda - h)), h = prm->lambda1_hint required). */
+GAPLRA_API int gaplra_accsvrg_solve(gaplra_ctx* ctx, const gaplra_matrix* x, double lambda, int p, const double* b,
+                                    double* w, const gaplra_svrg_params* prm, int64_t solve_id, int* epochs,
+                                    double* history, int hist_cap, int* hist_len);
 GAPLRA_API int gaplra_cg_solve(gaplra_ctx* ctx, const gaplra_matrix* x, double lambda, int p, const double* b,
                                double* w, double tol, int max_iter, int* iterations, double* history, int hist_cap,
                                int* hist_len);

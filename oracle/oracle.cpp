@@ -488,6 +488,66 @@ SolveResult svrg_solve(const Mat& x, double lambda, const Block& b, Block& w,
   return res;
 }
 
+// solve_accelerated_svrg (design :363): a Catalyst outer
+// loop around solve_svrg.  mu = lambda - h (h = prm->lambda1_hint, required),
+// kappa = sqrt(h mu), q = mu / (mu + kappa), beta = (1 - sqrt q) / (1 + sqrt q).
+// x = guess or 0, y = x; per outer step k: the residual of the original system
+// r = b - D x (one gram pass), stop when max_c |r_c| / |b_c| <= tol; else
+// x' = solve_svrg((lambda + kappa) I - X Xᵀ, b + kappa y) warm-started at x,
+// inner tol max(tol / 10, res / 10), stream ids (solve_id << 10) | k; then
+// y = x' + beta (x' - x), x = x'.  Outer cap ceil(200 ln(1/tol)).
+SolveResult accsvrg_solve(const Mat& x, double lambda, const Block& b, Block& w, const orc_svrg_params* prm,
+                          int64_t solve_id, orc_ledger* led, int nthreads, const Block* guess = nullptr) {
+  const int d = x.d(), p = b.p;
+  const double h = prm->lambda1_hint;
+  if (!(h > 0.0) || !(lambda > h)) throw Status(ORC_CONTRACT_VIOLATION);
+  const double mu = lambda - h, kappa = std::sqrt(h * mu), q = mu / (mu + kappa);
+  const double beta = (1.0 - std::sqrt(q)) / (1.0 + std::sqrt(q));
+  const int cap = prm->epoch_cap > 0 ? prm->epoch_cap : static_cast<int>(std::ceil(200.0 * std::log(1.0 / prm->tol)));
+  std::vector<double> bnorm(p);
+  for (int c = 0; c < p; ++c) {
+    double acc = 0.0;
+    for (int i = 0; i < d; ++i) acc += b.at(i, c) * b.at(i, c);
+    bnorm[c] = std::sqrt(acc);
+  }
+  Block xc = guess ? *guess : Block(d, p), yc = xc, z, rhs(d, p), xn;
+  SolveResult res;
+  for (int k = 0;; ++k) {
+    gram_block(x, xc, z, nullptr, nthreads);
+    if (led) led->gram_applies += p;
+    double r = 0.0;
+    for (int c = 0; c < p; ++c) {
+      double acc = 0.0;
+      for (int i = 0; i < d; ++i) {
+        const double rr = b.at(i, c) - (lambda * xc.at(i, c) - z.at(i, c));
+        acc += rr * rr;
+      }
+      const double rc = std::sqrt(acc) / (bnorm[c] > 0.0 ? bnorm[c] : 1.0);
+      r = std::isfinite(rc) ? std::max(r, rc) : rc;
+    }
+    res.history.push_back(r);
+    if (!std::isfinite(r)) throw Status(ORC_SOLVER_STALLED);
+    if (r <= prm->tol) break;
+    if (k >= cap) throw Status(ORC_SOLVER_STALLED);
+    for (int c = 0; c < p; ++c)
+      for (int i = 0; i < d; ++i) rhs.at(i, c) = b.at(i, c) + kappa * yc.at(i, c);
+    orc_svrg_params pin = *prm;
+    pin.tol = std::max(0.1 * prm->tol, 0.1 * r);
+    pin.epoch_cap = 0;
+    const SolveResult in = svrg_solve(x, lambda + kappa, rhs, xn, &pin, (solve_id << 10) | (k & 1023), led, nthreads,
+                                      &xc);
+    res.epochs += in.epochs;
+    for (int c = 0; c < p; ++c)
+      for (int i = 0; i < d; ++i) {
+        const double xv = xn.at(i, c);
+        yc.at(i, c) = xv + beta * (xv - xc.at(i, c));
+        xc.at(i, c) = xv;
+      }
+  }
+  w = xc;
+  return res;
+}
+
 // ---------------------------------------------------------------------------
 // Operators for the subspace engine.
 // ---------------------------------------------------------------------------
@@ -621,6 +681,22 @@ CgResult cg_solve(const Mat& x, double lambda, const Block& b, Block& w, double 
   if (led) led->linear_solves++;
   return res;
 }
+
+// inverse_operator(accsvrg, lambda) (backend = accsvrg)
+struct AccOp : BlockOp {
+  Mat x;
+  double lambda;
+  orc_svrg_params prm;
+  int64_t* solve_counter;
+  orc_ledger* led;
+  int nthreads;
+  AccOp(const Mat& xx, double lam, const orc_svrg_params& pr, int64_t* sc, orc_ledger* l, int nt)
+      : x(xx), lambda(lam), prm(pr), solve_counter(sc), led(l), nthreads(nt) {}
+  void apply(const Block& in, Block& out, const Block* guess = nullptr) override {
+    accsvrg_solve(x, lambda, in, out, &prm, (*solve_counter)++, led, nthreads, guess);
+    if (led) led->operator_applies += in.p;
+  }
+};
 
 // inverse_operator(cg, lambda) (backend = cg)
 struct CgOp : BlockOp {
@@ -1249,7 +1325,10 @@ int orc_shift_invert(const orc_mat* x, const orc_si_config* cfg, double* w, doub
     prm.lambda1_hint = rep->lambda1_hint;
     InverseOp dinv(m, rep->lambda, prm, &solves, &rep->ledger, nthreads);
     CgOp dcg(m, rep->lambda, cfg->tol_solve, 0, &rep->ledger, nthreads);
-    BlockOp& op = cfg->backend == 1 ? static_cast<BlockOp&>(dcg) : static_cast<BlockOp&>(dinv);
+    AccOp dacc(m, rep->lambda, prm, &solves, &rep->ledger, nthreads);
+    BlockOp& op = cfg->backend == 1   ? static_cast<BlockOp&>(dcg)
+                  : cfg->backend == 2 ? static_cast<BlockOp&>(dacc)
+                                      : static_cast<BlockOp&>(dinv);
     rep->outer_cap = outer_cap(cfg, x->d);
     Block s = subspace_iterate(op, x->d, cfg->p, rep->outer_cap, derive_seed(cfg->seed, kTagSubspace),
                                cfg->conv_tol, &rep->outer_iterations, &rep->ledger);
@@ -1333,6 +1412,23 @@ int orc_approximate(const orc_mat* x, const orc_si_config* cfg, double* w, doubl
     wb.to_rowmajor(w);
     std::copy(r.begin(), r.end(), ritz);
   });
+}
+
+int orc_accsvrg_solve(const orc_mat* x, double lambda, int p, const double* b, double* w,
+                      const orc_svrg_params* prm, int64_t solve_id, int* epochs, double* history, int hist_cap,
+                      int* hist_len, int nthreads) {
+  if (!valid(x) || p < 1 || !prm || !(prm->tol > 0.0)) return ORC_CONTRACT_VIOLATION;
+  SolveResult res;
+  int code = guarded([&] {
+    Block bb = Block::from_rowmajor(x->d, p, b), wb;
+    res = accsvrg_solve(Mat(x), lambda, bb, wb, prm, solve_id, nullptr, nthreads);
+    wb.to_rowmajor(w);
+  });
+  if (epochs) *epochs = res.epochs;
+  if (hist_len) *hist_len = static_cast<int>(res.history.size());
+  if (history)
+    for (int i = 0; i < std::min<int>(hist_cap, static_cast<int>(res.history.size())); ++i) history[i] = res.history[i];
+  return code;
 }
 
 int orc_cg_solve(const orc_mat* x, double lambda, int p, const double* b, double* w, double tol, int max_iter,

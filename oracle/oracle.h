@@ -89,7 +89,7 @@ typedef struct {
   int epoch_cap;      /* 0: spec cap                                       */
   double monotone_slack;
   double lambda1_hint; /* with an explicit lambda: upper estimate of lambda_1 (0: none) */
-  int backend;         /* inverse_operator backend: 0 svrg, 1 cg */
+  int backend;         /* inverse_operator backend: 0 svrg, 1 cg, 2 accsvrg */
 } orc_si_config;
 
 typedef struct {
@@ -169,6 +169,9 @@ int orc_estimate_eigenvalues(const orc_mat* x, int inverse, double lambda, int k
 int orc_find_gap_budget(const orc_mat* x, int k, int p, uint64_t seed, double rq_tol, double* delta, int nthreads);
 int orc_approximate(const orc_mat* x, const orc_si_config* cfg, double* w_rowmajor, double* ritz,
                     orc_ap_report* rep, int nthreads);
+int orc_accsvrg_solve(const orc_mat* x, double lambda, int p, const double* b_rowmajor, double* w_rowmajor,
+                      const orc_svrg_params* prm, int64_t solve_id, int* epochs, double* history, int hist_cap,
+                      int* hist_len, int nthreads);
 int orc_cg_solve(const orc_mat* x, double lambda, int p, const double* b_rowmajor, double* w_rowmajor,
                  double tol, int max_iter, int* iterations, double* history, int hist_cap, int* hist_len,
                  int nthreads);

@@ -117,6 +117,8 @@ _SIGS = {
                                               C.c_uint64, C.c_double, C.POINTER(SvrgParams), _dp, _ip]),
     "gaplra_find_gap_budget": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_uint64, C.c_double, _dp]),
     "gaplra_approximate": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(SiConfig), _dp, _dp, C.POINTER(ApReport)]),
+    "gaplra_accsvrg_solve": (C.c_int, [C.c_void_p, C.c_void_p, C.c_double, C.c_int, _dp, _dp, C.POINTER(SvrgParams),
+                                       C.c_int64, _ip, _dp, C.c_int, _ip]),
     "gaplra_cg_solve": (C.c_int, [C.c_void_p, C.c_void_p, C.c_double, C.c_int, _dp, _dp, C.c_double, C.c_int,
                                   _ip, _dp, C.c_int, _ip]),
     "gaplra_error_report": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, _dp, C.c_int, C.c_uint64, _dp, _dp]),

@@ -376,6 +376,16 @@ __global__ void k_symmetrize(double* __restrict__ H, int k) {
   }
 }
 
+// out = alpha A + beta B (d x p row-major blocks, leading dimension ld; out may alias A or B)
+__global__ void k_axpby(double alpha, const double* A, double beta, const double* Bm, double* out, int64_t ld, int d,
+                        int p) {
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < static_cast<int64_t>(d) * p;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t i = e / p, o = i * ld + (e - i * p);
+    out[o] = alpha * A[o] + beta * Bm[o];
+  }
+}
+
 }  // namespace
 
 void launch_qr_mgs2(double* Y, int64_t ldy, int d, int p, double* colmajor_scratch, int* status,
@@ -480,6 +490,12 @@ void launch_scale_inv_sqrt(double* v, int64_t ld, int d, int p, const double* s2
 void launch_symmetrize(double* H, int k, cudaStream_t st) {
   if (k < 2) return;
   k_symmetrize<<<1, 256, 0, st>>>(H, k);
+  GAPLRA_LAUNCH_CHECK();
+}
+
+void launch_axpby(double alpha, const double* A, double beta, const double* B, double* out, int64_t ld, int d, int p,
+                  cudaStream_t st) {
+  k_axpby<<<ew_grid(static_cast<int64_t>(d) * p), 256, 0, st>>>(alpha, A, beta, B, out, ld, d, p);
   GAPLRA_LAUNCH_CHECK();
 }
 

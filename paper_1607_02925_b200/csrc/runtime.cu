@@ -773,6 +773,91 @@ CgResult cg_solve_dev(Context& c, Matrix& X, double lambda, int p, const double*
   return out;
 }
 
+// solve_accelerated_svrg, the device form of oracle.cpp
+// accsvrg_solve: Catalyst outer loop (kappa = sqrt(h mu), extrapolation
+// beta = (1 - sqrt q)/(1 + sqrt q), q = mu/(mu + kappa)) around block SVRG
+// solves of (lambda + kappa) I - X Xᵀ, inner tol max(tol/10, res/10), stream
+// ids (solve_id << 10) | k, warm-started at the current iterate.
+SvrgResult accsvrg_solve_dev(Context& c, Matrix& X, double lambda, int p, const double* B, double* W,
+                             const gaplra_svrg_params& prm, int64_t solve_id, bool warm) {
+  const double h = prm.lambda1_hint;
+  if (!(h > 0.0) || !(lambda > h))
+    throw Error(kContractViolation, "solve_accelerated_svrg: needs lambda1_hint h > 0 and lambda > h");
+  const double mu = lambda - h, kappa = std::sqrt(h * mu), q = mu / (mu + kappa);
+  const double beta = (1.0 - std::sqrt(q)) / (1.0 + std::sqrt(q));
+  const int cap = prm.epoch_cap > 0 ? prm.epoch_cap : static_cast<int>(std::ceil(200.0 * std::log(1.0 / prm.tol)));
+  const int d = X.d;
+  const int64_t ld = ldp_of(p), dp = X.d_pad();
+  const size_t blk = static_cast<size_t>(dp) * ld;
+  DBuf<double> xb, yb, rb, zb, qb, nb;
+  double* xc = xb.ensure(blk);
+  double* yc = yb.ensure(blk);
+  double* rhs = rb.ensure(blk);
+  double* Zg = zb.ensure(blk);
+  double* Q = qb.ensure(blk);
+  double* xn = nb.ensure(blk);
+  if (warm)
+    GAPLRA_CUDA_CHECK(cudaMemcpyAsync(xc, W, blk * sizeof(double), cudaMemcpyDeviceToDevice, c.st));
+  else
+    GAPLRA_CUDA_CHECK(cudaMemsetAsync(xc, 0, blk * sizeof(double), c.st));
+  GAPLRA_CUDA_CHECK(cudaMemcpyAsync(yc, xc, blk * sizeof(double), cudaMemcpyDeviceToDevice, c.st));
+  double* part = c.tmp.ensure(static_cast<size_t>(small_gram_parts(d)) * 64 + 8);
+  double* nv = c.scal.ensure(8 + 2 * 64) + 8;
+  launch_col_dots(B, ld, B, ld, d, p, part, nv, c.st);
+  GAPLRA_CUDA_CHECK(cudaMemcpyAsync(c.pin, nv, p * sizeof(double), cudaMemcpyDeviceToHost, c.st));
+  c.sync();
+  std::vector<double> bnorm(p);
+  for (int k = 0; k < p; ++k) bnorm[k] = std::sqrt(c.pin[k]);
+  SvrgResult out;
+  for (int k = 0;; ++k) {
+    gram_block_dev(c, X, p, xc, ld, Zg, ld, nullptr, 0);
+    launch_cg_dq(xc, Zg, lambda, Q, ld, d, p, c.st);  // Q = D x
+    launch_cg_dq(B, Q, 1.0, rhs, ld, d, p, c.st);     // r = b - D x (in rhs)
+    launch_col_dots(rhs, ld, rhs, ld, d, p, part, nv, c.st);
+    GAPLRA_CUDA_CHECK(cudaMemcpyAsync(c.pin, nv, p * sizeof(double), cudaMemcpyDeviceToHost, c.st));
+    c.sync();
+    double r = 0.0;
+    for (int j = 0; j < p; ++j) {
+      const double rj = std::sqrt(c.pin[j]) / (bnorm[j] > 0.0 ? bnorm[j] : 1.0);
+      r = std::isfinite(rj) ? std::max(r, rj) : rj;
+    }
+    out.history.push_back(r);
+    if (!std::isfinite(r)) throw Error(kSolverStalled, "solve_accelerated_svrg: non-finite residual");
+    if (r <= prm.tol) break;
+    if (k >= cap) throw Error(kSolverStalled, "solve_accelerated_svrg: outer cap reached");
+    launch_axpby(1.0, B, kappa, yc, rhs, ld, d, p, c.st);  // b + kappa y
+    gaplra_svrg_params pin = prm;
+    pin.tol = std::max(0.1 * prm.tol, 0.1 * r);
+    pin.epoch_cap = 0;
+    GAPLRA_CUDA_CHECK(cudaMemcpyAsync(xn, xc, blk * sizeof(double), cudaMemcpyDeviceToDevice, c.st));
+    const SvrgResult in = svrg_solve_dev(c, X, lambda + kappa, p, rhs, xn, pin, (solve_id << 10) | (k & 1023), nullptr,
+                                         true);
+    out.epochs += in.epochs;
+    launch_axpby(1.0 + beta, xn, -beta, xc, yc, ld, d, p, c.st);  // y = x' + beta (x' - x)
+    GAPLRA_CUDA_CHECK(cudaMemcpyAsync(xc, xn, blk * sizeof(double), cudaMemcpyDeviceToDevice, c.st));
+  }
+  GAPLRA_CUDA_CHECK(cudaMemcpyAsync(W, xc, blk * sizeof(double), cudaMemcpyDeviceToDevice, c.st));
+  return out;
+}
+
+// inverse_operator(accsvrg, lambda)
+struct AccOp : Op {
+  Context& c;
+  Matrix& X;
+  double lambda;
+  gaplra_svrg_params prm;
+  int64_t* counter;
+  AccOp(Context& cc, Matrix& xx, double lam, const gaplra_svrg_params& pr, int64_t* sc)
+      : c(cc), X(xx), lambda(lam), prm(pr), counter(sc) {}
+  void apply(const double* in, double* out, int p, const double* guess = nullptr) override {
+    if (guess)
+      GAPLRA_CUDA_CHECK(cudaMemcpyAsync(out, guess, static_cast<size_t>(X.d_pad()) * ldp_of(p) * sizeof(double),
+                                        cudaMemcpyDeviceToDevice, c.st));
+    accsvrg_solve_dev(c, X, lambda, p, in, out, prm, (*counter)++, guess != nullptr);
+    c.led.operator_applies += p;
+  }
+};
+
 // inverse_operator(cg, lambda)
 struct CgOp : Op {
   Context& c;
@@ -1793,7 +1878,8 @@ int gaplra_shift_invert(gaplra_ctx* ctx, const gaplra_matrix* x, const gaplra_si
       prm.lambda1_hint = rep->lambda1_hint;
       InverseOp dinv(c, X, rep->lambda, prm, &solves);
       CgOp dcg(c, X, rep->lambda, cfg->tol_solve);
-      Op& op = cfg->backend == 1 ? static_cast<Op&>(dcg) : static_cast<Op&>(dinv);
+      AccOp dacc(c, X, rep->lambda, prm, &solves);
+      Op& op = cfg->backend == 1 ? static_cast<Op&>(dcg) : cfg->backend == 2 ? static_cast<Op&>(dacc) : static_cast<Op&>(dinv);
       rep->outer_cap = outer_cap(*cfg, X.d);
       rep->outer_iterations = subspace_iterate_dev(c, op, X.d, dp, p, rep->outer_cap,
                                                    derive_seed(cfg->seed, kTagSubspace), cfg->conv_tol, S);
@@ -1944,6 +2030,31 @@ int gaplra_find_gap_budget(gaplra_ctx* ctx, const gaplra_matrix* x, int k, int p
                            double* delta) {
   if (!ctx || !x || !delta) return GAPLRA_CONTRACT_VIOLATION;
   return guard(ctx, [&] { *delta = find_gap_budget_dev(ctx->c, const_cast<gaplra_matrix*>(x)->m, k, p, seed, rq_tol); });
+}
+
+int gaplra_accsvrg_solve(gaplra_ctx* ctx, const gaplra_matrix* x, double lambda, int p, const double* b, double* w,
+                         const gaplra_svrg_params* prm, int64_t solve_id, int* epochs, double* history, int hist_cap,
+                         int* hist_len) {
+  if (!ctx || !x || !prm) return GAPLRA_CONTRACT_VIOLATION;
+  return guard(ctx, [&] {
+    require(p >= 1 && p <= 64 && b && w && prm->tol > 0.0, "solve_accelerated_svrg: bad arguments");
+    require(all_finite(b, static_cast<size_t>(x->m.d) * p), "solve_accelerated_svrg: non-finite right-hand side");
+    Context& c = ctx->c;
+    Matrix& X = const_cast<gaplra_matrix*>(x)->m;
+    const int64_t ld = ldp_of(p), dp = X.d_pad();
+    DBuf<double> bd, wd;
+    bd.ensure(static_cast<size_t>(dp) * ld);
+    wd.ensure(static_cast<size_t>(dp) * ld);
+    GAPLRA_CUDA_CHECK(cudaMemsetAsync(bd.p, 0, static_cast<size_t>(dp) * ld * sizeof(double), c.st));
+    upload_block(c, b, X.d, p, bd.p, ld);
+    const SvrgResult r = accsvrg_solve_dev(c, X, lambda, p, bd.p, wd.p, *prm, solve_id, false);
+    download_block(c, wd.p, ld, X.d, p, w);
+    c.sync();
+    if (epochs) *epochs = r.epochs;
+    if (hist_len) *hist_len = static_cast<int>(r.history.size());
+    if (history)
+      for (int i = 0; i < std::min<int>(hist_cap, static_cast<int>(r.history.size())); ++i) history[i] = r.history[i];
+  });
 }
 
 }  // extern "C"

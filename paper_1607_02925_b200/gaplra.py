@@ -353,6 +353,25 @@ def solve_svrg(x: DeviceMatrix, lam: float, b: np.ndarray, tol: float, seed: int
     return SolverReport(w, ep.value, ep.value * m, history[-1] if history else float("nan"), history)
 
 
+def solve_accelerated_svrg(x: DeviceMatrix, lam: float, b: np.ndarray, tol: float, lambda1_hint: float,
+                           seed: int = 0, solve_id: int = 0, epoch_cap: int = 0) -> SolverReport:
+    """solve_accelerated_svrg: Catalyst outer loop around the
+    block SVRG solve; needs the caller's λ₁ hint."""
+    b = _f64(b)
+    if b.ndim == 1:
+        b = b[:, None]
+    p = b.shape[1]
+    w = np.zeros_like(b)
+    prm = N.SvrgParams(0.0, 0, tol, epoch_cap, 10.0, seed, lambda1_hint)
+    ep, hl = C.c_int(0), C.c_int(0)
+    hist = np.zeros(8192)
+    rc = x.ctx.lib.gaplra_accsvrg_solve(x.ctx.h, x.h, lam, p, _p(b), _p(w), C.byref(prm), solve_id, C.byref(ep),
+                                        _p(hist), 8192, C.byref(hl))
+    history = hist[:hl.value].tolist()
+    x.ctx.check(rc, history)
+    return SolverReport(w, ep.value, ep.value * 2 * x.n, history[-1] if history else float("nan"), history)
+
+
 def solve_cg(x: DeviceMatrix, lam: float, b: np.ndarray, tol: float, max_iter: int = 0) -> SolverReport:
     """Block CG solve of (λI − XXᵀ)W = B; column_samples = 0
     and `epochs` counts CG iterations."""
@@ -497,14 +516,15 @@ class SIConfig:
     epoch_cap: int = 0
     monotone_slack: float = 10.0
     lambda1_hint: float = 0.0
-    backend: str = "svrg"  # inverse_operator backend: "svrg" | "cg"
+    backend: str = "svrg"  # inverse_operator backend: "svrg" | "cg" | "accsvrg"
 
     def native(self) -> N.SiConfig:
-        if self.backend not in ("svrg", "cg"):
-            raise ContractViolation(f"unknown solver backend {self.backend!r} (svrg | cg)")
+        if self.backend not in ("svrg", "cg", "accsvrg"):
+            raise ContractViolation(f"unknown solver backend {self.backend!r} (svrg | cg | accsvrg)")
         return N.SiConfig(self.k, self.p, self.eps, self.mu, self.delta, self.lam, self.seed, self.tol_solve,
                           self.tol_tune, self.conv_tol, self.rq_tol, self.max_outer, int(self.force),
-                          self.epoch_cap, self.monotone_slack, self.lambda1_hint, int(self.backend == "cg"))
+                          self.epoch_cap, self.monotone_slack, self.lambda1_hint,
+                          {"svrg": 0, "cg": 1, "accsvrg": 2}[self.backend])
 
 
 @dataclass

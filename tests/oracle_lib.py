@@ -247,6 +247,17 @@ class Oracle:
         rc = self.lib.orc_approximate(C.byref(m), C.byref(cfg), _ptr(w), _ptr(ritz), C.byref(rep), self.nthreads)
         return rc, w, ritz, rep
 
+    def accsvrg_solve(self, m, lam, b, tol, seed=0, solve_id=0, hint=0.0, epoch_cap=0):
+        b = c64(b)
+        w = np.zeros_like(b)
+        prm = OrcSvrgParams(0.0, 0, tol, epoch_cap, 10.0, seed, hint)
+        ep, hl = C.c_int(0), C.c_int(0)
+        hist = np.zeros(8192)
+        rc = self.lib.orc_accsvrg_solve(C.byref(m), C.c_double(lam), b.shape[1], _ptr(b), _ptr(w), C.byref(prm),
+                                        C.c_int64(solve_id), C.byref(ep), _ptr(hist), 8192, C.byref(hl),
+                                        self.nthreads)
+        return rc, w, ep.value, hist[:hl.value]
+
     def cg_solve(self, m, lam, b, tol, max_iter=0):
         b = c64(b)
         w = np.zeros_like(b)

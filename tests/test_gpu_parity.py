@@ -478,3 +478,21 @@ def test_binary_x_to_device(g, tmp_path):
     W = np.random.default_rng(0).standard_normal((301, 7))
     assert np.array_equal(g.gram_block(x, W), g.gram_block(g.DeviceMatrix.dense(X), W))
     assert side["sigma"] == sig.tolist()
+
+
+def test_accelerated_svrg_device(g, oracle):
+    X, U, sig = planted_dense(300, 900, seed=31)
+    l1 = sig[0] ** 2
+    lam = 1.02 * l1
+    b = np.random.default_rng(3).standard_normal((300, 4))
+    r = g.solve_accelerated_svrg(g.DeviceMatrix.dense(X), lam, b, 1e-10, lambda1_hint=l1, seed=2)
+    rc, wo, ep, _ = oracle.accsvrg_solve(oracle.dense(X), lam, b, 1e-10, seed=2, hint=l1)
+    assert rc == 0 and abs(r.epochs - ep) <= max(2, ep // 20)
+    ref = np.linalg.solve(lam * np.eye(300) - X @ X.T, b)
+    assert rel(r.solution, ref) <= 1e-8 and rel(r.solution, wo) <= 1e-8
+    # inside the pipeline (backend accsvrg) the subspace matches the svrg backend's
+    x = g.DeviceMatrix.dense(X)
+    kw = dict(k=3, p=6, lam=l1 + 0.05, seed=2, max_outer=80, lambda1_hint=l1)
+    ra = g.shift_invert(x, g.SIConfig(backend="accsvrg", **kw))
+    rs_ = g.shift_invert(x, g.SIConfig(**kw))
+    assert oracle.sin_theta(ra.W, rs_.W) <= 1e-7
