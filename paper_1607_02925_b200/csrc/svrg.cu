@@ -1071,15 +1071,24 @@ __host__ __device__ constexpr int v3_reducers(int pc) { return pc >= 2 ? 2 : 1; 
 // + one push warp: sums the row warps' partials and bulk-copies Â_{t+1} to the
 // peers, so the rows go straight from products(t+1) to update(t)
 __host__ __device__ constexpr int v3_threads(int pc) { return 32 * (kV3Rows + v3_reducers(pc) + 1 + v3_producers(pc)); }
+// RR layout (PC = 1, 256 rows): three warpgroups — rows (warps 0-3, registers
+// raised to 232 by setmaxnreg), reducer + pusher + 2 idle (warps 4-7), four
+// producers (warps 8-11, lowered to 40) — so four producer warps feed the ring
+// without capping the rows' register-resident update
+constexpr int kV3RRThreads = 384;
+template <bool RR>
+__host__ __device__ constexpr int v3_block(int pc) { return RR ? kV3RRThreads : v3_threads(pc); }
 // layouts the warp-specialised chain runs: 256 rows per CTA (H = 1, PC <= 3) or
 // 512 rows (H = 2, PC = 1: only there do three 512-row stages fit beside the
 // receive slots; with two, the stage re-read by the update would stall the ring)
 inline bool v3_supports(int pc, int rows) { return pc <= 3 && (rows <= 256 || (rows <= 512 && pc == 1)); }
 
 // H: 256-row halves per row thread (rows 2·tid + {0,1} + 256·h): 256·H rows per CTA.
-template <int PC, int B, int H = 1>
-__global__ void __launch_bounds__(v3_threads(PC), 1) k_svrg_chain_v3(EpochArgs a) {
+template <int PC, int B, int H = 1, bool RR = false>
+__global__ void __launch_bounds__(v3_block<RR>(PC), 1) k_svrg_chain_v3(EpochArgs a) {
   static_assert(B == 16, "lane permutation j = i ^ (lane >> 1) covers 16 slices");
+  static_assert(!RR || PC == 1, "RR layout: PC = 1");
+  constexpr int NPROD = RR ? 4 : v3_producers(PC);
   constexpr bool XREG = PC == 1 && H == 1;  // update from the products' registers (else re-read the stage)
   extern __shared__ __align__(128) double sm[];
   cg::cluster_group cluster = cg::this_cluster();
@@ -1119,7 +1128,7 @@ __global__ void __launch_bounds__(v3_threads(PC), 1) k_svrg_chain_v3(EpochArgs a
   for (size_t e = tid; e < L.off_v; e += blockDim.x) sm[e] = 0.0;  // pad rows / unwritten slices read as 0
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
-      mbar_init(&full[s], v3_producers(PC));
+      mbar_init(&full[s], NPROD);
       mbar_init(&empty[s], kV3Rows + NRD);
     }
     for (int q = 0; q < kRecvSlots; ++q) mbar_init(&rbar[q], 1);
@@ -1139,9 +1148,12 @@ __global__ void __launch_bounds__(v3_threads(PC), 1) k_svrg_chain_v3(EpochArgs a
     }
   };
 
-  if (warp >= kV3Rows + NRD + 1) {  // ------------------------------------- producers
-    chain_produce<PC, B, v3_producers(PC)>(a, warp - kV3Rows - NRD - 1, lane, nb, last_bt, S, rc, r0, RP, grp,
-                                       sm + L.off_stage, L.stage_len, full, empty);
+  constexpr int kFirstProd = RR ? 8 : kV3Rows + NRD + 1;
+  if (warp >= kFirstProd) {  // ------------------------------------------- producers
+    if constexpr (RR) asm volatile("setmaxnreg.dec.sync.aligned.u32 40;" ::: "memory");
+    chain_produce<PC, B, NPROD>(a, warp - kFirstProd, lane, nb, last_bt, S, rc, r0, RP, grp, sm + L.off_stage,
+                                L.stage_len, full, empty);
+  } else if (RR && warp > kV3Rows + NRD) {  // ----------------------------- idle (RR)
   } else if (warp == kV3Rows + NRD) {  // ---------------------------------- pusher
     // Â_u: wait for the rows' red(u) (named barrier 5 / 6 by parity; the rows
     // cannot arrive for u + 2 first, since products(u + 2) follows update(u),
@@ -1268,6 +1280,7 @@ __global__ void __launch_bounds__(v3_threads(PC), 1) k_svrg_chain_v3(EpochArgs a
       for (int kk = 6; kk < 8; ++kk) a.dbg[cta * 8 + kk] = tacc[kk];
     }
   } else {  // --------------------------------------------------------------- rows
+    if constexpr (RR) asm volatile("setmaxnreg.inc.sync.aligned.u32 232;" ::: "memory");
     const int pm = lane >> 1;  // product order j = i ^ pm
     const int ra = 2 * tid;    // rows ra + 256 h, ra + 1 + 256 h
     bool own0[H], own1[H];
@@ -1902,9 +1915,14 @@ void launch_chain_pc(const EpochArgs& a, const EpochConfig& cfg, cudaStream_t st
   auto kern = mode == 1 ? k_svrg_chain<PC, kBlock, false> : k_svrg_chain<PC, kBlock, true>;
   if constexpr (PC <= 3) {
     if (v3) kern = k_svrg_chain_v3<PC, kBlock, 1>;
+    if constexpr (PC == 1) {
+      static const int env_rr = getenv("GAPLRA_CHAIN_RR") ? atoi(getenv("GAPLRA_CHAIN_RR")) : 1;
+      if (v3 && env_rr && cfg.rows_per_cta <= 256) kern = k_svrg_chain_v3<1, kBlock, 1, true>;
+    }
   }
   if constexpr (PC == 1) {
-    if (v3 && cfg.rows_per_cta > 256) kern = k_svrg_chain_v3<1, kBlock, 2>;
+    static const int env_rr2 = getenv("GAPLRA_CHAIN_RR") ? atoi(getenv("GAPLRA_CHAIN_RR")) : 1;
+    if (v3 && cfg.rows_per_cta > 256) kern = env_rr2 ? k_svrg_chain_v3<1, kBlock, 2, true> : k_svrg_chain_v3<1, kBlock, 2>;
   }
   int stages = cfg.stages;
   size_t smem = cfg.smem;
@@ -1934,7 +1952,11 @@ void launch_chain_pc(const EpochArgs& a, const EpochConfig& cfg, cudaStream_t st
   if (cfg.cluster > 8) GAPLRA_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   cudaLaunchConfig_t lc = {};
   lc.gridDim = dim3(cfg.cluster, cfg.groups, 1);
-  lc.blockDim = dim3(use_v4 ? v4::kThreads : (v3 ? v3_threads(PC) : kChainThreads + 32 * kChainProducers), 1, 1);
+  bool rr = false;
+  if constexpr (PC == 1) rr = kern == k_svrg_chain_v3<1, kBlock, 1, true> || kern == k_svrg_chain_v3<1, kBlock, 2, true>;
+  lc.blockDim = dim3(use_v4 ? v4::kThreads
+                            : (rr ? kV3RRThreads : (v3 ? v3_threads(PC) : kChainThreads + 32 * kChainProducers)),
+                     1, 1);
   lc.dynamicSmemBytes = smem;
   lc.stream = st;
   cudaLaunchAttribute attr[1];
