@@ -1897,6 +1897,9 @@ EpochConfig choose_epoch_config(int d_pad, int p) {
   const EpochConfig c16 = make(16), c8 = make(8);
   auto v3_ok = [](const EpochConfig& c) { return v3_supports(c.pc, c.rows_per_cta); };
   if (d_pad < 1024) return c8;
+  // 8 peers instead of 16 when 8 CTAs cover the rows at <= 256 each (C3 p = 1:
+  // 16.3 vs 17.5 ms per epoch: the all-reduce and its slot sum halve)
+  if (v3_ok(c8) && c8.rows_per_cta <= 256) return c8;
   if (v3_ok(c16)) return c16;
   if (v3_ok(c8)) return c8;
   return c16;
