@@ -172,6 +172,9 @@ def load_ledger(prof=None):
 
 
 # ----------------------------------------------------------------- rooflines
+HBM_READ_GBS = 6963.0  # profiles/r01_microbench.txt: 4 GB read-only buffer
+
+
 def rooflines(prof):
     peaks = json.loads(PEAKS.read_text()) if PEAKS.exists() else {}
     hbm = float(peaks.get("hbm_gbs", 6650.0))
@@ -196,6 +199,10 @@ def rooflines(prof):
             out[name] = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
                          "peak_source": hbm_src, "traffic": traffic.get(name), "launches": per,
                          "ms_per_launch": v["ms"] / per, "tflops": v["flops"] / t / 1e12}
+            if name in ("gram_p1", "h_pass"):  # X read once, nothing comparable written
+                out[name]["note"] = (f"read-only stream: hbm_gbs is a copy (read + write) figure; a 4 GB read "
+                                     f"measured {HBM_READ_GBS} GB/s (profiles/r01_microbench.txt), "
+                                     f"frac {ach / HBM_READ_GBS:.3f} of that")
     return out
 
 

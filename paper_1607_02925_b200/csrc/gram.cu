@@ -1224,6 +1224,122 @@ int clusters_for(const DenseX& X, int pc, const Plan& pl) {
 }  // namespace fused
 
 // ---------------------------------------------------------------------------
+// Single-pass p = 1 gram pass (Alg. 3's power steps, tune_shift's estimates,
+// every p = 1 SVRG epoch's anchor): z = X (Xᵀ w), y = Xᵀ w with X read once.
+// The two-pass kernels read X twice (~1.15 ms at C2, 5.7 TB/s of traffic).
+// One 512-thread CTA per SM owns a contiguous column range; a thread owns rows
+// {2·tid, 2·tid + 1} + 1024·k of every column (16-byte loads), so a pair of
+// columns sits in registers while the CTA reduces their dots (warp shuffles,
+// then the 16 warp partials summed in fixed order by every thread) and then
+// folds x_j y_j into the thread's z rows.  The next pair's loads are issued
+// before the current pair's reduction.  Per-CTA z partials are summed in CTA
+// order by k_p1_sum (deterministic).
+// ---------------------------------------------------------------------------
+namespace p1 {
+constexpr int kThreads = 512;
+constexpr int kWarps = kThreads / 32;
+
+// KR: double2 row pairs per thread (ld <= 1024 * KR); WZ = false: y = Xᵀ w only
+// (the p = 1 epoch's H = Xᵀ C)
+template <int KR, bool WZ>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_gram_p1(const double* __restrict__ X, int64_t ldx, int n, const double* __restrict__ W, int64_t ldw,
+              double* __restrict__ Y, int64_t ldy, double* __restrict__ part, int64_t cols_per_cta) {
+  __shared__ double red[2][kWarps][2];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t j0 = static_cast<int64_t>(blockIdx.x) * cols_per_cta;
+  const int64_t j1 = min(static_cast<int64_t>(n), j0 + cols_per_cta);
+  double2 w[KR], z[KR];
+#pragma unroll
+  for (int k = 0; k < KR; ++k) {
+    const int64_t r = 2 * tid + 1024 * k;
+    w[k].x = r < ldx ? W[r * ldw] : 0.0;
+    w[k].y = r + 1 < ldx ? W[(r + 1) * ldw] : 0.0;
+    z[k] = make_double2(0.0, 0.0);
+  }
+  auto load = [&](int64_t j, double2 (&xx)[2][KR]) {
+#pragma unroll
+    for (int c = 0; c < 2; ++c)
+#pragma unroll
+      for (int k = 0; k < KR; ++k) {
+        const int64_t r = 2 * tid + 1024 * k;
+        xx[c][k] = j + c < j1 && r < ldx ? __ldcs(reinterpret_cast<const double2*>(X + (j + c) * ldx + r))
+                                          : make_double2(0.0, 0.0);
+      }
+  };
+  auto consume = [&](int64_t j, const double2 (&xx)[2][KR], int par) {
+    double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+    for (int k = 0; k < KR; ++k) {
+      s0 = fma(xx[0][k].x, w[k].x, fma(xx[0][k].y, w[k].y, s0));
+      s1 = fma(xx[1][k].x, w[k].x, fma(xx[1][k].y, w[k].y, s1));
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+      s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+      s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+    }
+    if (lane == 0) {
+      red[par][warp][0] = s0;
+      red[par][warp][1] = s1;
+    }
+    __syncthreads();  // (two parities: a thread writes red[par] again only after the next barrier)
+    double y0 = 0.0, y1 = 0.0;
+#pragma unroll
+    for (int q = 0; q < kWarps; ++q) {
+      y0 += red[par][q][0];
+      y1 += red[par][q][1];
+    }
+    if (tid == 0) {
+      if (j < j1) Y[j * ldy] = y0;
+      if (j + 1 < j1) Y[(j + 1) * ldy] = y1;
+    }
+    if constexpr (WZ) {
+#pragma unroll
+      for (int k = 0; k < KR; ++k) {
+        z[k].x = fma(xx[1][k].x, y1, fma(xx[0][k].x, y0, z[k].x));
+        z[k].y = fma(xx[1][k].y, y1, fma(xx[0][k].y, y0, z[k].y));
+      }
+    }
+  };
+  double2 xa[2][KR], xb[2][KR];
+  int64_t j = j0;
+  if (j < j1) load(j, xa);
+#pragma unroll 1
+  for (; j < j1; j += 4) {
+    load(j + 2, xb);
+    consume(j, xa, 0);
+    if (j + 2 >= j1) break;
+    load(j + 4, xa);
+    consume(j + 2, xb, 1);
+  }
+  if constexpr (WZ) {
+#pragma unroll
+    for (int k = 0; k < KR; ++k) {
+      const int64_t r = 2 * tid + 1024 * k;
+      if (r < ldx) *reinterpret_cast<double2*>(part + blockIdx.x * ldx + r) = z[k];
+    }
+  }
+}
+
+__global__ void k_p1_sum(const double* __restrict__ part, int nblk, int64_t ldx, double* __restrict__ Z, int64_t ldz) {
+  const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r >= ldx) return;
+  double s = 0.0;
+  for (int b = 0; b < nblk; ++b) s += part[b * ldx + r];
+  Z[r * ldz] = s;
+}
+
+inline int ctas(const DenseX& X) { return std::max(1, std::min(sm_count(), static_cast<int>(ceil_div(X.n, 2)))); }
+
+// GAPLRA_GRAM_P1=0 keeps the two-pass kernels at p = 1
+bool applies(const DenseX& X) {
+  static const int env = getenv("GAPLRA_GRAM_P1") ? atoi(getenv("GAPLRA_GRAM_P1")) : 1;
+  return env && X.ld <= 4096 && X.ld % 2 == 0;
+}
+}  // namespace p1
+
+// ---------------------------------------------------------------------------
 // Z = X Y with X streamed through shared memory by a TMA producer warp
 // (cp.async.bulk column slices into a 3-6 stage ring, the 16 Y rows of the
 // tile in the same stage) and 8 DMMA warps — the single-pass kernel's phase B
@@ -1523,6 +1639,7 @@ static int64_t ldp_even(int p) { return p == 1 ? 1 : (p + 1) / 2 * 2; }
 
 size_t gram_work_elems(const DenseX& X, int p) {
   size_t need = 0;
+  if (p == 1 && p1::applies(X)) need = static_cast<size_t>(p1::ctas(X)) * X.ld;
   for (int c0 = 0; c0 < p; c0 += 32) {
     const int pc = std::min(32, p - c0);
     if (xyt::applies(pc, ldp_even(p))) {
@@ -1546,6 +1663,32 @@ size_t gram_work_elems(const DenseX& X, int p) {
     if (b.s > 1) need = std::max(need, static_cast<size_t>(b.s) * X.ld * pc);
   }
   return need;
+}
+
+bool gram_p1_applies(const DenseX& X) { return p1::applies(X); }
+
+// Z == nullptr: y = Xᵀ w only (no workspace)
+void launch_gram_p1(const DenseX& X, const double* W, int64_t ldw, double* Y, int64_t ldy, double* Z, int64_t ldz,
+                    GramWork& work, cudaStream_t st) {
+  if (!p1::applies(X)) throw Error(kContractViolation, "gram_p1: layout does not apply");
+  const int nblk = p1::ctas(X);
+  if (Z && work.part_elems < static_cast<size_t>(nblk) * X.ld) throw Error(kContractViolation, "gram_p1: workspace");
+  const int64_t cpc = (ceil_div(X.n, nblk) + 1) / 2 * 2;
+  const int grid = static_cast<int>(ceil_div(X.n, cpc));
+  auto go = [&](auto kern) { kern<<<grid, p1::kThreads, 0, st>>>(X.x, X.ld, X.n, W, ldw, Y, ldy, work.part, cpc); };
+  if (Z) {
+    if (X.ld <= 1024) go(p1::k_gram_p1<1, true>);
+    else if (X.ld <= 2048) go(p1::k_gram_p1<2, true>);
+    else go(p1::k_gram_p1<4, true>);
+  } else {
+    if (X.ld <= 1024) go(p1::k_gram_p1<1, false>);
+    else if (X.ld <= 2048) go(p1::k_gram_p1<2, false>);
+    else go(p1::k_gram_p1<4, false>);
+  }
+  GAPLRA_LAUNCH_CHECK();
+  if (!Z) return;
+  p1::k_p1_sum<<<static_cast<int>(ceil_div(X.ld, 256)), 256, 0, st>>>(work.part, grid, X.ld, Z, ldz);
+  GAPLRA_LAUNCH_CHECK();
 }
 
 bool gram_fused_applies(const DenseX& X, int p) {

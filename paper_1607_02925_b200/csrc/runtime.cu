@@ -336,6 +336,8 @@ void gram_block_dev(Context& c, const Matrix& X, int p, const double* W, int64_t
     w.part = w.part_elems ? c.gw.ensure(w.part_elems) : nullptr;
     if (gram_fused_applies(D, p)) {  // one pass over X (d <= 4096)
       launch_gram_fused(D, W, ldw, p, Y, ldy, Z, ldz, w, c.st);
+    } else if (p == 1 && gram_p1_applies(D)) {  // one pass, 1024 < d <= 4096
+      launch_gram_p1(D, W, ldw, Y, ldy, Z, ldz, w, c.st);
     } else {
       launch_xtw(D, W, ldw, p, Y, ldy, w, c.st);
       launch_xy(D, Y, ldy, p, Z, ldz, w, c.st);
@@ -460,7 +462,10 @@ void epoch_run_dev(Context& c, Matrix& X, int p, double* W, const double* C, con
     w.part = w.part_elems ? c.gw.ensure(w.part_elems) : nullptr;
     {
       Prof prof(c, kProfHPass, 8.0 * X.d * X.n, 2.0 * X.nnz * p);
-      launch_xtw(D, C, ld, p, H, ld, w, c.st);
+      if (p == 1 && gram_p1_applies(D))
+        launch_gram_p1(D, C, ld, H, ld, nullptr, 0, w, c.st);
+      else
+        launch_xtw(D, C, ld, p, H, ld, w, c.st);
     }
     EpochArgs a{};
     a.X = X.x;

@@ -52,11 +52,14 @@ def test_gram_block_dense(g, oracle, p):
 
 
 @pytest.mark.parametrize("d,n,p", [(4096, 3001, 20), (4096, 5, 1), (4096, 1000, 33), (2048, 4099, 32), (1000, 1601, 10),
-                                   (1000, 777, 64), (300, 16, 2), (8192, 300, 3)])
+                                   (1000, 777, 64), (300, 16, 2), (8192, 300, 3), (2050, 4099, 1), (1500, 1001, 1),
+                                   (4096, 20001, 1), (1030, 3, 1), (8192, 301, 1)])
 def test_gram_block_layouts(g, d, n, p):
     # every single-pass layout (16- / 8- / 4-CTA clusters, 256 / 128 rows per
-    # CTA, ragged last tile, several clusters, 32-column chunks) and the
-    # two-pass fallback (d = 8192) against a float64 numpy product
+    # CTA, ragged last tile, several clusters, 32-column chunks), the p = 1
+    # single-pass kernel (1024 < d <= 4096: 2 / 4 / 8 rows per thread, odd n,
+    # fewer columns than CTAs) and the two-pass fallback (d = 8192) against a
+    # float64 numpy product
     rng = np.random.default_rng(d + n + p)
     X = rng.standard_normal((d, n))
     W = rng.standard_normal((d, p))
@@ -103,6 +106,10 @@ def test_gram_block_deterministic(g):
     a = g.gram_block(x, W)
     b = g.gram_block(x, W)
     assert np.array_equal(a, b)
+    X = rng.standard_normal((2048, 5000))  # p = 1 single-pass kernel
+    w = rng.standard_normal((2048, 1))
+    x = g.DeviceMatrix.dense(X)
+    assert np.array_equal(g.gram_block(x, w), g.gram_block(x, w))
 
 
 def test_gram_apply_kats(g):
@@ -250,6 +257,20 @@ def test_svrg_solve_matches_oracle_and_direct(g, oracle):
     assert rel(r.solution, wo) <= 1e-8
     wd = np.linalg.solve(lam * np.eye(60) - X @ X.T, b)
     assert rel(r.solution, wd) <= 1e-8
+
+
+def test_svrg_solve_p1_single_pass_layout(g, oracle):
+    # p = 1 at 1024 < d <= 4096: the anchor's gram pass and H = Xᵀ C take the
+    # single-pass p = 1 kernel
+    X, _, sig = planted_dense(1500, 2000, seed=3)
+    lam = 1.05 * sig[0] ** 2
+    b = np.random.default_rng(3).standard_normal((1500, 1))
+    r = g.solve_svrg(g.DeviceMatrix.dense(X), lam, b, 1e-10, seed=5)
+    rc, wo, ep, hist = oracle.svrg_solve(oracle.dense(X), lam, b, 1e-10, seed=5)
+    assert rc == 0
+    assert abs(r.epochs - ep) <= 1
+    assert rel(r.solution, wo) <= 1e-8
+    assert rel(r.solution, np.linalg.solve(lam * np.eye(1500) - X @ X.T, b)) <= 1e-8
 
 
 def test_svrg_solve_zero_matrix(g):
