@@ -200,17 +200,23 @@ __global__ void __launch_bounds__(kPrepThreads + 32 * kPrepProducers, kPrepCtas)
     const int rc = warp * kPrepColsPerProducer + lane;
     int stage = 0;
     uint32_t phase = 0;
-    for (int64_t t = t_begin; t < t_end; t += t_step) {
-      const int64_t s0 = t * B;
-      const int bt = static_cast<int>(a.m - s0 < B ? a.m - s0 : B);
+    auto col_of = [&](int64_t t) {  // this lane's ring column of block t (zeros when masked)
       const double* col = a.zcol;
-      if (lane < kPrepColsPerProducer) {
+      if (t < t_end && lane < kPrepColsPerProducer) {
+        const int64_t s0 = t * B;
+        const int bt = static_cast<int>(a.m - s0 < B ? a.m - s0 : B);
         if (rc < B) {
           if (rc < bt) col = a.X + static_cast<int64_t>(a.idx[s0 + rc]) * a.ldx;
         } else if (t > 0) {
           col = a.X + static_cast<int64_t>(a.idx[s0 - B + (rc - B)]) * a.ldx;
         }
       }
+      return col;
+    };
+    const double* ncol = col_of(t_begin);
+    for (int64_t t = t_begin; t < t_end; t += t_step) {
+      const double* col = ncol;
+      ncol = col_of(t + t_step);  // next block's index load off the refill path
       for (int kc = 0; kc < nkc; ++kc) {
         const int k0 = kc * kPrepKC;
         const int len = a.d_pad - k0 < kPrepKC ? a.d_pad - k0 : kPrepKC;
@@ -434,11 +440,20 @@ __device__ __forceinline__ void chain_produce(const EpochArgs& a, int pw, int la
   static_assert(B % NP == 0 && CPP <= 31, "producers cover the B columns; lane 31 issues the slab");
   int s = 0;
   uint32_t eph = 0;  // parity of the next empty-barrier completion per wrap
+  const int j0 = pw * CPP;
+  // this lane's sampled column of block u, loaded one block ahead: the index
+  // load's L2 latency stays off the refill path (empty -> TMA issue)
+  auto col_of = [&](int u) {
+    const int bu = u == nb - 1 ? last_bt : B;
+    return u < nb && lane < CPP && j0 + lane < bu ? __ldg(a.idx + static_cast<int64_t>(u) * B + j0 + lane) : 0;
+  };
+  int ncol = col_of(0);
   for (int t = 0; t < nb; ++t) {
+    const int col = ncol;
+    ncol = col_of(t + 1);
     if (t >= S) mbar_wait_backoff(&empty[s], eph);
     const int bt = t == nb - 1 ? last_bt : B;
     double* st = stages + static_cast<size_t>(s) * stage_len;
-    const int j0 = pw * CPP;
     const int mine = rc > 0 ? max(0, min(CPP, bt - j0)) : 0;
     if (lane == 0) {
       fence_proxy_async();
@@ -447,8 +462,7 @@ __device__ __forceinline__ void chain_produce(const EpochArgs& a, int pw, int la
     __syncwarp();
     if (lane < mine) {
       const int j = j0 + lane;
-      tma_load_1d(st + j * RP, a.X + static_cast<int64_t>(__ldg(a.idx + static_cast<int64_t>(t) * B + j)) * a.ldx + r0,
-                  rc * 8u, &full[s]);
+      tma_load_1d(st + j * RP, a.X + static_cast<int64_t>(col) * a.ldx + r0, rc * 8u, &full[s]);
     }
     // L2 prefetch of the same slices a.prefetch blocks ahead: the index
     // stream is known for the whole epoch, so the ring's TMA loads hit L2
