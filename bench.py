@@ -348,7 +348,7 @@ def run_reference(args, rank, world):
     v = sum(vals[args.warmup:]) / max(1, args.steps)
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": v * 1e3, "higher_is_better": False, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic (host sample with BASELINE.json's C2 recipe)",
+            "vs_baseline": None, "dtype": "f64", "data": f"synthetic (host sample with BASELINE.json's {args.config} recipe)",
             "config": {"workload": workload_desc(spec), "d": spec.d, "n": spec.n, "k": spec.k, "p": spec.p,
                        "eps": spec.eps},
             "cpu_baseline": {"value": v, "unit": "s", "cores": nth, "kind": "port",
