@@ -1322,6 +1322,78 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// 4096 < ld <= 8192 (C5): a pair of 8192-row columns would not fit in the
+// registers beside w and z, so w moves to shared memory and the columns go one
+// at a time (still double-buffered: column j + 1's loads before column j's
+// reduction)
+template <bool WZ>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_gram_p1_wide(const double* __restrict__ X, int64_t ldx, int n, const double* __restrict__ W, int64_t ldw,
+                   double* __restrict__ Y, int64_t ldy, double* __restrict__ part, int64_t cols_per_cta) {
+  constexpr int KR = 8;
+  extern __shared__ __align__(16) double ws[];  // w, ldx doubles
+  __shared__ double red[2][kWarps];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t j0 = static_cast<int64_t>(blockIdx.x) * cols_per_cta;
+  const int64_t j1 = min(static_cast<int64_t>(n), j0 + cols_per_cta);
+  for (int64_t r = tid; r < ldx; r += kThreads) ws[r] = W[r * ldw];
+  __syncthreads();
+  double2 z[KR];
+#pragma unroll
+  for (int k = 0; k < KR; ++k) z[k] = make_double2(0.0, 0.0);
+  auto load = [&](int64_t j, double2 (&xx)[KR]) {
+#pragma unroll
+    for (int k = 0; k < KR; ++k) {
+      const int64_t r = 2 * tid + 1024 * k;
+      xx[k] = j < j1 && r < ldx ? __ldcs(reinterpret_cast<const double2*>(X + j * ldx + r)) : make_double2(0.0, 0.0);
+    }
+  };
+  auto consume = [&](int64_t j, const double2 (&xx)[KR], int par) {
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < KR; ++k) {
+      const int r = 2 * tid + 1024 * k;
+      if (r < ldx) {
+        const double2 w2 = *reinterpret_cast<const double2*>(ws + r);
+        s = fma(xx[k].x, w2.x, fma(xx[k].y, w2.y, s));
+      }
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) red[par][warp] = s;
+    __syncthreads();
+    double y = 0.0;
+#pragma unroll
+    for (int q = 0; q < kWarps; ++q) y += red[par][q];
+    if (tid == 0 && j < j1) Y[j * ldy] = y;
+    if constexpr (WZ) {
+#pragma unroll
+      for (int k = 0; k < KR; ++k) {
+        z[k].x = fma(xx[k].x, y, z[k].x);
+        z[k].y = fma(xx[k].y, y, z[k].y);
+      }
+    }
+  };
+  double2 xa[KR], xb[KR];
+  int64_t j = j0;
+  if (j < j1) load(j, xa);
+#pragma unroll 1
+  for (; j < j1; j += 2) {
+    load(j + 1, xb);
+    consume(j, xa, 0);
+    if (j + 1 >= j1) break;
+    load(j + 2, xa);
+    consume(j + 1, xb, 1);
+  }
+  if constexpr (WZ) {
+#pragma unroll
+    for (int k = 0; k < KR; ++k) {
+      const int64_t r = 2 * tid + 1024 * k;
+      if (r < ldx) *reinterpret_cast<double2*>(part + blockIdx.x * ldx + r) = z[k];
+    }
+  }
+}
+
 __global__ void k_p1_sum(const double* __restrict__ part, int nblk, int64_t ldx, double* __restrict__ Z, int64_t ldz) {
   const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (r >= ldx) return;
@@ -1335,7 +1407,7 @@ inline int ctas(const DenseX& X) { return std::max(1, std::min(sm_count(), stati
 // GAPLRA_GRAM_P1=0 keeps the two-pass kernels at p = 1
 bool applies(const DenseX& X) {
   static const int env = getenv("GAPLRA_GRAM_P1") ? atoi(getenv("GAPLRA_GRAM_P1")) : 1;
-  return env && X.ld <= 4096 && X.ld % 2 == 0;
+  return env && X.ld <= 8192 && X.ld % 2 == 0;
 }
 }  // namespace p1
 
@@ -1676,14 +1748,21 @@ void launch_gram_p1(const DenseX& X, const double* W, int64_t ldw, double* Y, in
   const int64_t cpc = (ceil_div(X.n, nblk) + 1) / 2 * 2;
   const int grid = static_cast<int>(ceil_div(X.n, cpc));
   auto go = [&](auto kern) { kern<<<grid, p1::kThreads, 0, st>>>(X.x, X.ld, X.n, W, ldw, Y, ldy, work.part, cpc); };
+  auto go_wide = [&](auto kern) {
+    const int smem = static_cast<int>(X.ld * sizeof(double));
+    GAPLRA_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    kern<<<grid, p1::kThreads, smem, st>>>(X.x, X.ld, X.n, W, ldw, Y, ldy, work.part, cpc);
+  };
   if (Z) {
     if (X.ld <= 1024) go(p1::k_gram_p1<1, true>);
     else if (X.ld <= 2048) go(p1::k_gram_p1<2, true>);
-    else go(p1::k_gram_p1<4, true>);
+    else if (X.ld <= 4096) go(p1::k_gram_p1<4, true>);
+    else go_wide(p1::k_gram_p1_wide<true>);
   } else {
     if (X.ld <= 1024) go(p1::k_gram_p1<1, false>);
     else if (X.ld <= 2048) go(p1::k_gram_p1<2, false>);
-    else go(p1::k_gram_p1<4, false>);
+    else if (X.ld <= 4096) go(p1::k_gram_p1<4, false>);
+    else go_wide(p1::k_gram_p1_wide<false>);
   }
   GAPLRA_LAUNCH_CHECK();
   if (!Z) return;

@@ -57,7 +57,8 @@ void launch_gram_fused(const DenseX& X, const double* W, int64_t ldw, int p, dou
                        int64_t ldz, GramWork& work, cudaStream_t st);
 
 // Single-pass p = 1 pass (X read once; 512-thread CTA per SM, a column pair in
-// registers while its dots are reduced), X.ld <= 4096; gram_p1_applies says.
+// registers while its dots are reduced; w in shared memory and single columns
+// above 4096 rows), X.ld <= 8192; gram_p1_applies says.
 // Z == nullptr: Y = Xᵀ W only.
 bool gram_p1_applies(const DenseX& X);
 void launch_gram_p1(const DenseX& X, const double* W, int64_t ldw, double* Y, int64_t ldy, double* Z, int64_t ldz,

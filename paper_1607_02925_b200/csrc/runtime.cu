@@ -336,7 +336,7 @@ void gram_block_dev(Context& c, const Matrix& X, int p, const double* W, int64_t
     w.part = w.part_elems ? c.gw.ensure(w.part_elems) : nullptr;
     if (gram_fused_applies(D, p)) {  // one pass over X (d <= 4096)
       launch_gram_fused(D, W, ldw, p, Y, ldy, Z, ldz, w, c.st);
-    } else if (p == 1 && gram_p1_applies(D)) {  // one pass, 1024 < d <= 4096
+    } else if (p == 1 && gram_p1_applies(D)) {  // one pass, 1024 < d <= 8192
       launch_gram_p1(D, W, ldw, Y, ldy, Z, ldz, w, c.st);
     } else {
       launch_xtw(D, W, ldw, p, Y, ldy, w, c.st);

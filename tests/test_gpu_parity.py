@@ -53,13 +53,13 @@ def test_gram_block_dense(g, oracle, p):
 
 @pytest.mark.parametrize("d,n,p", [(4096, 3001, 20), (4096, 5, 1), (4096, 1000, 33), (2048, 4099, 32), (1000, 1601, 10),
                                    (1000, 777, 64), (300, 16, 2), (8192, 300, 3), (2050, 4099, 1), (1500, 1001, 1),
-                                   (4096, 20001, 1), (1030, 3, 1), (8192, 301, 1)])
+                                   (4096, 20001, 1), (1030, 3, 1), (8192, 301, 1), (6002, 999, 1)])
 def test_gram_block_layouts(g, d, n, p):
     # every single-pass layout (16- / 8- / 4-CTA clusters, 256 / 128 rows per
     # CTA, ragged last tile, several clusters, 32-column chunks), the p = 1
-    # single-pass kernel (1024 < d <= 4096: 2 / 4 / 8 rows per thread, odd n,
-    # fewer columns than CTAs) and the two-pass fallback (d = 8192) against a
-    # float64 numpy product
+    # single-pass kernels (1024 < d <= 8192: 2 / 4 / 8 rows per thread, w in
+    # shared memory above 4096, odd n, fewer columns than CTAs) and the
+    # two-pass fallback (d = 8192, p = 3) against a float64 numpy product
     rng = np.random.default_rng(d + n + p)
     X = rng.standard_normal((d, n))
     W = rng.standard_normal((d, p))
