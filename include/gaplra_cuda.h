@@ -164,7 +164,10 @@ GAPLRA_API int gaplra_profile_reset(gaplra_ctx* ctx);
  * dense: column-major, ldx >= d.  on_device = 0: host pointer, copied in.
  *        on_device = 1: device pointer, BORROWED (caller keeps it alive, as
  *        GramOperator borrows X, linear_operator.hpp:53-60); requires
- *        ldx % 4 == 0 and rows [d, ldx) zero.
+ *        ldx == round_up(d, 4) and rows [d, ldx) zero.
+ *        Either way X is read once on the device at creation: a non-finite
+ *        entry (sparse_matrix.cpp:29) or a non-zero pad row is a
+ *        GAPLRA_CONTRACT_VIOLATION.
  * csc:   colptr[n+1], rowidx (strictly increasing per column), val. */
 GAPLRA_API int gaplra_matrix_dense(gaplra_ctx* ctx, int d, int n, const double* x, int64_t ldx, int on_device,
                         gaplra_matrix** out);

@@ -1679,6 +1679,26 @@ __global__ void k_colnorm2_dense(const double* __restrict__ X, int64_t ldx, int 
   }
 }
 
+// X validation at matrix creation (sparse_matrix.cpp:29 rejects non-finite
+// entries): flags[0] |= 1 on a non-finite entry in rows < d, |= 2 on a
+// non-zero pad row (rows d..ld-1 must be zero: the kernels read whole columns).
+__global__ void k_check_dense(const double* __restrict__ X, int64_t ldx, int d, int n, int* __restrict__ flags) {
+  const int lane = threadIdx.x & 31;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  int bad = 0;
+  for (int j = warp; j < n; j += nwarps) {
+    const double* col = X + static_cast<int64_t>(j) * ldx;
+    for (int i = lane; i < ldx; i += 32) {
+      const double v = col[i];
+      if (i < d) bad |= isfinite(v) ? 0 : 1;
+      else bad |= v == 0.0 ? 0 : 2;
+    }
+  }
+  bad = __reduce_or_sync(0xffffffffu, bad);
+  if (lane == 0 && bad) atomicOr(flags, bad);
+}
+
 __global__ void k_colnorm2_sparse(int n, const int64_t* __restrict__ colptr, const double* __restrict__ val,
                                   double* __restrict__ out) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1862,6 +1882,12 @@ void launch_xy_sparse(const SparseX& X, const double* Y, int64_t ldy, int p, dou
 
 void col_norm2_dense(const DenseX& X, double* out, cudaStream_t st) {
   k_colnorm2_dense<<<sm_count() * 8, 256, 0, st>>>(X.x, X.ld, X.d, X.n, out);
+  GAPLRA_LAUNCH_CHECK();
+}
+
+void check_dense(const DenseX& X, int* flags, cudaStream_t st) {
+  GAPLRA_CUDA_CHECK(cudaMemsetAsync(flags, 0, sizeof(int), st));
+  k_check_dense<<<sm_count() * 8, 256, 0, st>>>(X.x, X.ld, X.d, X.n, flags);
   GAPLRA_LAUNCH_CHECK();
 }
 

@@ -72,6 +72,8 @@ void launch_xy_sparse(const SparseX& X, const double* Y, int64_t ldy, int p, dou
 // Per-column |x_j|^2 into out[n]; reduce_sum_max: out2 = {sum, max} (SVRG step size).
 void col_norm2_dense(const DenseX& X, double* out, cudaStream_t st);
 void col_norm2_sparse(const SparseX& X, double* out, cudaStream_t st);
+// flags[0] = 1 (non-finite entry) | 2 (non-zero pad row d..ld-1); one read of X.
+void check_dense(const DenseX& X, int* flags, cudaStream_t st);
 void reduce_sum_max(const double* v, int n, double* out2, cudaStream_t st);
 
 }  // namespace gaplra_cuda

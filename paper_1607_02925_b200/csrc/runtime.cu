@@ -720,7 +720,9 @@ CgResult cg_solve_dev(Context& c, Matrix& X, double lambda, int p, const double*
   double* Zg = zb.ensure(blk);
   double* v = vb.ensure(5 * 64);
   double *rr = v, *rr_new = v + 64, *pq = v + 128, *alpha = v + 192, *bn2 = v + 256;
-  double* part = c.tmp.ensure(static_cast<size_t>(small_gram_parts(d)) * 64 + 8);
+  // sized for project_out_dev's use of the same workspace (a smaller c.tmp
+  // would be reallocated under `part` inside the loop)
+  double* part = c.tmp.ensure(static_cast<size_t>(small_gram_parts(d)) * 64 * 64 + 8);
   int* status = c.status.ensure(2);
   GAPLRA_CUDA_CHECK(cudaMemsetAsync(status, 0, 2 * sizeof(int), c.st));
   launch_col_dots(B, ld, B, ld, d, p, part, bn2, c.st);
@@ -1526,7 +1528,9 @@ int gaplra_matrix_dense(gaplra_ctx* ctx, int d, int n, const double* x, int64_t 
     m.nnz = static_cast<int64_t>(d) * n;
     m.device = ctx->c.device;
     if (on_device) {
-      require(ldx % 4 == 0, "matrix_dense: borrowed device X needs ldx % 4 == 0 (zero pad rows)");
+      // the kernels size W, Z and the per-CTA row split by ld: a borrowed X must
+      // use the library's own layout, ld = round4(d), with zero pad rows
+      require(ldx == round4(d), "matrix_dense: borrowed device X needs ldx == round_up(d, 4) (zero pad rows)");
       m.ld = ldx;
       m.x = x;
     } else {
@@ -1535,8 +1539,14 @@ int gaplra_matrix_dense(gaplra_ctx* ctx, int d, int n, const double* x, int64_t 
       GAPLRA_CUDA_CHECK(cudaMemcpy2DAsync(buf, m.ld * sizeof(double), x, ldx * sizeof(double), d * sizeof(double), n,
                                           cudaMemcpyHostToDevice, ctx->c.st));
       m.x = buf;
-      ctx->c.sync();
     }
+    // one device read of X: finite entries (sparse_matrix.cpp:29) and zero pad rows
+    int* flags = ctx->c.status.ensure(2);
+    check_dense(m.dense(), flags, ctx->c.st);
+    GAPLRA_CUDA_CHECK(cudaMemcpyAsync(ctx->c.pin_i, flags, sizeof(int), cudaMemcpyDeviceToHost, ctx->c.st));
+    ctx->c.sync();
+    require(!(ctx->c.pin_i[0] & 1), "matrix_dense: X has a non-finite entry");
+    require(!(ctx->c.pin_i[0] & 2), "matrix_dense: borrowed X has non-zero pad rows (rows d..ldx-1 must be zero)");
   });
   if (rc != GAPLRA_OK) {
     delete M;

@@ -190,17 +190,22 @@ class DeviceMatrix:
 
     @classmethod
     def from_device(cls, ptr: int, d: int, n: int, ldx: int, ctx: Context | None = None, keep=None):
-        """Borrow a device column-major X (ldx % 4 == 0); `keep` holds its owner."""
+        """Borrow a device column-major X with ldx == round_up(d, 4) and zero pad
+        rows (checked on the device, with finiteness); `keep` holds its owner."""
         ctx = ctx or default_context()
         h = C.c_void_p()
         ctx.check(ctx.lib.gaplra_matrix_dense(ctx.h, d, n, C.c_void_p(ptr), ldx, 1, C.byref(h)))
         return cls(ctx, h, keep)
 
     @classmethod
-    def from_torch(cls, xt, ctx: Context | None = None):
-        """Borrow a CUDA float64 tensor of shape (n, ld) holding X column-major
-        (i.e. Xᵀ row-major), d <= ld, ld % 4 == 0."""
-        raise NotImplementedError("use from_device(xt.data_ptr(), d, n, ld, keep=xt)")
+    def from_torch(cls, xt, d: int | None = None, ctx: Context | None = None):
+        """Borrow a contiguous CUDA float64 tensor of shape (n, ld) holding X
+        column-major (i.e. Xᵀ row-major); d defaults to ld."""
+        if str(getattr(xt, "dtype", "")) != "torch.float64" or not xt.is_cuda or xt.dim() != 2 \
+                or not xt.is_contiguous():
+            raise ContractViolation("from_torch: need a contiguous (n, ld) float64 CUDA tensor")
+        n, ld = xt.shape
+        return cls.from_device(xt.data_ptr(), d or ld, n, ld, ctx=ctx, keep=xt)
 
     @classmethod
     def csc(cls, d, n, colptr, rowidx, val, ctx: Context | None = None):

@@ -10,6 +10,7 @@ sys.path.insert(0, str(ROOT / "tests"))
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200) and the built libgaplra_cuda.so")
+    config.addinivalue_line("markers", "fullsize: device-vs-oracle parity at the BASELINE.json configs' sizes (minutes)")
 
 
 @pytest.fixture(scope="session")
