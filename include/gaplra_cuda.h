@@ -61,7 +61,8 @@ typedef enum {
   GAPLRA_NO_PRECONDITIONING_NEEDED = 7,/* SPEC.md:425 signal */
   GAPLRA_DEVICE_ERROR = 8,
   GAPLRA_OUT_OF_MEMORY = 9,
-  GAPLRA_NO_USABLE_GAP = 10            /* find_gap_budget */
+  GAPLRA_NO_USABLE_GAP = 10,           /* find_gap_budget */
+  GAPLRA_DEGENERATE_PROGRESS = 11      /* gaplra::DegenerateProgress (errors.hpp:95-98) */
 } gaplra_status;
 
 typedef struct gaplra_ctx gaplra_ctx;

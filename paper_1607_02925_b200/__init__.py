@@ -10,7 +10,7 @@ from .gaplra import (  # noqa: F401
     gaussian_init, gram_apply, gram_block, index_stream, jacobi_eigh, orthonormality_defect, qr_orthonormalize,
     restricted_projection, shift_invert, solve_svrg, svrg_epoch, tune_shift, solve_cg, error_report,
     principal_angles, detect_multiplicative_gap, detect_additive_gap, estimate_eigenvalues, approximate,
-    RankKProjection, find_gap_budget, NoUsableGap, solve_accelerated_svrg,
+    RankKProjection, find_gap_budget, NoUsableGap, DegenerateProgress, solve_accelerated_svrg,
 )
 
 __version__ = "0.1.0"

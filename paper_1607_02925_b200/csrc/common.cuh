@@ -22,6 +22,7 @@ enum Status : int {
   kDeviceError = 8,
   kOutOfMemory = 9,
   kNoUsableGap = 10,
+  kDegenerateProgress = 11,
 };
 
 struct Error : std::runtime_error {

@@ -1284,7 +1284,7 @@ void approximate_dev(Context& c, Matrix& X, const gaplra_si_config& cfg, double*
   int64_t solves = 0;
   int s = 1;
   for (int j = 0; s <= k; ++j) {
-    if (j >= k) throw Error(kRankDeficient, "approximate: no progress (DegenerateProgress)");
+    if (j >= k) throw Error(kDegenerateProgress, "approximate: more intervals than target indices (DegenerateProgress)");
     gaplra_si_config cj = cfg;
     cj.seed = derive_seed(cfg.seed, kTagInterval + static_cast<uint64_t>(j));
     GramOp a0(c, X);
@@ -1337,9 +1337,15 @@ void approximate_dev(Context& c, Matrix& X, const gaplra_si_config& cfg, double*
                                      cfg.conv_tol, S);
       }
     }
-    // deflation_basis_extend (oracle.cpp basis_extend): project, QR, append
+    // deflation_basis_extend (oracle.cpp basis_extend): project, QR, append;
+    // a new column in span(U) is a duplicated eigendirection
     project_out_dev(c, U, m, S, ldp_of(width), d, width);
-    qr_dev(c, S, ldp_of(width), d, width, /*count=*/false);
+    try {
+      qr_dev(c, S, ldp_of(width), d, width, /*count=*/false);
+    } catch (const Error& e) {
+      if (e.code != kRankDeficient || m == 0) throw;
+      throw Error(kDegenerateProgress, std::string("approximate: deflation_basis_extend: ") + e.what(), e.payload);
+    }
     const int m2 = m + width;
     if (m2 > 64) throw Error(kContractViolation, "approximate: basis wider than 64 columns");
     double* U2 = ubs[cur ^ 1].ensure(static_cast<size_t>(dp) * ldp_of(m2));

@@ -67,6 +67,11 @@ class NoUsableGap(Error):
     """find_gap_budget found no gap above the floor."""
 
 
+class DegenerateProgress(Error):
+    """approximate stopped making progress: a duplicated eigendirection or more
+    intervals than target indices (errors.hpp:95-98)."""
+
+
 class DeviceError(Error):
     pass
 
@@ -76,7 +81,7 @@ class OutOfMemory(DeviceError):
 
 
 _CODES = {1: ContractViolation, 3: IndefiniteShift, 5: ShiftOutOfRange, 7: NoPreconditioningNeeded,
-          8: DeviceError, 9: OutOfMemory, 10: NoUsableGap}
+          8: DeviceError, 9: OutOfMemory, 10: NoUsableGap, 11: DegenerateProgress}
 
 
 def _f64(a, shape=None):

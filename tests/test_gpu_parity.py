@@ -517,3 +517,37 @@ def test_accelerated_svrg_device(g, oracle):
     ra = g.shift_invert(x, g.SIConfig(backend="accsvrg", **kw))
     rs_ = g.shift_invert(x, g.SIConfig(**kw))
     assert oracle.sin_theta(ra.W, rs_.W) <= 1e-7
+
+
+def test_non_finite_inputs_rejected(g):
+    """ContractViolation at the boundary, as the reference constructor / spmv
+    do (sparse_matrix.cpp:29,70): non-finite X (checked on the device at
+    creation), non-finite W / B, and a borrowed X with non-zero pad rows."""
+    import torch
+
+    X = np.random.default_rng(0).standard_normal((10, 7))
+    X[3, 4] = np.nan
+    with pytest.raises(g.ContractViolation):
+        g.DeviceMatrix.dense(X)
+    X[3, 4] = np.inf
+    with pytest.raises(g.ContractViolation):
+        g.DeviceMatrix.dense(X)
+    X[3, 4] = 0.5
+    x = g.DeviceMatrix.dense(X)
+    w = np.ones((10, 2))
+    w[1, 1] = np.nan
+    with pytest.raises(g.ContractViolation):
+        g.gram_block(x, w)
+    with pytest.raises(g.ContractViolation):
+        g.solve_svrg(x, 100.0, w, 1e-8)
+    # borrowed device X: ld must be round_up(d, 4) and the pad rows zero
+    xt = torch.zeros((7, 12), dtype=torch.float64, device="cuda")
+    xt[:, :10] = torch.from_numpy(X.T.copy()).cuda()
+    ok = g.DeviceMatrix.from_torch(xt, d=10)
+    assert np.allclose(g.gram_block(ok, np.ones((10, 1))), X @ (X.T @ np.ones((10, 1))), rtol=1e-13)
+    xt[2, 11] = 1.0
+    with pytest.raises(g.ContractViolation):
+        g.DeviceMatrix.from_torch(xt, d=10)
+    xt2 = torch.zeros((7, 16), dtype=torch.float64, device="cuda")
+    with pytest.raises(g.ContractViolation):
+        g.DeviceMatrix.from_device(xt2.data_ptr(), 10, 7, 16, keep=xt2)
