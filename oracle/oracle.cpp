@@ -998,12 +998,17 @@ void restricted_projection(const Mat& x, const Block& s, int k, Block& w, std::v
 }
 
 // deflation_basis_extend: project the new block against the
-// current basis (project_out), QR it, append; RankDeficient -> DegenerateProgress
-// (reported as ORC_RANK_DEFICIENT).
+// current basis (project_out), QR it, append; RankDeficient against a non-empty
+// basis -> DegenerateProgress.
 Block basis_extend(const Block& cur, const Block& nb) {
   Block q = nb;
   project_out_block(cur, q);
-  qr_inplace(q);
+  try {
+    qr_inplace(q);
+  } catch (const Status& e) {
+    if (e.code != ORC_RANK_DEFICIENT || cur.p == 0) throw;
+    throw Status(ORC_DEGENERATE_PROGRESS, e.payload);
+  }
   Block out(cur.d, cur.p + q.p);
   std::copy(cur.a.begin(), cur.a.end(), out.a.begin());
   std::copy(q.a.begin(), q.a.end(), out.a.begin() + cur.a.size());
@@ -1057,7 +1062,7 @@ void approximate(const Mat& x, const orc_si_config* cfg, Block& w, std::vector<d
   int64_t solves = 0;
   int s = 1;
   for (int j = 0; s <= k; ++j) {
-    if (j >= k) throw Status(ORC_RANK_DEFICIENT);  // DegenerateProgress
+    if (j >= k) throw Status(ORC_DEGENERATE_PROGRESS);
     orc_si_config cj = *cfg;
     cj.seed = derive_seed(cfg->seed, kTagInterval + static_cast<uint64_t>(j));
     GramOp a0(x, &rep->ledger, nthreads);

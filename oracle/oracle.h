@@ -39,7 +39,8 @@ enum {
   ORC_SHIFT_OUT_OF_RANGE = 5,
   ORC_SHIFT_TUNING_STALLED = 6,
   ORC_NO_PRECONDITIONING_NEEDED = 7,
-  ORC_NO_USABLE_GAP = 10 /* find_gap_budget */
+  ORC_NO_USABLE_GAP = 10, /* find_gap_budget */
+  ORC_DEGENERATE_PROGRESS = 11 /* errors.hpp:95-98 */
 };
 
 /* X in R^{d x n}: kind 0 = dense column-major (ld = d), kind 1 = CSC

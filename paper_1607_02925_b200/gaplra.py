@@ -544,6 +544,7 @@ class ShiftState:
     inv_gap_estimate: float
     lambda1_hat: float
     history: list = field(default_factory=list)
+    lambda1_hint: float = 0.0  # the λ₁ upper estimate the main phase sizes its SVRG step with
 
 
 def _history(rep):
@@ -556,7 +557,7 @@ def tune_shift(x: DeviceMatrix, delta: float, cfg: SIConfig) -> ShiftState:
     rc = x.ctx.lib.gaplra_tune_shift(x.ctx.h, x.h, delta, C.byref(cfg.native()), C.byref(sc), C.byref(rep))
     x.ctx.check(rc, _history(rep))
     h = _history(rep)
-    return ShiftState(rep.lambda_, h[-1][1] if h else float("nan"), rep.lambda1_hat, h)
+    return ShiftState(rep.lambda_, h[-1][1] if h else float("nan"), rep.lambda1_hat, h, rep.lambda1_hint)
 
 
 def restricted_projection(x: DeviceMatrix, s: np.ndarray, k: int):
@@ -580,6 +581,7 @@ class ShiftInvertResult:
     outer_cap: int
     ledger: dict
     ms: dict
+    lambda1_hint: float = 0.0  # step-size hint used by the subspace phase (pass it back with an explicit lam)
 
 
 def shift_invert(x: DeviceMatrix, cfg: SIConfig) -> ShiftInvertResult:
@@ -594,4 +596,4 @@ def shift_invert(x: DeviceMatrix, cfg: SIConfig) -> ShiftInvertResult:
     return ShiftInvertResult(w, ritz, s, rep.lambda_, rep.lambda1_hat, _history(rep), rep.outer_iterations,
                              rep.outer_cap, rep.ledger.as_dict(),
                              {"tune": rep.ms_tune, "subspace": rep.ms_subspace,
-                              "rayleigh_ritz": rep.ms_rayleigh_ritz, "total": rep.ms_total})
+                              "rayleigh_ritz": rep.ms_rayleigh_ritz, "total": rep.ms_total}, rep.lambda1_hint)
