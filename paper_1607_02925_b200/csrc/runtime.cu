@@ -183,6 +183,8 @@ struct Context {
   DBuf<int32_t> idx, idx2;  // index streams of even / odd epochs
   DBuf<double> tmat2;        // slab of odd epochs (tmat: even)
   DBuf<unsigned int> rej, rej2;
+  DBuf<double> xgs;      // L2-exchange chains (EpochConfig::xg): partial slots
+  DBuf<unsigned> xgc;    //   and their arrival counters
   DBuf<double> spd;  // blocked sparse epoch: b, u
   DBuf<int> spi;     // blocked sparse epoch: row lists, pairs, counters
   // Side stream for the next epoch's W-independent precompute (index stream +
@@ -486,6 +488,10 @@ void epoch_run_dev(Context& c, Matrix& X, int p, double* W, const double* C, con
     const EpochConfig& cfg = pre.cfg;
     a.slab = pre.slab;
     a.zcol = c.zcol.ensure(static_cast<size_t>(X.ld));
+    if (cfg.xg) {
+      a.xg_slot = c.xgs.ensure(xg_slot_elems(cfg));
+      a.xg_count = c.xgc.ensure(xg_count_elems(cfg));
+    }
     {
       Prof prof(c, kProfBlockU, 16.0 * m * p, 2.0 * kEpochBlock * m * p);
       launch_block_u(a, cfg, c.st);

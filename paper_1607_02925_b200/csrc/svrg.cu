@@ -96,6 +96,34 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
+// ---- global-memory (L2) all-reduce among the CTAs of a column group (XG
+// chains: no thread-block cluster, so a group may span any CTAs; C5's 8 groups
+// of 16 CTAs exceed the 7 sixteen-CTA clusters that fit at once).  Block u's
+// partials go to slot u % kXgSlots; each peer publishes with a release and one
+// counter increment; a reader waits for G * (uses of the slot) arrivals and
+// reads the partials through L2 (ld.cg: the slot's previous use may sit in L1).
+// Slot reuse: a CTA publishes block u + 1 only after it received every peer's
+// block u - 1, so no peer still reads slot u + 1 - kXgSlots >= 4 blocks back.
+constexpr int kXgSlots = 8;
+__device__ __forceinline__ void xg_publish(unsigned* count) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(count) : "memory");
+}
+__device__ __forceinline__ void xg_wait(const unsigned* count, unsigned need) {
+  unsigned v;
+  for (;;) {
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(count) : "memory");
+    if (v >= need) break;
+  }
+}
+__device__ __forceinline__ double ld_cg(const double* p) {
+  double v;
+  asm volatile("ld.global.cg.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_cg(double* p, double v) {
+  asm volatile("st.global.cg.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                : "+d"(c0), "+d"(c1)
@@ -970,6 +998,11 @@ int shrink_pc(int pc) { return pc == 8 ? 6 : (pc == 6 ? 4 : std::max(1, pc - 1))
 
 }  // namespace
 
+size_t xg_slot_elems(const EpochConfig& cfg) {
+  return cfg.xg ? static_cast<size_t>(kXgSlots) * cfg.groups * cfg.cluster * kBlock * cfg.pc : 0;
+}
+size_t xg_count_elems(const EpochConfig& cfg) { return cfg.xg ? static_cast<size_t>(kXgSlots) * cfg.groups : 0; }
+
 int64_t epoch_slab_len(const EpochConfig& cfg) {
   return 2 * kBlock * kBlock + static_cast<int64_t>(kBlock) * cfg.pc * cfg.groups;
 }
@@ -1098,18 +1131,23 @@ __host__ __device__ constexpr int v3_block(int pc) { return RR ? kV3RRThreads : 
 inline bool v3_supports(int pc, int rows) { return pc <= 3 && (rows <= 256 || (rows <= 512 && pc == 1)); }
 
 // H: 256-row halves per row thread (rows 2·tid + {0,1} + 256·h): 256·H rows per CTA.
-template <int PC, int B, int H = 1, bool RR = false>
+// XG: plain CTAs (gridDim.x of them) exchanging the partials through L2
+// instead of a DSMEM cluster, so the rows spread over more SMs than a cluster
+// holds (p = 1: 128 rows per CTA, 32 CTAs at C2, 64 at C5).
+template <int PC, int B, int H = 1, bool RR = false, bool XG = false>
 __global__ void __launch_bounds__(v3_block<RR>(PC), 1) k_svrg_chain_v3(EpochArgs a) {
   static_assert(B == 16, "lane permutation j = i ^ (lane >> 1) covers 16 slices");
   static_assert(!RR || PC == 1, "RR layout: PC = 1");
+  static_assert(!XG || (PC == 1 && RR), "L2 exchange: the p = 1 RR layout");
   constexpr int NPROD = RR ? 4 : v3_producers(PC);
   constexpr bool XREG = PC == 1 && H == 1;  // update from the products' registers (else re-read the stage)
   extern __shared__ __align__(128) double sm[];
-  cg::cluster_group cluster = cg::this_cluster();
-  const int G = static_cast<int>(cluster.num_blocks());
-  const int g = static_cast<int>(cluster.block_rank());
+  const int G = XG ? static_cast<int>(gridDim.x) : static_cast<int>(cg::this_cluster().num_blocks());
+  const int g = XG ? static_cast<int>(blockIdx.x) : static_cast<int>(cg::this_cluster().block_rank());
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int NV = B * PC;
+  double* xg_slots = XG ? a.xg_slot : nullptr;  // [kXgSlots][G][NV]
+  unsigned* xg_cnt = XG ? a.xg_count : nullptr;
   constexpr int NRD = v3_reducers(PC);
   constexpr int EPW = (NV + NRD - 1) / NRD;  // entries per reducer warp
   static_assert(EPW <= 32, "one entry per reducer lane");
@@ -1148,7 +1186,10 @@ __global__ void __launch_bounds__(v3_block<RR>(PC), 1) k_svrg_chain_v3(EpochArgs
     for (int q = 0; q < kRecvSlots; ++q) mbar_init(&rbar[q], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  cluster.sync();
+  if constexpr (XG)
+    __syncthreads();
+  else
+    cg::this_cluster().sync();
   // GAPLRA_EPOCH_TIMING: cycles per block; rows (tid 0) in slots 0..5, reducer (lane 0) in 6..7
   long long tacc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   long long tp;
@@ -1178,10 +1219,18 @@ __global__ void __launch_bounds__(v3_block<RR>(PC), 1) k_svrg_chain_v3(EpochArgs
         asm volatile("bar.sync 6, %0;" ::"n"(32 * (kV3Rows + 1)) : "memory");
       else
         asm volatile("bar.sync 5, %0;" ::"n"(32 * (kV3Rows + 1)) : "memory");
-      if (lane < G) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+      if (!XG && lane < G) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
       __syncwarp();
       const double* rb = red + (u & 1) * kV3Rows * NV;
       double* ov = outv + (u & 1) * NV;
+      if constexpr (XG) {  // partial -> L2 slot, then one release-increment
+        double* dst = xg_slots + (static_cast<size_t>(u % kXgSlots) * G + g) * NV;
+        for (int e = lane; e < NV; e += 32) st_cg(dst + e, (rb[e] + rb[NV + e]) + (rb[2 * NV + e] + rb[3 * NV + e]));
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) xg_publish(xg_cnt + u % kXgSlots);
+        continue;
+      }
       for (int e = lane; e < NV; e += 32) ov[e] = (rb[e] + rb[NV + e]) + (rb[2 * NV + e] + rb[3 * NV + e]);
       fence_proxy_async();
       __syncwarp();
@@ -1192,7 +1241,7 @@ __global__ void __launch_bounds__(v3_block<RR>(PC), 1) k_svrg_chain_v3(EpochArgs
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
       }
     }
-    if (lane < G) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    if (!XG && lane < G) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   } else if (warp >= kV3Rows) {  // ------------------------------------------ reducers
     const int rw = warp - kV3Rows;
     const int me = rw * EPW + lane;  // this lane's entry
@@ -1204,7 +1253,7 @@ __global__ void __launch_bounds__(v3_block<RR>(PC), 1) k_svrg_chain_v3(EpochArgs
         __syncwarp();
     };
     auto arm = [&](int u) {
-      if (rw == 0 && lane == 0)
+      if (!XG && rw == 0 && lane == 0)
         mbar_expect_tx(&rbar[u & (kRecvSlots - 1)], static_cast<uint32_t>(G * NV * 8));  // full vectors
     };
     if (nb > 0) {
@@ -1223,10 +1272,30 @@ __global__ void __launch_bounds__(v3_block<RR>(PC), 1) k_svrg_chain_v3(EpochArgs
       if (more) arm(t + 1);
       const int par = t & (kRecvSlots - 1);
       tick(7);
-      mbar_wait(&rbar[par], static_cast<uint32_t>((t >> 2) & 1));
-      tick(6);
       const int nv = bt_of(t) * PC;
-      if (mine) {
+      if constexpr (XG) {
+        // NV = 16 entries; lane e and e + 16 split the peers (q mod 4 in {0,1} / {2,3}),
+        // (s0 + s1) + (s2 + s3) in the same order as the DSMEM form
+        if (lane == 0) xg_wait(xg_cnt + t % kXgSlots, static_cast<unsigned>(G) * (t / kXgSlots + 1));
+        __syncwarp();
+        tick(6);
+        const int e = lane & 15, hq = (lane >> 4) * 2;
+        const double* sl = xg_slots + static_cast<size_t>(t % kXgSlots) * G * NV + e;
+        double sa = 0.0, sb = 0.0;
+#pragma unroll 4
+        for (int q = 0; q < G; q += 4) {
+          sa += ld_cg(sl + (q + hq) * NV);
+          sb += ld_cg(sl + (q + hq + 1) * NV);
+        }
+        double sv = sa + sb;
+        const double other = __shfl_down_sync(0xffffffffu, sv, 16);
+        if (lane < 16) Ahat[e] = e < nv ? sv + other : 0.0;
+        __syncwarp();
+      } else {
+        mbar_wait(&rbar[par], static_cast<uint32_t>((t >> 2) & 1));
+        tick(6);
+      }
+      if (!XG && mine) {
         const int e = me;
         double s = 0.0;
         if (e < nv) {
@@ -1468,7 +1537,7 @@ __global__ void __launch_bounds__(v3_block<RR>(PC), 1) k_svrg_chain_v3(EpochArgs
           }
         }
   }
-  cluster.sync();
+  if constexpr (!XG) cg::this_cluster().sync();
 }
 
 // ---------------------------------------------------------------------------
@@ -1484,14 +1553,15 @@ __global__ void __launch_bounds__(v3_block<RR>(PC), 1) k_svrg_chain_v3(EpochArgs
 //             the registers
 // Slice pitch RP ≡ 4 (mod 16) doubles: the update's LDS.64 B fragments and the
 // products' LDS.128 (rows 2tq, 2tq+1, slices permuted 0 2 1 3 4 6 5 7) are
-// bank-conflict free; coef is stored [slice][12].  Warps: 4 rows (64 rows
-// each), 4 reducers (one Â / coef entry per lane), 1 pusher (sums the row
+// bank-conflict free; coef is stored [slice][12].  Warps: 8 rows (ROWS / 8
+// rows each), 4 reducers (one Â / coef entry per lane), 1 pusher (sums the row
 // warps' partials, bulk-copies Â_{t+1} to the 16 peers), 2 producers.
+// ROWS = 256 (C2, C3) or 512 (C5: d = 8192 on 16-CTA clusters; a 512-row
+// stage is 71 KB, so the ring has 2 stages next to the 64 KB receive slots).
 // ---------------------------------------------------------------------------
 namespace v4 {
 constexpr int PC = 8, B = 16, NV = B * PC;
 constexpr int kRows = 8, kRed = 4, kProd = 2;
-constexpr int kRW = 256 / kRows, kTiles = kRW / 8;  // rows and 8-row tiles per row warp
 constexpr int kThreads = 32 * (kRows + kRed + 1 + kProd);
 constexpr int CP = 12;  // coef pitch (doubles)
 
@@ -1499,15 +1569,15 @@ struct Smem {
   int rp, stages;
   size_t stage_len, off_recv, off_red, off_outv, off_cf, off_ahat, off_pre, off_bar, total;
 };
-__host__ __device__ inline Smem smem(int rows, int stages) {
+__host__ __device__ inline int span(int rows) { return rows <= 256 ? 256 : 512; }
+__host__ __device__ inline Smem smem(int rows, int stages, bool xg = false) {
   Smem L;
-  (void)rows;  // the 4 row warps always span 256 rows (pad rows are zero)
-  L.rp = 256 + 4;
+  L.rp = span(rows) + 4;  // the 8 row warps always span 256 or 512 rows (pad rows are zero)
   L.stages = stages;
   L.stage_len = static_cast<size_t>(B) * L.rp + 2 * B * B + B * PC;
   size_t o = L.stage_len * stages;
   L.off_recv = o;
-  o += static_cast<size_t>(kRecvSlots) * kMaxCluster * NV;
+  if (!xg) o += static_cast<size_t>(kRecvSlots) * kMaxCluster * NV;  // XG: partials arrive through L2
   L.off_red = o;
   o += 2 * kRows * NV;
   L.off_outv = o;
@@ -1525,19 +1595,23 @@ __host__ __device__ inline Smem smem(int rows, int stages) {
 }
 }  // namespace v4
 
+template <int ROWS, bool XG>
 __global__ void __launch_bounds__(v4::kThreads, 1) k_svrg_chain_v4(EpochArgs a) {
   using namespace v4;
+  constexpr int kRW = ROWS / kRows, kTiles = kRW / 8;  // rows and 8-row tiles per row warp
   extern __shared__ __align__(128) double sm[];
-  cg::cluster_group cluster = cg::this_cluster();
-  const int G = static_cast<int>(cluster.num_blocks());
-  const int g = static_cast<int>(cluster.block_rank());
+  // peers: the cluster (DSMEM exchange) or, XG, the gridDim.x plain CTAs of this group (L2 exchange)
+  const int G = XG ? static_cast<int>(gridDim.x) : static_cast<int>(cg::this_cluster().num_blocks());
+  const int g = XG ? static_cast<int>(blockIdx.x) : static_cast<int>(cg::this_cluster().block_rank());
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int gq = lane >> 2, tq = lane & 3;
   const int grp = blockIdx.y;
   const int c0 = grp * PC;
   const int pc = min(PC, a.p - c0);
-  const Smem L = smem(a.rows_per_cta, a.stages);
+  const Smem L = smem(ROWS, a.stages, XG);
   const int S = L.stages, RP = L.rp;
+  double* xg_slots = XG ? a.xg_slot + static_cast<size_t>(blockIdx.y) * kXgSlots * G * NV : nullptr;  // [slot][G][NV]
+  unsigned* xg_cnt = XG ? a.xg_count + static_cast<size_t>(blockIdx.y) * kXgSlots : nullptr;
   const int r0 = g * a.rows_per_cta;
   const int rc = max(0, min(a.rows_per_cta, a.d_pad - r0));
   double* recv = sm + L.off_recv;  // [kRecvSlots][kMaxCluster][NV]
@@ -1567,7 +1641,10 @@ __global__ void __launch_bounds__(v4::kThreads, 1) k_svrg_chain_v4(EpochArgs a) 
     for (int q = 0; q < kRecvSlots; ++q) mbar_init(&rbar[q], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  cluster.sync();
+  if constexpr (XG)
+    __syncthreads();
+  else
+    cg::this_cluster().sync();
   // GAPLRA_EPOCH_TIMING: cycles per block; rows (tid 0): 0 wait stage, 1 products,
   // 2 wait coef, 3 update; reducer (warp 4 lane 0): 4 wait Â, 5 reduce + coef,
   // 6 pre; pusher (lane 0): 7 wait red + push
@@ -1602,10 +1679,25 @@ __global__ void __launch_bounds__(v4::kThreads, 1) k_svrg_chain_v4(EpochArgs a) 
         asm volatile("bar.sync 6, %0;" ::"n"(32 * (kRows + 1)) : "memory");
       else
         asm volatile("bar.sync 5, %0;" ::"n"(32 * (kRows + 1)) : "memory");
-      if (lane < G) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+      if (!XG && lane < G) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
       __syncwarp();
       const double* rb = red + (u & 1) * kRows * NV;
       double* ov = outv + (u & 1) * NV;
+      if constexpr (XG) {  // partial -> L2 slot, then one release-increment
+        double* dst = xg_slots + (static_cast<size_t>(u % kXgSlots) * G + g) * NV;
+#pragma unroll
+        for (int q = 0; q < NV / 32; ++q) {
+          const int e = q * 32 + lane;
+          double sum = 0.0;
+#pragma unroll
+          for (int w = 0; w < kRows; w += 2) sum += rb[w * NV + e] + rb[(w + 1) * NV + e];
+          st_cg(dst + e, sum);
+        }
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) xg_publish(xg_cnt + u % kXgSlots);
+        continue;
+      }
 #pragma unroll
       for (int q = 0; q < NV / 32; ++q) {
         const int e = q * 32 + lane;
@@ -1623,7 +1715,7 @@ __global__ void __launch_bounds__(v4::kThreads, 1) k_svrg_chain_v4(EpochArgs a) 
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
       }
     }
-    if (lane < G) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    if (!XG && lane < G) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     tick(7);
     if (a.dbg && lane == 0) a.dbg[(blockIdx.y * gridDim.x + blockIdx.x) * 8 + 7] = tacc[7];
   } else if (warp >= kRows) {  // --------------------------------------------- reducers
@@ -1632,7 +1724,7 @@ __global__ void __launch_bounds__(v4::kThreads, 1) k_svrg_chain_v4(EpochArgs a) 
     const int j = e / PC, c = e - (e / PC) * PC;
     auto red_sync = []() { asm volatile("bar.sync 4, %0;" ::"n"(32 * kRed) : "memory"); };
     auto arm = [&](int u) {
-      if (rw == 0 && lane == 0)
+      if (!XG && rw == 0 && lane == 0)
         mbar_expect_tx(&rbar[u & (kRecvSlots - 1)], static_cast<uint32_t>(G * NV * 8));
     };
     if (nb > 0) {
@@ -1650,18 +1742,35 @@ __global__ void __launch_bounds__(v4::kThreads, 1) k_svrg_chain_v4(EpochArgs a) 
       if (more) arm(t + 1);
       const int par = t & (kRecvSlots - 1);
       tick(6);
-      mbar_wait(&rbar[par], static_cast<uint32_t>((t >> 2) & 1));
+      if constexpr (XG) {
+        if (rw == 0 && lane == 0) xg_wait(xg_cnt + t % kXgSlots, static_cast<unsigned>(G) * (t / kXgSlots + 1));
+        red_sync();  // every peer's partial of block t is in L2
+      } else {
+        mbar_wait(&rbar[par], static_cast<uint32_t>((t >> 2) & 1));
+      }
       tick(4);
       double sacc = 0.0;
       if (e < bt_of(t) * PC) {
-        const double* sl = recv + par * kMaxCluster * NV + e;
         double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        if constexpr (XG) {
+          const double* sl = xg_slots + static_cast<size_t>(t % kXgSlots) * G * NV + e;
+          // all G loads in flight (L2 latency, not a loop-carried chain, sets the cost)
+#pragma unroll 4
+          for (int q = 0; q < G; q += 4) {
+            s0 += ld_cg(sl + q * NV);
+            s1 += ld_cg(sl + (q + 1) * NV);
+            s2 += ld_cg(sl + (q + 2) * NV);
+            s3 += ld_cg(sl + (q + 3) * NV);
+          }
+        } else {
+          const double* sl = recv + par * kMaxCluster * NV + e;
 #pragma unroll 1
-        for (int q = 0; q < G; q += 4) {
-          s0 += sl[q * NV];
-          s1 += sl[(q + 1) * NV];
-          s2 += sl[(q + 2) * NV];
-          s3 += sl[(q + 3) * NV];
+          for (int q = 0; q < G; q += 4) {
+            s0 += sl[q * NV];
+            s1 += sl[(q + 1) * NV];
+            s2 += sl[(q + 2) * NV];
+            s3 += sl[(q + 3) * NV];
+          }
         }
         sacc = (s0 + s1) + (s2 + s3);
       }
@@ -1772,15 +1881,30 @@ __global__ void __launch_bounds__(v4::kThreads, 1) k_svrg_chain_v4(EpochArgs a) 
       double af[4];
 #pragma unroll
       for (int ks = 0; ks < 4; ++ks) af[ks] = cf[(4 * ks + tq) * CP + gq];
-      double bx[4][kTiles];
+      if constexpr (kTiles <= 4) {
+        double bx[4][kTiles];
 #pragma unroll
-      for (int ks = 0; ks < 4; ++ks)
+        for (int ks = 0; ks < 4; ++ks)
 #pragma unroll
-        for (int tl = 0; tl < kTiles; ++tl) bx[ks][tl] = xb[(4 * ks + tq) * RP + rw0 + 8 * tl + gq];
+          for (int tl = 0; tl < kTiles; ++tl) bx[ks][tl] = xb[(4 * ks + tq) * RP + rw0 + 8 * tl + gq];
 #pragma unroll
-      for (int ks = 0; ks < 4; ++ks)
+        for (int ks = 0; ks < 4; ++ks)
 #pragma unroll
-        for (int tl = 0; tl < kTiles; ++tl) dmma(v[tl][0], v[tl][1], af[ks], bx[ks][tl]);
+          for (int tl = 0; tl < kTiles; ++tl) dmma(v[tl][0], v[tl][1], af[ks], bx[ks][tl]);
+      } else {  // 512 rows: two k-steps of B fragments in flight (register budget of 480 threads)
+#pragma unroll
+        for (int k2 = 0; k2 < 4; k2 += 2) {
+          double bx[2][kTiles];
+#pragma unroll
+          for (int ks = 0; ks < 2; ++ks)
+#pragma unroll
+            for (int tl = 0; tl < kTiles; ++tl) bx[ks][tl] = xb[(4 * (k2 + ks) + tq) * RP + rw0 + 8 * tl + gq];
+#pragma unroll
+          for (int ks = 0; ks < 2; ++ks)
+#pragma unroll
+            for (int tl = 0; tl < kTiles; ++tl) dmma(v[tl][0], v[tl][1], af[k2 + ks], bx[ks][tl]);
+        }
+      }
 #pragma unroll
       for (int tl = 0; tl < kTiles; ++tl) {
         v[tl][0] *= rn;
@@ -1830,7 +1954,7 @@ __global__ void __launch_bounds__(v4::kThreads, 1) k_svrg_chain_v4(EpochArgs a) 
           }
         }
   }
-  cluster.sync();
+  if constexpr (!XG) cg::this_cluster().sync();  // no CTA leaves while a peer may still copy into it
 }
 
 // Clusters of `cluster` one-SM CTAs that can be resident at once (a cluster
@@ -1896,7 +2020,7 @@ EpochConfig choose_epoch_config(int d_pad, int p) {
   static const int env_pc = getenv("GAPLRA_CHAIN_PC") ? atoi(getenv("GAPLRA_CHAIN_PC")) : 0;
   // (d <= 1024 keeps v3: with <= 128 rows per CTA half of v4's row warps idle;
   // C1 measured 0.31 s with v4 against 0.28 s)
-  if (env_v4 && env_pc == 0 && p >= 4 && d_pad > 1024 && d_pad <= 16 * 256) {
+  if (env_v4 && env_pc == 0 && p >= 4 && d_pad > 1024 && d_pad <= 16 * 512) {
     EpochConfig cfg;
     cfg.b = kBlock;
     cfg.cluster = d_pad <= 8 * 256 ? 8 : 16;
@@ -1906,7 +2030,39 @@ EpochConfig choose_epoch_config(int d_pad, int p) {
     cfg.stages = 3;
     while (cfg.stages > 2 && v4::smem(cfg.rows_per_cta, cfg.stages).total > 227 * 1024) --cfg.stages;
     cfg.smem = v4::smem(cfg.rows_per_cta, cfg.stages).total;
-    if (cfg.groups <= max_active_clusters(cfg.cluster)) return cfg;
+    // more groups than resident clusters (C5: 8 groups of 16 CTAs, 7 sixteen-CTA
+    // clusters fit): plain CTAs exchanging through L2, one wave on 128 SMs.
+    // GAPLRA_CHAIN_XG=0 never, 2 always (where the CTAs fit one wave)
+    static const int env_xg = getenv("GAPLRA_CHAIN_XG") ? atoi(getenv("GAPLRA_CHAIN_XG")) : 1;
+    if (cfg.groups <= max_active_clusters(cfg.cluster) && env_xg != 2) return cfg;
+    if (env_xg && cfg.groups * cfg.cluster <= sm_count_dev()) {
+      cfg.xg = 1;
+      cfg.stages = 3;
+      while (cfg.stages > 2 && v4::smem(cfg.rows_per_cta, cfg.stages, true).total > 227 * 1024) --cfg.stages;
+      cfg.smem = v4::smem(cfg.rows_per_cta, cfg.stages, true).total;
+      return cfg;
+    }
+  }
+  // p = 1, 1024 < d <= 8192: the rows spread over d / 128 plain CTAs that
+  // exchange through L2 (C2 32, C3 16, C5 64 SMs instead of one cluster of
+  // 8 / 16, whose TMA feed capped the epoch).  GAPLRA_P1_XG=0 keeps the
+  // cluster layout; GAPLRA_P1_XG_ROWS sets the rows per CTA.
+  static const int env_xg1 = getenv("GAPLRA_P1_XG") ? atoi(getenv("GAPLRA_P1_XG")) : 1;
+  static const int env_xg_rows = getenv("GAPLRA_P1_XG_ROWS") ? atoi(getenv("GAPLRA_P1_XG_ROWS")) : 128;
+  if (p == 1 && env_xg1 && env_pc == 0 && d_pad > 1024 && d_pad <= 8192) {
+    EpochConfig cfg;
+    cfg.b = kBlock;
+    cfg.pc = 1;
+    cfg.groups = 1;
+    cfg.xg = 1;
+    const int want = std::max(16, std::min(256, env_xg_rows));
+    cfg.cluster = static_cast<int>(ceil_div(ceil_div(d_pad, want), 4) * 4);  // the peer sum runs 4 at a time
+    cfg.rows_per_cta = static_cast<int>(ceil_div(ceil_div(d_pad, cfg.cluster), 4) * 4);
+    if (cfg.cluster <= sm_count_dev()) {
+      cfg.stages = 4;
+      cfg.smem = chain_smem<1, kBlock, true>(cfg.rows_per_cta, cfg.stages).total;
+      return cfg;
+    }
   }
   const EpochConfig c16 = make(16), c8 = make(8);
   auto v3_ok = [](const EpochConfig& c) { return v3_supports(c.pc, c.rows_per_cta); };
@@ -1943,17 +2099,28 @@ void launch_chain_pc(const EpochArgs& a, const EpochConfig& cfg, cudaStream_t st
   }
   int stages = cfg.stages;
   size_t smem = cfg.smem;
-  // the DMMA chain v4 at PC = 8 (rows <= 256 per CTA); GAPLRA_CHAIN_MODE=4 forces it
-  const bool use_v4 = PC == 8 && cfg.rows_per_cta <= 256 && (env_mode == 0 || env_mode == 4);
+  // the DMMA chain v4 at PC = 8 (rows <= 512 per CTA); GAPLRA_CHAIN_MODE=4 forces it
+  const bool use_v4 = PC == 8 && cfg.rows_per_cta <= 512 && (env_mode == 0 || env_mode == 4);
+  const bool xg = cfg.xg != 0;
   if (use_v4) {
     stages = 2;
     for (int sN = 4; sN > 2; --sN)
-      if (v4::smem(cfg.rows_per_cta, sN).total <= 227 * 1024) {
+      if (v4::smem(cfg.rows_per_cta, sN, xg).total <= 227 * 1024) {
         stages = sN;
         break;
       }
-    smem = v4::smem(cfg.rows_per_cta, stages).total;
-    kern = k_svrg_chain_v4;
+    smem = v4::smem(cfg.rows_per_cta, stages, xg).total;
+    if (xg)
+      kern = cfg.rows_per_cta <= 256 ? k_svrg_chain_v4<256, true> : k_svrg_chain_v4<512, true>;
+    else
+      kern = cfg.rows_per_cta <= 256 ? k_svrg_chain_v4<256, false> : k_svrg_chain_v4<512, false>;
+  } else if (xg) {
+    if constexpr (PC == 1) {
+      if (!v3 || cfg.rows_per_cta > 256) throw Error(kContractViolation, "epoch: p = 1 L2-exchange layout needs v3 RR");
+      kern = k_svrg_chain_v3<1, kBlock, 1, true, true>;
+    } else {
+      throw Error(kContractViolation, "epoch: L2-exchange layout needs the v4 chain or p = 1");
+    }
   }
   if (v3 && !use_v4) {  // pitch ≡ 0 (mod 16) layout; up to GAPLRA_CHAIN_STAGES (<= 8) stages as fit
     static const int max_st = getenv("GAPLRA_CHAIN_STAGES") ? std::min(8, atoi(getenv("GAPLRA_CHAIN_STAGES"))) : 4;
@@ -1966,11 +2133,14 @@ void launch_chain_pc(const EpochArgs& a, const EpochConfig& cfg, cudaStream_t st
     smem = chain_smem<PC, kBlock, true>(cfg.rows_per_cta, stages).total;
   }
   GAPLRA_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-  if (cfg.cluster > 8) GAPLRA_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  if (cfg.cluster > 8 && !xg)
+    GAPLRA_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   cudaLaunchConfig_t lc = {};
   lc.gridDim = dim3(cfg.cluster, cfg.groups, 1);
   bool rr = false;
-  if constexpr (PC == 1) rr = kern == k_svrg_chain_v3<1, kBlock, 1, true> || kern == k_svrg_chain_v3<1, kBlock, 2, true>;
+  if constexpr (PC == 1)
+    rr = kern == k_svrg_chain_v3<1, kBlock, 1, true> || kern == k_svrg_chain_v3<1, kBlock, 2, true> ||
+         kern == k_svrg_chain_v3<1, kBlock, 1, true, true>;
   lc.blockDim = dim3(use_v4 ? v4::kThreads
                             : (rr ? kV3RRThreads : (v3 ? v3_threads(PC) : kChainThreads + 32 * kChainProducers)),
                      1, 1);
@@ -1982,7 +2152,11 @@ void launch_chain_pc(const EpochArgs& a, const EpochConfig& cfg, cudaStream_t st
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   lc.attrs = attr;
-  lc.numAttrs = 1;
+  lc.numAttrs = xg ? 0 : 1;  // XG: plain CTAs (all co-resident: groups x cluster <= SMs, one CTA per SM)
+  if (xg) {
+    if (!a.xg_slot || !a.xg_count) throw Error(kContractViolation, "epoch: XG layout without exchange buffers");
+    GAPLRA_CUDA_CHECK(cudaMemsetAsync(a.xg_count, 0, xg_count_elems(cfg) * sizeof(unsigned), st));
+  }
   EpochArgs args = a;
   args.rows_per_cta = cfg.rows_per_cta;
   args.stages = stages;

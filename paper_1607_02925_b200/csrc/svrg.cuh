@@ -27,6 +27,9 @@ struct EpochArgs {
   long long* dbg;  // optional per-CTA phase cycle counters (8 per CTA)
   int skip;        // debug ablation mask: 1 coef, 2 dots, 4 update (results invalid)
   int prefetch;    // chain producers: L2-prefetch the slices this many blocks ahead (0: off)
+  // XG chains (cfg.xg): the group's all-reduce goes through L2 instead of DSMEM
+  double* xg_slot;   // [kXgSlots][groups][cluster][NV] partials
+  unsigned* xg_count;  // [groups][kXgSlots] arrivals, zeroed before each launch
 };
 
 struct SparseEpochArgs {
@@ -47,7 +50,11 @@ struct SparseEpochArgs {
 struct EpochConfig {
   int cluster, pc, b, rows_per_cta, groups, stages;
   size_t smem;
+  int xg = 0;  // 1: the `cluster` CTAs of a group are plain CTAs exchanging through L2 (no cluster launch)
 };
+// XG exchange buffers of an epoch layout (doubles / counters); 0 when !cfg.xg
+size_t xg_slot_elems(const EpochConfig& cfg);
+size_t xg_count_elems(const EpochConfig& cfg);
 
 EpochConfig choose_epoch_config(int d_pad, int p);
 // doubles of the per-block slabs of an m-step epoch
