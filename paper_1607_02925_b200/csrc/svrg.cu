@@ -102,6 +102,11 @@ __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.
 // partials go to slot u % kXgSlots; each peer publishes with a release and one
 // counter increment; a reader waits for G * (uses of the slot) arrivals and
 // reads the partials through L2 (ld.cg: the slot's previous use may sit in L1).
+// No gpu-scope fence / acquire in the loops: on this part those invalidate L1
+// (CCTL.IVALL), which stalled the row warps' shared-memory traffic (an
+// acquire-spinning reducer made the p = 1 update 4x slower).  The publisher's
+// red.release orders the warp's stores (issued before it, the lanes joined by
+// __syncwarp) ahead of the count; the reader polls relaxed and reads L2 after.
 // Slot reuse: a CTA publishes block u + 1 only after it received every peer's
 // block u - 1, so no peer still reads slot u + 1 - kXgSlots >= 4 blocks back.
 constexpr int kXgSlots = 8;
@@ -111,7 +116,7 @@ __device__ __forceinline__ void xg_publish(unsigned* count) {
 __device__ __forceinline__ void xg_wait(const unsigned* count, unsigned need) {
   unsigned v;
   for (;;) {
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(count) : "memory");
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(count) : "memory");
     if (v >= need) break;
   }
 }
@@ -1226,7 +1231,6 @@ __global__ void __launch_bounds__(v3_block<RR>(PC), 1) k_svrg_chain_v3(EpochArgs
       if constexpr (XG) {  // partial -> L2 slot, then one release-increment
         double* dst = xg_slots + (static_cast<size_t>(u % kXgSlots) * G + g) * NV;
         for (int e = lane; e < NV; e += 32) st_cg(dst + e, (rb[e] + rb[NV + e]) + (rb[2 * NV + e] + rb[3 * NV + e]));
-        __threadfence();
         __syncwarp();
         if (lane == 0) xg_publish(xg_cnt + u % kXgSlots);
         continue;
@@ -1593,12 +1597,81 @@ __host__ __device__ inline Smem smem(int rows, int stages, bool xg = false) {
   L.total = o * sizeof(double);
   return L;
 }
+// 512-row layout (C5, L2 exchange): a block's 16 slices are two half-stages
+// of 8 (33 KB each) in a ring of kHalves, with the slab part (TT | M | U) in
+// its own ring of kSlabs.  The update releases a block's first half after its
+// first two k-steps, so the ring holds blocks t and t + 1 plus one half in
+// flight and the feed overlaps the chain (two 71 KB full stages did not: the
+// rows waited ~2000 cycles per block for the refill).
+constexpr int kHalves = 5, kSlabs = 3, kSlabLen = 2 * B * B + B * PC;
+__host__ __device__ inline Smem smem_half() {
+  Smem L;
+  L.rp = 512 + 4;
+  L.stages = 0;
+  L.stage_len = static_cast<size_t>(B / 2) * L.rp;  // one half-stage
+  size_t o = L.stage_len * kHalves + static_cast<size_t>(kSlabs) * kSlabLen;
+  L.off_recv = o;  // XG only: no receive slots
+  L.off_red = o;
+  o += 2 * kRows * NV;
+  L.off_outv = o;
+  o += 2 * NV;
+  L.off_cf = o;
+  o += 2 * B * CP;
+  L.off_ahat = o;
+  o += NV;
+  L.off_pre = o;
+  o += NV;
+  L.off_bar = o;
+  o += 24;  // fullH[5] emptyH[5] fullS[3] emptyS[3]
+  L.total = o * sizeof(double);
+  return L;
+}
 }  // namespace v4
+
+// Producer of the half-stage ring: warp h streams half h (slices 8h .. 8h+7)
+// of every block; warp 0 also the block's slab part.
+__device__ __forceinline__ void chain_produce_half(const EpochArgs& a, int h, int lane, int nb, int last_bt, int rc,
+                                                   int r0, int RP, int grp, double* halves, size_t half_len,
+                                                   double* slabs, uint64_t* fullH, uint64_t* emptyH, uint64_t* fullS,
+                                                   uint64_t* emptyS) {
+  using namespace v4;
+  auto col_of = [&](int u) {
+    const int bu = u == nb - 1 ? last_bt : B;
+    return u < nb && lane < B / 2 && 8 * h + lane < bu ? __ldg(a.idx + static_cast<int64_t>(u) * B + 8 * h + lane) : 0;
+  };
+  int ncol = col_of(0);
+  for (int t = 0; t < nb; ++t) {
+    const int col = ncol;
+    ncol = col_of(t + 1);
+    const int k = 2 * t + h, slot = k % kHalves, use = k / kHalves;
+    if (use > 0) mbar_wait_backoff(&emptyH[slot], static_cast<uint32_t>((use - 1) & 1));
+    const int ss = t % kSlabs, su = t / kSlabs;
+    if (h == 0 && su > 0) mbar_wait_backoff(&emptyS[ss], static_cast<uint32_t>((su - 1) & 1));
+    const int bt = t == nb - 1 ? last_bt : B;
+    const int mine = rc > 0 ? max(0, min(B / 2, bt - 8 * h)) : 0;
+    double* dst = halves + static_cast<size_t>(slot) * half_len;
+    if (lane == 0) {
+      fence_proxy_async();
+      mbar_expect_tx(&fullH[slot], static_cast<uint32_t>(mine * rc) * 8u);
+      if (h == 0) mbar_expect_tx(&fullS[ss], static_cast<uint32_t>(kSlabLen) * 8u);
+    }
+    __syncwarp();
+    if (lane < mine) tma_load_1d(dst + lane * RP, a.X + static_cast<int64_t>(col) * a.ldx + r0, rc * 8u, &fullH[slot]);
+    if (h == 0 && lane == 31) {
+      const double* slab = a.slab + static_cast<int64_t>(t) * a.slab_len;
+      double* sd = slabs + static_cast<size_t>(ss) * kSlabLen;
+      tma_load_1d(sd, slab, 2 * B * B * 8u, &fullS[ss]);
+      tma_load_1d(sd + 2 * B * B, slab + 2 * B * B + static_cast<size_t>(grp) * B * PC, B * PC * 8u, &fullS[ss]);
+    }
+  }
+}
 
 template <int ROWS, bool XG>
 __global__ void __launch_bounds__(v4::kThreads, 1) k_svrg_chain_v4(EpochArgs a) {
   using namespace v4;
   constexpr int kRW = ROWS / kRows, kTiles = kRW / 8;  // rows and 8-row tiles per row warp
+  constexpr bool HALF = ROWS > 256;                    // half-stage ring (512 rows, L2 exchange)
+  static_assert(!HALF || XG, "the 512-row layout exchanges through L2");
   extern __shared__ __align__(128) double sm[];
   // peers: the cluster (DSMEM exchange) or, XG, the gridDim.x plain CTAs of this group (L2 exchange)
   const int G = XG ? static_cast<int>(gridDim.x) : static_cast<int>(cg::this_cluster().num_blocks());
@@ -1608,8 +1681,10 @@ __global__ void __launch_bounds__(v4::kThreads, 1) k_svrg_chain_v4(EpochArgs a) 
   const int grp = blockIdx.y;
   const int c0 = grp * PC;
   const int pc = min(PC, a.p - c0);
-  const Smem L = smem(ROWS, a.stages, XG);
+  const Smem L = HALF ? smem_half() : smem(ROWS, a.stages, XG);
   const int S = L.stages, RP = L.rp;
+  double* halves = sm;                                             // HALF: [kHalves][8][RP]
+  double* slabs = sm + L.stage_len * kHalves;                      // HALF: [kSlabs][kSlabLen]
   double* xg_slots = XG ? a.xg_slot + static_cast<size_t>(blockIdx.y) * kXgSlots * G * NV : nullptr;  // [slot][G][NV]
   unsigned* xg_cnt = XG ? a.xg_count + static_cast<size_t>(blockIdx.y) * kXgSlots : nullptr;
   const int r0 = g * a.rows_per_cta;
@@ -1623,7 +1698,14 @@ __global__ void __launch_bounds__(v4::kThreads, 1) k_svrg_chain_v4(EpochArgs a) 
   uint64_t* full = reinterpret_cast<uint64_t*>(sm + L.off_bar);  // [S <= 4]
   uint64_t* empty = full + 4;                                     // [S]
   uint64_t* rbar = full + 8;                                      // [kRecvSlots]
+  uint64_t* fullH = full;                                         // HALF: [kHalves]
+  uint64_t* emptyH = full + kHalves;                              // HALF: [kHalves]
+  uint64_t* fullS = full + 2 * kHalves;                           // HALF: [kSlabs]
+  uint64_t* emptyS = fullS + kSlabs;                              // HALF: [kSlabs]
   auto stage_at = [&](int s_idx) { return sm + static_cast<size_t>(s_idx) * L.stage_len; };
+  auto slab_tt = [&](int t) {  // TT_t (then M_t, U_t)
+    return HALF ? slabs + static_cast<size_t>(t % kSlabs) * kSlabLen : stage_at(t % S) + B * RP;
+  };
   const int nb = static_cast<int>((a.m + B - 1) / B);
   const int last_bt = static_cast<int>(a.m - static_cast<int64_t>(nb - 1) * B);
   auto bt_of = [&](int t) { return t == nb - 1 ? last_bt : B; };
@@ -1634,11 +1716,22 @@ __global__ void __launch_bounds__(v4::kThreads, 1) k_svrg_chain_v4(EpochArgs a) 
   for (size_t e = tid; e < L.off_recv; e += blockDim.x) sm[e] = 0.0;  // pad rows / unwritten slices read as 0
   for (int e = tid; e < 2 * B * CP; e += blockDim.x) cfb[e] = 0.0;
   if (tid == 0) {
-    for (int s = 0; s < S; ++s) {
-      mbar_init(&full[s], kProd);
-      mbar_init(&empty[s], kRows + kRed);
+    if constexpr (HALF) {
+      for (int q = 0; q < kHalves; ++q) {
+        mbar_init(&fullH[q], 1);
+        mbar_init(&emptyH[q], kRows);
+      }
+      for (int q = 0; q < kSlabs; ++q) {
+        mbar_init(&fullS[q], 1);
+        mbar_init(&emptyS[q], kRed);
+      }
+    } else {
+      for (int s = 0; s < S; ++s) {
+        mbar_init(&full[s], kProd);
+        mbar_init(&empty[s], kRows + kRed);
+      }
+      for (int q = 0; q < kRecvSlots; ++q) mbar_init(&rbar[q], 1);
     }
-    for (int q = 0; q < kRecvSlots; ++q) mbar_init(&rbar[q], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if constexpr (XG)
@@ -1666,8 +1759,12 @@ __global__ void __launch_bounds__(v4::kThreads, 1) k_svrg_chain_v4(EpochArgs a) 
   };
 
   if (warp >= kRows + kRed + 1) {  // ------------------------------------------ producers
-    chain_produce<PC, B, kProd>(a, warp - kRows - kRed - 1, lane, nb, last_bt, S, rc, r0, RP, grp, sm,
-                                L.stage_len, full, empty);
+    if constexpr (HALF)
+      chain_produce_half(a, warp - kRows - kRed - 1, lane, nb, last_bt, rc, r0, RP, grp, halves, L.stage_len, slabs,
+                         fullH, emptyH, fullS, emptyS);
+    else
+      chain_produce<PC, B, kProd>(a, warp - kRows - kRed - 1, lane, nb, last_bt, S, rc, r0, RP, grp, sm,
+                                  L.stage_len, full, empty);
   } else if (warp == kRows + kRed) {  // ---------------------------------------- pusher
     // Â_u partials of the 4 row warps -> fixed-order sum -> outv[u & 1] ->
     // one bulk copy per peer (lane q -> peer q).  The rows cannot arrive for
@@ -1693,7 +1790,6 @@ __global__ void __launch_bounds__(v4::kThreads, 1) k_svrg_chain_v4(EpochArgs a) 
           for (int w = 0; w < kRows; w += 2) sum += rb[w * NV + e] + rb[(w + 1) * NV + e];
           st_cg(dst + e, sum);
         }
-        __threadfence();
         __syncwarp();
         if (lane == 0) xg_publish(xg_cnt + u % kXgSlots);
         continue;
@@ -1729,8 +1825,8 @@ __global__ void __launch_bounds__(v4::kThreads, 1) k_svrg_chain_v4(EpochArgs a) 
     };
     if (nb > 0) {
       arm(0);
-      mbar_wait(&full[0], 0);
-      pre[e] = stage_at(0)[B * RP + 2 * B * B + e];
+      mbar_wait(HALF ? &fullS[0] : &full[0], 0);
+      pre[e] = slab_tt(0)[2 * B * B + e];
     }
     int cs = 0;
     uint32_t cph = 0;
@@ -1776,7 +1872,7 @@ __global__ void __launch_bounds__(v4::kThreads, 1) k_svrg_chain_v4(EpochArgs a) 
       }
       Ahat[e] = sacc;
       red_sync();  // Â_t complete
-      const double* TT = stage_at(cs) + B * RP;
+      const double* TT = slab_tt(t);
       double* cf = cfb + (t & 1) * B * CP;
       {
         double s0 = pre[e], s1 = 0.0, s2 = 0.0, s3 = 0.0;
@@ -1795,11 +1891,14 @@ __global__ void __launch_bounds__(v4::kThreads, 1) k_svrg_chain_v4(EpochArgs a) 
         asm volatile("bar.arrive 2, %0;" ::"n"(32 * (kRows + kRed)) : "memory");
       tick(5);
       __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[cs]);  // TT_t was the reducers' last use of stage t
+      if (lane == 0) mbar_arrive(HALF ? &emptyS[t % kSlabs] : &empty[cs]);  // TT_t: the reducers' last use
       if (more) {  // pre_{t+1} = M_{t+1} coef_t + U_{t+1}
         red_sync();  // coef_t complete; Â reads done
-        mbar_wait(&full[ns], nph);
-        const double* M = stage_at(ns) + B * RP + B * B;
+        if constexpr (HALF)
+          mbar_wait(&fullS[(t + 1) % kSlabs], static_cast<uint32_t>(((t + 1) / kSlabs) & 1));
+        else
+          mbar_wait(&full[ns], nph);
+        const double* M = slab_tt(t + 1) + B * B;
         const double* Ub = M + B * B;
         double s0 = Ub[e], s1 = 0.0, s2 = 0.0, s3 = 0.0;
 #pragma unroll
@@ -1839,23 +1938,25 @@ __global__ void __launch_bounds__(v4::kThreads, 1) k_svrg_chain_v4(EpochArgs a) 
       }
       return s;
     };
-    // Âᵀ partial over the warp's 64 rows: 2 slice tiles, K = 16 k-steps
-    auto products = [&](const double* xb, int u_blk) {
+    auto half_ptr = [&](int k) { return halves + static_cast<size_t>(k % kHalves) * L.stage_len; };
+    auto wait_half = [&](int k) { mbar_wait(&fullH[k % kHalves], static_cast<uint32_t>((k / kHalves) & 1)); };
+    // Âᵀ partial over the warp's rows: 2 slice tiles (slices 0-7 at xb0, 8-15 at
+    // xb1), K = the rows; HALF: half kw (then kw + 1) is waited for just before use
+    auto products = [&](const double* xb0, const double* xb1, int u_blk, int kw) {
       double acc[2][2][2];  // [slice tile][chain][elem]
 #pragma unroll
       for (int n2 = 0; n2 < 2; ++n2)
 #pragma unroll
         for (int ch = 0; ch < 2; ++ch) acc[n2][ch][0] = acc[n2][ch][1] = 0.0;
 #pragma unroll
-      for (int tl = 0; tl < kTiles; ++tl) {
-        double2 xv[2];
+      for (int n2 = 0; n2 < 2; ++n2) {
+        if constexpr (HALF) wait_half(kw + n2);
+        const double* xb = n2 ? xb1 : xb0;
 #pragma unroll
-        for (int n2 = 0; n2 < 2; ++n2)
-          xv[n2] = *reinterpret_cast<const double2*>(xb + (8 * n2 + perm) * RP + rw0 + 8 * tl + 2 * tq);
-#pragma unroll
-        for (int n2 = 0; n2 < 2; ++n2) {
-          dmma(acc[n2][tl & 1][0], acc[n2][tl & 1][1], v[tl][0], xv[n2].x);
-          dmma(acc[n2][tl & 1][0], acc[n2][tl & 1][1], v[tl][1], xv[n2].y);
+        for (int tl = 0; tl < kTiles; ++tl) {
+          const double2 xv = *reinterpret_cast<const double2*>(xb + perm * RP + rw0 + 8 * tl + 2 * tq);
+          dmma(acc[n2][tl & 1][0], acc[n2][tl & 1][1], v[tl][0], xv.x);
+          dmma(acc[n2][tl & 1][0], acc[n2][tl & 1][1], v[tl][1], xv.y);
         }
       }
       // C fragment (column gq, slices 8 n2 + perm(2 tq), 8 n2 + perm(2 tq + 1)) -> red(u_blk) in [j PC + c]
@@ -1869,8 +1970,9 @@ __global__ void __launch_bounds__(v4::kThreads, 1) k_svrg_chain_v4(EpochArgs a) 
       }
       bar_red_arrive(u_blk);
     };
-    // Vᵀ = rn (Vᵀ + coefᵀ X_Bᵀ)
-    auto update = [&](const double* xb, int t, double rn) {
+    // Vᵀ = rn (Vᵀ + coefᵀ X_Bᵀ); HALF: each half-stage is released after its two k-steps
+    auto update = [&](const double* xb0, const double* xb1, int t, double rn) {
+      const double* xb = xb0;
       tick(1);
       if (t & 1)
         asm volatile("bar.sync 3, %0;" ::"n"(32 * (kRows + kRed)) : "memory");
@@ -1894,15 +1996,20 @@ __global__ void __launch_bounds__(v4::kThreads, 1) k_svrg_chain_v4(EpochArgs a) 
       } else {  // 512 rows: two k-steps of B fragments in flight (register budget of 480 threads)
 #pragma unroll
         for (int k2 = 0; k2 < 4; k2 += 2) {
+          const double* xh = k2 ? xb1 : xb0;  // slices 4 (k2 + ks) + tq = 8 (k2 / 2) + 4 ks + tq
           double bx[2][kTiles];
 #pragma unroll
           for (int ks = 0; ks < 2; ++ks)
 #pragma unroll
-            for (int tl = 0; tl < kTiles; ++tl) bx[ks][tl] = xb[(4 * (k2 + ks) + tq) * RP + rw0 + 8 * tl + gq];
+            for (int tl = 0; tl < kTiles; ++tl) bx[ks][tl] = xh[(4 * ks + tq) * RP + rw0 + 8 * tl + gq];
 #pragma unroll
           for (int ks = 0; ks < 2; ++ks)
 #pragma unroll
             for (int tl = 0; tl < kTiles; ++tl) dmma(v[tl][0], v[tl][1], af[k2 + ks], bx[ks][tl]);
+          if constexpr (HALF) {  // this half's slices are in registers / consumed
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&emptyH[(2 * t + k2 / 2) % kHalves]);
+          }
         }
       }
 #pragma unroll
@@ -1912,8 +2019,12 @@ __global__ void __launch_bounds__(v4::kThreads, 1) k_svrg_chain_v4(EpochArgs a) 
       }
     };
     if (nb > 0) {  // Â_0 = X_{B_0}ᵀ Ŵ_0, then V_0 = ρ^{b_0} Ŵ_0
-      const int s = wait_stage();
-      products(stage_at(s), 0);
+      if constexpr (HALF) {
+        products(half_ptr(0), half_ptr(1), 0, 0);
+      } else {
+        const int s = wait_stage();
+        products(stage_at(s), stage_at(s) + 8 * RP, 0, 0);
+      }
       double rb0 = 1.0;
       for (int jj = 0; jj < bt_of(0); ++jj) rb0 *= a.rho;
 #pragma unroll
@@ -1928,15 +2039,24 @@ __global__ void __launch_bounds__(v4::kThreads, 1) k_svrg_chain_v4(EpochArgs a) 
       const bool more = t + 1 < nb;
       if (more) {
         tick(3);
-        const int s = wait_stage();
-        tick(0);
-        products(stage_at(s), t + 1);
+        if constexpr (HALF) {
+          tick(0);
+          products(half_ptr(2 * t + 2), half_ptr(2 * t + 3), t + 1, 2 * t + 2);
+        } else {
+          const int s = wait_stage();
+          tick(0);
+          products(stage_at(s), stage_at(s) + 8 * RP, t + 1, 0);
+        }
       }
       const double rn = !more ? 1.0 : (t + 1 == nb - 1 ? rho_last : rho_b);
-      update(stage_at(cs), t, rn);
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[cs]);
-      cs = cs + 1 == S ? 0 : cs + 1;
+      if constexpr (HALF) {
+        update(half_ptr(2 * t), half_ptr(2 * t + 1), t, rn);
+      } else {
+        update(stage_at(cs), stage_at(cs) + 8 * RP, t, rn);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[cs]);
+        cs = cs + 1 == S ? 0 : cs + 1;
+      }
     }
     tick(3);
     if (a.dbg && tid == 0)
@@ -2034,20 +2154,26 @@ EpochConfig choose_epoch_config(int d_pad, int p) {
     // clusters fit): plain CTAs exchanging through L2, one wave on 128 SMs.
     // GAPLRA_CHAIN_XG=0 never, 2 always (where the CTAs fit one wave)
     static const int env_xg = getenv("GAPLRA_CHAIN_XG") ? atoi(getenv("GAPLRA_CHAIN_XG")) : 1;
-    if (cfg.groups <= max_active_clusters(cfg.cluster) && env_xg != 2) return cfg;
-    if (env_xg && cfg.groups * cfg.cluster <= sm_count_dev()) {
+    // (512 rows per CTA always exchange through L2: the half-stage ring and
+    // the 64 KB of DSMEM receive slots do not fit together)
+    if (cfg.groups <= max_active_clusters(cfg.cluster) && env_xg != 2 && cfg.rows_per_cta <= 256) return cfg;
+    if ((env_xg || cfg.rows_per_cta > 256) && cfg.groups * cfg.cluster <= sm_count_dev()) {
       cfg.xg = 1;
       cfg.stages = 3;
       while (cfg.stages > 2 && v4::smem(cfg.rows_per_cta, cfg.stages, true).total > 227 * 1024) --cfg.stages;
-      cfg.smem = v4::smem(cfg.rows_per_cta, cfg.stages, true).total;
+      cfg.smem = cfg.rows_per_cta > 256 ? v4::smem_half().total : v4::smem(cfg.rows_per_cta, cfg.stages, true).total;
       return cfg;
     }
   }
-  // p = 1, 1024 < d <= 8192: the rows spread over d / 128 plain CTAs that
-  // exchange through L2 (C2 32, C3 16, C5 64 SMs instead of one cluster of
-  // 8 / 16, whose TMA feed capped the epoch).  GAPLRA_P1_XG=0 keeps the
-  // cluster layout; GAPLRA_P1_XG_ROWS sets the rows per CTA.
-  static const int env_xg1 = getenv("GAPLRA_P1_XG") ? atoi(getenv("GAPLRA_P1_XG")) : 1;
+  // p = 1, 1024 < d <= 8192, GAPLRA_P1_XG=1 (experiment, off by default): the
+  // rows spread over d / 128 plain CTAs that exchange through L2 (C2 32, C3
+  // 16, C5 64 SMs).  Measured slower than the one-cluster layout (C2 18.0 vs
+  // 8.8 ms, C3 30.4 vs 15.1, C5 267 (197 at 256 rows) vs 143 ms per epoch):
+  // the L2 hop (publisher MEMBAR.GPU ~700 cycles + poll + loads) puts ~2000
+  // cycles per block on the reducer's critical path, where the DSMEM
+  // all-reduce costs ~500 (ncu: profiles/r02_ncu_v3xg.json).  GAPLRA_P1_XG_ROWS
+  // sets the rows per CTA.
+  static const int env_xg1 = getenv("GAPLRA_P1_XG") ? atoi(getenv("GAPLRA_P1_XG")) : 0;
   static const int env_xg_rows = getenv("GAPLRA_P1_XG_ROWS") ? atoi(getenv("GAPLRA_P1_XG_ROWS")) : 128;
   if (p == 1 && env_xg1 && env_pc == 0 && d_pad > 1024 && d_pad <= 8192) {
     EpochConfig cfg;
@@ -2110,10 +2236,13 @@ void launch_chain_pc(const EpochArgs& a, const EpochConfig& cfg, cudaStream_t st
         break;
       }
     smem = v4::smem(cfg.rows_per_cta, stages, xg).total;
-    if (xg)
-      kern = cfg.rows_per_cta <= 256 ? k_svrg_chain_v4<256, true> : k_svrg_chain_v4<512, true>;
-    else
-      kern = cfg.rows_per_cta <= 256 ? k_svrg_chain_v4<256, false> : k_svrg_chain_v4<512, false>;
+    if (cfg.rows_per_cta > 256) {  // half-stage ring, L2 exchange
+      if (!xg) throw Error(kContractViolation, "epoch: 512-row chain layout needs the L2 exchange");
+      smem = v4::smem_half().total;
+      kern = k_svrg_chain_v4<512, true>;
+    } else {
+      kern = xg ? k_svrg_chain_v4<256, true> : k_svrg_chain_v4<256, false>;
+    }
   } else if (xg) {
     if constexpr (PC == 1) {
       if (!v3 || cfg.rows_per_cta > 256) throw Error(kContractViolation, "epoch: p = 1 L2-exchange layout needs v3 RR");
