@@ -191,7 +191,7 @@ struct Context {
   // k_block_prep), run beside the current epoch's chain on the SMs the chain
   // leaves idle.  Events order it against the main stream.
   cudaStream_t aux = nullptr;
-  cudaEvent_t pre_done[2] = {nullptr, nullptr}, chain_done[2] = {nullptr, nullptr};
+  cudaEvent_t pre_done[2] = {nullptr, nullptr}, chain_done[2] = {nullptr, nullptr}, u_done = nullptr;
   cudaStream_t aux_stream() {
     if (!aux) {
       GAPLRA_CUDA_CHECK(cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking));
@@ -199,6 +199,7 @@ struct Context {
         GAPLRA_CUDA_CHECK(cudaEventCreateWithFlags(&pre_done[i], cudaEventDisableTiming));
         GAPLRA_CUDA_CHECK(cudaEventCreateWithFlags(&chain_done[i], cudaEventDisableTiming));
       }
+      GAPLRA_CUDA_CHECK(cudaEventCreateWithFlags(&u_done, cudaEventDisableTiming));
     }
     return aux;
   }
@@ -243,6 +244,7 @@ struct Context {
         cudaEventDestroy(pre_done[i]);
         cudaEventDestroy(chain_done[i]);
       }
+      cudaEventDestroy(u_done);
       cudaStreamDestroy(aux);
     }
     if (own) cudaStreamDestroy(own);
@@ -496,6 +498,7 @@ void epoch_run_dev(Context& c, Matrix& X, int p, double* W, const double* C, con
       Prof prof(c, kProfBlockU, 16.0 * m * p, 2.0 * kEpochBlock * m * p);
       launch_block_u(a, cfg, c.st);
     }
+    if (c.u_done) GAPLRA_CUDA_CHECK(cudaEventRecord(c.u_done, c.st));
     static const bool timing = getenv("GAPLRA_EPOCH_TIMING") != nullptr;
     static const int skip = getenv("GAPLRA_EPOCH_SKIP") ? atoi(getenv("GAPLRA_EPOCH_SKIP")) : 0;
     a.skip = skip;
@@ -593,7 +596,11 @@ SvrgResult svrg_solve_dev(Context& c, Matrix& X, double lambda, int p, const dou
   double best = INFINITY;
   // epoch e+1's index stream + k_block_prep run on the side stream beside
   // epoch e's chain (dense X); GAPLRA_OVERLAP=0 keeps everything on one stream
-  static const bool overlap = !(getenv("GAPLRA_OVERLAP") && atoi(getenv("GAPLRA_OVERLAP")) == 0);
+  // GAPLRA_OVERLAP: 0 serial; 1 (default) epoch e+1's prep starts once chain
+  // e−1 is done; 2 it also waits for epoch e's k_block_u (prep then shares the
+  // SMs with chain e only, not with the H pass / block_u, whose CTAs it starved)
+  static const int overlap_mode = getenv("GAPLRA_OVERLAP") ? atoi(getenv("GAPLRA_OVERLAP")) : 1;
+  static const bool overlap = overlap_mode != 0;
   const bool side = overlap && X.kind == 0;
   EpochPre next;
   bool have_next = false;
@@ -635,6 +642,7 @@ SvrgResult svrg_solve_dev(Context& c, Matrix& X, double lambda, int p, const dou
       GAPLRA_CUDA_CHECK(cudaEventRecord(c.chain_done[parity], c.st));
       // buffers of parity e+1 were last read by epoch e−1's chain
       GAPLRA_CUDA_CHECK(cudaStreamWaitEvent(aux, c.chain_done[parity ^ 1], 0));
+      if (overlap_mode == 2) GAPLRA_CUDA_CHECK(cudaStreamWaitEvent(aux, c.u_done, 0));
       next = epoch_pre_dev(c, X, p, prm.eta, lambda, svrg_stream_seed(prm.root, solve_id, e + 1), prm.m, parity ^ 1,
                            aux);
       GAPLRA_CUDA_CHECK(cudaEventRecord(c.pre_done[parity ^ 1], aux));
