@@ -596,10 +596,11 @@ SvrgResult svrg_solve_dev(Context& c, Matrix& X, double lambda, int p, const dou
   double best = INFINITY;
   // epoch e+1's index stream + k_block_prep run on the side stream beside
   // epoch e's chain (dense X); GAPLRA_OVERLAP=0 keeps everything on one stream
-  // GAPLRA_OVERLAP: 0 serial; 1 (default) epoch e+1's prep starts once chain
+  // GAPLRA_OVERLAP: 0 serial; 1 epoch e+1's prep starts once chain
   // e−1 is done; 2 it also waits for epoch e's k_block_u (prep then shares the
-  // SMs with chain e only, not with the H pass / block_u, whose CTAs it starved)
-  static const int overlap_mode = getenv("GAPLRA_OVERLAP") ? atoi(getenv("GAPLRA_OVERLAP")) : 1;
+  // SMs with chain e only, not with the H pass / block_u, whose CTAs it starved;
+  // default: C5 p = 64 epoch 434 -> 377 ms, p = 1 210 -> 169 ms, C2 / C3 1-3 % faster)
+  static const int overlap_mode = getenv("GAPLRA_OVERLAP") ? atoi(getenv("GAPLRA_OVERLAP")) : 2;
   static const bool overlap = overlap_mode != 0;
   const bool side = overlap && X.kind == 0;
   EpochPre next;
