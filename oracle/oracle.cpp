@@ -778,6 +778,31 @@ Block orth_init(int d, int p, uint64_t seed) {
   }
 }
 
+// Rank completion of an iterate: when the operator's range
+// has dimension < p (X of exact rank < p, SPEC.md:541's "perfect recovery
+// regime"), C·S is rank deficient and MGS2 stops at the first dependent column
+// j; that column is replaced by a fresh Gaussian direction
+// gaussian_init(d, 1, derive_seed(seed, j + 64·attempt)) and the QR redone (the same
+// draws every iteration, so a completed iterate is a fixed point and the
+// projector early stop still fires) —
+// columns before j are unchanged, the new one lies outside range(C), S stays
+// orthonormal.  Only S⁰ keeps the SPEC's redraw-once rule.
+constexpr uint64_t kTagComplete = 0x636f6d70ull;  // "comp"
+void qr_complete(Block& q, uint64_t seed) {
+  Block orig = q;
+  for (int attempt = 0;; ++attempt) {
+    try {
+      qr_inplace(q);
+      return;
+    } catch (const Status& st) {
+      if (st.code != ORC_RANK_DEFICIENT || attempt >= q.p) throw;
+      const Block g = gaussian_init(q.d, 1, derive_seed(seed, static_cast<uint64_t>(st.payload + 64 * attempt)));
+      for (int i = 0; i < q.d; ++i) orig.at(i, st.payload) = g.at(i, 0);
+      q = orig;
+    }
+  }
+}
+
 // Alg. 1 with projector-difference early stop.
 Block subspace_iterate(BlockOp& op, int d, int p, int L, uint64_t seed, double conv_tol,
                        int* iters, orc_ledger* led) {
@@ -789,7 +814,7 @@ Block subspace_iterate(BlockOp& op, int d, int p, int L, uint64_t seed, double c
   for (int l = 1; l <= L; ++l) {
     op.apply(s, y, have_guess ? &guess : nullptr);
     Block q = y;
-    qr_inplace(q);
+    qr_complete(q, derive_seed(seed, kTagComplete));
     if (led) led->qr_factorizations++;
     it = l;
     const double diff = projector_diff(s, q, &g);
@@ -876,7 +901,7 @@ std::vector<double> estimate_eigs(BlockOp& op, int d, int k, double eps_prime, u
     for (int a = 0; a < k && stop; ++a) stop = std::fabs(theta[a] - prev[a]) <= rq_tol * std::fabs(theta[a]);
     if (stop || l == L + 1) break;
     Block q = y;
-    qr_inplace(q);
+    qr_complete(q, derive_seed(seed, kTagComplete));
     if (led) led->qr_factorizations++;
     guess = warm_guess(q, y, gram_ab(s, q));
     have_guess = true;

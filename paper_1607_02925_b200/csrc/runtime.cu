@@ -183,6 +183,8 @@ struct Context {
   DBuf<int32_t> idx, idx2;  // index streams of even / odd epochs
   DBuf<double> tmat2;        // slab of odd epochs (tmat: even)
   DBuf<unsigned int> rej, rej2;
+  DBuf<double> qrc;      // rank completion: the iterate before QR, with replaced columns
+  const double* qr_in = nullptr;
   DBuf<double> xgs;      // L2-exchange chains (EpochConfig::xg): partial slots
   DBuf<unsigned> xgc;    //   and their arrival counters
   DBuf<double> spd;  // blocked sparse epoch: b, u
@@ -965,6 +967,35 @@ void warm_guess_dev(Context& c, const double* Q, const double* Y, int d, int p, 
   launch_small_mul(Q, ld, p, RG, p, p, d, 0.0, 1.0, guess, ld, c.st);
 }
 
+// Rank completion of an iterate (oracle.cpp qr_complete): a
+// dependent column j of C·S (operator range of dimension < p) is replaced by
+// gaussian_init(d, 1, derive_seed(seed, j + 64·attempt)) and the QR redone (the same
+// draws every iteration, so a completed iterate is a fixed point and the
+// projector early stop still fires).
+constexpr uint64_t kTagComplete = 0x636f6d70ull;  // "comp"
+void qr_complete_dev(Context& c, double* Q, int64_t ld, int d, int p, uint64_t seed) {
+  const size_t blk = static_cast<size_t>(round4(d)) * ld;
+  double* orig = nullptr;
+  std::vector<double> h(static_cast<size_t>(d));
+  for (int attempt = 0;; ++attempt) {
+    try {
+      qr_dev(c, Q, ld, d, p, /*count=*/false);
+      return;
+    } catch (const Error& e) {
+      if (e.code != kRankDeficient || attempt >= p) throw;
+      if (!orig) {  // the block before QR: the caller's copy in c.sbuf (op output) is not touched
+        orig = c.qrc.ensure(blk);
+        GAPLRA_CUDA_CHECK(cudaMemcpyAsync(orig, c.qr_in, blk * sizeof(double), cudaMemcpyDeviceToDevice, c.st));
+      }
+      gaussian_init_host(d, 1, derive_seed(seed, static_cast<uint64_t>(e.payload + 64 * attempt)), h.data(), 1);
+      GAPLRA_CUDA_CHECK(cudaMemcpy2DAsync(orig + e.payload, ld * sizeof(double), h.data(), sizeof(double),
+                                          sizeof(double), d, cudaMemcpyHostToDevice, c.st));
+      GAPLRA_CUDA_CHECK(cudaMemcpyAsync(Q, orig, blk * sizeof(double), cudaMemcpyDeviceToDevice, c.st));
+      c.sync();  // h is reused by the next attempt
+    }
+  }
+}
+
 // Alg. 1 with projector early stop and warm-started solves; final S in `S`.
 int subspace_iterate_dev(Context& c, Op& op, int d, int64_t dp, int p, int L, uint64_t seed, double conv_tol,
                          double* S) {
@@ -980,7 +1011,9 @@ int subspace_iterate_dev(Context& c, Op& op, int d, int64_t dp, int p, int L, ui
   for (int l = 1; l <= L; ++l) {
     op.apply(S, Yb, p, have_guess ? guess : nullptr);
     GAPLRA_CUDA_CHECK(cudaMemcpyAsync(Q, Yb, blk * sizeof(double), cudaMemcpyDeviceToDevice, c.st));
-    qr_dev(c, Q, ld, d, p);
+    c.qr_in = Yb;
+    qr_complete_dev(c, Q, ld, d, p, derive_seed(seed, kTagComplete));
+    c.led.qr_factorizations++;
     it = l;
     const double diff = projector_diff_dev(c, S, Q, d, p);
     const bool stop = conv_tol > 0.0 && diff <= conv_tol;
@@ -1064,7 +1097,9 @@ std::vector<double> estimate_eigs_dev(Context& c, Op& op, int d, int64_t dp, int
     for (int a = 0; a < k && stop; ++a) stop = std::fabs(theta[a] - prev[a]) <= rq_tol * std::fabs(theta[a]);
     if (stop || l == L + 1) break;
     GAPLRA_CUDA_CHECK(cudaMemcpyAsync(Q, Yb, blk * sizeof(double), cudaMemcpyDeviceToDevice, c.st));
-    qr_dev(c, Q, ld, d, k);
+    c.qr_in = Yb;
+    qr_complete_dev(c, Q, ld, d, k, derive_seed(seed, kTagComplete));
+    c.led.qr_factorizations++;
     launch_small_gram(S, ld, k, Q, ld, k, d, part, G, c.st);  // G = S_oldᵀ Q
     warm_guess_dev(c, Q, Yb, d, k, guess);
     have_guess = true;

@@ -551,3 +551,20 @@ def test_non_finite_inputs_rejected(g):
     xt2 = torch.zeros((7, 16), dtype=torch.float64, device="cuda")
     with pytest.raises(g.ContractViolation):
         g.DeviceMatrix.from_device(xt2.data_ptr(), 10, 7, 16, keep=xt2)
+
+
+def test_approximate_exact_rank_k_device(g, oracle):
+    """SPEC.md:541 exact-rank-k KAT on the device: the oversampled iterates are
+    rank deficient and completed identically to the oracle."""
+    from oracle_lib import default_si_config
+
+    X, _, _ = planted_dense(40, 60, sigma=np.array([3.0, 2.0, 1.5]), seed=10)
+    for delta in (1.5, 0.0):
+        ap = g.approximate(g.DeviceMatrix.dense(X), g.SIConfig(k=3, p=6, eps=1e-6, delta=delta, seed=2))
+        rc, wo, ro, rep = oracle.approximate(oracle.dense(X), default_si_config(3, 6, eps=1e-6, delta=delta, seed=2))
+        assert rc == 0
+        assert [(q["s"], q["q"], q["strategy"], q["width"]) for q in ap.plan] == \
+               [(q["s"], q["q"], q["strategy"], q["width"]) for q in rep.plan()]
+        assert np.linalg.norm(X - ap.W @ (ap.W.T @ X)) <= 1e-8 * np.linalg.norm(X)
+        assert np.allclose(ap.ritz, ro, rtol=1e-10)
+        assert oracle.sin_theta(wo, ap.W) <= 1e-8
