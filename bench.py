@@ -299,6 +299,8 @@ def run_ours(args, rank, world, local_rank):
             full["sin_theta_vs_eigh"] = float(np.sqrt(max(np.linalg.eigvalsh(R.T @ R).max(), 0.0)))
             full["ritz_max_rel_err_vs_eigh"] = float(np.max(np.abs(res.ritz - ev) / ev))
             del A
+    elif args.lam > 0.0:
+        lam, hint = args.lam, args.hint
     elif spec.name != "C1":
         st = g.tune_shift(x_res, spec.delta(), base)
         lam, hint = st.lam, st.lambda1_hint
@@ -426,6 +428,9 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=16.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-full", action="store_true", help="skip the once-per-run full time-to-eps pipeline")
+    ap.add_argument("--lam", type=float, default=0.0,
+                    help="profiling aid: the tuned shift (with --hint), skipping tune_shift when --no-full")
+    ap.add_argument("--hint", type=float, default=0.0)
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
