@@ -226,7 +226,8 @@ __global__ void __launch_bounds__(kMmaThreads) k_xtw_mma(const double* __restric
                                                          double* __restrict__ out, int64_t ldo,
                                                          size_t split_stride) {
   constexpr int BP = b_pitch<NT>();
-  __shared__ __align__(16) double Ws[2][kKC * BP];
+  extern __shared__ __align__(16) double xtw_ws[];  // [2][kKC * BP]: 74 KB at NT = 8 (dynamic)
+  auto Ws = [&](int b) { return xtw_ws + b * (kKC * BP); };
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int gq = lane >> 2, tq = lane & 3;
   const int col0 = (blockIdx.x * (kMmaThreads / 32) + warp) * (8 * MW);
@@ -250,7 +251,7 @@ __global__ void __launch_bounds__(kMmaThreads) k_xtw_mma(const double* __restric
       const int rr = e / (8 * NT), c = e - rr * (8 * NT);
       const int r = rbase + rr;
       const bool ok = c < pc && r < r1;
-      cp_async8(&Ws[buf][rr * BP + c], W + (ok ? static_cast<int64_t>(r) * ldw + c : 0), ok);
+      cp_async8(Ws(buf) + rr * BP + c, W + (ok ? static_cast<int64_t>(r) * ldw + c : 0), ok);
     }
     cp_async_commit();
   };
@@ -260,7 +261,7 @@ __global__ void __launch_bounds__(kMmaThreads) k_xtw_mma(const double* __restric
   __syncthreads();
   for (int rb = r0; rb < r1; rb += kKC) {
     if (rb + kKC < r1) stage_w(buf ^ 1, rb + kKC);
-    const double* ws = Ws[buf];
+    const double* ws = Ws(buf);
     const int nkb = (min(kKC, r1 - rb) + 15) / 16;
     double av[4][MW][4];
 #pragma unroll
@@ -506,18 +507,26 @@ template <int NT>
 void xtw_mma_chunk(const DenseX& X, const double* W, int64_t ldw, int pc, double* Y, int64_t ldy, GramWork& work,
                    cudaStream_t st, int rs, int rows_per_split) {
   constexpr int MW = 2;
+  constexpr size_t smem = 2 * kKC * b_pitch<NT>() * sizeof(double);
+  static bool attr = false;
+  if (!attr && smem > 48 * 1024) {
+    GAPLRA_CUDA_CHECK(cudaFuncSetAttribute(k_xtw_mma<NT, MW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           static_cast<int>(smem)));
+    attr = true;
+  }
   const int rows_total = static_cast<int>(X.ld);
   const int col_tiles = static_cast<int>(ceil_div(X.n, (kMmaThreads / 32) * 8 * MW));
   dim3 grid(col_tiles, rs);
   if (rs == 1) {
-    k_xtw_mma<NT, MW><<<grid, kMmaThreads, 0, st>>>(X.x, X.ld, X.n, rows_per_split, rows_total, W, ldw, pc, Y, ldy, 0);
+    k_xtw_mma<NT, MW><<<grid, kMmaThreads, smem, st>>>(X.x, X.ld, X.n, rows_per_split, rows_total, W, ldw, pc, Y, ldy,
+                                                       0);
     GAPLRA_LAUNCH_CHECK();
     return;
   }
   const size_t stride = static_cast<size_t>(X.n) * pc;
   if (work.part_elems < stride * rs) throw Error(kContractViolation, "xtw_mma: workspace too small");
-  k_xtw_mma<NT, MW><<<grid, kMmaThreads, 0, st>>>(X.x, X.ld, X.n, rows_per_split, rows_total, W, ldw, pc, work.part,
-                                                  pc, stride);
+  k_xtw_mma<NT, MW><<<grid, kMmaThreads, smem, st>>>(X.x, X.ld, X.n, rows_per_split, rows_total, W, ldw, pc,
+                                                     work.part, pc, stride);
   GAPLRA_LAUNCH_CHECK();
   k_sum_splits<<<sm_count() * 4, 256, 0, st>>>(work.part, rs, stride, X.n, pc, pc, Y, ldy);
   GAPLRA_LAUNCH_CHECK();
@@ -1437,7 +1446,10 @@ struct Args {
   int cols_per_split, stages;
 };
 
-__host__ __device__ inline int stage_len(int64_t ldy) { return kNB * kXP + static_cast<int>(kNB * ldy); }
+// Y tile pitch ≡ 4 (mod 16) doubles: the B-fragment loads (k = 4 ks + tq, c = 8 nt + gq)
+// are then conflict-free (a pitch ≡ 0, e.g. ldy = 64 at C5, was 4-way conflicted)
+__host__ __device__ inline int64_t y_pitch(int64_t ldy) { return ldy + ((4 - ldy % 16) + 16) % 16; }
+__host__ __device__ inline int stage_len(int64_t ldy) { return kNB * kXP + static_cast<int>(kNB * y_pitch(ldy)); }
 __host__ __device__ inline size_t smem_bytes(int64_t ldy, int stages) {
   return (static_cast<size_t>(stage_len(ldy)) * stages + 16) * sizeof(double);
 }
@@ -1449,6 +1461,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_xy_tma(Args a) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int gq = lane >> 2, tq = lane & 3;
   const int S = a.stages, SL = stage_len(a.ldy);
+  const int YP = static_cast<int>(y_pitch(a.ldy));
   uint64_t* full = reinterpret_cast<uint64_t*>(sm + static_cast<size_t>(SL) * S);
   uint64_t* empty = full + 8;
   const int r0 = blockIdx.x * kR;
@@ -1477,7 +1490,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_xy_tma(Args a) {
         for (int c = 0; c < nv; ++c)
           bulk_g2s(st + c * kXP, a.X + static_cast<int64_t>(j + c) * a.ldx + r0, static_cast<uint32_t>(rc * 8),
                    &full[q]);
-        bulk_g2s(st + kNB * kXP, a.Y + static_cast<int64_t>(j) * a.ldy, static_cast<uint32_t>(nv * a.ldy * 8), &full[q]);
+        if (YP == a.ldy) {
+          bulk_g2s(st + kNB * kXP, a.Y + static_cast<int64_t>(j) * a.ldy, static_cast<uint32_t>(nv * a.ldy * 8),
+                   &full[q]);
+        } else {  // row by row into the padded pitch
+          for (int c = 0; c < nv; ++c)
+            bulk_g2s(st + kNB * kXP + c * YP, a.Y + static_cast<int64_t>(j + c) * a.ldy,
+                     static_cast<uint32_t>(a.ldy * 8), &full[q]);
+        }
       }
     return;
   }
@@ -1503,7 +1523,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_xy_tma(Args a) {
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) {
         const int c = nt * 8 + gq;
-        b[nt] = (k < nv && c < a.pc) ? ys[k * a.ldy + c] : 0.0;
+        b[nt] = (k < nv && c < a.pc) ? ys[k * YP + c] : 0.0;
       }
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
@@ -1560,6 +1580,7 @@ template <int NT>
 void launch(const DenseX& X, const double* Y, int64_t ldy, int pc, double* Z, int64_t ldz, GramWork& work,
             cudaStream_t st) {
   const Plan pl = plan(X, ldy);
+  if (pc > 8 * NT) throw Error(kContractViolation, "xy_tma: pc > 8 NT");
   Args a;
   a.X = X.x;
   a.ldx = X.ld;
@@ -1732,12 +1753,16 @@ static int64_t ldp_even(int p) { return p == 1 ? 1 : (p + 1) / 2 * 2; }
 size_t gram_work_elems(const DenseX& X, int p) {
   size_t need = 0;
   if (p == 1 && p1::applies(X)) need = static_cast<size_t>(p1::ctas(X)) * X.ld;
+  if (p <= 64 && xyt::applies(p, ldp_even(p))) {
+    const xyt::Plan xp = xyt::plan(X, ldp_even(p));
+    if (xp.splits > 1) need = std::max(need, static_cast<size_t>(xp.splits) * X.ld * p);
+  }
+  if (p > 32 && p <= 64 && use_mma(p)) {  // launch_xtw's one-launch wide form
+    const MmaPlan m = mma_plan(X);
+    if (m.rs > 1) need = std::max(need, static_cast<size_t>(m.rs) * X.n * p);
+  }
   for (int c0 = 0; c0 < p; c0 += 32) {
     const int pc = std::min(32, p - c0);
-    if (xyt::applies(pc, ldp_even(p))) {
-      const xyt::Plan xp = xyt::plan(X, ldp_even(p));
-      if (xp.splits > 1) need = std::max(need, static_cast<size_t>(xp.splits) * X.ld * pc);
-    }
     const fused::Plan fp = fused::plan(X, pc);
     if (fp.g) {  // (the two-pass needs below still apply: H = Xᵀ C runs launch_xtw alone)
       const int ncl = fused::clusters_for(X, pc, fp);
@@ -1820,6 +1845,20 @@ void launch_gram_fused(const DenseX& X, const double* W, int64_t ldw, int p, dou
 
 void launch_xtw(const DenseX& X, const double* W, int64_t ldw, int p, double* Y, int64_t ldy, GramWork& work,
                 cudaStream_t st) {
+  // GAPLRA_XTW_WIDE=1: 32 < p <= 64 in one launch (each X fragment feeds 8 n-tiles,
+  // X read once).  Measured slower at C5 p = 64 (81.4 vs 76.5 ms per pass): 160
+  // registers leave one CTA per SM, so the two 32-column launches stay the default
+  static const int wide = getenv("GAPLRA_XTW_WIDE") ? atoi(getenv("GAPLRA_XTW_WIDE")) : 0;
+  if (wide && p > 32 && p <= 64 && use_mma(p)) {
+    const MmaPlan m = mma_plan(X);
+    switch ((p + 7) / 8) {
+      case 5: xtw_mma_chunk<5>(X, W, ldw, p, Y, ldy, work, st, m.rs, m.rows_per_split); break;
+      case 6: xtw_mma_chunk<6>(X, W, ldw, p, Y, ldy, work, st, m.rs, m.rows_per_split); break;
+      case 7: xtw_mma_chunk<7>(X, W, ldw, p, Y, ldy, work, st, m.rs, m.rows_per_split); break;
+      default: xtw_mma_chunk<8>(X, W, ldw, p, Y, ldy, work, st, m.rs, m.rows_per_split); break;
+    }
+    return;
+  }
   for (int c0 = 0; c0 < p; c0 += 32) {
     const int pc = std::min(32, p - c0);
 
@@ -1839,17 +1878,22 @@ void launch_xtw(const DenseX& X, const double* W, int64_t ldw, int p, double* Y,
 
 void launch_xy(const DenseX& X, const double* Y, int64_t ldy, int p, double* Z, int64_t ldz, GramWork& work,
                cudaStream_t st) {
+  // all p <= 64 columns in one TMA-fed pass (C5 p = 64: X read once, not in two 32-column chunks)
+  if (p <= 64 && xyt::applies(p, ldy)) {
+    switch ((p + 7) / 8) {
+      case 1: xyt::launch<1>(X, Y, ldy, p, Z, ldz, work, st); break;
+      case 2: xyt::launch<2>(X, Y, ldy, p, Z, ldz, work, st); break;
+      case 3: xyt::launch<3>(X, Y, ldy, p, Z, ldz, work, st); break;
+      case 4: xyt::launch<4>(X, Y, ldy, p, Z, ldz, work, st); break;
+      case 5: xyt::launch<5>(X, Y, ldy, p, Z, ldz, work, st); break;
+      case 6: xyt::launch<6>(X, Y, ldy, p, Z, ldz, work, st); break;
+      case 7: xyt::launch<7>(X, Y, ldy, p, Z, ldz, work, st); break;
+      default: xyt::launch<8>(X, Y, ldy, p, Z, ldz, work, st); break;
+    }
+    return;
+  }
   for (int c0 = 0; c0 < p; c0 += 32) {
     const int pc = std::min(32, p - c0);
-    if (p <= 32 && xyt::applies(pc, ldy)) {  // (chunks of a wider block would need a strided Y copy)
-      switch ((pc + 7) / 8) {
-        case 1: xyt::launch<1>(X, Y + c0, ldy, pc, Z + c0, ldz, work, st); break;
-        case 2: xyt::launch<2>(X, Y + c0, ldy, pc, Z + c0, ldz, work, st); break;
-        case 3: xyt::launch<3>(X, Y + c0, ldy, pc, Z + c0, ldz, work, st); break;
-        default: xyt::launch<4>(X, Y + c0, ldy, pc, Z + c0, ldz, work, st); break;
-      }
-      continue;
-    }
     if (use_mma(pc)) {
       const MmaPlan m = mma_plan(X);
       switch ((pc + 7) / 8) {
