@@ -37,7 +37,8 @@ struct Error : std::runtime_error {
     if (_e != cudaSuccess) {                                                                 \
       throw ::gaplra_cuda::Error(_e == cudaErrorMemoryAllocation ? ::gaplra_cuda::kOutOfMemory \
                                                                  : ::gaplra_cuda::kDeviceError, \
-                                 std::string(#expr) + ": " + cudaGetErrorString(_e));        \
+                                 std::string(#expr) + ": " + cudaGetErrorString(_e) + " (" +  \
+                                     __FILE__ + ":" + std::to_string(__LINE__) + ")");          \
     }                                                                                        \
   } while (0)
 

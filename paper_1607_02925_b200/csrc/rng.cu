@@ -103,10 +103,11 @@ BitMat power(BitMat base, uint64_t e) {
 
 __global__ void k_index_stream(uint64_t seed, uint64_t n, int64_t m, int chunk, int levels,
                                const uint64_t* __restrict__ cols, int32_t* __restrict__ out,
-                               unsigned int* __restrict__ rejects) {
+                               unsigned int* __restrict__ rejects, const uint64_t* __restrict__ dseed) {
   const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   const int64_t begin = t * chunk;
   if (begin >= m) return;
+  if (dseed) seed = *dseed;  // device-resident epoch loop: the seed of the epoch being prepared
   State st = seed_state(seed);
   for (int l = 0; l < levels; ++l) {
     if (!((t >> l) & 1)) continue;
@@ -142,8 +143,9 @@ __global__ void k_index_stream(uint64_t seed, uint64_t n, int64_t m, int chunk, 
 
 // Exact serial regeneration, only taken when some draw was rejected.
 __global__ void k_index_fixup(uint64_t seed, uint64_t n, int64_t m, int32_t* __restrict__ out,
-                              const unsigned int* __restrict__ rejects) {
+                              const unsigned int* __restrict__ rejects, const uint64_t* __restrict__ dseed) {
   if (*rejects == 0 || threadIdx.x != 0 || blockIdx.x != 0) return;
+  if (dseed) seed = *dseed;
   State st = seed_state(seed);
   const uint64_t limit = n * (~0ull / n);
   for (int64_t k = 0; k < m; ++k) {
@@ -194,15 +196,15 @@ uint64_t svrg_stream_seed(uint64_t root, int64_t solve_id, int epoch) {
 }
 
 void launch_index_stream(uint64_t seed, uint64_t n, int64_t m, int32_t* out, unsigned int* rejects,
-                         cudaStream_t st) {
+                         cudaStream_t st, const uint64_t* dseed) {
   if (m <= 0) return;
   if (n == 0 || ceil_div(m, kChunk) > (int64_t{1} << kLevels)) throw Error(kContractViolation, "index stream size");
   const uint64_t* table = jump_table();
   const int64_t threads = ceil_div(m, kChunk);
   GAPLRA_CUDA_CHECK(cudaMemsetAsync(rejects, 0, sizeof(unsigned int), st));
-  k_index_stream<<<ceil_div(threads, 128), 128, 0, st>>>(seed, n, m, kChunk, kLevels, table, out, rejects);
+  k_index_stream<<<ceil_div(threads, 128), 128, 0, st>>>(seed, n, m, kChunk, kLevels, table, out, rejects, dseed);
   GAPLRA_LAUNCH_CHECK();
-  k_index_fixup<<<1, 32, 0, st>>>(seed, n, m, out, rejects);
+  k_index_fixup<<<1, 32, 0, st>>>(seed, n, m, out, rejects, dseed);
   GAPLRA_LAUNCH_CHECK();
 }
 

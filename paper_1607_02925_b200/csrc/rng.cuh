@@ -17,8 +17,9 @@ uint64_t derive_seed(uint64_t root, uint64_t tag);
 uint64_t svrg_stream_seed(uint64_t root, int64_t solve_id, int epoch);
 
 // out[k] = Rng(seed).uniform_index(n) for k < m (int32, n < 2^31).
-// `rejects` is one device unsigned int of scratch.
+// `rejects` is one device unsigned int of scratch.  dseed (optional): read the
+// seed from device memory at run time (the device-resident epoch loop).
 void launch_index_stream(uint64_t seed, uint64_t n, int64_t m, int32_t* out, unsigned int* rejects,
-                         cudaStream_t st);
+                         cudaStream_t st, const uint64_t* dseed = nullptr);
 
 }  // namespace gaplra_cuda

@@ -183,6 +183,7 @@ struct Context {
   DBuf<int32_t> idx, idx2;  // index streams of even / odd epochs
   DBuf<double> tmat2;        // slab of odd epochs (tmat: even)
   DBuf<unsigned int> rej, rej2;
+  DBuf<double> ghist, gctl;  // device-resident epoch loop: residual history, control block
   DBuf<double> qrc;      // rank completion: the iterate before QR, with replaced columns
   const double* qr_in = nullptr;
   DBuf<double> xgs;      // L2-exchange chains (EpochConfig::xg): partial slots
@@ -423,13 +424,14 @@ struct EpochPre {
 };
 
 EpochPre epoch_pre_dev(Context& c, Matrix& X, int p, double eta, double lambda, uint64_t stream_seed, int64_t m,
-                       int parity, cudaStream_t s) {
+                       int parity, cudaStream_t s, const uint64_t* dseed = nullptr) {
   EpochPre pre;
   pre.m = m;
   pre.idx = (parity ? c.idx2 : c.idx).ensure(static_cast<size_t>(m));
   {
     Prof prof(c, kProfIndex, 4.0 * m, 0.0, s);
-    launch_index_stream(stream_seed, static_cast<uint64_t>(X.n), m, pre.idx, (parity ? c.rej2 : c.rej).ensure(1), s);
+    launch_index_stream(stream_seed, static_cast<uint64_t>(X.n), m, pre.idx, (parity ? c.rej2 : c.rej).ensure(1), s,
+                        dseed);
   }
   if (X.kind != 0) return pre;
   const double col_nnz = static_cast<double>(X.nnz) / X.n;
@@ -575,6 +577,107 @@ void epoch_dev(Context& c, Matrix& X, int p, double* W, const double* C, const d
   epoch_run_dev(c, X, p, W, C, Y, eta, lambda, pre);
 }
 
+// Device-resident epoch loop (north star item 5): epochs 1, 2, ... of a dense
+// solve as one CUDA graph with a WHILE node, so the host does not read a
+// residual per epoch.  Entered after the host ran epoch 0 and evaluated the
+// anchor of epoch 1 (all buffers exist; epoch 1's index stream and slab are in
+// the parity-1 buffers).  Body (one iteration = epoch e):
+//   H pass, k_block_u (parity-1 "cur" buffers) -> fork: chain e ‖ index stream +
+//   k_block_prep of epoch e+1 into the parity-0 "nxt" buffers (seed from the
+//   device) -> join -> copy nxt -> cur -> anchor of epoch e+1 (gram pass +
+//   k_anchor) -> k_epoch_control (the host loop's tests, history, next seed,
+//   loop condition).
+// Returns the device control block after the graph; the caller turns its
+// status into the host loop's outcome.  One sync per solve instead of one per epoch.
+struct GraphEpochs {
+  EpochCtl ctl{};
+  std::vector<double> hist;
+};
+GraphEpochs run_epochs_graph(Context& c, Matrix& X, int p, double* W, double* Z, double* C, double* Y,
+                             const double* B, double* part, double* bn, double* res, double lambda,
+                             const SvrgParams& prm, int64_t solve_id, const EpochPre& cur, double best) {
+  const int64_t ld = ldp_of(p), dp = X.d_pad();
+  const int hist_cap = prm.cap + 2;
+  double* hist = c.ghist.ensure(static_cast<size_t>(hist_cap));
+  EpochCtl* ctl = reinterpret_cast<EpochCtl*>(c.gctl.ensure(4));
+  uint64_t* dseed = reinterpret_cast<uint64_t*>(&ctl->next_seed);
+  EpochCtl h0{};
+  h0.best = best;
+  h0.e = 1;
+  h0.status = 0;
+  h0.next_seed = svrg_stream_seed(prm.root, solve_id, 2);
+  GAPLRA_CUDA_CHECK(cudaMemcpyAsync(ctl, &h0, sizeof(h0), cudaMemcpyHostToDevice, c.st));
+  // buffers of the prep (parity 0) and their sizes, allocated before capture
+  const EpochConfig cfg = cur.cfg;
+  const size_t slab_elems = epoch_slab_elems(prm.m, cfg);
+  double* slab_nxt = c.tmat.ensure(slab_elems);
+  int32_t* idx_nxt = c.idx.ensure(static_cast<size_t>(prm.m));
+  c.rej.ensure(1);
+  cudaStream_t aux = c.aux_stream();
+  cudaGraph_t g = nullptr;
+  cudaGraphExec_t ge = nullptr;
+  GAPLRA_CUDA_CHECK(cudaGraphCreate(&g, 0));
+  struct GraphGuard {
+    cudaGraph_t& g;
+    cudaGraphExec_t& ge;
+    ~GraphGuard() {
+      if (ge) cudaGraphExecDestroy(ge);
+      if (g) cudaGraphDestroy(g);
+    }
+  } guard{g, ge};
+  cudaGraphConditionalHandle cond;
+  GAPLRA_CUDA_CHECK(cudaGraphConditionalHandleCreate(&cond, g, 1, cudaGraphCondAssignDefault));
+  cudaGraphNodeParams np{};
+  np.type = cudaGraphNodeTypeConditional;
+  np.conditional.handle = cond;
+  np.conditional.type = cudaGraphCondTypeWhile;
+  np.conditional.size = 1;
+  cudaGraphNode_t node;
+  GAPLRA_CUDA_CHECK(cudaGraphAddNode(&node, g, nullptr, 0, &np));
+  cudaGraph_t body = np.conditional.phGraph_out[0];
+  GAPLRA_CUDA_CHECK(cudaStreamBeginCaptureToGraph(c.st, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+  const unsigned long long launches0 = launch_counter();
+  try {
+    epoch_run_dev(c, X, p, W, C, Y, prm.eta, lambda, cur);  // records c.u_done after k_block_u
+    GAPLRA_CUDA_CHECK(cudaStreamWaitEvent(aux, c.u_done, 0));
+    const EpochPre nxt = epoch_pre_dev(c, X, p, prm.eta, lambda, 0, prm.m, 0, aux, dseed);
+    GAPLRA_CUDA_CHECK(cudaEventRecord(c.pre_done[0], aux));
+    GAPLRA_CUDA_CHECK(cudaStreamWaitEvent(c.st, c.pre_done[0], 0));
+    GAPLRA_CUDA_CHECK(cudaMemcpyAsync(cur.idx, nxt.idx, static_cast<size_t>(prm.m) * sizeof(int32_t),
+                                      cudaMemcpyDeviceToDevice, c.st));
+    if (nxt.slab)
+      GAPLRA_CUDA_CHECK(cudaMemcpyAsync(cur.slab, nxt.slab, slab_elems * sizeof(double), cudaMemcpyDeviceToDevice,
+                                        c.st));
+    gram_block_dev(c, X, p, W, ld, Z, ld, Y, ld);
+    launch_anchor(W, Z, B, ld, static_cast<int>(dp), p, lambda, prm.eta, C, part, bn, nullptr, res, c.st);
+    launch_epoch_control(res, ctl, hist, hist_cap, prm.tol, prm.slack, prm.cap, prm.root, solve_id, cond, c.st);
+  } catch (...) {
+    cudaGraph_t tmp = nullptr;
+    cudaStreamEndCapture(c.st, &tmp);
+    throw;
+  }
+  cudaGraph_t captured = nullptr;
+  GAPLRA_CUDA_CHECK(cudaStreamEndCapture(c.st, &captured));
+  const unsigned long long per_body = launch_counter() - launches0;  // kernels of one iteration (counted at capture)
+  (void)slab_nxt;
+  (void)idx_nxt;
+  // events last recorded inside the capture cannot be waited on outside it: re-record them
+  GAPLRA_CUDA_CHECK(cudaEventRecord(c.pre_done[0], aux));
+  GAPLRA_CUDA_CHECK(cudaEventRecord(c.u_done, c.st));
+  GAPLRA_CUDA_CHECK(cudaGraphInstantiate(&ge, g, 0));
+  GAPLRA_CUDA_CHECK(cudaGraphLaunch(ge, c.st));
+  GraphEpochs out;
+  GAPLRA_CUDA_CHECK(cudaMemcpyAsync(&out.ctl, ctl, sizeof(EpochCtl), cudaMemcpyDeviceToHost, c.st));
+  c.sync();
+  if (out.ctl.e > 2) launch_counter() += per_body * static_cast<unsigned long long>(out.ctl.e - 2);  // executions
+  const int last = std::min(out.ctl.e, hist_cap - 1);
+  if (last >= 2) {
+    out.hist.resize(static_cast<size_t>(last - 1));
+    GAPLRA_CUDA_CHECK(cudaMemcpy(out.hist.data(), hist + 2, out.hist.size() * sizeof(double), cudaMemcpyDeviceToHost));
+  }
+  return out;
+}
+
 // Block solve (λI − XXᵀ)W = B with W0 = 0; B, W device blocks with ld = ldp(p).
 // warm = true: W holds the initial guess on entry, else W0 = 0.
 SvrgResult svrg_solve_dev(Context& c, Matrix& X, double lambda, int p, const double* B, double* W,
@@ -629,6 +732,31 @@ SvrgResult svrg_solve_dev(Context& c, Matrix& X, double lambda, int p, const dou
       throw Error(kSolverStalled, "solve_svrg: residual grew above slack x best (epoch " + std::to_string(e) + ")");
     best = std::min(best, r);
     if (e >= prm.cap) throw Error(kSolverStalled, "solve_svrg: epoch cap reached");
+    // from epoch 1 on, the loop runs on the device (GAPLRA_GRAPH=0: host loop)
+    static const bool graph_env = !(getenv("GAPLRA_GRAPH") && atoi(getenv("GAPLRA_GRAPH")) == 0);
+    static const bool timing_env = getenv("GAPLRA_EPOCH_TIMING") != nullptr;
+    if (e == 1 && have_next && side && overlap_mode == 2 && graph_env && !timing_env && !c.profiling) {
+      GAPLRA_CUDA_CHECK(cudaStreamWaitEvent(c.st, c.pre_done[1], 0));
+      const GraphEpochs ge = run_epochs_graph(c, X, p, W, Z, C, Y, B, part, bn, res, lambda, prm, solve_id, next, best);
+      const int runs = ge.ctl.e - 1;  // epochs 1 .. e-1 ran in the graph, each followed by one anchor
+      // the captured anchor's gram pass counted its p applies once, at capture time
+      c.led.gram_applies += static_cast<uint64_t>(p) * static_cast<uint64_t>(std::max(0, runs - 1));
+      out.epochs += runs;
+      c.led.epochs += static_cast<uint64_t>(runs);
+      c.led.solver_column_samples += static_cast<uint64_t>(runs) * static_cast<uint64_t>(prm.m);
+      for (double v : ge.hist) out.history.push_back(v);
+      have_next = false;
+      switch (ge.ctl.status) {
+        case 1: break;
+        case 2: throw Error(kSolverStalled, "solve_svrg: non-finite residual (indefinite shift?)");
+        case 3:
+          throw Error(kSolverStalled,
+                      "solve_svrg: residual grew above slack x best (epoch " + std::to_string(ge.ctl.e) + ")");
+        case 4: throw Error(kSolverStalled, "solve_svrg: epoch cap reached");
+        default: throw Error(kDeviceError, "solve_svrg: device epoch loop ended without a status");
+      }
+      break;
+    }
     const int parity = e & 1;
     EpochPre pre;
     if (have_next) {

@@ -25,6 +25,7 @@
 
 #include "common.cuh"
 #include "svrg.cuh"
+#include "rng.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -2310,6 +2311,52 @@ void launch_svrg_epoch_dense(const EpochArgs& a, const EpochConfig& cfg, cudaStr
 
 void launch_svrg_epoch_sparse(const SparseEpochArgs& a, cudaStream_t st) {
   k_svrg_epoch_sparse<<<ceil_div(a.p, 32), 32, 0, st>>>(a);
+  GAPLRA_LAUNCH_CHECK();
+}
+
+namespace {
+__device__ __forceinline__ uint64_t splitmix_dev(uint64_t& x) {  // rng.cpp:9-16 (the host derive_seed)
+  uint64_t z = (x += 0x9E3779B97F4A7C15ull);
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+__device__ __forceinline__ uint64_t derive_seed_dev(uint64_t root, uint64_t tag) {
+  uint64_t x = root ^ (0xA0761D6478BD642Full * (tag + 1));
+  const uint64_t a = splitmix_dev(x);
+  const uint64_t b = splitmix_dev(x);
+  return a ^ ((b << 32) | (b >> 32));
+}
+__global__ void k_epoch_control(const double* __restrict__ res, EpochCtl* __restrict__ ctl, double* __restrict__ hist,
+                                int hist_cap, double tol, double slack, int cap, uint64_t root, int64_t solve_id,
+                                cudaGraphConditionalHandle cond) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const int e = ctl->e + 1;
+  const double r = *res;
+  if (e < hist_cap) hist[e] = r;
+  int status = 0;
+  if (!isfinite(r)) {
+    status = 2;
+  } else if (r <= tol) {
+    status = 1;
+  } else if (slack > 0.0 && e >= 1 && r > slack * ctl->best) {
+    status = 3;
+  } else {
+    ctl->best = fmin(ctl->best, r);
+    if (e >= cap) status = 4;
+  }
+  ctl->e = e;
+  ctl->status = status;
+  ctl->next_seed = derive_seed_dev(root, kTagSvrg ^ (static_cast<uint64_t>(solve_id) << 20) ^
+                                             static_cast<uint64_t>(e + 1));
+  cudaGraphSetConditional(cond, status == 0 ? 1u : 0u);
+}
+}  // namespace
+
+void launch_epoch_control(const double* res, EpochCtl* ctl, double* hist, int hist_cap, double tol, double slack,
+                          int cap, uint64_t root, int64_t solve_id, unsigned long long cond, cudaStream_t st) {
+  k_epoch_control<<<1, 32, 0, st>>>(res, ctl, hist, hist_cap, tol, slack, cap, root, solve_id,
+                                    static_cast<cudaGraphConditionalHandle>(cond));
   GAPLRA_LAUNCH_CHECK();
 }
 

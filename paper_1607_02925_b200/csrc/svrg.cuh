@@ -74,6 +74,20 @@ size_t sparse_scratch_ints(int d, int bs, int max_col_nnz);
 void launch_svrg_epoch_sparse_blocked(const SparseEpochArgs& a, int bs, int max_col_nnz, double* dbuf, int* ibuf,
                                       cudaStream_t st);
 
+// Device-resident control of a solve's epoch loop (a CUDA-graph WHILE node):
+// after each anchor, k_epoch_control applies the host loop's tests to the
+// residual (non-finite / <= tol / > slack x best / epoch cap), appends it to
+// the history, derives the next epoch's index-stream seed and sets the loop
+// condition.  status: 0 running, 1 converged, 2 non-finite, 3 stalled, 4 cap.
+struct EpochCtl {
+  double best;
+  int e;       // index of the last anchor evaluated
+  int status;
+  unsigned long long next_seed;  // stream seed of epoch e + 1 (its k_block_prep runs in the next iteration)
+};
+void launch_epoch_control(const double* res, EpochCtl* ctl, double* hist, int hist_cap, double tol, double slack,
+                          int cap, uint64_t root, int64_t solve_id, unsigned long long cond, cudaStream_t st);
+
 // C = η(Z + B), per-column |λW − Z − B|; out_max = max_c |M_c| / bnorm_c
 // (NaN if any is non-finite).  part needs anchor_parts(d) * 64 doubles.
 int anchor_parts(int d);
