@@ -155,8 +155,12 @@ GAPLRA_API int gaplra_ctx_synchronize(gaplra_ctx* ctx);
 GAPLRA_API int gaplra_ledger_get(const gaplra_ctx* ctx, gaplra_ledger* out);
 GAPLRA_API int gaplra_ledger_reset(gaplra_ctx* ctx);
 GAPLRA_API int gaplra_version(void);
-/* number of kernels this library has launched (process-wide) */
+/* number of kernels this library has launched (process-wide; kernels replayed by
+ * the device-resident epoch loop's CUDA graph are counted per execution) */
 GAPLRA_API unsigned long long gaplra_launch_count(void);
+/* times the host has waited on the context's stream (device-resident control:
+ * a dense SVRG solve waits ~3 times, not once per epoch) */
+GAPLRA_API unsigned long long gaplra_host_syncs(const gaplra_ctx* ctx);
 GAPLRA_API int gaplra_profile_enable(gaplra_ctx* ctx, int on);
 GAPLRA_API int gaplra_profile_get(gaplra_ctx* ctx, gaplra_profile* out);
 GAPLRA_API int gaplra_profile_reset(gaplra_ctx* ctx);

@@ -74,6 +74,7 @@ class Profile(C.Structure):
 
 _SIGS = {
     "gaplra_launch_count": (C.c_ulonglong, []),
+    "gaplra_host_syncs": (C.c_ulonglong, [C.c_void_p]),
     "gaplra_profile_enable": (C.c_int, [C.c_void_p, C.c_int]),
     "gaplra_profile_get": (C.c_int, [C.c_void_p, C.POINTER(Profile)]),
     "gaplra_profile_reset": (C.c_int, [C.c_void_p]),

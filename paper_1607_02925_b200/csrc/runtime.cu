@@ -252,7 +252,9 @@ struct Context {
     }
     if (own) cudaStreamDestroy(own);
   }
+  unsigned long long host_syncs = 0;  // host waits on the device (gaplra_host_syncs)
   void sync() {
+    ++host_syncs;
     GAPLRA_CUDA_CHECK(cudaStreamSynchronize(st));
     if (!pending.empty()) resolve();
   }
@@ -1672,6 +1674,8 @@ int gaplra_ledger_reset(gaplra_ctx* ctx) {
 }
 
 unsigned long long gaplra_launch_count(void) { return launch_counter(); }
+
+unsigned long long gaplra_host_syncs(const gaplra_ctx* ctx) { return ctx ? ctx->c.host_syncs : 0ull; }
 
 int gaplra_profile_enable(gaplra_ctx* ctx, int on) {
   if (!ctx) return GAPLRA_CONTRACT_VIOLATION;

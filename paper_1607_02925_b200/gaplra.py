@@ -137,6 +137,10 @@ class Context:
     def synchronize(self):
         self.check(self.lib.gaplra_ctx_synchronize(self.h))
 
+    def host_syncs(self) -> int:
+        """Times the host has waited on this context's stream."""
+        return int(self.lib.gaplra_host_syncs(self.h))
+
     def ledger(self) -> dict:
         L = N.Ledger()
         self.check(self.lib.gaplra_ledger_get(self.h, C.byref(L)))

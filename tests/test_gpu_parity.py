@@ -568,3 +568,25 @@ def test_approximate_exact_rank_k_device(g, oracle):
         assert np.linalg.norm(X - ap.W @ (ap.W.T @ X)) <= 1e-8 * np.linalg.norm(X)
         assert np.allclose(ap.ritz, ro, rtol=1e-10)
         assert oracle.sin_theta(wo, ap.W) <= 1e-8
+
+
+def test_device_resident_epoch_loop(g, oracle):
+    """North star item 5: a dense solve's epochs run on the device (CUDA-graph
+    WHILE node, k_epoch_control): the host waits a fixed number of times per
+    solve, not once per epoch, and the result, history and epoch count equal
+    the oracle's host-driven loop."""
+    X, _, sig = planted_dense(2048, 4000, seed=6)
+    lam = 1.05 * sig[0] ** 2
+    b = np.random.default_rng(6).standard_normal((2048, 4))
+    x = g.DeviceMatrix.dense(X)
+    ctx = x.ctx
+    s0 = ctx.host_syncs()
+    r = g.solve_svrg(x, lam, b, 1e-10, seed=3)
+    syncs = ctx.host_syncs() - s0
+    assert r.epochs >= 10
+    assert syncs <= 6, (syncs, r.epochs)
+    rc, wo, ep, hist = oracle.svrg_solve(oracle.dense(X), lam, b, 1e-10, seed=3)
+    assert rc == 0 and abs(r.epochs - ep) <= 1
+    assert rel(r.solution, wo) <= 1e-8
+    n = min(len(hist), len(r.residual_history))
+    assert np.allclose(r.residual_history[:n], hist[:n], rtol=1e-6)
