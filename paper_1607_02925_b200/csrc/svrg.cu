@@ -1944,11 +1944,14 @@ __global__ void __launch_bounds__(v4::kThreads, 1) k_svrg_chain_v4(EpochArgs a) 
     // Âᵀ partial over the warp's rows: 2 slice tiles (slices 0-7 at xb0, 8-15 at
     // xb1), K = the rows; HALF: half kw (then kw + 1) is waited for just before use
     auto products = [&](const double* xb0, const double* xb1, int u_blk, int kw) {
-      double acc[2][2][2];  // [slice tile][chain][elem]
+      // four independent accumulator chains per slice tile (the two k-steps of
+      // a row tile go to different chains): DMMA latency, not issue, bounded
+      // the two-chain form
+      double acc[2][4][2];  // [slice tile][chain][elem]
 #pragma unroll
       for (int n2 = 0; n2 < 2; ++n2)
 #pragma unroll
-        for (int ch = 0; ch < 2; ++ch) acc[n2][ch][0] = acc[n2][ch][1] = 0.0;
+        for (int ch = 0; ch < 4; ++ch) acc[n2][ch][0] = acc[n2][ch][1] = 0.0;
 #pragma unroll
       for (int n2 = 0; n2 < 2; ++n2) {
         if constexpr (HALF) wait_half(kw + n2);
@@ -1956,8 +1959,9 @@ __global__ void __launch_bounds__(v4::kThreads, 1) k_svrg_chain_v4(EpochArgs a) 
 #pragma unroll
         for (int tl = 0; tl < kTiles; ++tl) {
           const double2 xv = *reinterpret_cast<const double2*>(xb + perm * RP + rw0 + 8 * tl + 2 * tq);
-          dmma(acc[n2][tl & 1][0], acc[n2][tl & 1][1], v[tl][0], xv.x);
-          dmma(acc[n2][tl & 1][0], acc[n2][tl & 1][1], v[tl][1], xv.y);
+          const int ca = (2 * tl) & 3, cb = (2 * tl + 1) & 3;
+          dmma(acc[n2][ca][0], acc[n2][ca][1], v[tl][0], xv.x);
+          dmma(acc[n2][cb][0], acc[n2][cb][1], v[tl][1], xv.y);
         }
       }
       // C fragment (column gq, slices 8 n2 + perm(2 tq), 8 n2 + perm(2 tq + 1)) -> red(u_blk) in [j PC + c]
@@ -1966,8 +1970,8 @@ __global__ void __launch_bounds__(v4::kThreads, 1) k_svrg_chain_v4(EpochArgs a) 
       const int pb = ((2 * tq + 1) & 1) << 1 | (((2 * tq + 1) >> 1) & 1) | ((2 * tq + 1) & 4);
 #pragma unroll
       for (int n2 = 0; n2 < 2; ++n2) {
-        rb[(8 * n2 + pa) * PC + gq] = acc[n2][0][0] + acc[n2][1][0];
-        rb[(8 * n2 + pb) * PC + gq] = acc[n2][0][1] + acc[n2][1][1];
+        rb[(8 * n2 + pa) * PC + gq] = (acc[n2][0][0] + acc[n2][1][0]) + (acc[n2][2][0] + acc[n2][3][0]);
+        rb[(8 * n2 + pb) * PC + gq] = (acc[n2][0][1] + acc[n2][1][1]) + (acc[n2][2][1] + acc[n2][3][1]);
       }
       bar_red_arrive(u_blk);
     };
