@@ -42,6 +42,8 @@ void launch_symmetrize(double* H, int k, cudaStream_t st);
 // out = alpha A + beta B (d x p row-major, ld; out may alias A or B)
 void launch_axpby(double alpha, const double* A, double beta, const double* B, double* out, int64_t ld, int d, int p,
                   cudaStream_t st);
+// device-to-device copy by the SMs (cudaMemcpyAsync fallback when unaligned)
+void launch_copy(const void* src, void* dst, size_t bytes, cudaStream_t st);
 // v *= 1 / sqrt(*s2) when *s2 > 0 (device scalar)
 void launch_scale_inv_sqrt(double* v, int64_t ld, int d, int p, const double* s2, cudaStream_t st);
 

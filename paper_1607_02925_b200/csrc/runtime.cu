@@ -6,6 +6,7 @@
 // behind the C ABI of include/gaplra_cuda.h.  Every pinned choice (seeds,
 // stopping rules, W0 = 0, last iterate) matches oracle/oracle.cpp; see
 // DESIGN.md §2.  There is no CPU compute path: every numeric step is a kernel.
+#include <chrono>
 #include <cmath>
 #include <cstdlib>
 #include <cstdio>
@@ -197,7 +198,12 @@ struct Context {
   cudaEvent_t pre_done[2] = {nullptr, nullptr}, chain_done[2] = {nullptr, nullptr}, u_done = nullptr;
   cudaStream_t aux_stream() {
     if (!aux) {
-      GAPLRA_CUDA_CHECK(cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking));
+      // lowest priority: when chain e and prep e+1 become ready together (a graph
+      // launches its branches in no fixed order), the chain's CTAs are dispatched
+      // first and the prep fills the SMs it leaves idle
+      int lo = 0, hi = 0;
+      GAPLRA_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+      GAPLRA_CUDA_CHECK(cudaStreamCreateWithPriority(&aux, cudaStreamNonBlocking, lo));
       for (int i = 0; i < 2; ++i) {
         GAPLRA_CUDA_CHECK(cudaEventCreateWithFlags(&pre_done[i], cudaEventDisableTiming));
         GAPLRA_CUDA_CHECK(cudaEventCreateWithFlags(&chain_done[i], cudaEventDisableTiming));
@@ -637,6 +643,8 @@ GraphEpochs run_epochs_graph(Context& c, Matrix& X, int p, double* W, double* Z,
   cudaGraphNode_t node;
   GAPLRA_CUDA_CHECK(cudaGraphAddNode(&node, g, nullptr, 0, &np));
   cudaGraph_t body = np.conditional.phGraph_out[0];
+  static const bool gdebug = getenv("GAPLRA_GRAPH_DEBUG") != nullptr;
+  const auto t_cap0 = std::chrono::steady_clock::now();
   GAPLRA_CUDA_CHECK(cudaStreamBeginCaptureToGraph(c.st, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
   const unsigned long long launches0 = launch_counter();
   try {
@@ -645,11 +653,8 @@ GraphEpochs run_epochs_graph(Context& c, Matrix& X, int p, double* W, double* Z,
     const EpochPre nxt = epoch_pre_dev(c, X, p, prm.eta, lambda, 0, prm.m, 0, aux, dseed);
     GAPLRA_CUDA_CHECK(cudaEventRecord(c.pre_done[0], aux));
     GAPLRA_CUDA_CHECK(cudaStreamWaitEvent(c.st, c.pre_done[0], 0));
-    GAPLRA_CUDA_CHECK(cudaMemcpyAsync(cur.idx, nxt.idx, static_cast<size_t>(prm.m) * sizeof(int32_t),
-                                      cudaMemcpyDeviceToDevice, c.st));
-    if (nxt.slab)
-      GAPLRA_CUDA_CHECK(cudaMemcpyAsync(cur.slab, nxt.slab, slab_elems * sizeof(double), cudaMemcpyDeviceToDevice,
-                                        c.st));
+    launch_copy(nxt.idx, cur.idx, static_cast<size_t>(prm.m) * sizeof(int32_t), c.st);
+    if (nxt.slab) launch_copy(nxt.slab, cur.slab, slab_elems * sizeof(double), c.st);
     gram_block_dev(c, X, p, W, ld, Z, ld, Y, ld);
     launch_anchor(W, Z, B, ld, static_cast<int>(dp), p, lambda, prm.eta, C, part, bn, nullptr, res, c.st);
     launch_epoch_control(res, ctl, hist, hist_cap, prm.tol, prm.slack, prm.cap, prm.root, solve_id, cond, c.st);
@@ -666,11 +671,31 @@ GraphEpochs run_epochs_graph(Context& c, Matrix& X, int p, double* W, double* Z,
   // events last recorded inside the capture cannot be waited on outside it: re-record them
   GAPLRA_CUDA_CHECK(cudaEventRecord(c.pre_done[0], aux));
   GAPLRA_CUDA_CHECK(cudaEventRecord(c.u_done, c.st));
+  const auto t_cap1 = std::chrono::steady_clock::now();
   GAPLRA_CUDA_CHECK(cudaGraphInstantiate(&ge, g, 0));
+  const auto t_inst = std::chrono::steady_clock::now();
+  cudaEvent_t ga = nullptr, gb = nullptr;
+  if (gdebug) {
+    cudaEventCreate(&ga);
+    cudaEventCreate(&gb);
+    cudaEventRecord(ga, c.st);
+  }
   GAPLRA_CUDA_CHECK(cudaGraphLaunch(ge, c.st));
+  if (gdebug) cudaEventRecord(gb, c.st);
   GraphEpochs out;
   GAPLRA_CUDA_CHECK(cudaMemcpyAsync(&out.ctl, ctl, sizeof(EpochCtl), cudaMemcpyDeviceToHost, c.st));
   c.sync();
+  if (gdebug) {
+    float gms = 0.f;
+    cudaEventElapsedTime(&gms, ga, gb);
+    fprintf(stderr, "{\"graph\": {\"capture_ms\": %.3f, \"instantiate_ms\": %.3f, \"run_ms\": %.3f, \"epochs\": %d, "
+            "\"ms_per_epoch\": %.3f, \"kernels_per_epoch\": %llu}}\n",
+            std::chrono::duration<double, std::milli>(t_cap1 - t_cap0).count(),
+            std::chrono::duration<double, std::milli>(t_inst - t_cap1).count(), gms, out.ctl.e - 1,
+            gms / std::max(1, out.ctl.e - 1), per_body);
+    cudaEventDestroy(ga);
+    cudaEventDestroy(gb);
+  }
   if (out.ctl.e > 2) launch_counter() += per_body * static_cast<unsigned long long>(out.ctl.e - 2);  // executions
   const int last = std::min(out.ctl.e, hist_cap - 1);
   if (last >= 2) {
@@ -1627,7 +1652,9 @@ int gaplra_ctx_create(int device, gaplra_ctx** out) {
     if (device < 0 || device >= count) throw Error(kDeviceError, "no such CUDA device");
     ctx->c.device = device;
     GAPLRA_CUDA_CHECK(cudaSetDevice(device));
-    GAPLRA_CUDA_CHECK(cudaStreamCreateWithFlags(&ctx->c.own, cudaStreamNonBlocking));
+    int lo = 0, hi = 0;
+    GAPLRA_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    GAPLRA_CUDA_CHECK(cudaStreamCreateWithPriority(&ctx->c.own, cudaStreamNonBlocking, hi));  // main: highest
     ctx->c.st = ctx->c.own;
     GAPLRA_CUDA_CHECK(cudaMallocHost(&ctx->c.pin, 64 * sizeof(double)));
     GAPLRA_CUDA_CHECK(cudaMallocHost(&ctx->c.pin_i, 64 * sizeof(int)));
