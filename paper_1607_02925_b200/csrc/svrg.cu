@@ -176,35 +176,51 @@ constexpr int kPrepKC = 64;
 constexpr int kPrepPitch = kPrepKC + 4;
 constexpr int kPrepStages = 4;
 constexpr int kPrepCols = 32;
-constexpr size_t kPrepRingBytes = size_t(kPrepStages) * kPrepCols * kPrepPitch * sizeof(double);
+// LA = 2 (two-block lookahead chain): a third group of 16 columns, block t−2,
+// for the second cross-Gram Kxx_t = X_{B_t}ᵀ X_{B_{t−2}}
+template <int LA>
+__host__ __device__ constexpr int prep_cols() { return 16 * (LA + 1); }
+template <int LA>
+__host__ __device__ constexpr size_t prep_ring_bytes() { return size_t(kPrepStages) * prep_cols<LA>() * kPrepPitch * sizeof(double); }
+constexpr size_t kPrepRingBytes = prep_ring_bytes<1>();
 // cp.async.bulk takes warp-uniform operands, so one warp issues its lanes'
 // copies one after another (~50 cycles each): 4 producer warps, one per SM
 // sub-partition, 8 columns each.
 constexpr int kPrepProducers = 4;
 constexpr int kPrepCtas = 2;  // CTAs per SM: one's serial tail overlaps the other's Gram loop
 constexpr int kPrepColsPerProducer = kPrepCols / kPrepProducers;
+// the consumers' per-warp partial Grams live after the ring (dynamic smem)
+template <int LA>
+__host__ __device__ constexpr size_t prep_red_bytes() {
+  return size_t(kPrepThreads / 32) * (3 + 4 * LA) * 64 * sizeof(double);
+}
 
 __device__ __forceinline__ void prep_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kPrepThreads) : "memory"); }
 
-template <int B>
+template <int B, int LA>
 __global__ void __launch_bounds__(kPrepThreads + 32 * kPrepProducers, kPrepCtas) k_block_prep(EpochArgs a) {
   static_assert(B == 16, "T = (I+L)(I+L^2)(I+L^4)(I+L^8) and the 32-column ring assume B = 16");
+  static_assert(LA == 1 || LA == 2, "one- or two-block lookahead");
   constexpr int G8 = B / 8;
   constexpr int NW = G8 * (G8 + 1) / 2;  // within-block lower tiles
-  constexpr int NX = G8 * G8;            // cross tiles
-  constexpr int NT = NW + NX;
+  constexpr int NX = G8 * G8;            // cross tiles per previous block
+  constexpr int NT = NW + LA * NX;
+  constexpr int NCOL = prep_cols<LA>();
+  constexpr int CPP = NCOL / kPrepProducers;  // ring columns per producer warp
   constexpr int NWARP = kPrepThreads / 32;
   constexpr int RPW = kPrepKC / NWARP;  // rows of a chunk per consumer warp
   static_assert(RPW % 4 == 0, "whole m8n8k4 k-steps per warp");
+  static_assert(prep_red_bytes<LA>() == size_t(NWARP) * NT * 64 * sizeof(double), "red layout");
   extern __shared__ __align__(128) double ring[];
-  __shared__ double red[NWARP][NT][64];
+  auto red = reinterpret_cast<double (*)[NT][64]>(ring + size_t(kPrepStages) * NCOL * kPrepPitch);
   __shared__ double K[B][B + 1];
   __shared__ double Kx[B][B + 1];
+  __shared__ double Kxx[LA == 2 ? B : 1][B + 1];
   __shared__ double T[B][B + 1];
   __shared__ double TT[B][B + 1];
   __shared__ double rp[B + 1], gm[B + 1];
   __shared__ __align__(8) uint64_t full[kPrepStages], empty[kPrepStages];
-  static_assert(sizeof(red) >= 4 * B * (B + 1) * sizeof(double), "P aliases red");
+  static_assert(prep_red_bytes<LA>() >= 4 * B * (B + 1) * sizeof(double), "P aliases red");
   // L, L², L⁴, L⁸ then the running products; red is dead once K/Kx are reduced
   auto P = reinterpret_cast<double (*)[B][B + 1]>(&red[0][0][0]);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -230,19 +246,22 @@ __global__ void __launch_bounds__(kPrepThreads + 32 * kPrepProducers, kPrepCtas)
   }
   __syncthreads();
   if (warp < kPrepProducers) {  // ------------------------------------- producers
-    // producer warp w stages ring columns [8w, 8w+8): 0..15 block t, 16..31 block t−1
-    const int rc = warp * kPrepColsPerProducer + lane;
+    // producer warp w stages ring columns [CPP w, CPP (w+1)): 0..15 block t,
+    // 16..31 block t−1, (LA = 2) 32..47 block t−2
+    const int rc = warp * CPP + lane;
     int stage = 0;
     uint32_t phase = 0;
     auto col_of = [&](int64_t t) {  // this lane's ring column of block t (zeros when masked)
       const double* col = a.zcol;
-      if (t < t_end && lane < kPrepColsPerProducer) {
+      if (t < t_end && lane < CPP) {
         const int64_t s0 = t * B;
         const int bt = static_cast<int>(a.m - s0 < B ? a.m - s0 : B);
         if (rc < B) {
           if (rc < bt) col = a.X + static_cast<int64_t>(a.idx[s0 + rc]) * a.ldx;
-        } else if (t > 0) {
-          col = a.X + static_cast<int64_t>(a.idx[s0 - B + (rc - B)]) * a.ldx;
+        } else if (rc < 2 * B) {
+          if (t > 0) col = a.X + static_cast<int64_t>(a.idx[s0 - B + (rc - B)]) * a.ldx;
+        } else if (t > 1) {
+          col = a.X + static_cast<int64_t>(a.idx[s0 - 2 * B + (rc - 2 * B)]) * a.ldx;
         }
       }
       return col;
@@ -256,11 +275,10 @@ __global__ void __launch_bounds__(kPrepThreads + 32 * kPrepProducers, kPrepCtas)
         const int len = a.d_pad - k0 < kPrepKC ? a.d_pad - k0 : kPrepKC;
         const uint32_t bytes = static_cast<uint32_t>(len) * sizeof(double);
         mbar_wait_backoff(&empty[stage], phase ^ 1);
-        if (lane == 0) mbar_expect_tx(&full[stage], bytes * kPrepColsPerProducer);
+        if (lane == 0) mbar_expect_tx(&full[stage], bytes * CPP);
         __syncwarp();
-        if (lane < kPrepColsPerProducer)
-          tma_load_1d(ring + (static_cast<size_t>(stage) * kPrepCols + rc) * kPrepPitch, col + k0, bytes,
-                      &full[stage]);
+        if (lane < CPP)
+          tma_load_1d(ring + (static_cast<size_t>(stage) * NCOL + rc) * kPrepPitch, col + k0, bytes, &full[stage]);
         if (++stage == kPrepStages) {
           stage = 0;
           phase ^= 1;
@@ -284,16 +302,17 @@ __global__ void __launch_bounds__(kPrepThreads + 32 * kPrepProducers, kPrepCtas)
     for (int kc = 0; kc < nkc; ++kc) {
       const int len = a.d_pad - kc * kPrepKC < kPrepKC ? a.d_pad - kc * kPrepKC : kPrepKC;
       mbar_wait(&full[stage], phase);
-      const double* sb = ring + static_cast<size_t>(stage) * kPrepCols * kPrepPitch + fr * kPrepPitch + fc;
+      const double* sb = ring + static_cast<size_t>(stage) * NCOL * kPrepPitch + fr * kPrepPitch + fc;
 #pragma unroll
       for (int ks = 0; ks < RPW / 4; ++ks) {
         const int kk = cw * RPW + ks * 4;
         if (kk < len) {
-          double f[G8], fp[G8];
+          double f[G8], fp[LA][G8];
 #pragma unroll
           for (int g = 0; g < G8; ++g) {
             f[g] = sb[g * 8 * kPrepPitch + kk];
-            fp[g] = sb[(B + g * 8) * kPrepPitch + kk];
+#pragma unroll
+            for (int q = 0; q < LA; ++q) fp[q][g] = sb[((q + 1) * B + g * 8) * kPrepPitch + kk];
           }
           int qq = 0;
 #pragma unroll
@@ -301,9 +320,11 @@ __global__ void __launch_bounds__(kPrepThreads + 32 * kPrepProducers, kPrepCtas)
 #pragma unroll
             for (int gl = 0; gl <= gj; ++gl, ++qq) dmma(acc[qq][0], acc[qq][1], f[gj], f[gl]);
 #pragma unroll
-          for (int gj = 0; gj < G8; ++gj)
+          for (int q = 0; q < LA; ++q)
 #pragma unroll
-            for (int gl = 0; gl < G8; ++gl, ++qq) dmma(acc[qq][0], acc[qq][1], f[gj], fp[gl]);
+            for (int gj = 0; gj < G8; ++gj)
+#pragma unroll
+              for (int gl = 0; gl < G8; ++gl, ++qq) dmma(acc[qq][0], acc[qq][1], f[gj], fp[q][gl]);
         }
       }
       __syncwarp();
@@ -333,9 +354,12 @@ __global__ void __launch_bounds__(kPrepThreads + 32 * kPrepProducers, kPrepCtas)
           ++gj;
         }
         K[gj * 8 + mi][rem * 8 + ni] = s;
-      } else {
+      } else if (qq < NW + NX) {
         const int x = qq - NW;
         Kx[(x / G8) * 8 + mi][(x % G8) * 8 + ni] = s;
+      } else if constexpr (LA == 2) {
+        const int x = qq - NW - NX;
+        Kxx[(x / G8) * 8 + mi][(x % G8) * 8 + ni] = s;
       }
     }
     prep_sync();
@@ -382,6 +406,13 @@ __global__ void __launch_bounds__(kPrepThreads + 32 * kPrepProducers, kPrepCtas)
 #pragma unroll
         for (int k = 0; k < B; ++k) s = fma(TT[j][k], Kx[k][l], s);
       slab[B * B + l * B + j] = s;
+      if constexpr (LA == 2) {  // M2_t = TT_t Kxx_t (the ρ^{b_{t−1}} scale is applied by the chain)
+        double s2 = 0.0;
+        if (t > 1)
+#pragma unroll
+          for (int k = 0; k < B; ++k) s2 = fma(TT[j][k], Kxx[k][l], s2);
+        slab[2 * B * B + l * B + j] = s2;
+      }
     }
     prep_sync();
   }
@@ -469,7 +500,7 @@ constexpr int kChainProducers = 4;
 template <int PC, int B, int NP = kChainProducers>
 __device__ __forceinline__ void chain_produce(const EpochArgs& a, int pw, int lane, int nb, int last_bt, int S, int rc,
                                               int r0, int RP, int grp, double* stages, size_t stage_len,
-                                              uint64_t* full, uint64_t* empty) {
+                                              uint64_t* full, uint64_t* empty, int head = 2 * B * B) {
   constexpr int CPP = B / NP;  // columns per producer warp
   static_assert(B % NP == 0 && CPP <= 31, "producers cover the B columns; lane 31 issues the slab");
   int s = 0;
@@ -491,7 +522,7 @@ __device__ __forceinline__ void chain_produce(const EpochArgs& a, int pw, int la
     const int mine = rc > 0 ? max(0, min(CPP, bt - j0)) : 0;
     if (lane == 0) {
       fence_proxy_async();
-      mbar_expect_tx(&full[s], static_cast<uint32_t>(mine * rc + (pw == 0 ? 2 * B * B + B * PC : 0)) * 8u);
+      mbar_expect_tx(&full[s], static_cast<uint32_t>(mine * rc + (pw == 0 ? head + B * PC : 0)) * 8u);
     }
     __syncwarp();
     if (lane < mine) {
@@ -513,9 +544,8 @@ __device__ __forceinline__ void chain_produce(const EpochArgs& a, int pw, int la
     }
     if (pw == 0 && lane == 31) {
       const double* slab = a.slab + static_cast<int64_t>(t) * a.slab_len;
-      tma_load_1d(st + B * RP, slab, 2 * B * B * 8u, &full[s]);
-      tma_load_1d(st + B * RP + 2 * B * B, slab + 2 * B * B + static_cast<size_t>(grp) * B * PC, B * PC * 8u,
-                  &full[s]);
+      tma_load_1d(st + B * RP, slab, static_cast<uint32_t>(head) * 8u, &full[s]);
+      tma_load_1d(st + B * RP + head, slab + head + static_cast<size_t>(grp) * B * PC, B * PC * 8u, &full[s]);
     }
     if (++s == S) {
       s = 0;
@@ -1004,13 +1034,15 @@ int shrink_pc(int pc) { return pc == 8 ? 6 : (pc == 6 ? 4 : std::max(1, pc - 1))
 
 }  // namespace
 
+int slab_head(const EpochConfig& cfg) { return (cfg.la == 2 ? 3 : 2) * kBlock * kBlock; }
+
 size_t xg_slot_elems(const EpochConfig& cfg) {
   return cfg.xg ? static_cast<size_t>(kXgSlots) * cfg.groups * cfg.cluster * kBlock * cfg.pc : 0;
 }
 size_t xg_count_elems(const EpochConfig& cfg) { return cfg.xg ? static_cast<size_t>(kXgSlots) * cfg.groups : 0; }
 
 int64_t epoch_slab_len(const EpochConfig& cfg) {
-  return 2 * kBlock * kBlock + static_cast<int64_t>(kBlock) * cfg.pc * cfg.groups;
+  return slab_head(cfg) + static_cast<int64_t>(kBlock) * cfg.pc * cfg.groups;
 }
 
 size_t epoch_slab_elems(int64_t m, const EpochConfig& cfg) {
@@ -1064,7 +1096,7 @@ __global__ void __launch_bounds__(kBlockUThreads) k_block_u(EpochArgs a) {
 #pragma unroll
         for (int l = 0; l < B; ++l) s = fma(TTs[l * B + j], q[l][c], s);
       }
-      slab[2 * B * B + e] = s;
+      slab[a.slab_head + e] = s;
     }
   }
 }
@@ -1074,6 +1106,7 @@ void launch_block_u(const EpochArgs& a, const EpochConfig& cfg, cudaStream_t st)
   args.pc = cfg.pc;
   args.groups = cfg.groups;
   args.slab_len = epoch_slab_len(cfg);
+  args.slab_head = slab_head(cfg);
   const int64_t nblocks = ceil_div(a.m, kBlock);
   const int grid = static_cast<int>(std::min<int64_t>(nblocks, sm_count_dev() * 16));
   k_block_u<<<grid, kBlockUThreads, 0, st>>>(args);
@@ -1086,15 +1119,23 @@ void launch_block_prep(const EpochArgs& a, const EpochConfig& cfg, cudaStream_t 
   args.pc = cfg.pc;
   args.groups = cfg.groups;
   args.slab_len = epoch_slab_len(cfg);
+  args.slab_head = slab_head(cfg);
   const int64_t nblocks = ceil_div(a.m, kBlock);
   const int grid = static_cast<int>(std::min<int64_t>(nblocks, sm_count_dev() * kPrepCtas));
+  constexpr size_t smem1 = prep_ring_bytes<1>() + prep_red_bytes<1>();
+  constexpr size_t smem2 = prep_ring_bytes<2>() + prep_red_bytes<2>();
   static const bool attr = [] {
-    GAPLRA_CUDA_CHECK(cudaFuncSetAttribute(k_block_prep<kBlock>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           static_cast<int>(kPrepRingBytes)));
+    GAPLRA_CUDA_CHECK(cudaFuncSetAttribute(k_block_prep<kBlock, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           static_cast<int>(smem1)));
+    GAPLRA_CUDA_CHECK(cudaFuncSetAttribute(k_block_prep<kBlock, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           static_cast<int>(smem2)));
     return true;
   }();
   (void)attr;
-  k_block_prep<kBlock><<<grid, kPrepThreads + 32 * kPrepProducers, kPrepRingBytes, st>>>(args);
+  if (cfg.la == 2)
+    k_block_prep<kBlock, 2><<<grid, kPrepThreads + 32 * kPrepProducers, smem2, st>>>(args);
+  else
+    k_block_prep<kBlock, 1><<<grid, kPrepThreads + 32 * kPrepProducers, smem1, st>>>(args);
   GAPLRA_LAUNCH_CHECK();
 }
 
@@ -2082,6 +2123,334 @@ __global__ void __launch_bounds__(v4::kThreads, 1) k_svrg_chain_v4(EpochArgs a) 
   if constexpr (!XG) cg::this_cluster().sync();  // no CTA leaves while a peer may still copy into it
 }
 
+// ---------------------------------------------------------------------------
+// k_chain_p1_la2: the p = 1 chain with a TWO-block lookahead.
+// With V_t = ρ^{b_t} Ŵ_t (V_{−1} = V_{−2} = Ŵ_0) and Â'_t = X_{B_t}ᵀ V_{t−2}:
+//   P̂_t = X_{B_t}ᵀ Ŵ_t = ρ^{b_{t−1}} (Â'_t + Kxx_t coef_{t−2}) + Kx_t coef_{t−1}
+//   coef_t = TT_t P̂_t + U_t
+//          = ρ^{b_{t−1}} (TT_t Â'_t + M2_t coef_{t−2}) + M_t coef_{t−1} + U_t
+// (M = TT Kx, M2 = TT Kxx from k_block_prep<16, 2>; b_{−1} = 0) — the same
+// recurrence as the one-block chains in exact arithmetic.  The rows push Â'_{t+2}
+// (products with V_t) at iteration t, so the all-reduce has two blocks of
+// slack: enough for the L2 exchange (XG) as well as DSMEM, and the rows can be
+// spread thinner (more SMs pull X).  Warps: 4 rows (2 rows per thread; the
+// update re-reads the stage), 1 reducer (lane = entry), 1 pusher, 4 producers.
+// Ring of S >= 5 stages (blocks t, t+1, t+2 live), 8 receive slots (re-armed
+// after use), coef in 4 buffers; named barriers 1-4 hand coef_t to the rows,
+// 5-8 hand the rows' partials of block u to the pusher (by t, u mod 4).
+// ---------------------------------------------------------------------------
+namespace la2 {
+constexpr int B = 16, kRows = 4, kProd = 4, kSlots = 8;
+constexpr int kThreads = 32 * (kRows + 2 + kProd);
+constexpr int kHead = 3 * B * B;  // TT | M | M2
+struct Smem {
+  int rp, stages;
+  size_t stage_len, off_recv, off_red, off_cf, off_ahat, off_outv, off_bar, total;
+};
+__host__ __device__ inline Smem smem(int rows, int stages, bool xg) {
+  Smem L;
+  L.rp = (rows + 15) / 16 * 16;  // ≡ 0 (mod 16): the lane-permuted LDS.128 are conflict free
+  L.stages = stages;
+  L.stage_len = static_cast<size_t>(B) * L.rp + kHead + B;  // slices | TT M M2 | U
+  size_t o = L.stage_len * stages;
+  L.off_recv = o;
+  if (!xg) o += static_cast<size_t>(kSlots) * kMaxCluster * B;
+  L.off_red = o;
+  o += 4 * kRows * B;
+  L.off_cf = o;
+  o += 4 * B;
+  L.off_ahat = o;
+  o += B;
+  L.off_outv = o;
+  o += 4 * B;
+  L.off_bar = o;
+  o += 32;  // full[<=12] | empty[<=12] | rbar[8]
+  L.total = o * sizeof(double);
+  return L;
+}
+}  // namespace la2
+
+template <bool XG>
+__global__ void __launch_bounds__(la2::kThreads, 1) k_chain_p1_la2(EpochArgs a) {
+  using namespace la2;
+  extern __shared__ __align__(128) double sm[];
+  const int G = XG ? static_cast<int>(gridDim.x) : static_cast<int>(cg::this_cluster().num_blocks());
+  const int g = XG ? static_cast<int>(blockIdx.x) : static_cast<int>(cg::this_cluster().block_rank());
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const Smem L = smem(a.rows_per_cta, a.stages, XG);
+  const int S = L.stages, RP = L.rp;
+  const int r0 = g * a.rows_per_cta;
+  const int rc = max(0, min(a.rows_per_cta, a.d_pad - r0));
+  double* recv = sm + L.off_recv;  // [kSlots][kMaxCluster][B]
+  double* red = sm + L.off_red;    // [4][kRows][B]
+  double* cf = sm + L.off_cf;      // [4][B]: coef_t in cf[t & 3]
+  double* Ahat = sm + L.off_ahat;  // [B]
+  double* outv = sm + L.off_outv;  // [4][B]
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + L.off_bar);
+  uint64_t* empty = full + 12;
+  uint64_t* rbar = full + 24;
+  double* xg_slots = XG ? a.xg_slot : nullptr;  // [kSlots][G][B]
+  unsigned* xg_cnt = XG ? a.xg_count : nullptr;  // [kSlots]
+  auto stage_at = [&](int t) { return sm + static_cast<size_t>(t % S) * L.stage_len; };
+  const int nb = static_cast<int>((a.m + B - 1) / B);
+  const int last_bt = static_cast<int>(a.m - static_cast<int64_t>(nb - 1) * B);
+  auto bt_of = [&](int t) { return t == nb - 1 ? last_bt : B; };
+  double rho_b = 1.0, rho_last = 1.0;
+  for (int j = 0; j < B; ++j) rho_b *= a.rho;
+  for (int j = 0; j < last_bt; ++j) rho_last *= a.rho;
+  auto rho_of = [&](int t) { return t < 0 ? 1.0 : (t == nb - 1 ? rho_last : rho_b); };  // ρ^{b_t}
+#pragma unroll 1
+  for (size_t e = tid; e < L.off_recv; e += blockDim.x) sm[e] = 0.0;  // pad rows / unwritten slices read as 0
+  for (int e = tid; e < 4 * B; e += blockDim.x) cf[e] = 0.0;        // coef_{−1} = coef_{−2} = 0
+  if (tid == 0) {
+    for (int q = 0; q < S; ++q) {
+      mbar_init(&full[q], kProd);
+      mbar_init(&empty[q], kRows + 1);
+    }
+    for (int q = 0; q < kSlots; ++q) mbar_init(&rbar[q], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if constexpr (XG)
+    __syncthreads();
+  else
+    cg::this_cluster().sync();
+  long long tacc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long tp;
+  asm volatile("mov.u64 %0, %%clock64;" : "=l"(tp)::"memory");
+  auto tick = [&](int kk) {
+    if (a.dbg) {
+      long long now;
+      asm volatile("mov.u64 %0, %%clock64;" : "=l"(now)::"memory");
+      tacc[kk] += now - tp;
+      tp = now;
+    }
+  };
+  auto red_arrive = [](int u) {  // rows -> pusher: red(u) written (barriers 5..8)
+    switch (u & 3) {
+      case 0: asm volatile("bar.arrive 5, %0;" ::"n"(32 * (kRows + 1)) : "memory"); break;
+      case 1: asm volatile("bar.arrive 6, %0;" ::"n"(32 * (kRows + 1)) : "memory"); break;
+      case 2: asm volatile("bar.arrive 7, %0;" ::"n"(32 * (kRows + 1)) : "memory"); break;
+      default: asm volatile("bar.arrive 8, %0;" ::"n"(32 * (kRows + 1)) : "memory"); break;
+    }
+  };
+  auto red_sync = [](int u) {
+    switch (u & 3) {
+      case 0: asm volatile("bar.sync 5, %0;" ::"n"(32 * (kRows + 1)) : "memory"); break;
+      case 1: asm volatile("bar.sync 6, %0;" ::"n"(32 * (kRows + 1)) : "memory"); break;
+      case 2: asm volatile("bar.sync 7, %0;" ::"n"(32 * (kRows + 1)) : "memory"); break;
+      default: asm volatile("bar.sync 8, %0;" ::"n"(32 * (kRows + 1)) : "memory"); break;
+    }
+  };
+  auto coef_arrive = [](int t) {  // reducer -> rows: coef_t in cf[t & 3] (barriers 1..4)
+    switch (t & 3) {
+      case 0: asm volatile("bar.arrive 1, %0;" ::"n"(32 * (kRows + 1)) : "memory"); break;
+      case 1: asm volatile("bar.arrive 2, %0;" ::"n"(32 * (kRows + 1)) : "memory"); break;
+      case 2: asm volatile("bar.arrive 3, %0;" ::"n"(32 * (kRows + 1)) : "memory"); break;
+      default: asm volatile("bar.arrive 4, %0;" ::"n"(32 * (kRows + 1)) : "memory"); break;
+    }
+  };
+  auto coef_sync = [](int t) {
+    switch (t & 3) {
+      case 0: asm volatile("bar.sync 1, %0;" ::"n"(32 * (kRows + 1)) : "memory"); break;
+      case 1: asm volatile("bar.sync 2, %0;" ::"n"(32 * (kRows + 1)) : "memory"); break;
+      case 2: asm volatile("bar.sync 3, %0;" ::"n"(32 * (kRows + 1)) : "memory"); break;
+      default: asm volatile("bar.sync 4, %0;" ::"n"(32 * (kRows + 1)) : "memory"); break;
+    }
+  };
+
+  if (warp >= kRows + 2) {  // ------------------------------------------- producers
+    chain_produce<1, B, kProd>(a, warp - kRows - 2, lane, nb, last_bt, S, rc, r0, RP, 0, sm, L.stage_len, full,
+                               empty, kHead);
+  } else if (warp == kRows + 1) {  // -------------------------------------- pusher
+    for (int u = 0; u < nb; ++u) {
+      red_sync(u);
+      if (!XG && lane < G) asm volatile("cp.async.bulk.wait_group.read 3;" ::: "memory");  // outv[u & 3] free
+      __syncwarp();
+      const double* rb = red + (u & 3) * kRows * B;
+      const int e = lane & 15;
+      const double sum = (rb[e] + rb[B + e]) + (rb[2 * B + e] + rb[3 * B + e]);
+      if constexpr (XG) {
+        if (lane < B) st_cg(xg_slots + (static_cast<size_t>(u % kSlots) * G + g) * B + e, sum);
+        __syncwarp();
+        if (lane == 0) xg_publish(xg_cnt + u % kSlots);
+      } else {
+        double* ov = outv + (u & 3) * B;
+        if (lane < B) ov[e] = sum;
+        fence_proxy_async();
+        __syncwarp();
+        if (lane < G) {
+          const int q = u % kSlots;
+          dsmem_bulk_copy(mapa(smem_u32(recv + (q * kMaxCluster + g) * B), lane), smem_u32(ov), B * 8u,
+                          mapa(smem_u32(&rbar[q]), lane));
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+      }
+    }
+    if (!XG && lane < G) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  } else if (warp == kRows) {  // ----------------------------------------- reducer
+    const int j = lane & 15;
+    if (!XG && lane == 0)
+      for (int q = 0; q < kSlots && q < nb; ++q) mbar_expect_tx(&rbar[q], static_cast<uint32_t>(G * B * 8));
+#pragma unroll 1
+    for (int t = 0; t < nb; ++t) {
+      tick(7);
+      mbar_wait(&full[t % S], static_cast<uint32_t>((t / S) & 1));
+      const double* sl = stage_at(t) + B * RP;  // TT, M, M2 transposed ([l][j]), then U
+      const double rprev = rho_of(t - 1);
+      const double* c1 = cf + ((t - 1) & 3) * B;
+      const double* c2 = cf + ((t - 2) & 3) * B;
+      double pre;
+      {
+        double s0 = sl[3 * B * B + j], s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+        for (int l = 0; l < B; l += 2) {
+          s0 = fma(sl[B * B + l * B + j], c1[l], s0);
+          s1 = fma(sl[B * B + (l + 1) * B + j], c1[l + 1], s1);
+          s2 = fma(sl[2 * B * B + l * B + j], c2[l], s2);
+          s3 = fma(sl[2 * B * B + (l + 1) * B + j], c2[l + 1], s3);
+        }
+        pre = (s0 + s1) + rprev * (s2 + s3);
+      }
+      tick(6);
+      const int bt = bt_of(t);
+      if constexpr (XG) {
+        if (lane == 0) xg_wait(xg_cnt + t % kSlots, static_cast<unsigned>(G) * (t / kSlots + 1));
+        __syncwarp();
+        tick(5);
+        const int hq = (lane >> 4) * 2;
+        const double* ps = xg_slots + static_cast<size_t>(t % kSlots) * G * B + j;
+        double sa = 0.0, sb = 0.0;
+#pragma unroll 4
+        for (int q = 0; q < G; q += 4) {
+          sa += ld_cg(ps + (q + hq) * B);
+          sb += ld_cg(ps + (q + hq + 1) * B);
+        }
+        const double sv = sa + sb;
+        const double other = __shfl_down_sync(0xffffffffu, sv, 16);
+        if (lane < B) Ahat[j] = j < bt ? sv + other : 0.0;
+      } else {
+        mbar_wait(&rbar[t % kSlots], static_cast<uint32_t>((t / kSlots) & 1));
+        tick(5);
+        if (lane < B) {
+          const double* ps = recv + (t % kSlots) * kMaxCluster * B + j;
+          double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll 1
+          for (int q = 0; q < G; q += 4) {
+            s0 += ps[q * B];
+            s1 += ps[(q + 1) * B];
+            s2 += ps[(q + 2) * B];
+            s3 += ps[(q + 3) * B];
+          }
+          Ahat[j] = j < bt ? (s0 + s1) + (s2 + s3) : 0.0;
+        }
+      }
+      __syncwarp();
+      if (lane < B) {
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+        for (int l = 0; l < B; l += 4) {
+          s0 = fma(sl[l * B + j], Ahat[l], s0);
+          s1 = fma(sl[(l + 1) * B + j], Ahat[l + 1], s1);
+          s2 = fma(sl[(l + 2) * B + j], Ahat[l + 2], s2);
+          s3 = fma(sl[(l + 3) * B + j], Ahat[l + 3], s3);
+        }
+        cf[(t & 3) * B + j] = fma(rprev, (s0 + s1) + (s2 + s3), pre);
+      }
+      __syncwarp();
+      coef_arrive(t);
+      tick(4);
+      if (lane == 0) {
+        if (!XG && t + kSlots < nb) mbar_expect_tx(&rbar[t % kSlots], static_cast<uint32_t>(G * B * 8));
+        mbar_arrive(&empty[t % S]);  // TT, M, M2, U of block t: the reducer's last use
+      }
+    }
+    if (a.dbg && lane == 0) {
+      const int cta = blockIdx.y * gridDim.x + blockIdx.x;
+      for (int kk = 4; kk < 8; ++kk) a.dbg[cta * 8 + kk] = tacc[kk];
+    }
+  } else {  // --------------------------------------------------------------- rows
+    const int pm = lane >> 1;  // product order j = i ^ pm (select-free warp halving)
+    const int ra = 2 * tid;    // rows ra, ra + 1 of the CTA's slice
+    const bool own0 = ra < rc, own1 = ra + 1 < rc;
+    double v0 = own0 ? a.W[static_cast<int64_t>(r0 + ra) * a.ldw] : 0.0;
+    double v1 = own1 ? a.W[static_cast<int64_t>(r0 + ra + 1) * a.ldw] : 0.0;
+    auto wait_stage = [&](int t) { mbar_wait(&full[t % S], static_cast<uint32_t>((t / S) & 1)); };
+    auto load_rows = [&](const double* xb, double2 (&xr)[B]) {
+#pragma unroll
+      for (int i = 0; i < B; ++i) xr[i] = *reinterpret_cast<const double2*>(xb + (i ^ pm) * RP + ra);
+    };
+    auto products = [&](const double2 (&xr)[B], int u) {
+      double val[B];
+#pragma unroll
+      for (int i = 0; i < B; ++i) val[i] = fma(xr[i].x, v0, xr[i].y * v1);
+#pragma unroll
+      for (int o = 16, n = B / 2; o >= 2; o >>= 1, n >>= 1)
+#pragma unroll
+        for (int i = 0; i < n; ++i) val[i] += __shfl_xor_sync(0xffffffffu, val[i + n], o);
+      val[0] += __shfl_xor_sync(0xffffffffu, val[0], 1);
+      if (!(lane & 1)) red[(u & 3) * kRows * B + warp * B + pm] = val[0];
+      red_arrive(u);
+    };
+    auto update = [&](const double2 (&xr)[B], int t, double rn) {
+      tick(1);
+      coef_sync(t);
+      tick(2);
+      const double* c = cf + (t & 3) * B;
+      double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+      for (int i = 0; i < B; i += 2) {
+        const double k0 = c[i ^ pm], k1 = c[(i + 1) ^ pm];
+        v0 = fma(xr[i].x, k0, v0);
+        v1 = fma(xr[i].y, k0, v1);
+        a0 = fma(xr[i + 1].x, k1, a0);
+        a1 = fma(xr[i + 1].y, k1, a1);
+      }
+      v0 = own0 ? (v0 + a0) * rn : 0.0;
+      v1 = own1 ? (v1 + a1) * rn : 0.0;
+    };
+    double2 xr[B];
+    // Â'_0 = X_{B_0}ᵀ Ŵ_0 and Â'_1 = X_{B_1}ᵀ Ŵ_0 (V_{−2} = V_{−1} = Ŵ_0), then V_0 = ρ^{b_0} Ŵ_0
+    for (int u = 0; u < 2 && u < nb; ++u) {
+      wait_stage(u);
+      load_rows(stage_at(u), xr);
+      products(xr, u);
+    }
+    {
+      const double r = rho_of(0);
+      v0 *= r;
+      v1 *= r;
+    }
+#pragma unroll 1
+    for (int t = 0; t < nb; ++t) {
+      if (t + 2 < nb) {
+        tick(3);
+        wait_stage(t + 2);
+        tick(0);
+        load_rows(stage_at(t + 2), xr);
+        products(xr, t + 2);  // with V_t
+      }
+      load_rows(stage_at(t), xr);
+      update(xr, t, t + 1 < nb ? rho_of(t + 1) : 1.0);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[t % S]);
+    }
+    if (a.dbg && tid == 0) {
+      const int cta = blockIdx.y * gridDim.x + blockIdx.x;
+      for (int kk = 0; kk < 4; ++kk) a.dbg[cta * 8 + kk] = tacc[kk];
+    }
+    const double beta = -expm1(static_cast<double>(a.m) * log1p(a.rho - 1.0)) / (1.0 - a.rho);
+    if (own0) {
+      const int64_t o = static_cast<int64_t>(r0 + ra) * a.ldw;
+      a.W[o] = fma(beta, a.C[o], v0);
+    }
+    if (own1) {
+      const int64_t o = static_cast<int64_t>(r0 + ra + 1) * a.ldw;
+      a.W[o] = fma(beta, a.C[o], v1);
+    }
+  }
+  if constexpr (!XG) cg::this_cluster().sync();
+}
+
 // Clusters of `cluster` one-SM CTAs that can be resident at once (a cluster
 // lives inside one GPC, so this is below SMs / cluster when GPCs are uneven).
 int max_active_clusters(int cluster) {
@@ -2168,6 +2537,29 @@ EpochConfig choose_epoch_config(int d_pad, int p) {
       while (cfg.stages > 2 && v4::smem(cfg.rows_per_cta, cfg.stages, true).total > 227 * 1024) --cfg.stages;
       cfg.smem = cfg.rows_per_cta > 256 ? v4::smem_half().total : v4::smem(cfg.rows_per_cta, cfg.stages, true).total;
       return cfg;
+    }
+  }
+  // p = 1 with the two-block lookahead chain (k_chain_p1_la2): GAPLRA_P1_LA2=1,
+  // GAPLRA_LA2_ROWS rows per CTA (128), GAPLRA_LA2_XG=1 forces the L2 exchange
+  // (otherwise a DSMEM cluster when the CTAs fit one: <= 16)
+  static const int env_la2 = getenv("GAPLRA_P1_LA2") ? atoi(getenv("GAPLRA_P1_LA2")) : 0;
+  static const int env_la2_rows = getenv("GAPLRA_LA2_ROWS") ? atoi(getenv("GAPLRA_LA2_ROWS")) : 128;
+  static const int env_la2_xg = getenv("GAPLRA_LA2_XG") ? atoi(getenv("GAPLRA_LA2_XG")) : 0;
+  if (p == 1 && env_la2 && env_pc == 0 && d_pad > 1024 && d_pad <= 8192) {
+    EpochConfig cfg;
+    cfg.b = kBlock;
+    cfg.pc = 1;
+    cfg.groups = 1;
+    cfg.la = 2;
+    const int want = std::max(32, std::min(256, env_la2_rows));
+    cfg.cluster = static_cast<int>(ceil_div(ceil_div(d_pad, want), 4) * 4);
+    cfg.rows_per_cta = static_cast<int>(ceil_div(ceil_div(d_pad, cfg.cluster), 4) * 4);
+    cfg.xg = (env_la2_xg || cfg.cluster > 16) ? 1 : 0;
+    if (cfg.cluster <= sm_count_dev() && (cfg.xg || max_active_clusters(cfg.cluster) >= 1)) {
+      cfg.stages = 6;
+      while (cfg.stages > 5 && la2::smem(cfg.rows_per_cta, cfg.stages, cfg.xg).total > 227 * 1024) --cfg.stages;
+      cfg.smem = la2::smem(cfg.rows_per_cta, cfg.stages, cfg.xg).total;
+      if (cfg.smem <= 227 * 1024) return cfg;
     }
   }
   // p = 1, 1024 < d <= 8192, GAPLRA_P1_XG=1 (experiment, off by default): the
@@ -2301,8 +2693,46 @@ void launch_chain_pc(const EpochArgs& a, const EpochConfig& cfg, cudaStream_t st
   GAPLRA_LAUNCH_CHECK();
 }
 
+void launch_chain_la2(const EpochArgs& a, const EpochConfig& cfg, cudaStream_t st) {
+  const bool xg = cfg.xg != 0;
+  auto kern = xg ? k_chain_p1_la2<true> : k_chain_p1_la2<false>;
+  const size_t smem = la2::smem(cfg.rows_per_cta, cfg.stages, xg).total;
+  GAPLRA_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  if (!xg && cfg.cluster > 8)
+    GAPLRA_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3(cfg.cluster, 1, 1);
+  lc.blockDim = dim3(la2::kThreads, 1, 1);
+  lc.dynamicSmemBytes = smem;
+  lc.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cfg.cluster;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  lc.attrs = attr;
+  lc.numAttrs = xg ? 0 : 1;
+  if (xg) {
+    if (!a.xg_slot || !a.xg_count) throw Error(kContractViolation, "epoch: XG layout without exchange buffers");
+    GAPLRA_CUDA_CHECK(cudaMemsetAsync(a.xg_count, 0, xg_count_elems(cfg) * sizeof(unsigned), st));
+  }
+  EpochArgs args = a;
+  args.rows_per_cta = cfg.rows_per_cta;
+  args.stages = cfg.stages;
+  args.pc = 1;
+  args.groups = 1;
+  args.slab_len = epoch_slab_len(cfg);
+  args.slab_head = slab_head(cfg);
+  GAPLRA_CUDA_CHECK(cudaLaunchKernelEx(&lc, kern, args));
+  GAPLRA_LAUNCH_CHECK();
+}
+
 void launch_svrg_epoch_dense(const EpochArgs& a, const EpochConfig& cfg, cudaStream_t st) {
   if (cfg.smem > 227 * 1024) throw Error(kContractViolation, "epoch: d too large for the cluster row split");
+  if (cfg.la == 2) {
+    launch_chain_la2(a, cfg, st);
+    return;
+  }
   switch (cfg.pc) {
     case 1: launch_chain_pc<1>(a, cfg, st); break;
     case 2: launch_chain_pc<2>(a, cfg, st); break;

@@ -19,8 +19,9 @@ struct EpochArgs {
   const double* H;  // n x ldy: H_i = x_iᵀ C
   int64_t ldy;
   const double* zcol;  // d_pad zeros (masked Gram columns)
-  double* slab;     // per s-step block: [TT | M | U(groups)] (launch_block_prep)
+  double* slab;     // per s-step block: [TT | M | (M2) | U(groups)] (launch_block_prep)
   int64_t slab_len;
+  int slab_head;    // doubles before U: 2 B² (TT | M), 3 B² with the two-block lookahead (| M2)
   int p;
   double rho, eta_n;
   int rows_per_cta, stages, pc, groups;
@@ -51,7 +52,9 @@ struct EpochConfig {
   int cluster, pc, b, rows_per_cta, groups, stages;
   size_t smem;
   int xg = 0;  // 1: the `cluster` CTAs of a group are plain CTAs exchanging through L2 (no cluster launch)
+  int la = 1;  // chain lookahead in s-step blocks (2: the p = 1 chain k_chain_p1_la2)
 };
+int slab_head(const EpochConfig& cfg);
 // XG exchange buffers of an epoch layout (doubles / counters); 0 when !cfg.xg
 size_t xg_slot_elems(const EpochConfig& cfg);
 size_t xg_count_elems(const EpochConfig& cfg);
