@@ -187,13 +187,13 @@ def cpu_baseline(spec, x_cols, ledger, seconds):
 
 
 # ----------------------------------------------------------------- rooflines
-def rooflines(prof):
+def rooflines(prof, config="C5"):
     peaks = json.loads(PEAKS.read_text()) if PEAKS.exists() else {}
     hbm = float(peaks.get("hbm_gbs", 6650.0))
     hbm_src = "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6.65 TB/s (B200_PROFILING.md)"
     ridge = FP64_PEAK_TFLOPS * 1e12 / (hbm * 1e9)
-    traffic = json.loads(NCU_TRAFFIC.read_text()) if NCU_TRAFFIC.exists() else {}
-    tsrc = traffic.get("_source", str(NCU_TRAFFIC.relative_to(ROOT)))
+    traffic = json.loads(NCU_TRAFFIC.read_text()).get(config, {}) if NCU_TRAFFIC.exists() else {}
+    tsrc = f"{NCU_TRAFFIC.relative_to(ROOT)} [{config}]: " + traffic.get("_source", "")
     out = {}
     for name, v in prof.items():
         if not v["count"] or v["ms"] <= 0:
@@ -350,7 +350,7 @@ def run_ours(args, rank, world, local_rank):
         if dist:
             dist.destroy_process_group()
         return
-    rl = rooflines(prof)
+    rl = rooflines(prof, spec.name)
     dominant = max(rl, key=lambda kk: rl[kk]["ms_per_launch"] * rl[kk]["launches"]) if rl else None
     step_ledger = last.ledger  # ONE step's counts (the report is per call)
     out_dir = ROOT / "gpurun_out"
