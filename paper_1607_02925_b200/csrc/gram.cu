@@ -506,7 +506,7 @@ void xy_chunk(const DenseX& X, const double* Y, int64_t ldy, int pc, double* Z, 
 template <int NT>
 void xtw_mma_chunk(const DenseX& X, const double* W, int64_t ldw, int pc, double* Y, int64_t ldy, GramWork& work,
                    cudaStream_t st, int rs, int rows_per_split) {
-  constexpr int MW = 2;
+  constexpr int MW = 2;  // (MW = 1 at NT = 8, two CTAs per SM: 101 vs 81 ms at C5, slower still)
   constexpr size_t smem = 2 * kKC * b_pitch<NT>() * sizeof(double);
   static bool attr = false;
   if (!attr && smem > 48 * 1024) {
