@@ -1985,14 +1985,13 @@ __global__ void __launch_bounds__(v4::kThreads, 1) k_svrg_chain_v4(EpochArgs a) 
     // Âᵀ partial over the warp's rows: 2 slice tiles (slices 0-7 at xb0, 8-15 at
     // xb1), K = the rows; HALF: half kw (then kw + 1) is waited for just before use
     auto products = [&](const double* xb0, const double* xb1, int u_blk, int kw) {
-      // four independent accumulator chains per slice tile (the two k-steps of
-      // a row tile go to different chains): DMMA latency, not issue, bounded
-      // the two-chain form
-      double acc[2][4][2];  // [slice tile][chain][elem]
+      // (four accumulator chains per slice tile measured slower: products 1366 ->
+      // 1703 cycles per block at C5)
+      double acc[2][2][2];  // [slice tile][chain][elem]
 #pragma unroll
       for (int n2 = 0; n2 < 2; ++n2)
 #pragma unroll
-        for (int ch = 0; ch < 4; ++ch) acc[n2][ch][0] = acc[n2][ch][1] = 0.0;
+        for (int ch = 0; ch < 2; ++ch) acc[n2][ch][0] = acc[n2][ch][1] = 0.0;
 #pragma unroll
       for (int n2 = 0; n2 < 2; ++n2) {
         if constexpr (HALF) wait_half(kw + n2);
@@ -2000,9 +1999,8 @@ __global__ void __launch_bounds__(v4::kThreads, 1) k_svrg_chain_v4(EpochArgs a) 
 #pragma unroll
         for (int tl = 0; tl < kTiles; ++tl) {
           const double2 xv = *reinterpret_cast<const double2*>(xb + perm * RP + rw0 + 8 * tl + 2 * tq);
-          const int ca = (2 * tl) & 3, cb = (2 * tl + 1) & 3;
-          dmma(acc[n2][ca][0], acc[n2][ca][1], v[tl][0], xv.x);
-          dmma(acc[n2][cb][0], acc[n2][cb][1], v[tl][1], xv.y);
+          dmma(acc[n2][tl & 1][0], acc[n2][tl & 1][1], v[tl][0], xv.x);
+          dmma(acc[n2][tl & 1][0], acc[n2][tl & 1][1], v[tl][1], xv.y);
         }
       }
       // C fragment (column gq, slices 8 n2 + perm(2 tq), 8 n2 + perm(2 tq + 1)) -> red(u_blk) in [j PC + c]
@@ -2011,8 +2009,8 @@ __global__ void __launch_bounds__(v4::kThreads, 1) k_svrg_chain_v4(EpochArgs a) 
       const int pb = ((2 * tq + 1) & 1) << 1 | (((2 * tq + 1) >> 1) & 1) | ((2 * tq + 1) & 4);
 #pragma unroll
       for (int n2 = 0; n2 < 2; ++n2) {
-        rb[(8 * n2 + pa) * PC + gq] = (acc[n2][0][0] + acc[n2][1][0]) + (acc[n2][2][0] + acc[n2][3][0]);
-        rb[(8 * n2 + pb) * PC + gq] = (acc[n2][0][1] + acc[n2][1][1]) + (acc[n2][2][1] + acc[n2][3][1]);
+        rb[(8 * n2 + pa) * PC + gq] = acc[n2][0][0] + acc[n2][1][0];
+        rb[(8 * n2 + pb) * PC + gq] = acc[n2][0][1] + acc[n2][1][1];
       }
       bar_red_arrive(u_blk);
     };
@@ -2039,7 +2037,8 @@ __global__ void __launch_bounds__(v4::kThreads, 1) k_svrg_chain_v4(EpochArgs a) 
         for (int ks = 0; ks < 4; ++ks)
 #pragma unroll
           for (int tl = 0; tl < kTiles; ++tl) dmma(v[tl][0], v[tl][1], af[ks], bx[ks][tl]);
-      } else {  // 512 rows: two k-steps of B fragments in flight (register budget of 480 threads)
+      } else {  // 512 rows: two k-steps of B fragments in flight (register budget of 480 threads;
+                // a k-step software pipeline measured no faster: update 1821 vs 1803 cycles)
 #pragma unroll
         for (int k2 = 0; k2 < 4; k2 += 2) {
           const double* xh = k2 ? xb1 : xb0;  // slices 4 (k2 + ks) + tq = 8 (k2 / 2) + 4 ks + tq
