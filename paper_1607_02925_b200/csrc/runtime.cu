@@ -191,6 +191,7 @@ struct Context {
   DBuf<unsigned> xgc;    //   and their arrival counters
   DBuf<double> spd;  // blocked sparse epoch: b, u
   DBuf<int> spi;     // blocked sparse epoch: row lists, pairs, counters
+  DBuf<double> spl;  // level-scheduled sparse epoch: symbolic plan + b, u (bytes / 8)
   // Side stream for the next epoch's W-independent precompute (index stream +
   // k_block_prep), run beside the current epoch's chain on the SMs the chain
   // leaves idle.  Events order it against the main stream.
@@ -563,7 +564,13 @@ void epoch_run_dev(Context& c, Matrix& X, int p, double* W, const double* C, con
     a.eta_n = eta_n;
     static const bool blocked = !(getenv("GAPLRA_SPARSE_BLOCKED") && atoi(getenv("GAPLRA_SPARSE_BLOCKED")) == 0);
     Prof prof(c, p > 1 ? kProfEpoch : kProfEpochP1, col_bytes * m, 4.0 * col_nnz * p * m);
-    if (blocked && sparse_blocked_supported(p) && X.max_col_nnz > 0) {
+    // GAPLRA_SPARSE_LEVELS=0: the fixed-point block kernel of sparse_epoch.cu instead of the level-scheduled one
+    static const bool levels = !(getenv("GAPLRA_SPARSE_LEVELS") && atoi(getenv("GAPLRA_SPARSE_LEVELS")) == 0);
+    if (blocked && levels && sparse_levels_supported(p) && X.max_col_nnz > 0) {
+      const SparseLevelPlan plan = sparse_levels_plan(X.d, m, col_nnz, X.max_col_nnz);
+      void* scratch = c.spl.ensure((plan.bytes + 7) / 8);
+      launch_svrg_epoch_sparse_levels(a, plan, scratch, c.st);
+    } else if (blocked && sparse_blocked_supported(p) && X.max_col_nnz > 0) {
       const int bs = sparse_block_steps(X.d, col_nnz, p);
       double* db = c.spd.ensure(2 * static_cast<size_t>(bs) * p);
       const size_t ni = sparse_scratch_ints(X.d, bs, X.max_col_nnz);

@@ -130,6 +130,67 @@ __device__ __forceinline__ void st_cg(double* p, double v) {
   asm volatile("st.global.cg.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
 }
 
+// ---- flag-in-data ("LL") exchange cells: a partial travels as one 16-byte
+// cell {lo32, flag, hi32, flag}; 8-byte halves are written and read atomically,
+// so a reader that sees both flags equal to the expected value has the whole
+// double — no fence, no counter, one L2 store + one L2 load on the critical
+// path (the counter protocol above pays a MEMBAR.GPU + a counter round trip +
+// the partial loads).  flag = 1 + (uses of the slot so far); the cells are
+// zeroed before every launch, so a stale cell never matches.
+__device__ __forceinline__ void ll_store(uint4* cell, double v, uint32_t flag) {
+  asm volatile("st.volatile.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(cell), "r"(__double2loint(v)), "r"(flag),
+               "r"(__double2hiint(v)), "r"(flag)
+               : "memory");
+}
+__device__ __forceinline__ uint4 ll_load(const uint4* cell) {
+  uint4 w;
+  asm volatile("ld.volatile.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(w.x), "=r"(w.y), "=r"(w.z), "=r"(w.w)
+               : "l"(cell)
+               : "memory");
+  return w;
+}
+// Sum over the G peers of entry e = lane & 15 of a 16-entry slot ([G][16]
+// cells): lanes 0-15 take peers q, q + 1 and lanes 16-31 peers q + 2, q + 3 of
+// every four, (sa + sb) per half then half 0 + half 1 — the same fixed order as
+// the counter form.  Up to 16 cells per lane are polled at once.
+__device__ __forceinline__ double ll_gather16(const uint4* slot, int G, int lane, uint32_t flag) {
+  const int e = lane & 15, hq = (lane >> 4) * 2;
+  double sa = 0.0, sb = 0.0;
+#pragma unroll 1
+  for (int q0 = 0; q0 < G; q0 += 32) {
+    uint4 w[16];
+    unsigned pend = 0;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      const int peer = q0 + 4 * (k >> 1) + hq + (k & 1);
+      if (peer < G) {
+        w[k] = ll_load(slot + peer * 16 + e);
+        pend |= 1u << k;
+      } else {
+        w[k] = make_uint4(0u, flag, 0u, flag);
+      }
+    }
+    while (pend) {
+#pragma unroll
+      for (int k = 0; k < 16; ++k)
+        if (pend >> k & 1u) {
+          if (w[k].y == flag && w[k].w == flag)
+            pend &= ~(1u << k);
+          else
+            w[k] = ll_load(slot + (q0 + 4 * (k >> 1) + hq + (k & 1)) * 16 + e);
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      sa += __hiloint2double(static_cast<int>(w[2 * i].z), static_cast<int>(w[2 * i].x));
+      sb += __hiloint2double(static_cast<int>(w[2 * i + 1].z), static_cast<int>(w[2 * i + 1].x));
+    }
+  }
+  const double sv = sa + sb;
+  return sv + __shfl_down_sync(0xffffffffu, sv, 16);
+}
+
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                : "+d"(c0), "+d"(c1)
@@ -1036,8 +1097,8 @@ int shrink_pc(int pc) { return pc == 8 ? 6 : (pc == 6 ? 4 : std::max(1, pc - 1))
 
 int slab_head(const EpochConfig& cfg) { return (cfg.la == 2 ? 3 : 2) * kBlock * kBlock; }
 
-size_t xg_slot_elems(const EpochConfig& cfg) {
-  return cfg.xg ? static_cast<size_t>(kXgSlots) * cfg.groups * cfg.cluster * kBlock * cfg.pc : 0;
+size_t xg_slot_elems(const EpochConfig& cfg) {  // doubles; x 2 for the 16-byte flag-in-data cells
+  return cfg.xg ? 2 * static_cast<size_t>(kXgSlots) * cfg.groups * cfg.cluster * kBlock * cfg.pc : 0;
 }
 size_t xg_count_elems(const EpochConfig& cfg) { return cfg.xg ? static_cast<size_t>(kXgSlots) * cfg.groups : 0; }
 
@@ -1270,7 +1331,15 @@ __global__ void __launch_bounds__(v3_block<RR>(PC), 1) k_svrg_chain_v3(EpochArgs
       __syncwarp();
       const double* rb = red + (u & 1) * kV3Rows * NV;
       double* ov = outv + (u & 1) * NV;
-      if constexpr (XG) {  // partial -> L2 slot, then one release-increment
+      if constexpr (XG) {
+        if (a.xg_ll) {  // one flag-in-data cell per entry: no fence, no counter
+          uint4* dst = reinterpret_cast<uint4*>(xg_slots) + (static_cast<size_t>(u % kXgSlots) * G + g) * NV;
+          for (int e = lane; e < NV; e += 32)
+            ll_store(dst + e, (rb[e] + rb[NV + e]) + (rb[2 * NV + e] + rb[3 * NV + e]),
+                     static_cast<uint32_t>(u / kXgSlots + 1));
+          continue;
+        }
+        // partial -> L2 slot, then one release-increment
         double* dst = xg_slots + (static_cast<size_t>(u % kXgSlots) * G + g) * NV;
         for (int e = lane; e < NV; e += 32) st_cg(dst + e, (rb[e] + rb[NV + e]) + (rb[2 * NV + e] + rb[3 * NV + e]));
         __syncwarp();
@@ -1320,6 +1389,13 @@ __global__ void __launch_bounds__(v3_block<RR>(PC), 1) k_svrg_chain_v3(EpochArgs
       tick(7);
       const int nv = bt_of(t) * PC;
       if constexpr (XG) {
+       if (a.xg_ll) {
+        const double sv = ll_gather16(reinterpret_cast<const uint4*>(xg_slots) + static_cast<size_t>(t % kXgSlots) * G * NV,
+                                      G, lane, static_cast<uint32_t>(t / kXgSlots + 1));
+        tick(6);
+        if (lane < 16) Ahat[lane] = lane < nv ? sv : 0.0;
+        __syncwarp();
+       } else {
         // NV = 16 entries; lane e and e + 16 split the peers (q mod 4 in {0,1} / {2,3}),
         // (s0 + s1) + (s2 + s3) in the same order as the DSMEM form
         if (lane == 0) xg_wait(xg_cnt + t % kXgSlots, static_cast<unsigned>(G) * (t / kXgSlots + 1));
@@ -1337,6 +1413,7 @@ __global__ void __launch_bounds__(v3_block<RR>(PC), 1) k_svrg_chain_v3(EpochArgs
         const double other = __shfl_down_sync(0xffffffffu, sv, 16);
         if (lane < 16) Ahat[e] = e < nv ? sv + other : 0.0;
         __syncwarp();
+       }
       } else {
         mbar_wait(&rbar[par], static_cast<uint32_t>((t >> 2) & 1));
         tick(6);
@@ -1615,10 +1692,10 @@ struct Smem {
   int rp, stages;
   size_t stage_len, off_recv, off_red, off_outv, off_cf, off_ahat, off_pre, off_bar, total;
 };
-__host__ __device__ inline int span(int rows) { return rows <= 256 ? 256 : 512; }
+__host__ __device__ inline int span(int rows) { return rows <= 128 ? 128 : (rows <= 256 ? 256 : 512); }
 __host__ __device__ inline Smem smem(int rows, int stages, bool xg = false) {
   Smem L;
-  L.rp = span(rows) + 4;  // the 8 row warps always span 256 or 512 rows (pad rows are zero)
+  L.rp = span(rows) + 4;  // the 8 row warps always span 128, 256 or 512 rows (pad rows are zero)
   L.stages = stages;
   L.stage_len = static_cast<size_t>(B) * L.rp + 2 * B * B + B * PC;
   size_t o = L.stage_len * stages;
@@ -2269,9 +2346,15 @@ __global__ void __launch_bounds__(la2::kThreads, 1) k_chain_p1_la2(EpochArgs a) 
       const int e = lane & 15;
       const double sum = (rb[e] + rb[B + e]) + (rb[2 * B + e] + rb[3 * B + e]);
       if constexpr (XG) {
-        if (lane < B) st_cg(xg_slots + (static_cast<size_t>(u % kSlots) * G + g) * B + e, sum);
-        __syncwarp();
-        if (lane == 0) xg_publish(xg_cnt + u % kSlots);
+        if (a.xg_ll) {
+          if (lane < B)
+            ll_store(reinterpret_cast<uint4*>(xg_slots) + (static_cast<size_t>(u % kSlots) * G + g) * B + e, sum,
+                     static_cast<uint32_t>(u / kSlots + 1));
+        } else {
+          if (lane < B) st_cg(xg_slots + (static_cast<size_t>(u % kSlots) * G + g) * B + e, sum);
+          __syncwarp();
+          if (lane == 0) xg_publish(xg_cnt + u % kSlots);
+        }
       } else {
         double* ov = outv + (u & 3) * B;
         if (lane < B) ov[e] = sum;
@@ -2313,6 +2396,12 @@ __global__ void __launch_bounds__(la2::kThreads, 1) k_chain_p1_la2(EpochArgs a) 
       tick(6);
       const int bt = bt_of(t);
       if constexpr (XG) {
+       if (a.xg_ll) {
+        const double sv = ll_gather16(reinterpret_cast<const uint4*>(xg_slots) + static_cast<size_t>(t % kSlots) * G * B,
+                                      G, lane, static_cast<uint32_t>(t / kSlots + 1));
+        tick(5);
+        if (lane < B) Ahat[j] = j < bt ? sv : 0.0;
+       } else {
         if (lane == 0) xg_wait(xg_cnt + t % kSlots, static_cast<unsigned>(G) * (t / kSlots + 1));
         __syncwarp();
         tick(5);
@@ -2327,6 +2416,7 @@ __global__ void __launch_bounds__(la2::kThreads, 1) k_chain_p1_la2(EpochArgs a) 
         const double sv = sa + sb;
         const double other = __shfl_down_sync(0xffffffffu, sv, 16);
         if (lane < B) Ahat[j] = j < bt ? sv + other : 0.0;
+       }
       } else {
         mbar_wait(&rbar[t % kSlots], static_cast<uint32_t>((t / kSlots) & 1));
         tick(5);
@@ -2517,6 +2607,9 @@ EpochConfig choose_epoch_config(int d_pad, int p) {
     EpochConfig cfg;
     cfg.b = kBlock;
     cfg.cluster = d_pad <= 8 * 256 ? 8 : 16;
+    // GAPLRA_V4_ROWS=128: rows spread thinner (C2: 3 groups x 32 plain CTAs over L2; C3: 16-CTA clusters)
+    static const int env_v4_rows = getenv("GAPLRA_V4_ROWS") ? atoi(getenv("GAPLRA_V4_ROWS")) : 0;
+    if (env_v4_rows == 128) cfg.cluster = static_cast<int>(ceil_div(ceil_div(d_pad, 128), 4) * 4);
     cfg.pc = 8;
     cfg.rows_per_cta = static_cast<int>(ceil_div(ceil_div(d_pad, cfg.cluster), 4) * 4);
     cfg.groups = static_cast<int>(ceil_div(p, 8));
@@ -2529,7 +2622,8 @@ EpochConfig choose_epoch_config(int d_pad, int p) {
     static const int env_xg = getenv("GAPLRA_CHAIN_XG") ? atoi(getenv("GAPLRA_CHAIN_XG")) : 1;
     // (512 rows per CTA always exchange through L2: the half-stage ring and
     // the 64 KB of DSMEM receive slots do not fit together)
-    if (cfg.groups <= max_active_clusters(cfg.cluster) && env_xg != 2 && cfg.rows_per_cta <= 256) return cfg;
+    if (cfg.cluster <= 16 && cfg.groups <= max_active_clusters(cfg.cluster) && env_xg != 2 && cfg.rows_per_cta <= 256)
+      return cfg;
     if ((env_xg || cfg.rows_per_cta > 256) && cfg.groups * cfg.cluster <= sm_count_dev()) {
       cfg.xg = 1;
       cfg.stages = 3;
@@ -2597,6 +2691,12 @@ EpochConfig choose_epoch_config(int d_pad, int p) {
   return c16;
 }
 
+// GAPLRA_XG_LL=0: the counter protocol for the p = 1 L2-exchange chains (default: flag-in-data cells)
+int xg_ll_mode() {
+  static const int v = getenv("GAPLRA_XG_LL") ? atoi(getenv("GAPLRA_XG_LL")) : 1;
+  return v;
+}
+
 template <int PC>
 void launch_chain_pc(const EpochArgs& a, const EpochConfig& cfg, cudaStream_t st) {
   // GAPLRA_CHAIN_MODE: 0 auto (the warp-specialised v3 where it fits: PC <= 3
@@ -2637,7 +2737,10 @@ void launch_chain_pc(const EpochArgs& a, const EpochConfig& cfg, cudaStream_t st
       smem = v4::smem_half().total;
       kern = k_svrg_chain_v4<512, true>;
     } else {
-      kern = xg ? k_svrg_chain_v4<256, true> : k_svrg_chain_v4<256, false>;
+      if (cfg.rows_per_cta <= 128)
+        kern = xg ? k_svrg_chain_v4<128, true> : k_svrg_chain_v4<128, false>;
+      else
+        kern = xg ? k_svrg_chain_v4<256, true> : k_svrg_chain_v4<256, false>;
     }
   } else if (xg) {
     if constexpr (PC == 1) {
@@ -2681,8 +2784,10 @@ void launch_chain_pc(const EpochArgs& a, const EpochConfig& cfg, cudaStream_t st
   if (xg) {
     if (!a.xg_slot || !a.xg_count) throw Error(kContractViolation, "epoch: XG layout without exchange buffers");
     GAPLRA_CUDA_CHECK(cudaMemsetAsync(a.xg_count, 0, xg_count_elems(cfg) * sizeof(unsigned), st));
+    if (xg_ll_mode() && !use_v4) GAPLRA_CUDA_CHECK(cudaMemsetAsync(a.xg_slot, 0, xg_slot_elems(cfg) * sizeof(double), st));
   }
   EpochArgs args = a;
+  args.xg_ll = xg && !use_v4 ? xg_ll_mode() : 0;
   args.rows_per_cta = cfg.rows_per_cta;
   args.stages = stages;
   args.pc = cfg.pc;
@@ -2714,8 +2819,10 @@ void launch_chain_la2(const EpochArgs& a, const EpochConfig& cfg, cudaStream_t s
   if (xg) {
     if (!a.xg_slot || !a.xg_count) throw Error(kContractViolation, "epoch: XG layout without exchange buffers");
     GAPLRA_CUDA_CHECK(cudaMemsetAsync(a.xg_count, 0, xg_count_elems(cfg) * sizeof(unsigned), st));
+    if (xg_ll_mode()) GAPLRA_CUDA_CHECK(cudaMemsetAsync(a.xg_slot, 0, xg_slot_elems(cfg) * sizeof(double), st));
   }
   EpochArgs args = a;
+  args.xg_ll = xg ? xg_ll_mode() : 0;
   args.rows_per_cta = cfg.rows_per_cta;
   args.stages = cfg.stages;
   args.pc = 1;

@@ -31,6 +31,7 @@ struct EpochArgs {
   // XG chains (cfg.xg): the group's all-reduce goes through L2 instead of DSMEM
   double* xg_slot;   // [kXgSlots][groups][cluster][NV] partials
   unsigned* xg_count;  // [groups][kXgSlots] arrivals, zeroed before each launch
+  int xg_ll;         // p = 1 XG chains: partials as 16-byte flag-in-data cells (xg_slot zeroed before each launch)
 };
 
 struct SparseEpochArgs {
@@ -76,6 +77,22 @@ int sparse_block_steps(int d, double col_nnz, int p);
 size_t sparse_scratch_ints(int d, int bs, int max_col_nnz);
 void launch_svrg_epoch_sparse_blocked(const SparseEpochArgs& a, int bs, int max_col_nnz, double* dbuf, int* ibuf,
                                       cudaStream_t st);
+
+// Level-scheduled sparse epoch (sparse_levels.cu): the per-epoch symbolic plan
+// (entries by row, coupled pairs by target step, dependency levels) is built by
+// one kernel for all blocks, then a cooperative kernel runs b / solve / scatter
+// per block.  `bytes` of scratch; the plan depends on (d, m, nnz per column).
+struct SparseLevelPlan {
+  int bs, ecap, rcap, pcap, scap, sym_ctas, d;
+  int64_t nblk;
+  size_t bytes;
+  size_t off_meta, off_rows, off_rptr, off_ej, off_ev, off_pptr, off_pl, off_pv, off_lsteps, off_lptr, off_cnt,
+      off_off, off_pkey, off_b, off_u, off_rho;
+};
+bool sparse_levels_supported(int p);
+SparseLevelPlan sparse_levels_plan(int d, int64_t m, double col_nnz, int max_col_nnz);
+void launch_svrg_epoch_sparse_levels(const SparseEpochArgs& a, const SparseLevelPlan& plan, void* scratch,
+                                     cudaStream_t st);
 
 // Device-resident control of a solve's epoch loop (a CUDA-graph WHILE node):
 // after each anchor, k_epoch_control applies the host loop's tests to the
