@@ -49,6 +49,7 @@ constexpr int kNumThreads = 512;
 constexpr int kRowListCap = 48;    // entries of one row within a block (sorted by insertion)
 constexpr int kStepPairCap = 512;  // pairs of one target step (sorted by insertion)
 constexpr int kMaxBs = 2048;
+constexpr int kLpCap = 256;        // level starts kept in shared memory (deeper blocks read them from global)
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -92,8 +93,8 @@ struct SymPlan {
   int* pptr;             // [nblk][bs + 4]
   unsigned short* pl;    // [nblk][pcap]
   double* pv;            // [nblk][pcap]
-  unsigned short* lsteps;  // [nblk][bs]
-  int* lptr;             // [nblk][bs + 4]
+  uint2* lrec;           // [nblk][bs] steps in level order: x = step | pairs << 16, y = first pair
+  int* lptr;             // [nblk][bs + 4] first position of every level (nlev + 1 used)
   // per symbolic CTA scratch
   int* cnt;              // [ctas][d] zero between blocks
   int* off;              // [ctas][d]
@@ -161,7 +162,7 @@ __global__ void __launch_bounds__(kSymThreads, 1) k_sparse_symbolic(SymArgs A) {
     int* pptr = S.pptr + blk * (bs + 4);
     unsigned short* pl = S.pl + blk * S.pcap;
     double* pv = S.pv + blk * S.pcap;
-    unsigned short* lsteps = S.lsteps + blk * bs;
+    uint2* lrec = S.lrec + blk * bs;
     int* lptr = S.lptr + blk * (bs + 4);
     if (tid == 0) s_flag = 0;
     for (int j = tid; j <= bs; j += kSymThreads) pcnt[j] = 0;
@@ -361,7 +362,11 @@ __global__ void __launch_bounds__(kSymThreads, 1) k_sparse_symbolic(SymArgs A) {
       __syncthreads();
       for (int j = tid; j <= nlev; j += kSymThreads) lptr[j] = lp[j];
       __syncthreads();
-      for (int j = tid; j < bt; j += kSymThreads) lsteps[atomicAdd(&lp[lev[j]], 1)] = static_cast<unsigned short>(j);
+      for (int j = tid; j < bt; j += kSymThreads) {
+        const int g0 = pcnt[j], c = pcnt[j + 1] - g0;
+        lrec[atomicAdd(&lp[lev[j]], 1)] = make_uint2(static_cast<unsigned>(j) | (static_cast<unsigned>(c) << 16),
+                                                     static_cast<unsigned>(g0));
+      }
       if (tid == 0) {
         meta[0] = nrows;
         meta[1] = nent;
@@ -390,12 +395,101 @@ __global__ void k_rho_table(double* rp, double* gm, int bs, double rho) {
   }
 }
 
+// Triangular solve u_j = b_j + κ Σ_{l<j} K_jl u_l of one right-hand-side column,
+// level by level (rec[q]: step, pair count, first pair; lptr: level starts).
+// 4 lanes per step split its pairs; everything that does not depend on u — the
+// next level's step record and each lane's first three pairs — is loaded
+// BEFORE the level barrier, so the chain per level is barrier -> u gathers ->
+// FMAs -> two shuffles -> store.  (A barrier-free dataflow variant, groups
+// spinning on per-step ready tags in shared memory, measured 5x slower: the
+// spinning warps starve the working ones.)  u holds b on entry.
+constexpr int kSolveLanes = 4, kSolveGroups = kNumThreads / kSolveLanes, kPre = 6;
+constexpr unsigned kNoStep = 0xffffu;
+struct SolveItem {
+  int j, x_rest, x_end;  // step (-1: none); pairs beyond the preloaded ones: x_rest, x_rest + 4, ... < x_end
+  double bj;             // b_j (u[j] before the step is solved)
+  double v[kPre];
+  int l[kPre];
+};
+template <typename PV, typename PL>
+__device__ __forceinline__ SolveItem solve_load(const double* u, PV pv, PL pl, uint2 r, int sub) {
+  SolveItem it;
+  const unsigned js = r.x & 0xffffu;
+  it.j = js == kNoStep ? -1 : static_cast<int>(js);
+  const int cnt = js == kNoStep ? 0 : static_cast<int>(r.x >> 16), g0 = static_cast<int>(r.y);
+  it.x_end = g0 + cnt;
+  it.x_rest = g0 + sub + kPre * kSolveLanes;
+  it.bj = it.j >= 0 ? u[it.j] : 0.0;
+#pragma unroll
+  for (int k = 0; k < kPre; ++k) {
+    const int x = g0 + sub + k * kSolveLanes;
+    const bool in = x < it.x_end;
+    it.v[k] = in ? pv[x] : 0.0;
+    it.l[k] = in ? pl[x] : 0;
+  }
+  return it;
+}
+template <typename PV, typename PL>
+__device__ __forceinline__ void solve_apply(double* u, PV pv, PL pl, const SolveItem& it, int sub, double kappa) {
+  double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+  for (int k = 0; k < kPre; k += 2) {
+    a0 = fma(it.v[k], u[it.l[k]], a0);
+    a1 = fma(it.v[k + 1], u[it.l[k + 1]], a1);
+  }
+  double acc = a0 + a1;
+  for (int x = it.x_rest; x < it.x_end; x += kSolveLanes) acc = fma(pv[x], u[pl[x]], acc);
+  acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+  acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+  if (sub == 0 && it.j >= 0) u[it.j] = fma(kappa, acc, it.bj);
+}
+// (__noinline__: its own register allocation.)  Software pipeline over the
+// levels: at level L the group already holds its step of level L with the
+// first 6 pairs per lane and b_j in registers (loaded during level L - 1) and
+// the step record of level L + 1; it issues the record load of level L + 2 and
+// the pair loads of level L + 1 before touching u, so the dependent chain
+// between two barriers is u gathers -> FMAs -> two shuffles -> one store.
+// Levels wider than the 128 groups take further, unpipelined rounds.  (An unrolled-by-two form without the
+// register rotation spilled inside this function and measured slower: 20.2 vs 17.2 us per block.)
+template <typename PV, typename PL, typename REC, typename LP>
+__device__ __noinline__ void solve_levels(double* u, PV pv, PL pl, REC rec, LP lptr, int nlev, double kappa) {
+  const int tid = threadIdx.x, sub = tid & (kSolveLanes - 1), sg = tid / kSolveLanes;
+  __syncthreads();  // u = b complete
+  if (nlev < 2) return;
+  const int wg0 = (tid & ~31) / kSolveLanes;  // first group of this warp: a warp without steps skips the level
+  auto lp = [&](int k) { return lptr[k < nlev ? k : nlev]; };
+  auto rec_at = [&](int q0, int q1) { return q0 + sg < q1 ? rec[q0 + sg] : make_uint2(kNoStep, 0u); };
+  int b1 = lp(1), b2 = lp(2), b3 = lp(3), b4 = lp(4);  // level L + k spans [b_{k+1}, b_{k+2})
+  uint2 r2 = rec_at(b2, b3);
+  SolveItem it = solve_load(u, pv, pl, rec_at(b1, b2), sub);
+  for (int L = 1; L < nlev; ++L) {
+    const int b5 = lp(L + 4);
+    const uint2 r3 = rec_at(b3, b4);                        // level L + 2
+    const SolveItem nxt = solve_load(u, pv, pl, r2, sub);  // level L + 1
+    if (b1 + wg0 < b2) solve_apply(u, pv, pl, it, sub, kappa);
+    for (int qb = b1 + kSolveGroups; qb + wg0 < b2; qb += kSolveGroups) {
+      const SolveItem e = solve_load(u, pv, pl, rec_at(qb, b2), sub);
+      solve_apply(u, pv, pl, e, sub, kappa);
+    }
+    __syncthreads();
+    it = nxt;
+    r2 = r3;
+    b1 = b2;
+    b2 = b3;
+    b3 = b4;
+    b4 = b5;
+  }
+}
+
 struct NumArgs {
   SparseEpochArgs e;
   SymPlan s;
   double* b;      // [bs][p]
   double* u;      // [bs][p]
+  double* dcb;    // [2][bs][p] x_jᵀC of the block (parity), filled one block ahead by the CTAs not solving
+  double* yb;     // [2][bs][p] Y rows of the block's columns
   int scap;       // pairs that fit the shared tile
+  int skip;       // GAPLRA_SPARSE_SKIP: timing ablation mask (results invalid)
   const double* rp;  // [bs + 1] ρ^j
   const double* gm;  // [bs + 1] γ_j = Σ_{k<j} ρ^k
   unsigned long long* dbg;
@@ -410,16 +504,15 @@ __global__ void __launch_bounds__(kNumThreads, 1) k_sparse_epoch_levels(NumArgs 
   const SparseEpochArgs& a = A.e;
   const SymPlan& S = A.s;
   const int p = a.p, bs = S.bs;
-  // shared: u[bs] | pv[scap] | pptr[bs + 4] | lptr[bs + 4] | pl[scap] | lsteps[bs] | bar
+  // shared: u[bs] | pv[scap] | lrec[bs] | lptr[kLpCap] | pl[scap] | bar
   double* u = reinterpret_cast<double*>(smraw);
   double* spv = u + bs;
   const double* rp = A.rp;
   const double* gm = A.gm;
-  int* spptr = reinterpret_cast<int*>(spv + A.scap);
-  int* slptr = spptr + bs + 4;
-  unsigned short* spl = reinterpret_cast<unsigned short*>(slptr + bs + 4);
-  unsigned short* slsteps = spl + A.scap;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smraw + (((reinterpret_cast<unsigned char*>(slsteps + bs) - smraw) + 15) & ~15));
+  uint2* slrec = reinterpret_cast<uint2*>(spv + A.scap);
+  int* slp = reinterpret_cast<int*>(slrec + bs);
+  unsigned short* spl = reinterpret_cast<unsigned short*>(slp + kLpCap);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smraw + (((reinterpret_cast<unsigned char*>(spl + A.scap) - smraw) + 15) & ~15));
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int kGroups = kNumThreads / LPS;
   const int grp = tid / LPS, gl = tid % LPS;
@@ -432,7 +525,8 @@ __global__ void __launch_bounds__(kNumThreads, 1) k_sparse_epoch_levels(NumArgs 
   __syncthreads();
   const double kappa = a.eta_n / a.rho;
   double al = 1.0, be = 0.0;
-  unsigned long long tph[4] = {0, 0, 0, 0}, tlast = gtimer();
+  unsigned long long tph[8] = {0, 0, 0, 0, 0, 0, 0, 0}, tlast = gtimer();
+  long long lacc[3] = {0, 0, 0};
   auto mark = [&](int k) {
     if (A.dbg && blockIdx.x == 0 && tid == 0) {
       const unsigned long long now = gtimer();
@@ -443,24 +537,75 @@ __global__ void __launch_bounds__(kNumThreads, 1) k_sparse_epoch_levels(NumArgs 
   // prefetch of block t's solve data into shared memory (solver CTAs, thread 0)
   auto prefetch = [&](int64_t t) {
     const int* meta = S.meta + t * 8;
-    const int np = meta[2], nl = meta[3];
+    const int np = meta[2];
     if (meta[4] || np > A.scap) return;
     const int64_t s0 = t * bs;
     const int bt = static_cast<int>(a.m - s0 < bs ? a.m - s0 : bs);
     const uint32_t b_pv = static_cast<uint32_t>(pad4(np)) * 8u, b_pl = static_cast<uint32_t>((np + 7) & ~7) * 2u;
-    const uint32_t b_pp = static_cast<uint32_t>(pad4(bt + 1)) * 4u, b_lp = static_cast<uint32_t>(pad4(nl + 1)) * 4u;
-    const uint32_t b_ls = static_cast<uint32_t>((bt + 7) & ~7) * 2u;
+    const uint32_t b_lr = static_cast<uint32_t>((bt + 1) & ~1) * 8u;
+    const int nl = meta[3];
+    const uint32_t b_lp = nl + 1 <= kLpCap ? static_cast<uint32_t>(pad4(nl + 1)) * 4u : 0u;
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    mbar_expect_tx(bar, b_pv + b_pl + b_pp + b_lp + b_ls);
+    mbar_expect_tx(bar, b_pv + b_pl + b_lr + b_lp);
     if (b_pv) bulk_load(spv, S.pv + t * S.pcap, b_pv, bar);
     if (b_pl) bulk_load(spl, S.pl + t * S.pcap, b_pl, bar);
-    bulk_load(spptr, S.pptr + t * (bs + 4), b_pp, bar);
-    bulk_load(slptr, S.lptr + t * (bs + 4), b_lp, bar);
-    bulk_load(slsteps, S.lsteps + t * bs, b_ls, bar);
+    bulk_load(slrec, S.lrec + t * bs, b_lr, bar);
+    if (b_lp) bulk_load(slp, S.lptr + t * (bs + 4), b_lp, bar);
   };
   uint32_t bar_phase = 0;
   if (solver && tid == 0 && S.nblk > 0) prefetch(0);
   const int64_t nblk = S.nblk;
+  // Work that does not depend on W, done one block ahead by the CTAs that do not
+  // solve (they would idle through phase 2): x_jᵀC and the Y rows of the next
+  // block's steps (which also pulls that block's columns of X into L2), and an
+  // L2 prefetch of the current block's row lists for phase 3.
+  const bool all_help = static_cast<int>(gridDim.x) <= p;  // no spare CTAs: everyone helps after solving
+  const int hcta = all_help ? static_cast<int>(blockIdx.x) : static_cast<int>(blockIdx.x) - p;
+  const int nh = all_help ? static_cast<int>(gridDim.x) : static_cast<int>(gridDim.x) - p;
+  auto ahead = [&](int64_t t, int hc, int nhc) {  // dc, y of block t by CTAs hc of nhc
+    if (t >= nblk || hc < 0) return;
+    constexpr int kHalf = LPS == 16 ? 2 : 1;
+    const int col = LPS == 16 ? (lane & 15) : lane;
+    const int hs = LPS == 16 ? (lane >> 4) : 0;
+    const int64_t t0 = t * bs;
+    const int btt = static_cast<int>(a.m - t0 < bs ? a.m - t0 : bs);
+    double* dcb = A.dcb + static_cast<size_t>(t & 1) * bs * p;
+    double* yb = A.yb + static_cast<size_t>(t & 1) * bs * p;
+    for (int j = hc * (kNumThreads / 32) + warp; j < btt; j += nhc * (kNumThreads / 32)) {
+      const int i = a.idx[t0 + j];
+      const int64_t e0 = a.colptr[i], e1 = a.colptr[i + 1];
+      double dc = 0.0;
+      if (col < p) {
+        constexpr int kU = 5;
+        int64_t e = e0 + hs;
+        for (; e + (kU - 1) * kHalf < e1; e += kU * kHalf) {
+          double v[kU], cc[kU];
+#pragma unroll
+          for (int q = 0; q < kU; ++q) {
+            const int64_t r = a.rowidx[e + q * kHalf];
+            v[q] = __ldg(a.val + e + q * kHalf);
+            cc[q] = __ldg(a.C + r * a.ldw + col);
+          }
+#pragma unroll
+          for (int q = 0; q < kU; ++q) dc = fma(v[q], cc[q], dc);
+        }
+        for (; e < e1; e += kHalf) dc = fma(__ldg(a.val + e), __ldg(a.C + a.rowidx[e] * a.ldw + col), dc);
+      }
+      if (kHalf == 2) dc += __shfl_down_sync(0xffffffffu, dc, 16);
+      if (hs == 0 && col < p) {
+        dcb[static_cast<size_t>(j) * p + col] = dc;
+        yb[static_cast<size_t>(j) * p + col] = a.Y[static_cast<int64_t>(i) * a.ldy + col];
+      }
+    }
+  };
+  auto l2_touch = [&](const void* base, size_t bytes, int hc, int nhc) {
+    const char* b = static_cast<const char*>(base);
+    for (size_t o = (static_cast<size_t>(hc) * kNumThreads + tid) * 128; o < bytes;
+         o += static_cast<size_t>(nhc) * kNumThreads * 128)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(b + o));
+  };
+  ahead(0, static_cast<int>(blockIdx.x), static_cast<int>(gridDim.x));
+  grid.sync();
   for (int64_t blk = 0; blk < nblk; ++blk) {
     const int64_t s0 = blk * bs;
     const int bt = static_cast<int>(a.m - s0 < bs ? a.m - s0 : bs);
@@ -477,42 +622,47 @@ __global__ void __launch_bounds__(kNumThreads, 1) k_sparse_epoch_levels(NumArgs 
       grid.sync();
     }
     // ---------------------------------------------------------------- (1) b_j
+    // one warp per step; p <= 16: the two half-warps take alternate entries
+    // (lane = column within a half), partial dots joined in a fixed order
     if (!overflow) {
-      for (int j = ggrp; j < bt; j += ngrp) {
+      constexpr int kHalf = LPS == 16 ? 2 : 1;  // entry streams per warp
+      const int col = LPS == 16 ? (lane & 15) : lane;
+      const int hs = LPS == 16 ? (lane >> 4) : 0;
+      const int gwarp = blockIdx.x * (kNumThreads / 32) + warp, nwarp = gridDim.x * (kNumThreads / 32);
+      const double* dcb = A.dcb + static_cast<size_t>(blk & 1) * bs * p;
+      const double* yb = A.yb + static_cast<size_t>(blk & 1) * bs * p;
+      for (int j = gwarp; j < bt; j += nwarp) {
         const int i = a.idx[s0 + j];
         const int64_t e0 = a.colptr[i], e1 = a.colptr[i + 1];
-        if (gl < p) {
-          double dw = 0.0, dc = 0.0;
-          int64_t e = e0;
-          for (; e + 4 <= e1; e += 4) {
-            int64_t r[4];
-            double v[4], w[4], cc[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              r[q] = a.rowidx[e + q];
-              v[q] = __ldg(a.val + e + q);
-            }
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              w[q] = __ldcg(a.W + r[q] * a.ldw + gl);
-              cc[q] = __ldg(a.C + r[q] * a.ldw + gl);
-            }
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              dw = fma(v[q], w[q], dw);
-              dc = fma(v[q], cc[q], dc);
-            }
+        double dw = 0.0, dc = 0.0, yv = 0.0;
+        if (col < p) {
+          if (hs == 0) {
+            dc = __ldcg(dcb + static_cast<size_t>(j) * p + col);
+            yv = __ldcg(yb + static_cast<size_t>(j) * p + col);
           }
-          for (; e < e1; ++e) {
+          constexpr int kU = 5;
+          int64_t e = e0 + hs;
+          for (; e + (kU - 1) * kHalf < e1; e += kU * kHalf) {
+            double v[kU], w[kU];
+#pragma unroll
+            for (int q = 0; q < kU; ++q) {
+              const int64_t r = a.rowidx[e + q * kHalf];
+              v[q] = __ldg(a.val + e + q * kHalf);
+              w[q] = __ldcg(a.W + r * a.ldw + col);
+            }
+#pragma unroll
+            for (int q = 0; q < kU; ++q) dw = fma(v[q], w[q], dw);
+          }
+          for (; e < e1; e += kHalf) {
             const int64_t row = a.rowidx[e];
-            const double v = __ldg(a.val + e);
-            dw = fma(v, __ldcg(a.W + row * a.ldw + gl), dw);
-            dc = fma(v, __ldg(a.C + row * a.ldw + gl), dc);
+            dw = fma(__ldg(a.val + e), __ldcg(a.W + row * a.ldw + col), dw);
           }
+        }
+        if (kHalf == 2) dw += __shfl_down_sync(0xffffffffu, dw, 16);
+        if (hs == 0 && col < p) {
           const double aj = al * rp[j], bj = fma(rp[j], be, gm[j]);
           const double t = fma(aj, dw, bj * dc);
-          A.b[static_cast<size_t>(j) * p + gl] =
-              a.eta_n * (t - a.Y[static_cast<int64_t>(i) * a.ldy + gl]) / (al * rp[j + 1]);
+          A.b[static_cast<size_t>(j) * p + col] = a.eta_n * (t - yv) / (al * rp[j + 1]);
         }
       }
     }
@@ -527,29 +677,33 @@ __global__ void __launch_bounds__(kNumThreads, 1) k_sparse_epoch_levels(NumArgs 
           mbar_wait(bar, bar_phase);
           bar_phase ^= 1u;
         }
+        mark(3);
         for (int j = tid; j < bt; j += kNumThreads) u[j] = __ldcg(A.b + static_cast<size_t>(j) * p + c);
-        const double* pv = in_smem ? spv : S.pv + blk * S.pcap;
-        const unsigned short* pl = in_smem ? spl : S.pl + blk * S.pcap;
-        const int* pptr = in_smem ? spptr : S.pptr + blk * (bs + 4);
-        const int* lptr = in_smem ? slptr : S.lptr + blk * (bs + 4);
-        const unsigned short* lsteps = in_smem ? slsteps : S.lsteps + blk * bs;
-        __syncthreads();
-        for (int L = 1; L < nlev; ++L) {
-          const int q0 = lptr[L], q1 = lptr[L + 1];
-          for (int q = q0 + tid; q < q1; q += kNumThreads) {
-            const int j = lsteps[q];
-            const int g0 = pptr[j], g1 = pptr[j + 1];
-            double acc = 0.0;
-            for (int x = g0; x < g1; ++x) acc = fma(pv[x], u[pl[x]], acc);
-            u[j] = fma(kappa, acc, u[j]);
-          }
-          __syncthreads();
+        mark(4);
+        {
+          const int* lp_g = S.lptr + blk * (bs + 4);
+          if (in_smem && nlev + 1 <= kLpCap)
+            solve_levels(u, spv, spl, slrec, slp, nlev, kappa);
+          else if (in_smem)
+            solve_levels(u, spv, spl, slrec, lp_g, nlev, kappa);
+          else
+            solve_levels(u, S.pv + blk * S.pcap, S.pl + blk * S.pcap, S.lrec + blk * bs, lp_g, nlev, kappa);
         }
+        __syncthreads();
+        mark(5);
         for (int j = tid; j < bt; j += kNumThreads) A.u[static_cast<size_t>(j) * p + c] = u[j];
         __syncthreads();  // the shared tile is free: fetch the next block's
         if (tid == 0 && blk + 1 < nblk) prefetch(blk + 1);
       }
+      if (!solver || all_help) {
+        l2_touch(S.rows + blk * S.rcap, static_cast<size_t>(nrows) * 4, hcta, nh);
+        l2_touch(S.rptr + blk * (S.rcap + 4), static_cast<size_t>(nrows + 1) * 4, hcta, nh);
+        l2_touch(S.ej + blk * S.ecap, static_cast<size_t>(meta[1]) * 2, hcta, nh);
+        l2_touch(S.ev + blk * S.ecap, static_cast<size_t>(meta[1]) * 8, hcta, nh);
+        ahead(blk + 1, hcta, nh);
+      }
     } else {
+      ahead(blk + 1, static_cast<int>(blockIdx.x) - 1, static_cast<int>(gridDim.x) - 1);  // CTA 0 runs the fallback
       if (solver && tid == 0 && blk + 1 < nblk) prefetch(blk + 1);
       if (blockIdx.x == 0) {
         // exact serial fallback: step by step with immediate updates
@@ -584,13 +738,27 @@ __global__ void __launch_bounds__(kNumThreads, 1) k_sparse_epoch_levels(NumArgs 
       const int* rptr = S.rptr + blk * (S.rcap + 4);
       const unsigned short* ej = S.ej + blk * S.ecap;
       const double* ev = S.ev + blk * S.ecap;
-      for (int k = ggrp; k < nrows; k += ngrp) {
-        const int row = rows[k];
-        const int x0 = rptr[k], x1 = rptr[k + 1];
+      for (int k = ggrp; k < nrows; k += 2 * ngrp) {
+        const int k2 = k + ngrp;
+        const bool two = k2 < nrows;
+        const int row = __ldg(rows + k), row2 = two ? __ldg(rows + k2) : 0;
+        const int x0 = __ldg(rptr + k), x1 = __ldg(rptr + k + 1);
+        const int y0 = two ? __ldg(rptr + k2) : 0, y1 = two ? __ldg(rptr + k2 + 1) : 0;
         if (gl < p) {
           double w = __ldcg(a.W + static_cast<int64_t>(row) * a.ldw + gl);
-          for (int x = x0; x < x1; ++x) w = fma(ev[x], __ldcg(A.u + static_cast<size_t>(ej[x]) * p + gl), w);
+          double w2 = two ? __ldcg(a.W + static_cast<int64_t>(row2) * a.ldw + gl) : 0.0;
+          // first entries of both rows in flight together
+          double ea = __ldg(ev + x0), eb = two ? __ldg(ev + y0) : 0.0;
+          double ua = __ldcg(A.u + static_cast<size_t>(__ldg(ej + x0)) * p + gl);
+          double ub = two ? __ldcg(A.u + static_cast<size_t>(__ldg(ej + y0)) * p + gl) : 0.0;
+          w = fma(ea, ua, w);
+          for (int x = x0 + 1; x < x1; ++x) w = fma(__ldg(ev + x), __ldcg(A.u + static_cast<size_t>(__ldg(ej + x)) * p + gl), w);
           a.W[static_cast<int64_t>(row) * a.ldw + gl] = w;
+          if (two) {
+            w2 = fma(eb, ub, w2);
+            for (int x = y0 + 1; x < y1; ++x) w2 = fma(__ldg(ev + x), __ldcg(A.u + static_cast<size_t>(__ldg(ej + x)) * p + gl), w2);
+            a.W[static_cast<int64_t>(row2) * a.ldw + gl] = w2;
+          }
         }
       }
     }
@@ -600,7 +768,12 @@ __global__ void __launch_bounds__(kNumThreads, 1) k_sparse_epoch_levels(NumArgs 
     mark(2);
   }
   if (A.dbg && blockIdx.x == 0 && tid == 0)
-    for (int k = 0; k < 4; ++k) A.dbg[k] = tph[k];
+  {
+    for (int k = 0; k < 8; ++k) A.dbg[k] = tph[k];
+    A.dbg[6] = lacc[0];
+    A.dbg[7] = lacc[1];
+    A.dbg[2 + 8] = lacc[2];
+  }
   // W = α Ŵ + β C
   for (int64_t e = static_cast<int64_t>(blockIdx.x) * kNumThreads + tid; e < static_cast<int64_t>(a.d) * p;
        e += static_cast<int64_t>(gridDim.x) * kNumThreads) {
@@ -621,7 +794,7 @@ int sym_ctas() {
 
 // shared pair tile of the solver CTAs for a block size
 int shared_pair_cap(int bs) {
-  const size_t fixed = static_cast<size_t>(bs) * 8 + 2 * static_cast<size_t>(bs + 4) * 4 + static_cast<size_t>(bs) * 2 + 64;
+  const size_t fixed = static_cast<size_t>(bs) * (8 + 8) + kLpCap * 4 + 64;
   const size_t room = 226 * 1024 - fixed;
   return static_cast<int>(room / 10 / 8 * 8);
 }
@@ -637,14 +810,15 @@ SparseLevelPlan sparse_levels_plan(int d, int64_t m, double col_nnz, int max_col
   static const int env_bs = getenv("GAPLRA_SPARSE_BS") ? atoi(getenv("GAPLRA_SPARSE_BS")) : 0;
   int bs = kMaxBs;
   while (bs > 32 && (bs * col_nnz) * (bs * col_nnz) / (2.0 * d) > 0.9 * shared_pair_cap(bs)) bs /= 2;
-  if (env_bs >= 32 && env_bs <= kMaxBs && (env_bs & (env_bs - 1)) == 0) bs = env_bs;
+  if (env_bs >= 32 && env_bs <= kMaxBs && env_bs % 32 == 0) bs = env_bs;
   P.bs = bs;
+  const double expect = (bs * col_nnz) * (bs * col_nnz) / (2.0 * d);
   P.nblk = ceil_div(m, bs);
   P.ecap = static_cast<int>(align_up(static_cast<size_t>(bs) * std::max(1, max_col_nnz), 8));
   P.rcap = static_cast<int>(align_up(std::min<size_t>(static_cast<size_t>(d), P.ecap), 4));
-  const double expect = (bs * col_nnz) * (bs * col_nnz) / (2.0 * d);
   P.pcap = static_cast<int>(align_up(static_cast<size_t>(std::max(4096.0, 2.0 * expect)), 8));
-  P.scap = shared_pair_cap(bs);
+  // the shared tile: 25 % above the expected pairs (a smaller tile leaves more of the SM's L1 to the kernel)
+  P.scap = std::min(shared_pair_cap(bs), static_cast<int>(align_up(static_cast<size_t>(1.25 * expect) + 1024, 8)));
   P.sym_ctas = sym_ctas();
   const size_t nb = static_cast<size_t>(P.nblk);
   size_t o = 0;
@@ -661,13 +835,15 @@ SparseLevelPlan sparse_levels_plan(int d, int64_t m, double col_nnz, int max_col
   P.off_pptr = take(nb * (bs + 4) * 4);
   P.off_pl = take(nb * P.pcap * 2);
   P.off_pv = take(nb * P.pcap * 8);
-  P.off_lsteps = take(nb * bs * 2);
+  P.off_lrec = take(nb * bs * 8);
   P.off_lptr = take(nb * (bs + 4) * 4);
   P.off_cnt = take(static_cast<size_t>(P.sym_ctas) * d * 4);
   P.off_off = take(static_cast<size_t>(P.sym_ctas) * d * 4);
   P.off_pkey = take(static_cast<size_t>(P.sym_ctas) * P.pcap * 8);
   P.off_b = take(static_cast<size_t>(bs) * 32 * 8);
   P.off_u = take(static_cast<size_t>(bs) * 32 * 8);
+  P.off_dcb = take(2 * static_cast<size_t>(bs) * 32 * 8);
+  P.off_yb = take(2 * static_cast<size_t>(bs) * 32 * 8);
   P.off_rho = take(2 * static_cast<size_t>(bs + 2) * 8);
   P.bytes = o;
   P.d = d;
@@ -692,7 +868,7 @@ void launch_svrg_epoch_sparse_levels(const SparseEpochArgs& a, const SparseLevel
   S.pptr = reinterpret_cast<int*>(base + P.off_pptr);
   S.pl = reinterpret_cast<unsigned short*>(base + P.off_pl);
   S.pv = reinterpret_cast<double*>(base + P.off_pv);
-  S.lsteps = reinterpret_cast<unsigned short*>(base + P.off_lsteps);
+  S.lrec = reinterpret_cast<uint2*>(base + P.off_lrec);
   S.lptr = reinterpret_cast<int*>(base + P.off_lptr);
   S.cnt = reinterpret_cast<int*>(base + P.off_cnt);
   S.off = reinterpret_cast<int*>(base + P.off_off);
@@ -721,7 +897,11 @@ void launch_svrg_epoch_sparse_levels(const SparseEpochArgs& a, const SparseLevel
   N.s = S;
   N.b = reinterpret_cast<double*>(base + P.off_b);
   N.u = reinterpret_cast<double*>(base + P.off_u);
+  N.dcb = reinterpret_cast<double*>(base + P.off_dcb);
+  N.yb = reinterpret_cast<double*>(base + P.off_yb);
   N.scap = P.scap;
+  static const int env_skip = getenv("GAPLRA_SPARSE_SKIP") ? atoi(getenv("GAPLRA_SPARSE_SKIP")) : 0;
+  N.skip = env_skip;
   double* rho_tab = reinterpret_cast<double*>(base + P.off_rho);
   k_rho_table<<<1, 1, 0, st>>>(rho_tab, rho_tab + P.bs + 2, P.bs, a.rho);
   GAPLRA_LAUNCH_CHECK();
@@ -730,12 +910,11 @@ void launch_svrg_epoch_sparse_levels(const SparseEpochArgs& a, const SparseLevel
   static unsigned long long* dbg = nullptr;
   N.dbg = nullptr;
   if (timing) {
-    if (!dbg) GAPLRA_CUDA_CHECK(cudaMalloc(&dbg, 4 * sizeof(unsigned long long)));
+    if (!dbg) GAPLRA_CUDA_CHECK(cudaMalloc(&dbg, 16 * sizeof(unsigned long long)));
     N.dbg = dbg;
   }
   const int bs = P.bs;
-  const size_t smem = (static_cast<size_t>(bs) + P.scap) * 8 + 2 * static_cast<size_t>(bs + 4) * 4 +
-                      (static_cast<size_t>(P.scap) + bs) * 2 + 48;
+  const size_t smem = (static_cast<size_t>(bs) + P.scap) * 8 + static_cast<size_t>(bs) * 8 + kLpCap * 4 + static_cast<size_t>(P.scap) * 2 + 48;
   auto kern = a.p <= 16 ? k_sparse_epoch_levels<16> : k_sparse_epoch_levels<32>;
   GAPLRA_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   int per_sm = 0;
@@ -747,7 +926,7 @@ void launch_svrg_epoch_sparse_levels(const SparseEpochArgs& a, const SparseLevel
   GAPLRA_LAUNCH_CHECK();
   if (timing) {
     cudaEventRecord(ev2, st);
-    unsigned long long h[4];
+    unsigned long long h[16];
     GAPLRA_CUDA_CHECK(cudaMemcpyAsync(h, dbg, sizeof(h), cudaMemcpyDeviceToHost, st));
     GAPLRA_CUDA_CHECK(cudaStreamSynchronize(st));
     float ms_sym = 0, ms_num = 0;
@@ -768,9 +947,10 @@ void launch_svrg_epoch_sparse_levels(const SparseEpochArgs& a, const SparseLevel
     const double nbk = static_cast<double>(S.nblk);
     fprintf(stderr,
             "{\"sparse_levels\": {\"bs\": %d, \"blocks\": %.0f, \"symbolic_ms\": %.3f, \"numeric_ms\": %.3f, "
-            "\"us_per_block\": [%.2f, %.2f, %.2f], \"pairs_mean\": %.0f, \"pairs_max\": %d, \"scap\": %d, \"pcap\": %d, "
+            "\"us_per_block\": [%.2f, %.2f, %.2f], \"solve_us\": [%.2f, %.2f, %.2f], \"level_cycles_per_block\": [%.0f, %.0f, %.0f], \"pairs_mean\": %.0f, \"pairs_max\": %d, \"scap\": %d, \"pcap\": %d, "
             "\"levels_mean\": %.1f, \"levels_max\": %d, \"rows_mean\": %.0f, \"overflow_blocks\": %d}}\n",
-            bs, nbk, ms_sym, ms_num, h[0] / nbk / 1e3, h[1] / nbk / 1e3, h[2] / nbk / 1e3, sp / nbk, maxp, P.scap,
+            bs, nbk, ms_sym, ms_num, h[0] / nbk / 1e3, (h[1] + h[3] + h[4] + h[5]) / nbk / 1e3, h[2] / nbk / 1e3, h[3] / nbk / 1e3, h[4] / nbk / 1e3,
+            h[5] / nbk / 1e3, h[6] / nbk, h[7] / nbk, h[10] / nbk, sp / nbk, maxp, P.scap,
             P.pcap, sl / nbk, maxl, sr / nbk, ovf);
     cudaEventDestroy(ev0);
     cudaEventDestroy(ev1);

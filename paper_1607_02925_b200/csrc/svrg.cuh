@@ -86,8 +86,8 @@ struct SparseLevelPlan {
   int bs, ecap, rcap, pcap, scap, sym_ctas, d;
   int64_t nblk;
   size_t bytes;
-  size_t off_meta, off_rows, off_rptr, off_ej, off_ev, off_pptr, off_pl, off_pv, off_lsteps, off_lptr, off_cnt,
-      off_off, off_pkey, off_b, off_u, off_rho;
+  size_t off_meta, off_rows, off_rptr, off_ej, off_ev, off_pptr, off_pl, off_pv, off_lrec, off_lptr, off_cnt,
+      off_off, off_pkey, off_b, off_u, off_dcb, off_yb, off_rho;
 };
 bool sparse_levels_supported(int p);
 SparseLevelPlan sparse_levels_plan(int d, int64_t m, double col_nnz, int max_col_nnz);
