@@ -104,6 +104,7 @@ struct SymPlan {
 struct SymArgs {
   SparseEpochArgs e;
   SymPlan s;
+  int smem_cnt;  // row counters in shared memory (d <= 65536)
 };
 
 // Exclusive scan of one int per thread over the CTA (kSymThreads); returns the
@@ -151,6 +152,26 @@ __global__ void __launch_bounds__(kSymThreads, 1) k_sparse_symbolic(SymArgs A) {
   int* off = S.off + static_cast<size_t>(blockIdx.x) * d;
   unsigned long long* pkey = S.pkey + static_cast<size_t>(blockIdx.x) * S.pcap;
   const int chunk = (d + kSymThreads - 1) / kSymThreads;
+  // per-row entry counters: packed 16-bit pairs in shared memory when d fits (C4: 100 KB), else global (L2)
+  extern __shared__ unsigned scnt[];
+  const bool sc = A.smem_cnt != 0;
+  if (sc) {
+    for (int r = tid; r < (d + 1) / 2; r += kSymThreads) scnt[r] = 0u;
+    __syncthreads();
+  }
+  auto cnt_inc = [&](int row) {
+    if (sc)
+      atomicAdd(&scnt[row >> 1], 1u << (16 * (row & 1)));
+    else
+      atomicAdd(&cnt[row], 1);
+  };
+  auto cnt_get = [&](int row) -> int {
+    return sc ? static_cast<int>((scnt[row >> 1] >> (16 * (row & 1))) & 0xffffu) : __ldcg(cnt + row);
+  };
+  auto cnt_dec = [&](int row) -> int {  // returns the count before the decrement
+    if (sc) return static_cast<int>((atomicSub(&scnt[row >> 1], 1u << (16 * (row & 1))) >> (16 * (row & 1))) & 0xffffu);
+    return atomicSub(&cnt[row], 1);
+  };
   for (int64_t blk = blockIdx.x; blk < S.nblk; blk += gridDim.x) {
     const int64_t s0 = blk * bs;
     const int bt = static_cast<int>(a.m - s0 < bs ? a.m - s0 : bs);
@@ -175,7 +196,7 @@ __global__ void __launch_bounds__(kSymThreads, 1) k_sparse_symbolic(SymArgs A) {
     for (int j = warp; j < bt; j += kWarps) {
       const int i = a.idx[s0 + j];
       const int64_t e0 = a.colptr[i], e1 = a.colptr[i + 1];
-      for (int64_t e = e0 + lane; e < e1; e += 32) atomicAdd(&cnt[a.rowidx[e]], 1);
+      for (int64_t e = e0 + lane; e < e1; e += 32) cnt_inc(a.rowidx[e]);
     }
     __syncthreads();
     // ---- row offsets (exclusive scan over d) and the touched-row list
@@ -184,7 +205,7 @@ __global__ void __launch_bounds__(kSymThreads, 1) k_sparse_symbolic(SymArgs A) {
       const int r0 = tid * chunk, r1 = min(d, r0 + chunk);
       int se = 0, sr = 0;
       for (int r = r0; r < r1; ++r) {
-        const int c = __ldcg(cnt + r);
+        const int c = cnt_get(r);
         se += c;
         sr += c > 0;
       }
@@ -192,7 +213,7 @@ __global__ void __launch_bounds__(kSymThreads, 1) k_sparse_symbolic(SymArgs A) {
       const int pr = block_excl_scan(sr, tmp, &nrows);
       int oe = pe, orow = pr;
       for (int r = r0; r < r1; ++r) {
-        const int c = __ldcg(cnt + r);
+        const int c = cnt_get(r);
         off[r] = oe;
         if (c > 0) {
           if (orow < S.rcap) {
@@ -217,7 +238,7 @@ __global__ void __launch_bounds__(kSymThreads, 1) k_sparse_symbolic(SymArgs A) {
       const int64_t e0 = a.colptr[i], e1 = a.colptr[i + 1];
       for (int64_t e = e0 + lane; e < e1; e += 32) {
         const int row = a.rowidx[e];
-        const int pos = off[row] + atomicSub(&cnt[row], 1) - 1;
+        const int pos = off[row] + cnt_dec(row) - 1;
         if (fits) {
           ej[pos] = static_cast<unsigned short>(j);
           ev[pos] = a.val[e];
@@ -484,7 +505,7 @@ __device__ __noinline__ void solve_levels(double* u, PV pv, PL pl, REC rec, LP l
 struct NumArgs {
   SparseEpochArgs e;
   SymPlan s;
-  double* b;      // [bs][p]
+  double* b;      // [p][bs]
   double* u;      // [bs][p]
   double* dcb;    // [2][bs][p] x_jᵀC of the block (parity), filled one block ahead by the CTAs not solving
   double* yb;     // [2][bs][p] Y rows of the block's columns
@@ -662,7 +683,7 @@ __global__ void __launch_bounds__(kNumThreads, 1) k_sparse_epoch_levels(NumArgs 
         if (hs == 0 && col < p) {
           const double aj = al * rp[j], bj = fma(rp[j], be, gm[j]);
           const double t = fma(aj, dw, bj * dc);
-          A.b[static_cast<size_t>(j) * p + col] = a.eta_n * (t - yv) / (al * rp[j + 1]);
+          A.b[static_cast<size_t>(col) * bs + j] = a.eta_n * (t - yv) / (al * rp[j + 1]);  // [p][bs]: a solver reads one row
         }
       }
     }
@@ -678,7 +699,7 @@ __global__ void __launch_bounds__(kNumThreads, 1) k_sparse_epoch_levels(NumArgs 
           bar_phase ^= 1u;
         }
         mark(3);
-        for (int j = tid; j < bt; j += kNumThreads) u[j] = __ldcg(A.b + static_cast<size_t>(j) * p + c);
+        for (int j = tid; j < bt; j += kNumThreads) u[j] = __ldcg(A.b + static_cast<size_t>(c) * bs + j);
         mark(4);
         {
           const int* lp_g = S.lptr + blk * (bs + 4);
@@ -888,7 +909,11 @@ void launch_svrg_epoch_sparse_levels(const SparseEpochArgs& a, const SparseLevel
     A.e = a;
     A.s = S;
     const int grid = static_cast<int>(std::min<int64_t>(S.nblk, P.sym_ctas));
-    k_sparse_symbolic<<<grid, kSymThreads, 0, st>>>(A);
+    A.smem_cnt = a.d <= 65536 ? 1 : 0;
+    const size_t sym_smem = A.smem_cnt ? static_cast<size_t>((a.d + 1) / 2) * 4 : 0;
+    GAPLRA_CUDA_CHECK(cudaFuncSetAttribute(k_sparse_symbolic, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           static_cast<int>(std::max<size_t>(sym_smem, 4))));
+    k_sparse_symbolic<<<grid, kSymThreads, sym_smem, st>>>(A);
     GAPLRA_LAUNCH_CHECK();
   }
   if (timing) cudaEventRecord(ev1, st);

@@ -232,7 +232,7 @@ def test_svrg_epoch_sparse_lockstep(g, oracle):
     (40, 400, 20, 3, 997),         # row lists overflow: exact serial fallback per block
 ])
 def test_svrg_epoch_sparse_blocked_lockstep(g, oracle, d, n, z, p, m):
-    """Block-parallel sparse epoch (sparse_epoch.cu) against the oracle's step-by-step epoch."""
+    """Block-parallel sparse epoch (sparse_levels.cu) against the oracle's step-by-step epoch."""
     cp, ri, v = random_csc(d, n, z, seed=d + p)
     mo = oracle.csc(d, n, cp, ri, v)
     rng = np.random.default_rng(d)
@@ -244,6 +244,73 @@ def test_svrg_epoch_sparse_blocked_lockstep(g, oracle, d, n, z, p, m):
     rc, wo, _ = oracle.svrg_epoch(mo, w0, y, cblk, eta, lam, 5, m)
     wd = g.svrg_epoch(g.DeviceMatrix.csc(d, n, cp, ri, v), w0, y, cblk, eta, lam, 5, m)
     assert rel(wd, wo) <= 1e-10
+
+
+def test_svrg_epoch_sparse_dense_row_and_ragged(g, oracle):
+    """Level-scheduled sparse epoch (sparse_levels.cu) on patterns outside its fast path: a row present in
+    every column (its per-block list overflows: exact step-by-step fallback), and ragged columns incl. empty
+    ones; p = 20 takes the warp-per-step variant."""
+    rng = np.random.default_rng(17)
+    d, n, m = 600, 1800, 2500
+    cols = []
+    for j in range(n):
+        k = int(rng.integers(0, 9))  # 0..8 further rows: ragged, some columns hold only row 0
+        rr = np.sort(rng.choice(np.arange(1, d), k, replace=False)) if k else np.zeros(0, np.int64)
+        if j % 7 == 3:
+            rows = rr  # a few columns without the dense row (possibly empty)
+        else:
+            rows = np.concatenate([[0], rr])
+        cols.append(rows.astype(np.int32))
+    cp = np.zeros(n + 1, np.int64)
+    cp[1:] = np.cumsum([len(c) for c in cols])
+    ri = np.concatenate(cols).astype(np.int32)
+    v = rng.standard_normal(len(ri)) / np.sqrt(n)
+    mo = oracle.csc(d, n, cp, ri, v)
+    xs = g.DeviceMatrix.csc(d, n, cp, ri, v)
+    lam = 1.5 * float(np.sum(v * v))
+    eta = 1.0 / (4.0 * (lam + n * oracle.max_col_norm2(mo)))
+    for p in (5, 20):
+        w0 = rng.standard_normal((d, p))
+        _, zz, y = oracle.gram_block(mo, w0, want_y=True)
+        cblk = eta * (zz + rng.standard_normal((d, p)))
+        _, wo, _ = oracle.svrg_epoch(mo, w0, y, cblk, eta, lam, 5, m)
+        wd = g.svrg_epoch(xs, w0, y, cblk, eta, lam, 5, m)
+        assert rel(wd, wo) <= 1e-10
+        assert np.array_equal(wd, g.svrg_epoch(xs, w0, y, cblk, eta, lam, 5, m))
+
+
+def test_svrg_epoch_sparse_older_kernels(tmp_path):
+    """The fixed-point block kernel (GAPLRA_SPARSE_LEVELS=0) and the one-warp sequential kernel
+    (GAPLRA_SPARSE_BLOCKED=0) stay selectable: same epoch against the oracle in child processes."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = """
+import sys, numpy as np
+sys.path.insert(0, %r); sys.path.insert(0, %r)
+import paper_1607_02925_b200 as g
+from oracle_lib import Oracle
+from problems import random_csc
+o = Oracle()
+d, n, z, p, m = 5000, 20000, 20, 16, 20011
+cp, ri, v = random_csc(d, n, z, seed=3)
+mo = o.csc(d, n, cp, ri, v)
+rng = np.random.default_rng(1)
+w0 = rng.standard_normal((d, p))
+_, zz, y = o.gram_block(mo, w0, want_y=True)
+lam = 1.5 * float(np.sum(v * v))
+eta = 1.0 / (4.0 * (lam + n * o.max_col_norm2(mo)))
+c = eta * (zz + rng.standard_normal((d, p)))
+_, wo, _ = o.svrg_epoch(mo, w0, y, c, eta, lam, 5, m)
+wd = g.svrg_epoch(g.DeviceMatrix.csc(d, n, cp, ri, v), w0, y, c, eta, lam, 5, m)
+assert np.abs(wd - wo).max() <= 1e-10 * np.abs(wo).max()
+print("ok")
+""" % (root, os.path.join(root, "tests"))
+    for extra in ({"GAPLRA_SPARSE_LEVELS": "0"}, {"GAPLRA_SPARSE_BLOCKED": "0"}):
+        r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, **extra), capture_output=True,
+                           text=True, timeout=600)
+        assert r.returncode == 0 and "ok" in r.stdout, (extra, r.stdout + r.stderr)
 
 
 def test_svrg_solve_matches_oracle_and_direct(g, oracle):
