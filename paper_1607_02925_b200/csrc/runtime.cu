@@ -503,7 +503,7 @@ void epoch_run_dev(Context& c, Matrix& X, int p, double* W, const double* C, con
     const EpochConfig& cfg = pre.cfg;
     a.slab = pre.slab;
     a.zcol = c.zcol.ensure(static_cast<size_t>(X.ld));
-    if (cfg.xg) {
+    if (cfg.xg || cfg.nclusters > 1) {
       a.xg_slot = c.xgs.ensure(xg_slot_elems(cfg));
       a.xg_count = c.xgc.ensure(xg_count_elems(cfg));
     }
@@ -519,7 +519,7 @@ void epoch_run_dev(Context& c, Matrix& X, int p, double* W, const double* C, con
     a.prefetch = prefetch;
     DBuf<long long> dbg;
     if (timing) {
-      a.dbg = dbg.ensure(static_cast<size_t>(cfg.cluster) * cfg.groups * 8);
+      a.dbg = dbg.ensure(static_cast<size_t>(cfg.cluster) * cfg.nclusters * cfg.groups * 8);
       fprintf(stderr, "{\"epoch_layout\": {\"d_pad\": %d, \"p\": %d, \"cluster\": %d, \"pc\": %d, \"groups\": %d, "
               "\"rows_per_cta\": %d, \"stages\": %d, \"smem\": %zu}}\n", a.d_pad, p, cfg.cluster, cfg.pc, cfg.groups,
               cfg.rows_per_cta, cfg.stages, cfg.smem);
@@ -529,7 +529,7 @@ void epoch_run_dev(Context& c, Matrix& X, int p, double* W, const double* C, con
       launch_svrg_epoch_dense(a, cfg, c.st);
     }
     if (timing) {
-      std::vector<long long> h(static_cast<size_t>(cfg.cluster) * cfg.groups * 8);
+      std::vector<long long> h(static_cast<size_t>(cfg.cluster) * cfg.nclusters * cfg.groups * 8);
       GAPLRA_CUDA_CHECK(cudaMemcpyAsync(h.data(), dbg.p, h.size() * sizeof(long long), cudaMemcpyDeviceToHost, c.st));
       c.sync();
       const double nbk = static_cast<double>(ceil_div(m, cfg.b));

@@ -1098,6 +1098,7 @@ int shrink_pc(int pc) { return pc == 8 ? 6 : (pc == 6 ? 4 : std::max(1, pc - 1))
 int slab_head(const EpochConfig& cfg) { return (cfg.la == 2 ? 3 : 2) * kBlock * kBlock; }
 
 size_t xg_slot_elems(const EpochConfig& cfg) {  // doubles; x 2 for the 16-byte flag-in-data cells
+  if (cfg.nclusters > 1) return 2 * static_cast<size_t>(kXgSlots) * cfg.nclusters * cfg.cluster * kBlock * cfg.pc;
   return cfg.xg ? 2 * static_cast<size_t>(kXgSlots) * cfg.groups * cfg.cluster * kBlock * cfg.pc : 0;
 }
 size_t xg_count_elems(const EpochConfig& cfg) { return cfg.xg ? static_cast<size_t>(kXgSlots) * cfg.groups : 0; }
@@ -1252,6 +1253,11 @@ __global__ void __launch_bounds__(v3_block<RR>(PC), 1) k_svrg_chain_v3(EpochArgs
   extern __shared__ __align__(128) double sm[];
   const int G = XG ? static_cast<int>(gridDim.x) : static_cast<int>(cg::this_cluster().num_blocks());
   const int g = XG ? static_cast<int>(blockIdx.x) : static_cast<int>(cg::this_cluster().block_rank());
+  // PAIRED clusters (p = 1, a.ncl == 2): the rows are split over two clusters; each cluster all-reduces over
+  // DSMEM as usual, then CTA g of one cluster swaps its cluster sum with CTA g of the other through L2
+  // (flag-in-data cells, one writer and one reader per cell: no hot line), and adds them in cluster order.
+  const int ncl = XG ? 1 : a.ncl;
+  const int cl = ncl > 1 ? static_cast<int>(blockIdx.x) / G : 0;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int NV = B * PC;
   double* xg_slots = XG ? a.xg_slot : nullptr;  // [kXgSlots][G][NV]
@@ -1265,7 +1271,7 @@ __global__ void __launch_bounds__(v3_block<RR>(PC), 1) k_svrg_chain_v3(EpochArgs
   const ChainSmem L = chain_smem<PC, B, true>(a.rows_per_cta, a.stages);
   static_assert(2 * kV3Rows * NV + 6 * NV <= kChainThreads / 32 * (B / 8) * 64, "red[2] + coef + ahat + pre + outv fit");
   const int S = L.stages;
-  const int r0 = g * a.rows_per_cta;
+  const int r0 = (cl * G + g) * a.rows_per_cta;
   const int rc = max(0, min(a.rows_per_cta, a.d_pad - r0));
   const int RP = L.rows_pad;
   double* recv = sm + L.off_recv;  // [kRecvSlots][kMaxCluster][NV]
@@ -1432,6 +1438,18 @@ __global__ void __launch_bounds__(v3_block<RR>(PC), 1) k_svrg_chain_v3(EpochArgs
             s3 += sl[(q + 3) * NV];
           }
           s = (s0 + s1) + (s2 + s3);
+        }
+        if constexpr (PC == 1) {
+          if (ncl == 2) {  // swap cluster sums with the partner CTA (same rank, other cluster)
+            const uint32_t flag = static_cast<uint32_t>(t / kXgSlots + 1);
+            uint4* cells = reinterpret_cast<uint4*>(a.xg_slot) + static_cast<size_t>(t % kXgSlots) * 2 * G * NV;
+            ll_store(cells + (cl * G + g) * NV + e, s, flag);
+            const uint4* theirs = cells + ((cl ^ 1) * G + g) * NV + e;
+            uint4 w = ll_load(theirs);
+            while (w.y != flag || w.w != flag) w = ll_load(theirs);
+            const double o = __hiloint2double(static_cast<int>(w.z), static_cast<int>(w.x));
+            s = cl == 0 ? s + o : o + s;
+          }
         }
         Ahat[e] = s;
       }
@@ -1677,7 +1695,8 @@ __global__ void __launch_bounds__(v3_block<RR>(PC), 1) k_svrg_chain_v3(EpochArgs
 // Slice pitch RP ≡ 4 (mod 16) doubles: the update's LDS.64 B fragments and the
 // products' LDS.128 (rows 2tq, 2tq+1, slices permuted 0 2 1 3 4 6 5 7) are
 // bank-conflict free; coef is stored [slice][12].  Warps: 8 rows (ROWS / 8
-// rows each), 4 reducers (one Â / coef entry per lane), 1 pusher (sums the row
+// rows each), 4 reducers (each owns two right-hand-side columns: lane = (column, step), so Â -> coef -> pre
+// of a column stay inside one warp and the reducers never wait for each other), 1 pusher (sums the row
 // warps' partials, bulk-copies Â_{t+1} to the 16 peers), 2 producers.
 // ROWS = 256 (C2, C3) or 512 (C5: d = 8192 on 16-CTA clusters; a 512-row
 // stage is 71 KB, so the ring has 2 stages next to the 64 KB receive slots).
@@ -1687,6 +1706,9 @@ constexpr int PC = 8, B = 16, NV = B * PC;
 constexpr int kRows = 8, kRed = 4, kProd = 2;
 constexpr int kThreads = 32 * (kRows + kRed + 1 + kProd);
 constexpr int CP = 12;  // coef pitch (doubles)
+constexpr int RCP = 18;                // red: column-major [c][RCP] partials (pitch 18: the rows' stores are <= 2-way
+                                       // conflicted, the pusher's reads along j conflict free)
+constexpr int NVR = PC * RCP;          // one row warp's red vector
 
 struct Smem {
   int rp, stages;
@@ -1702,7 +1724,7 @@ __host__ __device__ inline Smem smem(int rows, int stages, bool xg = false) {
   L.off_recv = o;
   if (!xg) o += static_cast<size_t>(kRecvSlots) * kMaxCluster * NV;  // XG: partials arrive through L2
   L.off_red = o;
-  o += 2 * kRows * NV;
+  o += 2 * kRows * NVR;
   L.off_outv = o;
   o += 2 * NV;
   L.off_cf = o;
@@ -1731,7 +1753,7 @@ __host__ __device__ inline Smem smem_half() {
   size_t o = L.stage_len * kHalves + static_cast<size_t>(kSlabs) * kSlabLen;
   L.off_recv = o;  // XG only: no receive slots
   L.off_red = o;
-  o += 2 * kRows * NV;
+  o += 2 * kRows * NVR;
   L.off_outv = o;
   o += 2 * NV;
   L.off_cf = o;
@@ -1897,16 +1919,17 @@ __global__ void __launch_bounds__(v4::kThreads, 1) k_svrg_chain_v4(EpochArgs a) 
         asm volatile("bar.sync 5, %0;" ::"n"(32 * (kRows + 1)) : "memory");
       if (!XG && lane < G) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
       __syncwarp();
-      const double* rb = red + (u & 1) * kRows * NV;
+      const double* rb = red + (u & 1) * kRows * NVR;
       double* ov = outv + (u & 1) * NV;
+      // exchanged vector: entry en = c * 16 + j (column-major), read from the padded red [c][RCP]
       if constexpr (XG) {  // partial -> L2 slot, then one release-increment
         double* dst = xg_slots + (static_cast<size_t>(u % kXgSlots) * G + g) * NV;
 #pragma unroll
         for (int q = 0; q < NV / 32; ++q) {
-          const int e = q * 32 + lane;
+          const int e = q * 32 + lane, er = (e >> 4) * RCP + (e & 15);
           double sum = 0.0;
 #pragma unroll
-          for (int w = 0; w < kRows; w += 2) sum += rb[w * NV + e] + rb[(w + 1) * NV + e];
+          for (int w = 0; w < kRows; w += 2) sum += rb[w * NVR + er] + rb[(w + 1) * NVR + er];
           st_cg(dst + e, sum);
         }
         __syncwarp();
@@ -1915,10 +1938,10 @@ __global__ void __launch_bounds__(v4::kThreads, 1) k_svrg_chain_v4(EpochArgs a) 
       }
 #pragma unroll
       for (int q = 0; q < NV / 32; ++q) {
-        const int e = q * 32 + lane;
+        const int e = q * 32 + lane, er = (e >> 4) * RCP + (e & 15);
         double sum = 0.0;
 #pragma unroll
-        for (int w = 0; w < kRows; w += 2) sum += rb[w * NV + e] + rb[(w + 1) * NV + e];
+        for (int w = 0; w < kRows; w += 2) sum += rb[w * NVR + er] + rb[(w + 1) * NVR + er];
         ov[e] = sum;
       }
       fence_proxy_async();
@@ -1934,18 +1957,22 @@ __global__ void __launch_bounds__(v4::kThreads, 1) k_svrg_chain_v4(EpochArgs a) 
     tick(7);
     if (a.dbg && lane == 0) a.dbg[(blockIdx.y * gridDim.x + blockIdx.x) * 8 + 7] = tacc[7];
   } else if (warp >= kRows) {  // --------------------------------------------- reducers
+    // warp rw owns columns 2 rw, 2 rw + 1: lane = (c = 2 rw + (lane >> 4), j = lane & 15), exchanged entry
+    // e = c * 16 + j = 32 rw + lane.  Â[:, c], coef[:, c] and pre[:, c] live in this warp (a private 32-entry
+    // tile + registers), so there is no barrier among the reducer warps.
     const int rw = warp - kRows;
-    const int e = rw * 32 + lane;  // this lane's entry (j, c) = (e / PC, e % PC)
-    const int j = e / PC, c = e - (e / PC) * PC;
-    auto red_sync = []() { asm volatile("bar.sync 4, %0;" ::"n"(32 * kRed) : "memory"); };
+    const int e = rw * 32 + lane;
+    const int j = lane & 15, c = 2 * rw + (lane >> 4), hb = lane & 16;
+    double* aw = Ahat + rw * 32;  // this warp's Â (then coef) tile: [column half][16]
     auto arm = [&](int u) {
       if (!XG && rw == 0 && lane == 0)
         mbar_expect_tx(&rbar[u & (kRecvSlots - 1)], static_cast<uint32_t>(G * NV * 8));
     };
+    double pre_r = 0.0;
     if (nb > 0) {
       arm(0);
       mbar_wait(HALF ? &fullS[0] : &full[0], 0);
-      pre[e] = slab_tt(0)[2 * B * B + e];
+      pre_r = slab_tt(0)[2 * B * B + j * PC + c];
     }
     int cs = 0;
     uint32_t cph = 0;
@@ -1958,14 +1985,16 @@ __global__ void __launch_bounds__(v4::kThreads, 1) k_svrg_chain_v4(EpochArgs a) 
       const int par = t & (kRecvSlots - 1);
       tick(6);
       if constexpr (XG) {
+        // one poller per CTA (four pollers per CTA slowed the exchange: C5 coef wait 534 -> 879 cycles), then
+        // the reducer warps meet once on a named barrier
         if (rw == 0 && lane == 0) xg_wait(xg_cnt + t % kXgSlots, static_cast<unsigned>(G) * (t / kXgSlots + 1));
-        red_sync();  // every peer's partial of block t is in L2
+        asm volatile("bar.sync 4, %0;" ::"n"(32 * kRed) : "memory");  // every peer's partial of block t is in L2
       } else {
         mbar_wait(&rbar[par], static_cast<uint32_t>((t >> 2) & 1));
       }
       tick(4);
       double sacc = 0.0;
-      if (e < bt_of(t) * PC) {
+      if (j < bt_of(t)) {
         double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
         if constexpr (XG) {
           const double* sl = xg_slots + static_cast<size_t>(t % kXgSlots) * G * NV + e;
@@ -1979,7 +2008,7 @@ __global__ void __launch_bounds__(v4::kThreads, 1) k_svrg_chain_v4(EpochArgs a) 
           }
         } else {
           const double* sl = recv + par * kMaxCluster * NV + e;
-#pragma unroll 1
+#pragma unroll 4
           for (int q = 0; q < G; q += 4) {
             s0 += sl[q * NV];
             s1 += sl[(q + 1) * NV];
@@ -1989,45 +2018,49 @@ __global__ void __launch_bounds__(v4::kThreads, 1) k_svrg_chain_v4(EpochArgs a) 
         }
         sacc = (s0 + s1) + (s2 + s3);
       }
-      Ahat[e] = sacc;
-      red_sync();  // Â_t complete
+      aw[lane] = sacc;
+      __syncwarp();  // Â[:, c] of both columns complete
       const double* TT = slab_tt(t);
       double* cf = cfb + (t & 1) * B * CP;
+      double cv;
       {
-        double s0 = pre[e], s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        double s0 = pre_r, s1 = 0.0, s2 = 0.0, s3 = 0.0;
 #pragma unroll
         for (int l = 0; l < B; l += 4) {
-          s0 = fma(TT[l * B + j], Ahat[l * PC + c], s0);
-          s1 = fma(TT[(l + 1) * B + j], Ahat[(l + 1) * PC + c], s1);
-          s2 = fma(TT[(l + 2) * B + j], Ahat[(l + 2) * PC + c], s2);
-          s3 = fma(TT[(l + 3) * B + j], Ahat[(l + 3) * PC + c], s3);
+          s0 = fma(TT[l * B + j], aw[hb + l], s0);
+          s1 = fma(TT[(l + 1) * B + j], aw[hb + l + 1], s1);
+          s2 = fma(TT[(l + 2) * B + j], aw[hb + l + 2], s2);
+          s3 = fma(TT[(l + 3) * B + j], aw[hb + l + 3], s3);
         }
-        cf[j * CP + c] = (s0 + s1) + (s2 + s3);
+        cv = (s0 + s1) + (s2 + s3);
+        cf[j * CP + c] = cv;
       }
       if (t & 1)
         asm volatile("bar.arrive 3, %0;" ::"n"(32 * (kRows + kRed)) : "memory");
       else
         asm volatile("bar.arrive 2, %0;" ::"n"(32 * (kRows + kRed)) : "memory");
       tick(5);
-      __syncwarp();
+      __syncwarp();  // every lane's Â reads done
+      aw[lane] = cv;  // coef[:, c] for pre_{t+1}
       if (lane == 0) mbar_arrive(HALF ? &emptyS[t % kSlabs] : &empty[cs]);  // TT_t: the reducers' last use
       if (more) {  // pre_{t+1} = M_{t+1} coef_t + U_{t+1}
-        red_sync();  // coef_t complete; Â reads done
+        __syncwarp();
         if constexpr (HALF)
           mbar_wait(&fullS[(t + 1) % kSlabs], static_cast<uint32_t>(((t + 1) / kSlabs) & 1));
         else
           mbar_wait(&full[ns], nph);
         const double* M = slab_tt(t + 1) + B * B;
         const double* Ub = M + B * B;
-        double s0 = Ub[e], s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        double s0 = Ub[j * PC + c], s1 = 0.0, s2 = 0.0, s3 = 0.0;
 #pragma unroll
         for (int l = 0; l < B; l += 4) {
-          s0 = fma(M[l * B + j], cf[l * CP + c], s0);
-          s1 = fma(M[(l + 1) * B + j], cf[(l + 1) * CP + c], s1);
-          s2 = fma(M[(l + 2) * B + j], cf[(l + 2) * CP + c], s2);
-          s3 = fma(M[(l + 3) * B + j], cf[(l + 3) * CP + c], s3);
+          s0 = fma(M[l * B + j], aw[hb + l], s0);
+          s1 = fma(M[(l + 1) * B + j], aw[hb + l + 1], s1);
+          s2 = fma(M[(l + 2) * B + j], aw[hb + l + 2], s2);
+          s3 = fma(M[(l + 3) * B + j], aw[hb + l + 3], s3);
         }
-        pre[e] = (s0 + s1) + (s2 + s3);
+        pre_r = (s0 + s1) + (s2 + s3);
+        __syncwarp();  // the tile is free for the next Â
       }
       cs = ns;
       cph = nph;
@@ -2081,13 +2114,13 @@ __global__ void __launch_bounds__(v4::kThreads, 1) k_svrg_chain_v4(EpochArgs a) 
         }
       }
       // C fragment (column gq, slices 8 n2 + perm(2 tq), 8 n2 + perm(2 tq + 1)) -> red(u_blk) in [j PC + c]
-      double* rb = red + (u_blk & 1) * kRows * NV + warp * NV;
+      double* rb = red + (u_blk & 1) * kRows * NVR + warp * NVR;
       const int pa = ((2 * tq) & 1) << 1 | (((2 * tq) >> 1) & 1) | ((2 * tq) & 4);
       const int pb = ((2 * tq + 1) & 1) << 1 | (((2 * tq + 1) >> 1) & 1) | ((2 * tq + 1) & 4);
 #pragma unroll
       for (int n2 = 0; n2 < 2; ++n2) {
-        rb[(8 * n2 + pa) * PC + gq] = acc[n2][0][0] + acc[n2][1][0];
-        rb[(8 * n2 + pb) * PC + gq] = acc[n2][0][1] + acc[n2][1][1];
+        rb[gq * RCP + 8 * n2 + pa] = acc[n2][0][0] + acc[n2][1][0];
+        rb[gq * RCP + 8 * n2 + pb] = acc[n2][0][1] + acc[n2][1][1];
       }
       bar_red_arrive(u_blk);
     };
@@ -2680,6 +2713,20 @@ EpochConfig choose_epoch_config(int d_pad, int p) {
       return cfg;
     }
   }
+  // p = 1, 2048 < d <= 8192, GAPLRA_P1_PAIR=1 (experiment, off by default): two paired 16-CTA clusters.  The rows
+  // per CTA halve (C5 256, C2 128) and the cross-cluster hop is a pairwise L2 swap of flag-in-data cells (one
+  // writer, one reader per cell).  Measured slower: the swap alone costs ~1200 cycles per block on the
+  // reducer's chain (C2 17.0 vs 9.1 ms, C5 177 vs 146 ms per epoch).
+  static const int env_pair = getenv("GAPLRA_P1_PAIR") ? atoi(getenv("GAPLRA_P1_PAIR")) : 0;
+  if (p == 1 && env_pair && env_pc == 0 && env_cluster == 0 && d_pad > 2048 && d_pad <= 8192 &&
+      max_active_clusters(16) >= 2) {
+    EpochConfig cfg = make(16);
+    cfg.nclusters = 2;
+    cfg.rows_per_cta = static_cast<int>(ceil_div(ceil_div(d_pad, 32), 4) * 4);
+    cfg.stages = 4;
+    cfg.smem = smem_for(cfg.pc, cfg.rows_per_cta, cfg.stages);
+    return cfg;
+  }
   const EpochConfig c16 = make(16), c8 = make(8);
   auto v3_ok = [](const EpochConfig& c) { return v3_supports(c.pc, c.rows_per_cta); };
   if (d_pad < 1024) return c8;
@@ -2764,7 +2811,7 @@ void launch_chain_pc(const EpochArgs& a, const EpochConfig& cfg, cudaStream_t st
   if (cfg.cluster > 8 && !xg)
     GAPLRA_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   cudaLaunchConfig_t lc = {};
-  lc.gridDim = dim3(cfg.cluster, cfg.groups, 1);
+  lc.gridDim = dim3(cfg.cluster * std::max(1, cfg.nclusters), cfg.groups, 1);
   bool rr = false;
   if constexpr (PC == 1)
     rr = kern == k_svrg_chain_v3<1, kBlock, 1, true> || kern == k_svrg_chain_v3<1, kBlock, 2, true> ||
@@ -2786,7 +2833,13 @@ void launch_chain_pc(const EpochArgs& a, const EpochConfig& cfg, cudaStream_t st
     GAPLRA_CUDA_CHECK(cudaMemsetAsync(a.xg_count, 0, xg_count_elems(cfg) * sizeof(unsigned), st));
     if (xg_ll_mode() && !use_v4) GAPLRA_CUDA_CHECK(cudaMemsetAsync(a.xg_slot, 0, xg_slot_elems(cfg) * sizeof(double), st));
   }
+  if (cfg.nclusters > 1) {
+    if (!a.xg_slot) throw Error(kContractViolation, "epoch: paired clusters without exchange buffers");
+    if (PC != 1 || use_v4 || xg) throw Error(kContractViolation, "epoch: paired clusters are a p = 1 layout");
+    GAPLRA_CUDA_CHECK(cudaMemsetAsync(a.xg_slot, 0, xg_slot_elems(cfg) * sizeof(double), st));
+  }
   EpochArgs args = a;
+  args.ncl = std::max(1, cfg.nclusters);
   args.xg_ll = xg && !use_v4 ? xg_ll_mode() : 0;
   args.rows_per_cta = cfg.rows_per_cta;
   args.stages = stages;

@@ -31,6 +31,7 @@ struct EpochArgs {
   // XG chains (cfg.xg): the group's all-reduce goes through L2 instead of DSMEM
   double* xg_slot;   // [kXgSlots][groups][cluster][NV] partials
   unsigned* xg_count;  // [groups][kXgSlots] arrivals, zeroed before each launch
+  int ncl;           // clusters the rows are split over (2: paired clusters, k_svrg_chain_v3 at p = 1)
   int xg_ll;         // p = 1 XG chains: partials as 16-byte flag-in-data cells (xg_slot zeroed before each launch)
 };
 
@@ -53,6 +54,7 @@ struct EpochConfig {
   int cluster, pc, b, rows_per_cta, groups, stages;
   size_t smem;
   int xg = 0;  // 1: the `cluster` CTAs of a group are plain CTAs exchanging through L2 (no cluster launch)
+  int nclusters = 1;  // p = 1: 2 = two paired clusters (pairwise L2 swap of the cluster sums; needs xg_slot)
   int la = 1;  // chain lookahead in s-step blocks (2: the p = 1 chain k_chain_p1_la2)
 };
 int slab_head(const EpochConfig& cfg);
