@@ -424,7 +424,13 @@ __global__ void k_rho_table(double* rp, double* gm, int bs, double rho) {
 // FMAs -> two shuffles -> store.  (A barrier-free dataflow variant, groups
 // spinning on per-step ready tags in shared memory, measured 5x slower: the
 // spinning warps starve the working ones.)  u holds b on entry.
-constexpr int kSolveLanes = 4, kSolveGroups = kNumThreads / kSolveLanes, kPre = 6;
+#ifndef SL_LANES
+#define SL_LANES 4
+#endif
+#ifndef SL_PRE
+#define SL_PRE 6
+#endif
+constexpr int kSolveLanes = SL_LANES, kSolveGroups = kNumThreads / kSolveLanes, kPre = SL_PRE;
 constexpr unsigned kNoStep = 0xffffu;
 struct SolveItem {
   int j, x_rest, x_end;  // step (-1: none); pairs beyond the preloaded ones: x_rest, x_rest + 4, ... < x_end
@@ -460,8 +466,8 @@ __device__ __forceinline__ void solve_apply(double* u, PV pv, PL pl, const Solve
   }
   double acc = a0 + a1;
   for (int x = it.x_rest; x < it.x_end; x += kSolveLanes) acc = fma(pv[x], u[pl[x]], acc);
-  acc += __shfl_xor_sync(0xffffffffu, acc, 2);
-  acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+#pragma unroll
+  for (int o = kSolveLanes / 2; o >= 1; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
   if (sub == 0 && it.j >= 0) u[it.j] = fma(kappa, acc, it.bj);
 }
 // (__noinline__: its own register allocation.)  Software pipeline over the
