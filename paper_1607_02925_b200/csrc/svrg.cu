@@ -2109,6 +2109,7 @@ __global__ void __launch_bounds__(v4::kThreads, 1) k_svrg_chain_v4(EpochArgs a) 
 #pragma unroll
         for (int tl = 0; tl < kTiles; ++tl) {
           const double2 xv = *reinterpret_cast<const double2*>(xb + perm * RP + rw0 + 8 * tl + 2 * tq);
+          if (a.skip & 2) continue;  // GAPLRA_EPOCH_SKIP ablation (results invalid)
           dmma(acc[n2][tl & 1][0], acc[n2][tl & 1][1], v[tl][0], xv.x);
           dmma(acc[n2][tl & 1][0], acc[n2][tl & 1][1], v[tl][1], xv.y);
         }
@@ -2143,10 +2144,11 @@ __global__ void __launch_bounds__(v4::kThreads, 1) k_svrg_chain_v4(EpochArgs a) 
         for (int ks = 0; ks < 4; ++ks)
 #pragma unroll
           for (int tl = 0; tl < kTiles; ++tl) bx[ks][tl] = xb[(4 * ks + tq) * RP + rw0 + 8 * tl + gq];
+        if (!(a.skip & 4))
 #pragma unroll
-        for (int ks = 0; ks < 4; ++ks)
+          for (int ks = 0; ks < 4; ++ks)
 #pragma unroll
-          for (int tl = 0; tl < kTiles; ++tl) dmma(v[tl][0], v[tl][1], af[ks], bx[ks][tl]);
+            for (int tl = 0; tl < kTiles; ++tl) dmma(v[tl][0], v[tl][1], af[ks], bx[ks][tl]);
       } else {  // 512 rows: two k-steps of B fragments in flight (register budget of 480 threads;
                 // a k-step software pipeline measured no faster: update 1821 vs 1803 cycles)
 #pragma unroll
