@@ -914,7 +914,7 @@ void launch_svrg_epoch_sparse_levels(const SparseEpochArgs& a, const SparseLevel
     SymArgs A;
     A.e = a;
     A.s = S;
-    const int grid = static_cast<int>(std::min<int64_t>(S.nblk, P.sym_ctas));
+    const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(S.nblk, P.sym_ctas)));  // m = 0: no blocks
     A.smem_cnt = a.d <= 65536 ? 1 : 0;
     const size_t sym_smem = A.smem_cnt ? static_cast<size_t>((a.d + 1) / 2) * 4 : 0;
     GAPLRA_CUDA_CHECK(cudaFuncSetAttribute(k_sparse_symbolic, cudaFuncAttributeMaxDynamicSharedMemorySize,

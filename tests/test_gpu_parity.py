@@ -279,6 +279,25 @@ def test_svrg_epoch_sparse_dense_row_and_ragged(g, oracle):
         assert np.array_equal(wd, g.svrg_epoch(xs, w0, y, cblk, eta, lam, 5, m))
 
 
+def test_svrg_epoch_sparse_many_rows(g, oracle):
+    """d > 65536: the symbolic kernel keeps its row counters in global memory instead of shared memory."""
+    d, n, z, p, m = 70000, 3000, 5, 3, 4001
+    cp, ri, v = random_csc(d, n, z, seed=8)
+    mo = oracle.csc(d, n, cp, ri, v)
+    rng = np.random.default_rng(8)
+    w0 = rng.standard_normal((d, p))
+    _, zz, y = oracle.gram_block(mo, w0, want_y=True)
+    lam = 1.5 * float(np.sum(v * v))
+    eta = 1.0 / (4.0 * (lam + n * oracle.max_col_norm2(mo)))
+    cblk = eta * (zz + rng.standard_normal((d, p)))
+    _, wo, _ = oracle.svrg_epoch(mo, w0, y, cblk, eta, lam, 5, m)
+    xs = g.DeviceMatrix.csc(d, n, cp, ri, v)
+    wd = g.svrg_epoch(xs, w0, y, cblk, eta, lam, 5, m)
+    assert rel(wd, wo) <= 1e-10
+    # no steps: W = α Ŵ + β C with α = 1, β = 0
+    assert np.array_equal(g.svrg_epoch(xs, w0, y, cblk, eta, lam, 5, 0), w0)
+
+
 def test_svrg_epoch_sparse_older_kernels(tmp_path):
     """The fixed-point block kernel (GAPLRA_SPARSE_LEVELS=0) and the one-warp sequential kernel
     (GAPLRA_SPARSE_BLOCKED=0) stay selectable: same epoch against the oracle in child processes."""
