@@ -544,6 +544,14 @@ void epoch_run_dev(Context& c, Matrix& X, int p, double* W, const double* C, con
       }
       fprintf(stderr, "], \"cluster\": %d, \"pc\": %d, \"groups\": %d, \"stages\": %d}\n", cfg.cluster, cfg.pc,
               cfg.groups, cfg.stages);
+      if (p == 1 && m >= 1008 * kEpochBlock) {
+        long long hp[64];
+        read_chain_hops(hp);
+        fprintf(stderr, "{\"chain_hops_block_1002\": {\"rows_products_done\": 0, \"pusher_woken\": %lld, \"copies_issued\": %lld, "
+                "\"reducer_all_in\": %lld, \"coef_handed\": %lld, \"rows_coef_received\": %lld, \"next_products_done\": %lld}}\n",
+                hp[2 * 8 + 1] - hp[2 * 8], hp[2 * 8 + 2] - hp[2 * 8], hp[2 * 8 + 3] - hp[2 * 8], hp[2 * 8 + 4] - hp[2 * 8],
+                hp[2 * 8 + 5] - hp[2 * 8], hp[3 * 8] - hp[2 * 8]);
+      }
     }
   } else {
     SparseEpochArgs a{};

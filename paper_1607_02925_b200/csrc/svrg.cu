@@ -1216,6 +1216,17 @@ void launch_block_prep(const EpochArgs& a, const EpochConfig& cfg, cudaStream_t 
 // The coef hand-off alternates two named barriers (even / odd blocks), so the
 // reducer can never arrive twice on one barrier phase.
 // ---------------------------------------------------------------------------
+// GAPLRA_EPOCH_TIMING: clock stamps of one all-reduce loop (blocks 1000..1007 of CTA 0), per hop:
+// 0 rows: products done, 1 pusher: woken, 2 pusher: copies issued, 3 reducer: all partials in,
+// 4 reducer: coef handed to the rows, 5 rows: coef received (update starts)
+__device__ long long g_hop[8 * 8];
+__device__ __forceinline__ void hop_stamp(const EpochArgs& a, int blk, int k) {
+  if (a.dbg && blockIdx.x == 0 && blockIdx.y == 0 && blk >= 1000 && blk < 1008) {
+    long long now;
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(now)::"memory");
+    g_hop[(blk - 1000) * 8 + k] = now;
+  }
+}
 constexpr int kV3Rows = 4;       // row warps
 // producer warps: 4 at PC = 1 (each issues its lanes' bulk copies one after
 // another, so more warps raise the feed; PC > 1 needs the registers)
@@ -1333,7 +1344,8 @@ __global__ void __launch_bounds__(v3_block<RR>(PC), 1) k_svrg_chain_v3(EpochArgs
         asm volatile("bar.sync 6, %0;" ::"n"(32 * (kV3Rows + 1)) : "memory");
       else
         asm volatile("bar.sync 5, %0;" ::"n"(32 * (kV3Rows + 1)) : "memory");
-      if (!XG && lane < G) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+      if (lane == 0) hop_stamp(a, u, 1);
+      if (!XG && lane < G && !(PC == 1 && a.push_async)) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
       __syncwarp();
       const double* rb = red + (u & 1) * kV3Rows * NV;
       double* ov = outv + (u & 1) * NV;
@@ -1352,6 +1364,20 @@ __global__ void __launch_bounds__(v3_block<RR>(PC), 1) k_svrg_chain_v3(EpochArgs
         if (lane == 0) xg_publish(xg_cnt + u % kXgSlots);
         continue;
       }
+      if constexpr (PC == 1) {
+        // p = 1: 16 entries.  Each half-warp sums entry e = lane & 15 and stores it straight from the register
+        // into every second peer's receive slot (st.async: the store itself completes 8 bytes on the peer's
+        // barrier).  The staged bulk copy (sum -> shared -> fence.proxy.async -> one copy per peer) took ~1400
+        // cycles from the pusher's wake-up to the copies being issued.
+        if (a.push_async) {
+          const int e = lane & 15, par = u & (kRecvSlots - 1);
+          const double sum = (rb[e] + rb[NV + e]) + (rb[2 * NV + e] + rb[3 * NV + e]);
+          const uint32_t dst = smem_u32(recv + (par * kMaxCluster + g) * NV + e), bar = smem_u32(&rbar[par]);
+          for (int q = lane >> 4; q < G; q += 2) st_async_f64(mapa(dst, q), sum, mapa(bar, q));
+          if (lane == 0) hop_stamp(a, u, 2);
+          continue;
+        }
+      }
       for (int e = lane; e < NV; e += 32) ov[e] = (rb[e] + rb[NV + e]) + (rb[2 * NV + e] + rb[3 * NV + e]);
       fence_proxy_async();
       __syncwarp();
@@ -1361,6 +1387,7 @@ __global__ void __launch_bounds__(v3_block<RR>(PC), 1) k_svrg_chain_v3(EpochArgs
                         mapa(smem_u32(&rbar[par]), lane));
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
       }
+      if (lane == 0) hop_stamp(a, u, 2);
     }
     if (!XG && lane < G) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   } else if (warp >= kV3Rows) {  // ------------------------------------------ reducers
@@ -1377,6 +1404,115 @@ __global__ void __launch_bounds__(v3_block<RR>(PC), 1) k_svrg_chain_v3(EpochArgs
       if (!XG && rw == 0 && lane == 0)
         mbar_expect_tx(&rbar[u & (kRecvSlots - 1)], static_cast<uint32_t>(G * NV * 8));  // full vectors
     };
+    bool fast_done = false;
+    if constexpr (PC == 1 && !XG) {
+      if (a.ncl == 1 && a.fast_reducer) {
+        fast_done = true;
+        // p = 1, one cluster: the reducer warp is the chain's critical resource (the rows waited at the coef
+        // barrier a third of the time), so everything that does not depend on Â_t is in registers BEFORE the
+        // wait: this lane's columns of TT_t and M_{t+1} and U_{t+1}.  After the wait: 16 batched peer loads,
+        // one shared round trip for Â, 16 FMAs -> coef_t to the rows; then pre_{t+1} from coef_t.  Same
+        // summation orders as the generic path below (bitwise identical results).
+        const int e = lane & 15;  // lanes 16-31 shadow 0-15 (no stores)
+        const bool act = lane < 16;
+        double TTc[B], Mn[B], pre_r = 0.0;
+        auto load_col = [&](const double* src, double (&dst)[B]) {
+#pragma unroll
+          for (int l = 0; l < B; ++l) dst[l] = src[l * B + e];
+        };
+        if (nb > 0) {
+          arm(0);
+          mbar_wait(&full[0], 0);
+          const double* sl0 = stage_at(0) + B * RP;
+          load_col(sl0, TTc);
+          pre_r = sl0[2 * B * B + e];
+        }
+        int cs = 0;
+        uint32_t cph = 0;
+#pragma unroll 1
+        for (int t = 0; t < nb; ++t) {
+          const bool more = t + 1 < nb;
+          const int ns = cs + 1 == S ? 0 : cs + 1;
+          const uint32_t nph = ns == 0 ? cph ^ 1u : cph;
+          if (more) arm(t + 1);
+          const int par = t & (kRecvSlots - 1);
+          double Un = 0.0;
+          if (more) {  // stage t + 1 is complete (the rows' products of t + 1 ran before their update of t)
+            mbar_wait(&full[ns], nph);
+            const double* sn = stage_at(ns) + B * RP;
+            load_col(sn + B * B, Mn);
+            Un = sn[2 * B * B + e];
+          }
+          tick(7);
+          const int nv = bt_of(t);
+          mbar_wait(&rbar[par], static_cast<uint32_t>((t >> 2) & 1));
+          tick(6);
+          if (lane == 0) hop_stamp(a, t, 3);
+          double sv = 0.0;
+          {
+            const double* sl = recv + par * kMaxCluster * NV + e;
+            double x[kMaxCluster];
+#pragma unroll
+            for (int q = 0; q < kMaxCluster; ++q) x[q] = q < G ? sl[q * NV] : 0.0;
+            double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+            for (int q = 0; q < kMaxCluster; q += 4) {
+              if (q < G) {
+                s0 += x[q];
+                s1 += x[q + 1];
+                s2 += x[q + 2];
+                s3 += x[q + 3];
+              }
+            }
+            sv = e < nv ? (s0 + s1) + (s2 + s3) : 0.0;
+          }
+          if (act) Ahat[e] = sv;
+          __syncwarp();
+          double* cf = coef + (t & 1) * NV;
+          double cv;
+          {
+            double s0 = pre_r, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+            for (int l = 0; l < B; l += 4) {
+              s0 = fma(TTc[l], Ahat[l], s0);
+              s1 = fma(TTc[l + 1], Ahat[l + 1], s1);
+              s2 = fma(TTc[l + 2], Ahat[l + 2], s2);
+              s3 = fma(TTc[l + 3], Ahat[l + 3], s3);
+            }
+            cv = (s0 + s1) + (s2 + s3);
+          }
+          if (act) cf[e] = cv;
+          if (t & 1)
+            asm volatile("bar.arrive 3, %0;" ::"n"(32 * (kV3Rows + NRD)) : "memory");
+          else
+            asm volatile("bar.arrive 2, %0;" ::"n"(32 * (kV3Rows + NRD)) : "memory");
+          __syncwarp();
+          if (lane == 0) {
+            hop_stamp(a, t, 4);
+            mbar_arrive(&empty[cs]);  // TT_t (in registers since before the wait): the stage is free for the reducer
+          }
+          if (more) {
+            double s0 = Un, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+            for (int l = 0; l < B; l += 4) {
+              s0 = fma(Mn[l], cf[l], s0);
+              s1 = fma(Mn[l + 1], cf[l + 1], s1);
+              s2 = fma(Mn[l + 2], cf[l + 2], s2);
+              s3 = fma(Mn[l + 3], cf[l + 3], s3);
+            }
+            pre_r = (s0 + s1) + (s2 + s3);
+            load_col(stage_at(ns) + B * RP, TTc);  // TT_{t+1}
+          }
+          cs = ns;
+          cph = nph;
+        }
+        if (a.dbg && lane == 0) {
+          const int cta = blockIdx.y * gridDim.x + blockIdx.x;
+          for (int kk = 6; kk < 8; ++kk) a.dbg[cta * 8 + kk] = tacc[kk];
+        }
+      }
+    }
+    if (!fast_done) {
     if (nb > 0) {
       arm(0);
       mbar_wait(&full[0], 0);
@@ -1423,6 +1559,7 @@ __global__ void __launch_bounds__(v3_block<RR>(PC), 1) k_svrg_chain_v3(EpochArgs
       } else {
         mbar_wait(&rbar[par], static_cast<uint32_t>((t >> 2) & 1));
         tick(6);
+        if (rw == 0 && lane == 0) hop_stamp(a, t, 3);
       }
       if (!XG && mine) {
         const int e = me;
@@ -1475,6 +1612,7 @@ __global__ void __launch_bounds__(v3_block<RR>(PC), 1) k_svrg_chain_v3(EpochArgs
       else
         asm volatile("bar.arrive 2, %0;" ::"n"(32 * (kV3Rows + NRD)) : "memory");
       __syncwarp();
+      if (rw == 0 && lane == 0) hop_stamp(a, t, 4);
       if (lane == 0) mbar_arrive(&empty[cs]);  // TT_t was the reducers' last use of stage t
       if (more) {  // pre_{t+1} = M_{t+1} coef_t + U_{t+1}
         red_sync();  // coef_t complete (the other reducer's half); its Â reads done
@@ -1503,6 +1641,7 @@ __global__ void __launch_bounds__(v3_block<RR>(PC), 1) k_svrg_chain_v3(EpochArgs
       const int cta = blockIdx.y * gridDim.x + blockIdx.x;
       for (int kk = 6; kk < 8; ++kk) a.dbg[cta * 8 + kk] = tacc[kk];
     }
+    }  // !fast_done
   } else {  // --------------------------------------------------------------- rows
     if constexpr (RR) asm volatile("setmaxnreg.inc.sync.aligned.u32 232;" ::: "memory");
     const int pm = lane >> 1;  // product order j = i ^ pm
@@ -1565,6 +1704,7 @@ __global__ void __launch_bounds__(v3_block<RR>(PC), 1) k_svrg_chain_v3(EpochArgs
         asm volatile("bar.arrive 6, %0;" ::"n"(32 * (kV3Rows + 1)) : "memory");
       else
         asm volatile("bar.arrive 5, %0;" ::"n"(32 * (kV3Rows + 1)) : "memory");
+      if (tid == 0) hop_stamp(a, u, 0);
     };
     auto update = [&](const double2 (&xr)[H][B], int t, double rn) {
       if (t & 1)
@@ -1572,6 +1712,7 @@ __global__ void __launch_bounds__(v3_block<RR>(PC), 1) k_svrg_chain_v3(EpochArgs
       else
         asm volatile("bar.sync 2, %0;" ::"n"(32 * (kV3Rows + NRD)) : "memory");
       tick(4);
+      if (tid == 0) hop_stamp(a, t, 5);
       const double* cf = coef + (t & 1) * NV;
 #pragma unroll
       for (int h = 0; h < H; ++h) {
@@ -1968,10 +2109,18 @@ __global__ void __launch_bounds__(v4::kThreads, 1) k_svrg_chain_v4(EpochArgs a) 
       if (!XG && rw == 0 && lane == 0)
         mbar_expect_tx(&rbar[u & (kRecvSlots - 1)], static_cast<uint32_t>(G * NV * 8));
     };
-    double pre_r = 0.0;
+    // This lane's columns of TT_t and M_{t+1} and U_{t+1} are loaded into registers BEFORE the wait for the
+    // all-reduce (none depends on Â_t): after the wait the chain is peer sum -> one shared round trip for Â ->
+    // 16 FMAs -> coef to the rows, then pre_{t+1} from coef_t.  Same summation orders as before.
+    double pre_r = 0.0, TTc[B], Mn[B];
+    auto load_col = [&](const double* src, double (&dst)[B]) {
+#pragma unroll
+      for (int l = 0; l < B; ++l) dst[l] = src[l * B + j];
+    };
     if (nb > 0) {
       arm(0);
       mbar_wait(HALF ? &fullS[0] : &full[0], 0);
+      load_col(slab_tt(0), TTc);
       pre_r = slab_tt(0)[2 * B * B + j * PC + c];
     }
     int cs = 0;
@@ -1983,6 +2132,16 @@ __global__ void __launch_bounds__(v4::kThreads, 1) k_svrg_chain_v4(EpochArgs a) 
       const uint32_t nph = ns == 0 ? cph ^ 1u : cph;
       if (more) arm(t + 1);
       const int par = t & (kRecvSlots - 1);
+      double Un = 0.0;
+      if (more) {  // the slab of block t + 1 is in (its stage is filled before the rows' products of t + 1)
+        if constexpr (HALF)
+          mbar_wait(&fullS[(t + 1) % kSlabs], static_cast<uint32_t>(((t + 1) / kSlabs) & 1));
+        else
+          mbar_wait(&full[ns], nph);
+        const double* M = slab_tt(t + 1) + B * B;
+        load_col(M, Mn);
+        Un = M[B * B + j * PC + c];
+      }
       tick(6);
       if constexpr (XG) {
         // one poller per CTA (four pollers per CTA slowed the exchange: C5 coef wait 534 -> 879 cycles), then
@@ -2008,29 +2167,32 @@ __global__ void __launch_bounds__(v4::kThreads, 1) k_svrg_chain_v4(EpochArgs a) 
           }
         } else {
           const double* sl = recv + par * kMaxCluster * NV + e;
-#pragma unroll 4
-          for (int q = 0; q < G; q += 4) {
-            s0 += sl[q * NV];
-            s1 += sl[(q + 1) * NV];
-            s2 += sl[(q + 2) * NV];
-            s3 += sl[(q + 3) * NV];
-          }
+          double x[kMaxCluster];
+#pragma unroll
+          for (int q = 0; q < kMaxCluster; ++q) x[q] = q < G ? sl[q * NV] : 0.0;
+#pragma unroll
+          for (int q = 0; q < kMaxCluster; q += 4)
+            if (q < G) {
+              s0 += x[q];
+              s1 += x[q + 1];
+              s2 += x[q + 2];
+              s3 += x[q + 3];
+            }
         }
         sacc = (s0 + s1) + (s2 + s3);
       }
       aw[lane] = sacc;
       __syncwarp();  // Â[:, c] of both columns complete
-      const double* TT = slab_tt(t);
       double* cf = cfb + (t & 1) * B * CP;
       double cv;
       {
         double s0 = pre_r, s1 = 0.0, s2 = 0.0, s3 = 0.0;
 #pragma unroll
         for (int l = 0; l < B; l += 4) {
-          s0 = fma(TT[l * B + j], aw[hb + l], s0);
-          s1 = fma(TT[(l + 1) * B + j], aw[hb + l + 1], s1);
-          s2 = fma(TT[(l + 2) * B + j], aw[hb + l + 2], s2);
-          s3 = fma(TT[(l + 3) * B + j], aw[hb + l + 3], s3);
+          s0 = fma(TTc[l], aw[hb + l], s0);
+          s1 = fma(TTc[l + 1], aw[hb + l + 1], s1);
+          s2 = fma(TTc[l + 2], aw[hb + l + 2], s2);
+          s3 = fma(TTc[l + 3], aw[hb + l + 3], s3);
         }
         cv = (s0 + s1) + (s2 + s3);
         cf[j * CP + c] = cv;
@@ -2042,25 +2204,20 @@ __global__ void __launch_bounds__(v4::kThreads, 1) k_svrg_chain_v4(EpochArgs a) 
       tick(5);
       __syncwarp();  // every lane's Â reads done
       aw[lane] = cv;  // coef[:, c] for pre_{t+1}
-      if (lane == 0) mbar_arrive(HALF ? &emptyS[t % kSlabs] : &empty[cs]);  // TT_t: the reducers' last use
+      if (lane == 0) mbar_arrive(HALF ? &emptyS[t % kSlabs] : &empty[cs]);  // TT_t / M_{t+1} are in registers
       if (more) {  // pre_{t+1} = M_{t+1} coef_t + U_{t+1}
         __syncwarp();
-        if constexpr (HALF)
-          mbar_wait(&fullS[(t + 1) % kSlabs], static_cast<uint32_t>(((t + 1) / kSlabs) & 1));
-        else
-          mbar_wait(&full[ns], nph);
-        const double* M = slab_tt(t + 1) + B * B;
-        const double* Ub = M + B * B;
-        double s0 = Ub[j * PC + c], s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        double s0 = Un, s1 = 0.0, s2 = 0.0, s3 = 0.0;
 #pragma unroll
         for (int l = 0; l < B; l += 4) {
-          s0 = fma(M[l * B + j], aw[hb + l], s0);
-          s1 = fma(M[(l + 1) * B + j], aw[hb + l + 1], s1);
-          s2 = fma(M[(l + 2) * B + j], aw[hb + l + 2], s2);
-          s3 = fma(M[(l + 3) * B + j], aw[hb + l + 3], s3);
+          s0 = fma(Mn[l], aw[hb + l], s0);
+          s1 = fma(Mn[l + 1], aw[hb + l + 1], s1);
+          s2 = fma(Mn[l + 2], aw[hb + l + 2], s2);
+          s3 = fma(Mn[l + 3], aw[hb + l + 3], s3);
         }
         pre_r = (s0 + s1) + (s2 + s3);
-        __syncwarp();  // the tile is free for the next Â
+        load_col(slab_tt(t + 1), TTc);  // TT_{t+1}
+        __syncwarp();                   // the tile is free for the next Â
       }
       cs = ns;
       cph = nph;
@@ -2841,6 +2998,10 @@ void launch_chain_pc(const EpochArgs& a, const EpochConfig& cfg, cudaStream_t st
     GAPLRA_CUDA_CHECK(cudaMemsetAsync(a.xg_slot, 0, xg_slot_elems(cfg) * sizeof(double), st));
   }
   EpochArgs args = a;
+  static const int env_push = getenv("GAPLRA_PUSH_ASYNC") ? atoi(getenv("GAPLRA_PUSH_ASYNC")) : 1;
+  args.push_async = env_push;  // p = 1 DSMEM chains: st.async push (0: staged bulk copies)
+  static const int env_fr = getenv("GAPLRA_FAST_REDUCER") ? atoi(getenv("GAPLRA_FAST_REDUCER")) : 1;
+  args.fast_reducer = env_fr;  // p = 1 DSMEM chains: register-preloaded reducer (0: the generic reducer loop)
   args.ncl = std::max(1, cfg.nclusters);
   args.xg_ll = xg && !use_v4 ? xg_ll_mode() : 0;
   args.rows_per_cta = cfg.rows_per_cta;
@@ -2903,6 +3064,8 @@ void launch_svrg_epoch_dense(const EpochArgs& a, const EpochConfig& cfg, cudaStr
     default: launch_chain_pc<8>(a, cfg, st); break;
   }
 }
+
+void read_chain_hops(long long* out) { GAPLRA_CUDA_CHECK(cudaMemcpyFromSymbol(out, g_hop, sizeof(long long) * 64)); }
 
 void launch_svrg_epoch_sparse(const SparseEpochArgs& a, cudaStream_t st) {
   k_svrg_epoch_sparse<<<ceil_div(a.p, 32), 32, 0, st>>>(a);

@@ -31,6 +31,8 @@ struct EpochArgs {
   // XG chains (cfg.xg): the group's all-reduce goes through L2 instead of DSMEM
   double* xg_slot;   // [kXgSlots][groups][cluster][NV] partials
   unsigned* xg_count;  // [groups][kXgSlots] arrivals, zeroed before each launch
+  int fast_reducer;  // p = 1 DSMEM chain: TT / M columns preloaded in registers before the all-reduce wait
+  int push_async;    // p = 1 DSMEM chain: partials pushed with st.async from registers (0: staged bulk copies)
   int ncl;           // clusters the rows are split over (2: paired clusters, k_svrg_chain_v3 at p = 1)
   int xg_ll;         // p = 1 XG chains: partials as 16-byte flag-in-data cells (xg_slot zeroed before each launch)
 };
@@ -72,6 +74,7 @@ void launch_block_prep(const EpochArgs& a, const EpochConfig& cfg, cudaStream_t 
 void launch_block_u(const EpochArgs& a, const EpochConfig& cfg, cudaStream_t st);
 void launch_svrg_epoch_dense(const EpochArgs& a, const EpochConfig& cfg, cudaStream_t st);
 void launch_svrg_epoch_sparse(const SparseEpochArgs& a, cudaStream_t st);
+void read_chain_hops(long long* out);  // GAPLRA_EPOCH_TIMING: hop stamps of blocks 1000..1007 (p = 1 chain v3)
 // Block-parallel sparse epoch (sparse_epoch.cu): steps per block, scratch ints
 // (zeroed by the caller), and the launch (cooperative, one CTA per SM).
 bool sparse_blocked_supported(int p);
