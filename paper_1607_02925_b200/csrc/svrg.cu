@@ -549,6 +549,12 @@ __device__ __forceinline__ void st_async_f64(uint32_t remote_addr, double v, uin
                : "memory");
 }
 
+__device__ __forceinline__ void st_async_f64x2(uint32_t remote_addr, double v0, double v1, uint32_t remote_bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.b64 [%0], {%1, %2}, [%3];" ::"r"(remote_addr),
+               "l"(__double_as_longlong(v0)), "l"(__double_as_longlong(v1)), "r"(remote_bar)
+               : "memory");
+}
+
 __device__ __forceinline__ void consumers_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kChainThreads) : "memory"); }
 
 // Producer side of the chain kernels: block t's X slices (rows [r0, r0+rc) of
@@ -1837,7 +1843,10 @@ __global__ void __launch_bounds__(v3_block<RR>(PC), 1) k_svrg_chain_v3(EpochArgs
 // products' LDS.128 (rows 2tq, 2tq+1, slices permuted 0 2 1 3 4 6 5 7) are
 // bank-conflict free; coef is stored [slice][12].  Warps: 8 rows (ROWS / 8
 // rows each), 4 reducers (each owns two right-hand-side columns: lane = (column, step), so Â -> coef -> pre
-// of a column stay inside one warp and the reducers never wait for each other), 1 pusher (sums the row
+// of a column stay inside one warp and the reducers never wait for each other; measured and rejected: TT / M
+// columns preloaded into registers before the all-reduce wait — C2 14.9 vs 14.6 ms, the extra shared loads
+// queue behind the row warps' — and both matvecs as DMMAs in one reducer warp — C2 16.7 ms, C5 258 vs 238 ms,
+// one warp's dependent DMMA chains are slower than 128 lanes of FMAs), 1 pusher (sums the row
 // warps' partials, bulk-copies Â_{t+1} to the 16 peers), 2 producers.
 // ROWS = 256 (C2, C3) or 512 (C5: d = 8192 on 16-CTA clusters; a 512-row
 // stage is 71 KB, so the ring has 2 stages next to the 64 KB receive slots).
@@ -2058,7 +2067,7 @@ __global__ void __launch_bounds__(v4::kThreads, 1) k_svrg_chain_v4(EpochArgs a) 
         asm volatile("bar.sync 6, %0;" ::"n"(32 * (kRows + 1)) : "memory");
       else
         asm volatile("bar.sync 5, %0;" ::"n"(32 * (kRows + 1)) : "memory");
-      if (!XG && lane < G) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+      if (!XG && lane < G && a.push_async != 2) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
       __syncwarp();
       const double* rb = red + (u & 1) * kRows * NVR;
       double* ov = outv + (u & 1) * NV;
@@ -2075,6 +2084,28 @@ __global__ void __launch_bounds__(v4::kThreads, 1) k_svrg_chain_v4(EpochArgs a) 
         }
         __syncwarp();
         if (lane == 0) xg_publish(xg_cnt + u % kXgSlots);
+        continue;
+      }
+      if (a.push_async == 2) {  // GAPLRA_PUSH_ASYNC=2: measured not faster here (C2 15.5 vs 15.3 ms, C3 29.6 vs 29.0:
+                                // 16 KB per block to the peers is DSMEM-bandwidth-bound either way)
+        // straight from registers: lane sums entries (2 lane, 2 lane + 1) + 64 k and stores each pair into every
+        // peer's receive slot with one 16-byte st.async (it completes 16 bytes on the peer's barrier); no
+        // staging in shared memory, no async-proxy fence, no bulk-copy issue
+        const int par = u & (kRecvSlots - 1);
+        const uint32_t dst0 = smem_u32(recv + (par * kMaxCluster + g) * NV), bar0 = smem_u32(&rbar[par]);
+#pragma unroll
+        for (int k = 0; k < NV / 64; ++k) {
+          const int e = 64 * k + 2 * lane, er = (e >> 4) * RCP + (e & 15);
+          double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+          for (int w = 0; w < kRows; w += 2) {
+            const double2 x = *reinterpret_cast<const double2*>(rb + w * NVR + er);
+            const double2 y = *reinterpret_cast<const double2*>(rb + (w + 1) * NVR + er);
+            s0 += x.x + y.x;
+            s1 += x.y + y.y;
+          }
+          for (int q = 0; q < G; ++q) st_async_f64x2(mapa(dst0 + e * 8u, q), s0, s1, mapa(bar0, q));
+        }
         continue;
       }
 #pragma unroll
@@ -2109,18 +2140,10 @@ __global__ void __launch_bounds__(v4::kThreads, 1) k_svrg_chain_v4(EpochArgs a) 
       if (!XG && rw == 0 && lane == 0)
         mbar_expect_tx(&rbar[u & (kRecvSlots - 1)], static_cast<uint32_t>(G * NV * 8));
     };
-    // This lane's columns of TT_t and M_{t+1} and U_{t+1} are loaded into registers BEFORE the wait for the
-    // all-reduce (none depends on Â_t): after the wait the chain is peer sum -> one shared round trip for Â ->
-    // 16 FMAs -> coef to the rows, then pre_{t+1} from coef_t.  Same summation orders as before.
-    double pre_r = 0.0, TTc[B], Mn[B];
-    auto load_col = [&](const double* src, double (&dst)[B]) {
-#pragma unroll
-      for (int l = 0; l < B; ++l) dst[l] = src[l * B + j];
-    };
+    double pre_r = 0.0;
     if (nb > 0) {
       arm(0);
       mbar_wait(HALF ? &fullS[0] : &full[0], 0);
-      load_col(slab_tt(0), TTc);
       pre_r = slab_tt(0)[2 * B * B + j * PC + c];
     }
     int cs = 0;
@@ -2132,16 +2155,6 @@ __global__ void __launch_bounds__(v4::kThreads, 1) k_svrg_chain_v4(EpochArgs a) 
       const uint32_t nph = ns == 0 ? cph ^ 1u : cph;
       if (more) arm(t + 1);
       const int par = t & (kRecvSlots - 1);
-      double Un = 0.0;
-      if (more) {  // the slab of block t + 1 is in (its stage is filled before the rows' products of t + 1)
-        if constexpr (HALF)
-          mbar_wait(&fullS[(t + 1) % kSlabs], static_cast<uint32_t>(((t + 1) / kSlabs) & 1));
-        else
-          mbar_wait(&full[ns], nph);
-        const double* M = slab_tt(t + 1) + B * B;
-        load_col(M, Mn);
-        Un = M[B * B + j * PC + c];
-      }
       tick(6);
       if constexpr (XG) {
         // one poller per CTA (four pollers per CTA slowed the exchange: C5 coef wait 534 -> 879 cycles), then
@@ -2167,32 +2180,29 @@ __global__ void __launch_bounds__(v4::kThreads, 1) k_svrg_chain_v4(EpochArgs a) 
           }
         } else {
           const double* sl = recv + par * kMaxCluster * NV + e;
-          double x[kMaxCluster];
-#pragma unroll
-          for (int q = 0; q < kMaxCluster; ++q) x[q] = q < G ? sl[q * NV] : 0.0;
-#pragma unroll
-          for (int q = 0; q < kMaxCluster; q += 4)
-            if (q < G) {
-              s0 += x[q];
-              s1 += x[q + 1];
-              s2 += x[q + 2];
-              s3 += x[q + 3];
-            }
+#pragma unroll 4
+          for (int q = 0; q < G; q += 4) {
+            s0 += sl[q * NV];
+            s1 += sl[(q + 1) * NV];
+            s2 += sl[(q + 2) * NV];
+            s3 += sl[(q + 3) * NV];
+          }
         }
         sacc = (s0 + s1) + (s2 + s3);
       }
       aw[lane] = sacc;
       __syncwarp();  // Â[:, c] of both columns complete
+      const double* TT = slab_tt(t);
       double* cf = cfb + (t & 1) * B * CP;
       double cv;
       {
         double s0 = pre_r, s1 = 0.0, s2 = 0.0, s3 = 0.0;
 #pragma unroll
         for (int l = 0; l < B; l += 4) {
-          s0 = fma(TTc[l], aw[hb + l], s0);
-          s1 = fma(TTc[l + 1], aw[hb + l + 1], s1);
-          s2 = fma(TTc[l + 2], aw[hb + l + 2], s2);
-          s3 = fma(TTc[l + 3], aw[hb + l + 3], s3);
+          s0 = fma(TT[l * B + j], aw[hb + l], s0);
+          s1 = fma(TT[(l + 1) * B + j], aw[hb + l + 1], s1);
+          s2 = fma(TT[(l + 2) * B + j], aw[hb + l + 2], s2);
+          s3 = fma(TT[(l + 3) * B + j], aw[hb + l + 3], s3);
         }
         cv = (s0 + s1) + (s2 + s3);
         cf[j * CP + c] = cv;
@@ -2204,20 +2214,25 @@ __global__ void __launch_bounds__(v4::kThreads, 1) k_svrg_chain_v4(EpochArgs a) 
       tick(5);
       __syncwarp();  // every lane's Â reads done
       aw[lane] = cv;  // coef[:, c] for pre_{t+1}
-      if (lane == 0) mbar_arrive(HALF ? &emptyS[t % kSlabs] : &empty[cs]);  // TT_t / M_{t+1} are in registers
+      if (lane == 0) mbar_arrive(HALF ? &emptyS[t % kSlabs] : &empty[cs]);  // TT_t: the reducers' last use
       if (more) {  // pre_{t+1} = M_{t+1} coef_t + U_{t+1}
         __syncwarp();
-        double s0 = Un, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        if constexpr (HALF)
+          mbar_wait(&fullS[(t + 1) % kSlabs], static_cast<uint32_t>(((t + 1) / kSlabs) & 1));
+        else
+          mbar_wait(&full[ns], nph);
+        const double* M = slab_tt(t + 1) + B * B;
+        const double* Ub = M + B * B;
+        double s0 = Ub[j * PC + c], s1 = 0.0, s2 = 0.0, s3 = 0.0;
 #pragma unroll
         for (int l = 0; l < B; l += 4) {
-          s0 = fma(Mn[l], aw[hb + l], s0);
-          s1 = fma(Mn[l + 1], aw[hb + l + 1], s1);
-          s2 = fma(Mn[l + 2], aw[hb + l + 2], s2);
-          s3 = fma(Mn[l + 3], aw[hb + l + 3], s3);
+          s0 = fma(M[l * B + j], aw[hb + l], s0);
+          s1 = fma(M[(l + 1) * B + j], aw[hb + l + 1], s1);
+          s2 = fma(M[(l + 2) * B + j], aw[hb + l + 2], s2);
+          s3 = fma(M[(l + 3) * B + j], aw[hb + l + 3], s3);
         }
         pre_r = (s0 + s1) + (s2 + s3);
-        load_col(slab_tt(t + 1), TTc);  // TT_{t+1}
-        __syncwarp();                   // the tile is free for the next Â
+        __syncwarp();  // the tile is free for the next Â
       }
       cs = ns;
       cph = nph;
