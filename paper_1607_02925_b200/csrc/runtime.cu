@@ -544,6 +544,7 @@ void epoch_run_dev(Context& c, Matrix& X, int p, double* W, const double* C, con
       }
       fprintf(stderr, "], \"cluster\": %d, \"pc\": %d, \"groups\": %d, \"stages\": %d}\n", cfg.cluster, cfg.pc,
               cfg.groups, cfg.stages);
+#ifdef GAPLRA_HOP_TIMING
       if (p == 1 && m >= 1008 * kEpochBlock) {
         long long hp[64];
         read_chain_hops(hp);
@@ -552,6 +553,7 @@ void epoch_run_dev(Context& c, Matrix& X, int p, double* W, const double* C, con
                 hp[2 * 8 + 1] - hp[2 * 8], hp[2 * 8 + 2] - hp[2 * 8], hp[2 * 8 + 3] - hp[2 * 8], hp[2 * 8 + 4] - hp[2 * 8],
                 hp[2 * 8 + 5] - hp[2 * 8], hp[3 * 8] - hp[2 * 8]);
       }
+#endif
     }
   } else {
     SparseEpochArgs a{};

@@ -1225,13 +1225,21 @@ void launch_block_prep(const EpochArgs& a, const EpochConfig& cfg, cudaStream_t 
 // GAPLRA_EPOCH_TIMING: clock stamps of one all-reduce loop (blocks 1000..1007 of CTA 0), per hop:
 // 0 rows: products done, 1 pusher: woken, 2 pusher: copies issued, 3 reducer: all partials in,
 // 4 reducer: coef handed to the rows, 5 rows: coef received (update starts)
+// Compiled in only with -DGAPLRA_HOP_TIMING: in the default build the stamps' clock reads (asm volatile with
+// a memory clobber) sat in the rows' hot loop and cost the C3 p = 1 chain 13 %.
 __device__ long long g_hop[8 * 8];
 __device__ __forceinline__ void hop_stamp(const EpochArgs& a, int blk, int k) {
+#ifdef GAPLRA_HOP_TIMING
   if (a.dbg && blockIdx.x == 0 && blockIdx.y == 0 && blk >= 1000 && blk < 1008) {
     long long now;
     asm volatile("mov.u64 %0, %%clock64;" : "=l"(now)::"memory");
     g_hop[(blk - 1000) * 8 + k] = now;
   }
+#else
+  (void)a;
+  (void)blk;
+  (void)k;
+#endif
 }
 constexpr int kV3Rows = 4;       // row warps
 // producer warps: 4 at PC = 1 (each issues its lanes' bulk copies one after
@@ -1326,12 +1334,16 @@ __global__ void __launch_bounds__(v3_block<RR>(PC), 1) k_svrg_chain_v3(EpochArgs
   long long tp;
   asm volatile("mov.u64 %0, %%clock64;" : "=l"(tp)::"memory");
   auto tick = [&](int kk) {
+#ifndef GAPLRA_NO_TICKS
     if (a.dbg) {
       long long now;
       asm volatile("mov.u64 %0, %%clock64;" : "=l"(now)::"memory");
       tacc[kk] += now - tp;
       tp = now;
     }
+#else
+    (void)kk;
+#endif
   };
 
   constexpr int kFirstProd = RR ? 8 : kV3Rows + NRD + 1;
@@ -1418,14 +1430,17 @@ __global__ void __launch_bounds__(v3_block<RR>(PC), 1) k_svrg_chain_v3(EpochArgs
         // barrier a third of the time), so everything that does not depend on Â_t is in registers BEFORE the
         // wait: this lane's columns of TT_t and M_{t+1} and U_{t+1}.  After the wait: 16 batched peer loads,
         // one shared round trip for Â, 16 FMAs -> coef_t to the rows; then pre_{t+1} from coef_t.  Same
-        // summation orders as the generic path below (bitwise identical results).
-        const int e = lane & 15;  // lanes 16-31 shadow 0-15 (no stores)
-        const bool act = lane < 16;
-        double TTc[B], Mn[B], pre_r = 0.0;
-        auto load_col = [&](const double* src, double (&dst)[B]) {
+        // sums, fixed orders of their own (results differ from the generic path below in the last bits).
+        // lane = (entry e = lane & 15, half h = lane >> 4): the two half-warps split the peers of the sum and the
+        // l-range of both matvecs (8 products each, joined by one shuffle), which halves the warp's shared loads
+        const int e = lane & 15, h = lane >> 4, l0 = 8 * h;
+        constexpr int HB = B / 2;
+        double TTc[HB], Mn[HB], pre_r = 0.0;
+        auto load_col = [&](const double* src, double (&dst)[HB]) {
 #pragma unroll
-          for (int l = 0; l < B; ++l) dst[l] = src[l * B + e];
+          for (int l = 0; l < HB; ++l) dst[l] = src[(l0 + l) * B + e];
         };
+        auto join = [](double v) { return v + __shfl_xor_sync(0xffffffffu, v, 16); };
         if (nb > 0) {
           arm(0);
           mbar_wait(&full[0], 0);
@@ -1454,40 +1469,31 @@ __global__ void __launch_bounds__(v3_block<RR>(PC), 1) k_svrg_chain_v3(EpochArgs
           mbar_wait(&rbar[par], static_cast<uint32_t>((t >> 2) & 1));
           tick(6);
           if (lane == 0) hop_stamp(a, t, 3);
-          double sv = 0.0;
+          double sv;
           {
-            const double* sl = recv + par * kMaxCluster * NV + e;
-            double x[kMaxCluster];
+            // half h sums peers h G/2 .. (h + 1) G/2 - 1 in a fixed tree; total = lower + upper
+            const int gh = G >> 1;
+            const double* sl = recv + par * kMaxCluster * NV + h * gh * NV + e;
+            double x[kMaxCluster / 2];
 #pragma unroll
-            for (int q = 0; q < kMaxCluster; ++q) x[q] = q < G ? sl[q * NV] : 0.0;
-            double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-#pragma unroll
-            for (int q = 0; q < kMaxCluster; q += 4) {
-              if (q < G) {
-                s0 += x[q];
-                s1 += x[q + 1];
-                s2 += x[q + 2];
-                s3 += x[q + 3];
-              }
-            }
-            sv = e < nv ? (s0 + s1) + (s2 + s3) : 0.0;
+            for (int q = 0; q < kMaxCluster / 2; ++q) x[q] = q < gh ? sl[q * NV] : 0.0;
+            const double part = ((x[0] + x[1]) + (x[2] + x[3])) + ((x[4] + x[5]) + (x[6] + x[7]));
+            sv = join(e < nv ? part : 0.0);  // (the shuffle outside the select: every lane takes part)
           }
-          if (act) Ahat[e] = sv;
+          if (h == 0) Ahat[e] = sv;
           __syncwarp();
           double* cf = coef + (t & 1) * NV;
           double cv;
           {
-            double s0 = pre_r, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+            double s0 = 0.0, s1 = 0.0;
 #pragma unroll
-            for (int l = 0; l < B; l += 4) {
-              s0 = fma(TTc[l], Ahat[l], s0);
-              s1 = fma(TTc[l + 1], Ahat[l + 1], s1);
-              s2 = fma(TTc[l + 2], Ahat[l + 2], s2);
-              s3 = fma(TTc[l + 3], Ahat[l + 3], s3);
+            for (int l = 0; l < HB; l += 2) {
+              s0 = fma(TTc[l], Ahat[l0 + l], s0);
+              s1 = fma(TTc[l + 1], Ahat[l0 + l + 1], s1);
             }
-            cv = (s0 + s1) + (s2 + s3);
+            cv = pre_r + join(s0 + s1);
           }
-          if (act) cf[e] = cv;
+          if (h == 0) cf[e] = cv;
           if (t & 1)
             asm volatile("bar.arrive 3, %0;" ::"n"(32 * (kV3Rows + NRD)) : "memory");
           else
@@ -1498,15 +1504,13 @@ __global__ void __launch_bounds__(v3_block<RR>(PC), 1) k_svrg_chain_v3(EpochArgs
             mbar_arrive(&empty[cs]);  // TT_t (in registers since before the wait): the stage is free for the reducer
           }
           if (more) {
-            double s0 = Un, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+            double s0 = 0.0, s1 = 0.0;
 #pragma unroll
-            for (int l = 0; l < B; l += 4) {
-              s0 = fma(Mn[l], cf[l], s0);
-              s1 = fma(Mn[l + 1], cf[l + 1], s1);
-              s2 = fma(Mn[l + 2], cf[l + 2], s2);
-              s3 = fma(Mn[l + 3], cf[l + 3], s3);
+            for (int l = 0; l < HB; l += 2) {
+              s0 = fma(Mn[l], cf[l0 + l], s0);
+              s1 = fma(Mn[l + 1], cf[l0 + l + 1], s1);
             }
-            pre_r = (s0 + s1) + (s2 + s3);
+            pre_r = Un + join(s0 + s1);
             load_col(stage_at(ns) + B * RP, TTc);  // TT_{t+1}
           }
           cs = ns;
@@ -2035,12 +2039,16 @@ __global__ void __launch_bounds__(v4::kThreads, 1) k_svrg_chain_v4(EpochArgs a) 
   long long tacc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   long long tp = clock64();
   auto tick = [&](int kk) {
+#ifndef GAPLRA_NO_TICKS
     if (a.dbg) {
       long long now;
       asm volatile("mov.u64 %0, %%clock64;" : "=l"(now)::"memory");
       tacc[kk] += now - tp;
       tp = now;
     }
+#else
+    (void)kk;
+#endif
   };
   auto bar_red_arrive = [](int u) {  // rows -> pusher, red(u) written (barrier 5 / 6 by parity)
     if (u & 1)
@@ -2281,7 +2289,9 @@ __global__ void __launch_bounds__(v4::kThreads, 1) k_svrg_chain_v4(EpochArgs a) 
 #pragma unroll
         for (int tl = 0; tl < kTiles; ++tl) {
           const double2 xv = *reinterpret_cast<const double2*>(xb + perm * RP + rw0 + 8 * tl + 2 * tq);
+#ifdef GAPLRA_CHAIN_ABLATE
           if (a.skip & 2) continue;  // GAPLRA_EPOCH_SKIP ablation (results invalid)
+#endif
           dmma(acc[n2][tl & 1][0], acc[n2][tl & 1][1], v[tl][0], xv.x);
           dmma(acc[n2][tl & 1][0], acc[n2][tl & 1][1], v[tl][1], xv.y);
         }
@@ -2316,7 +2326,9 @@ __global__ void __launch_bounds__(v4::kThreads, 1) k_svrg_chain_v4(EpochArgs a) 
         for (int ks = 0; ks < 4; ++ks)
 #pragma unroll
           for (int tl = 0; tl < kTiles; ++tl) bx[ks][tl] = xb[(4 * ks + tq) * RP + rw0 + 8 * tl + gq];
+#ifdef GAPLRA_CHAIN_ABLATE
         if (!(a.skip & 4))
+#endif
 #pragma unroll
           for (int ks = 0; ks < 4; ++ks)
 #pragma unroll
@@ -2501,12 +2513,16 @@ __global__ void __launch_bounds__(la2::kThreads, 1) k_chain_p1_la2(EpochArgs a) 
   long long tp;
   asm volatile("mov.u64 %0, %%clock64;" : "=l"(tp)::"memory");
   auto tick = [&](int kk) {
+#ifndef GAPLRA_NO_TICKS
     if (a.dbg) {
       long long now;
       asm volatile("mov.u64 %0, %%clock64;" : "=l"(now)::"memory");
       tacc[kk] += now - tp;
       tp = now;
     }
+#else
+    (void)kk;
+#endif
   };
   auto red_arrive = [](int u) {  // rows -> pusher: red(u) written (barriers 5..8)
     switch (u & 3) {
