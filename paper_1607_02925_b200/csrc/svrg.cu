@@ -1334,7 +1334,7 @@ __global__ void __launch_bounds__(v3_block<RR>(PC), 1) k_svrg_chain_v3(EpochArgs
   long long tp;
   asm volatile("mov.u64 %0, %%clock64;" : "=l"(tp)::"memory");
   auto tick = [&](int kk) {
-#ifndef GAPLRA_NO_TICKS
+#ifdef GAPLRA_V3_TICKS  // the p <= 3 chain's phase ticks: off by default (3 % on the p = 1 chain)
     if (a.dbg) {
       long long now;
       asm volatile("mov.u64 %0, %%clock64;" : "=l"(now)::"memory");
