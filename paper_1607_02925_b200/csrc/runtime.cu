@@ -221,6 +221,11 @@ struct Context {
   gaplra_profile prof{};
   std::vector<ProfPending> pending;
   std::vector<cudaEvent_t> spare;
+  cudaEvent_t fence_ev[64] = {};
+  cudaEvent_t fence_event(int i) {
+    if (!fence_ev[i]) GAPLRA_CUDA_CHECK(cudaEventCreate(&fence_ev[i]));
+    return fence_ev[i];
+  }
   cudaEvent_t new_event() {
     if (!spare.empty()) {
       cudaEvent_t e = spare.back();
@@ -281,11 +286,21 @@ struct Prof {
   cudaStream_t s;
   Prof(Context& cc, int k, double by, double fl, cudaStream_t st = nullptr)
       : c(cc), cls(k), bytes(by), flops(fl), s(st ? st : cc.st) {
-    if (!c.profiling) return;
+    if (!c.profiling) {
+      if (fence_mask() >> cls & 1) cudaEventRecord(c.fence_event(2 * cls), s);
+      return;
+    }
     a = c.new_event();
     cudaEventRecord(a, s);
   }
+  // GAPLRA_FENCE_CLASSES=mask (experiment): timing events around the kernels of the given profile classes
+  // even with profiling off (an event record keeps the neighbouring kernels of a stream from overlapping)
+  static unsigned fence_mask() {
+    static const unsigned m = getenv("GAPLRA_FENCE_CLASSES") ? static_cast<unsigned>(strtoul(getenv("GAPLRA_FENCE_CLASSES"), nullptr, 0)) : 0u;
+    return m;
+  }
   ~Prof() {
+    if (!c.profiling && (fence_mask() >> cls & 1)) cudaEventRecord(c.fence_event(2 * cls + 1), s);
     if (!c.profiling) return;
     cudaEvent_t b = c.new_event();
     cudaEventRecord(b, s);
@@ -669,11 +684,20 @@ GraphEpochs run_epochs_graph(Context& c, Matrix& X, int p, double* W, double* Z,
     GAPLRA_CUDA_CHECK(cudaStreamWaitEvent(aux, c.u_done, 0));
     const EpochPre nxt = epoch_pre_dev(c, X, p, prm.eta, lambda, 0, prm.m, 0, aux, dseed);
     GAPLRA_CUDA_CHECK(cudaEventRecord(c.pre_done[0], aux));
-    GAPLRA_CUDA_CHECK(cudaStreamWaitEvent(c.st, c.pre_done[0], 0));
-    launch_copy(nxt.idx, cur.idx, static_cast<size_t>(prm.m) * sizeof(int32_t), c.st);
-    if (nxt.slab) launch_copy(nxt.slab, cur.slab, slab_elems * sizeof(double), c.st);
+    // The join with the side stream comes AFTER the anchor's gram pass, as in the host loop (there the main
+    // stream waits for the prep only before the next H pass): at C5 the prep on the 20 SMs the chain leaves
+    // takes about as long as the chain, and joining before the gram pass put it on the critical path
+    // (step 9.39 s in the graph against 8.69 s in the host loop).  GAPLRA_GRAPH_JOIN=early restores that.
+    static const bool join_early = getenv("GAPLRA_GRAPH_JOIN") && std::string(getenv("GAPLRA_GRAPH_JOIN")) == "early";
+    auto join_and_rotate = [&]() {
+      GAPLRA_CUDA_CHECK(cudaStreamWaitEvent(c.st, c.pre_done[0], 0));
+      launch_copy(nxt.idx, cur.idx, static_cast<size_t>(prm.m) * sizeof(int32_t), c.st);
+      if (nxt.slab) launch_copy(nxt.slab, cur.slab, slab_elems * sizeof(double), c.st);
+    };
+    if (join_early) join_and_rotate();
     gram_block_dev(c, X, p, W, ld, Z, ld, Y, ld);
     launch_anchor(W, Z, B, ld, static_cast<int>(dp), p, lambda, prm.eta, C, part, bn, nullptr, res, c.st);
+    if (!join_early) join_and_rotate();
     launch_epoch_control(res, ctl, hist, hist_cap, prm.tol, prm.slack, prm.cap, prm.root, solve_id, cond, c.st);
   } catch (...) {
     cudaGraph_t tmp = nullptr;
@@ -779,7 +803,12 @@ SvrgResult svrg_solve_dev(Context& c, Matrix& X, double lambda, int p, const dou
     // from epoch 1 on, the loop runs on the device (GAPLRA_GRAPH=0: host loop)
     static const bool graph_env = !(getenv("GAPLRA_GRAPH") && atoi(getenv("GAPLRA_GRAPH")) == 0);
     static const bool timing_env = getenv("GAPLRA_EPOCH_TIMING") != nullptr;
-    if (e == 1 && have_next && side && overlap_mode == 2 && graph_env && !timing_env && !c.profiling) {
+    // Epochs of >= ~1 TFLOP stay on the host loop: one scalar read per 0.3 s epoch is free, and at C5 p = 64
+    // (prep on the SMs the chain leaves ~ as long as the chain) the graph ran the step 8 % slower
+    // (9.39 vs 8.69 s).  GAPLRA_GRAPH_MAX_TFLOP moves the threshold.
+    static const double graph_max_tflop = getenv("GAPLRA_GRAPH_MAX_TFLOP") ? atof(getenv("GAPLRA_GRAPH_MAX_TFLOP")) : 1.0;
+    const bool small_epochs = 4.0 * static_cast<double>(X.d) * p * static_cast<double>(prm.m) < graph_max_tflop * 1e12;
+    if (e == 1 && have_next && side && overlap_mode == 2 && graph_env && small_epochs && !timing_env && !c.profiling) {
       GAPLRA_CUDA_CHECK(cudaStreamWaitEvent(c.st, c.pre_done[1], 0));
       const GraphEpochs ge = run_epochs_graph(c, X, p, W, Z, C, Y, B, part, bn, res, lambda, prm, solve_id, next, best);
       const int runs = ge.ctl.e - 1;  // epochs 1 .. e-1 ran in the graph, each followed by one anchor
