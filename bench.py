@@ -320,8 +320,9 @@ def run_ours(args, rank, world, local_rank):
 
     for _ in range(args.warmup):
         e2e_step()
-    # the timed steps run the production path (device-resident epoch loops,
-    # per-kernel profiling off); one extra profiled step afterwards gives the
+    # the timed steps run the production path (per-kernel profiling off; the
+    # epoch loop is host-driven for >= 1 TFLOP epochs, device-resident below);
+    # one extra profiled step afterwards gives the
     # per-kernel-class rooflines (same kernels, host-driven epoch loop)
     ctx.enable_profiling(False)
     launches0 = lib.gaplra_launch_count()
@@ -377,8 +378,10 @@ def run_ours(args, rank, world, local_rank):
         "step": {"lambda": lam, "lambda1_hint": hint, "outer_iterations": last.outer_iterations,
                  "ledger": step_ledger, "ms_phases": last.ms,
                  "profiled_step_ms": prof_res.ms["total"],
-                 "note": "value/e2e: device-resident epoch loops (CUDA-graph WHILE node per solve); rooflines: one "
-                         "extra untimed step with per-kernel CUDA events (host-driven loop, same kernels)"},
+                 "note": "value/e2e: the production path, no per-kernel events (epoch loop host-driven when an "
+                         "epoch is >= 1 TFLOP, as at C5 p = 64; a device-resident CUDA-graph WHILE loop below "
+                         "that); rooflines: one extra untimed step with per-kernel CUDA events (host-driven "
+                         "loop, same kernels)"},
         "gen_s": gen_s,
     }
     print(json.dumps(line), flush=True)
