@@ -516,7 +516,6 @@ struct NumArgs {
   double* dcb;    // [2][bs][p] x_jᵀC of the block (parity), filled one block ahead by the CTAs not solving
   double* yb;     // [2][bs][p] Y rows of the block's columns
   int scap;       // pairs that fit the shared tile
-  int skip;       // GAPLRA_SPARSE_SKIP: timing ablation mask (results invalid)
   const double* rp;  // [bs + 1] ρ^j
   const double* gm;  // [bs + 1] γ_j = Σ_{k<j} ρ^k
   unsigned long long* dbg;
@@ -553,7 +552,6 @@ __global__ void __launch_bounds__(kNumThreads, 1) k_sparse_epoch_levels(NumArgs 
   const double kappa = a.eta_n / a.rho;
   double al = 1.0, be = 0.0;
   unsigned long long tph[8] = {0, 0, 0, 0, 0, 0, 0, 0}, tlast = gtimer();
-  long long lacc[3] = {0, 0, 0};
   auto mark = [&](int k) {
     if (A.dbg && blockIdx.x == 0 && tid == 0) {
       const unsigned long long now = gtimer();
@@ -797,9 +795,6 @@ __global__ void __launch_bounds__(kNumThreads, 1) k_sparse_epoch_levels(NumArgs 
   if (A.dbg && blockIdx.x == 0 && tid == 0)
   {
     for (int k = 0; k < 8; ++k) A.dbg[k] = tph[k];
-    A.dbg[6] = lacc[0];
-    A.dbg[7] = lacc[1];
-    A.dbg[2 + 8] = lacc[2];
   }
   // W = α Ŵ + β C
   for (int64_t e = static_cast<int64_t>(blockIdx.x) * kNumThreads + tid; e < static_cast<int64_t>(a.d) * p;
@@ -931,8 +926,6 @@ void launch_svrg_epoch_sparse_levels(const SparseEpochArgs& a, const SparseLevel
   N.dcb = reinterpret_cast<double*>(base + P.off_dcb);
   N.yb = reinterpret_cast<double*>(base + P.off_yb);
   N.scap = P.scap;
-  static const int env_skip = getenv("GAPLRA_SPARSE_SKIP") ? atoi(getenv("GAPLRA_SPARSE_SKIP")) : 0;
-  N.skip = env_skip;
   double* rho_tab = reinterpret_cast<double*>(base + P.off_rho);
   k_rho_table<<<1, 1, 0, st>>>(rho_tab, rho_tab + P.bs + 2, P.bs, a.rho);
   GAPLRA_LAUNCH_CHECK();
@@ -978,10 +971,10 @@ void launch_svrg_epoch_sparse_levels(const SparseEpochArgs& a, const SparseLevel
     const double nbk = static_cast<double>(S.nblk);
     fprintf(stderr,
             "{\"sparse_levels\": {\"bs\": %d, \"blocks\": %.0f, \"symbolic_ms\": %.3f, \"numeric_ms\": %.3f, "
-            "\"us_per_block\": [%.2f, %.2f, %.2f], \"solve_us\": [%.2f, %.2f, %.2f], \"level_cycles_per_block\": [%.0f, %.0f, %.0f], \"pairs_mean\": %.0f, \"pairs_max\": %d, \"scap\": %d, \"pcap\": %d, "
+            "\"us_per_block\": [%.2f, %.2f, %.2f], \"solve_us\": [%.2f, %.2f, %.2f], \"pairs_mean\": %.0f, \"pairs_max\": %d, \"scap\": %d, \"pcap\": %d, "
             "\"levels_mean\": %.1f, \"levels_max\": %d, \"rows_mean\": %.0f, \"overflow_blocks\": %d}}\n",
             bs, nbk, ms_sym, ms_num, h[0] / nbk / 1e3, (h[1] + h[3] + h[4] + h[5]) / nbk / 1e3, h[2] / nbk / 1e3, h[3] / nbk / 1e3, h[4] / nbk / 1e3,
-            h[5] / nbk / 1e3, h[6] / nbk, h[7] / nbk, h[10] / nbk, sp / nbk, maxp, P.scap,
+            h[5] / nbk / 1e3, sp / nbk, maxp, P.scap,
             P.pcap, sl / nbk, maxl, sr / nbk, ovf);
     cudaEventDestroy(ev0);
     cudaEventDestroy(ev1);
