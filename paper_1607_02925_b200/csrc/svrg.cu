@@ -243,13 +243,11 @@ template <int LA>
 __host__ __device__ constexpr int prep_cols() { return 16 * (LA + 1); }
 template <int LA>
 __host__ __device__ constexpr size_t prep_ring_bytes() { return size_t(kPrepStages) * prep_cols<LA>() * kPrepPitch * sizeof(double); }
-constexpr size_t kPrepRingBytes = prep_ring_bytes<1>();
 // cp.async.bulk takes warp-uniform operands, so one warp issues its lanes'
 // copies one after another (~50 cycles each): 4 producer warps, one per SM
 // sub-partition, 8 columns each.
 constexpr int kPrepProducers = 4;
 constexpr int kPrepCtas = 2;  // CTAs per SM: one's serial tail overlaps the other's Gram loop
-constexpr int kPrepColsPerProducer = kPrepCols / kPrepProducers;
 // the consumers' per-warp partial Grams live after the ring (dynamic smem)
 template <int LA>
 __host__ __device__ constexpr size_t prep_red_bytes() {
@@ -1989,7 +1987,7 @@ __global__ void __launch_bounds__(v4::kThreads, 1) k_svrg_chain_v4(EpochArgs a) 
   double* outv = sm + L.off_outv;  // [2][NV]
   double* cfb = sm + L.off_cf;     // [2][B][CP]
   double* Ahat = sm + L.off_ahat;  // [NV]
-  double* pre = sm + L.off_pre;    // [NV]
+  // (sm + L.off_pre: a second NV-entry tile, unused by the column-owner reducers)
   uint64_t* full = reinterpret_cast<uint64_t*>(sm + L.off_bar);  // [S <= 4]
   uint64_t* empty = full + 4;                                     // [S]
   uint64_t* rbar = full + 8;                                      // [kRecvSlots]
@@ -3024,9 +3022,13 @@ void launch_chain_pc(const EpochArgs& a, const EpochConfig& cfg, cudaStream_t st
     if (xg_ll_mode() && !use_v4) GAPLRA_CUDA_CHECK(cudaMemsetAsync(a.xg_slot, 0, xg_slot_elems(cfg) * sizeof(double), st));
   }
   if (cfg.nclusters > 1) {
-    if (!a.xg_slot) throw Error(kContractViolation, "epoch: paired clusters without exchange buffers");
-    if (PC != 1 || use_v4 || xg) throw Error(kContractViolation, "epoch: paired clusters are a p = 1 layout");
-    GAPLRA_CUDA_CHECK(cudaMemsetAsync(a.xg_slot, 0, xg_slot_elems(cfg) * sizeof(double), st));
+    if constexpr (PC == 1) {
+      if (!a.xg_slot) throw Error(kContractViolation, "epoch: paired clusters without exchange buffers");
+      if (use_v4 || xg) throw Error(kContractViolation, "epoch: paired clusters are a p = 1 layout");
+      GAPLRA_CUDA_CHECK(cudaMemsetAsync(a.xg_slot, 0, xg_slot_elems(cfg) * sizeof(double), st));
+    } else {
+      throw Error(kContractViolation, "epoch: paired clusters are a p = 1 layout");
+    }
   }
   EpochArgs args = a;
   static const int env_push = getenv("GAPLRA_PUSH_ASYNC") ? atoi(getenv("GAPLRA_PUSH_ASYNC")) : 1;
