@@ -236,7 +236,6 @@ __device__ __forceinline__ void mat_mul_bb(const double (*A)[B + 1], const doubl
 constexpr int kPrepKC = 64;
 constexpr int kPrepPitch = kPrepKC + 4;
 constexpr int kPrepStages = 4;
-constexpr int kPrepCols = 32;
 // LA = 2 (two-block lookahead chain): a third group of 16 columns, block t−2,
 // for the second cross-Gram Kxx_t = X_{B_t}ᵀ X_{B_{t−2}}
 template <int LA>
