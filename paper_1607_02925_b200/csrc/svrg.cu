@@ -2077,7 +2077,21 @@ __global__ void __launch_bounds__(v4::kThreads, 1) k_svrg_chain_v4(EpochArgs a) 
       const double* rb = red + (u & 1) * kRows * NVR;
       double* ov = outv + (u & 1) * NV;
       // exchanged vector: entry en = c * 16 + j (column-major), read from the padded red [c][RCP]
-      if constexpr (XG) {  // partial -> L2 slot, then one release-increment
+      if constexpr (XG) {
+        if (a.xg_ll == 2) {  // GAPLRA_V4_LL=1: flag-in-data cells, no fence and no counter
+          uint4* cells = reinterpret_cast<uint4*>(a.xg_slot) + static_cast<size_t>(blockIdx.y) * kXgSlots * G * NV +
+                         (static_cast<size_t>(u % kXgSlots) * G + g) * NV;
+#pragma unroll
+          for (int q = 0; q < NV / 32; ++q) {
+            const int e = q * 32 + lane, er = (e >> 4) * RCP + (e & 15);
+            double sum = 0.0;
+#pragma unroll
+            for (int w = 0; w < kRows; w += 2) sum += rb[w * NVR + er] + rb[(w + 1) * NVR + er];
+            ll_store(cells + e, sum, static_cast<uint32_t>(u / kXgSlots + 1));
+          }
+          continue;
+        }
+        // partial -> L2 slot, then one release-increment
         double* dst = xg_slots + (static_cast<size_t>(u % kXgSlots) * G + g) * NV;
 #pragma unroll
         for (int q = 0; q < NV / 32; ++q) {
@@ -2164,8 +2178,10 @@ __global__ void __launch_bounds__(v4::kThreads, 1) k_svrg_chain_v4(EpochArgs a) 
       if constexpr (XG) {
         // one poller per CTA (four pollers per CTA slowed the exchange: C5 coef wait 534 -> 879 cycles), then
         // the reducer warps meet once on a named barrier
-        if (rw == 0 && lane == 0) xg_wait(xg_cnt + t % kXgSlots, static_cast<unsigned>(G) * (t / kXgSlots + 1));
-        asm volatile("bar.sync 4, %0;" ::"n"(32 * kRed) : "memory");  // every peer's partial of block t is in L2
+        if (a.xg_ll != 2) {
+          if (rw == 0 && lane == 0) xg_wait(xg_cnt + t % kXgSlots, static_cast<unsigned>(G) * (t / kXgSlots + 1));
+          asm volatile("bar.sync 4, %0;" ::"n"(32 * kRed) : "memory");  // every peer's partial of block t is in L2
+        }
       } else {
         mbar_wait(&rbar[par], static_cast<uint32_t>((t >> 2) & 1));
       }
@@ -2174,6 +2190,38 @@ __global__ void __launch_bounds__(v4::kThreads, 1) k_svrg_chain_v4(EpochArgs a) 
       if (j < bt_of(t)) {
         double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
         if constexpr (XG) {
+          if (a.xg_ll == 2) {  // poll this entry's cell of every peer (8 in flight), same summation order
+            const uint4* cl = reinterpret_cast<const uint4*>(a.xg_slot) +
+                              static_cast<size_t>(blockIdx.y) * kXgSlots * G * NV +
+                              static_cast<size_t>(t % kXgSlots) * G * NV + e;
+            const uint32_t flag = static_cast<uint32_t>(t / kXgSlots + 1);
+#pragma unroll 1
+            for (int q0 = 0; q0 < G; q0 += 8) {
+              uint4 w[8];
+#pragma unroll
+              for (int k = 0; k < 8; ++k) w[k] = ll_load(cl + (q0 + k) * NV);
+              unsigned pend = 0xffu;
+              while (pend) {
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                  if (pend >> k & 1u) {
+                    if (w[k].y == flag && w[k].w == flag)
+                      pend &= ~(1u << k);
+                    else
+                      w[k] = ll_load(cl + (q0 + k) * NV);
+                  }
+              }
+              auto val = [](const uint4& x) { return __hiloint2double(static_cast<int>(x.z), static_cast<int>(x.x)); };
+              s0 += val(w[0]);
+              s1 += val(w[1]);
+              s2 += val(w[2]);
+              s3 += val(w[3]);
+              s0 += val(w[4]);
+              s1 += val(w[5]);
+              s2 += val(w[6]);
+              s3 += val(w[7]);
+            }
+          } else {
           const double* sl = xg_slots + static_cast<size_t>(t % kXgSlots) * G * NV + e;
           // all G loads in flight (L2 latency, not a loop-carried chain, sets the cost)
 #pragma unroll 4
@@ -2182,6 +2230,7 @@ __global__ void __launch_bounds__(v4::kThreads, 1) k_svrg_chain_v4(EpochArgs a) 
             s1 += ld_cg(sl + (q + 1) * NV);
             s2 += ld_cg(sl + (q + 2) * NV);
             s3 += ld_cg(sl + (q + 3) * NV);
+          }
           }
         } else {
           const double* sl = recv + par * kMaxCluster * NV + e;
@@ -3036,6 +3085,11 @@ void launch_chain_pc(const EpochArgs& a, const EpochConfig& cfg, cudaStream_t st
   args.fast_reducer = env_fr;  // p = 1 DSMEM chains: register-preloaded reducer (0: the generic reducer loop)
   args.ncl = std::max(1, cfg.nclusters);
   args.xg_ll = xg && !use_v4 ? xg_ll_mode() : 0;
+  static const int env_v4_ll = getenv("GAPLRA_V4_LL") ? atoi(getenv("GAPLRA_V4_LL")) : 0;
+  if (xg && use_v4 && env_v4_ll) {  // experiment: flag-in-data cells for the v4 L2 exchange
+    args.xg_ll = 2;
+    GAPLRA_CUDA_CHECK(cudaMemsetAsync(a.xg_slot, 0, xg_slot_elems(cfg) * sizeof(double), st));
+  }
   args.rows_per_cta = cfg.rows_per_cta;
   args.stages = stages;
   args.pc = cfg.pc;
